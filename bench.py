@@ -1,0 +1,432 @@
+#!/usr/bin/env python
+"""Benchmark of the multisketch sketch-and-solve hot path on B200 (arXiv 2508.14209).
+
+One STEP = one pass of the whole hot path over one batch of synthetic input
+(SURVEY 8(a)): CountSketch apply of [A b] (a3) -> Gaussian stage Z = G(S[A b]) (a5)
+-> NCCL all-reduce of Z when N > 1 (a6) -> Householder solve (a7).  Codes (a1) and
+G (a4) live in the plan (timed separately as plan_ms); the normal-equations
+baseline (a8) is timed beside it on the same [A b].
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+Rank 0 prints ONE JSON line.  value = whole-job GB/s of [A b] sketched and solved
+(sum over ranks of d*(n+1)*8 bytes / max-over-ranks step time).  Weak scaling:
+every rank owns a d-row block of the row-partitioned global matrix.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CountSketch apply GB/s (% HBM peak) & multisketch-LS ms vs normal eqns, 1/2/4/8 B200"
+CONFIGS = {
+    "c1": dict(d=4096, n=8, k1=64, k2=16, kappa=None, name="C1: d=4096 n=8 k1=64 fp64"),
+    "c2": dict(d=1 << 24, n=64, k1=8192, k2=128, kappa=None,
+               name="C2: CountSketch d=2^24 n=64 (+b) k1=2n^2=8192 k2=2n=128 fp64 col-major, Gaussian A"),
+    "c3": dict(d=1 << 22, n=256, k1=131072, k2=512, kappa=None,
+               name="C3: multisketch d=2^22 n=256 (+b) k1=131072 k2=512 fp64, Gaussian A"),
+    "c4": dict(d=1 << 23, n=128, k1=32768, k2=256, kappa=1e10,
+               name="C4: multisketch LS [A b] d=2^23 n=128 k1=32768 k2=256 fp64, kappa(A)=1e10"),
+    "c5": dict(d=1 << 27, n=64, k1=8192, k2=128, kappa=None,
+               name="C5: row-partitioned d=2^27 n=64 (+b) k1=8192 k2=128 fp64 (strong scaling)"),
+}
+SKETCH_SEED, DATA_SEED = 1, 2
+FALLBACK_HBM_GBS = 6650.0
+NOMINAL_HBM_GBS = 8000.0
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------ peaks
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(workload_key, variant):
+    """dram bytes per launch of the dominant kernel from a committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            t = json.load(f)
+        e = t.get(workload_key, {}).get(str(variant))
+        return None if e is None else float(e["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int, period: float = 0.02):
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # noqa: BLE001
+            log(f"[bench] NVML unavailable: {e}")
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        names = [v for k, v in self.REASONS.items() if self.reasons & k and k != 0x1]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "reasons": names,
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ helpers
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def oracle_sample_rows(n, target_s, k1, k2):
+    """Rows of an oracle ms_lstsq sample that take about target_s seconds on one core."""
+    import numpy as np
+    import oracle
+    import synth
+    d0 = 1 << 15
+    A = synth.gaussian_matrix(d0, n, seed=DATA_SEED)
+    b = synth.rhs(A, "easy", seed=DATA_SEED)
+    t = time.perf_counter()
+    h, s = oracle.codes(d0, k1, SKETCH_SEED)
+    oracle.cs_apply(h, s, A, k1, b=b)
+    per_row = (time.perf_counter() - t) / d0
+    t = time.perf_counter()
+    G = oracle.gauss(k2, k1, SKETCH_SEED)
+    oracle.gemm_comp(G, np.zeros((k1, n + 1)))
+    fixed = time.perf_counter() - t
+    rows = int(max(1 << 12, (target_s - fixed) / max(per_row, 1e-12)))
+    return rows, per_row, fixed
+
+
+def run_oracle_sample(cfg, rows):
+    """Oracle multisketch LS on the first `rows` rows of a host-generated sample of the workload."""
+    import oracle
+    import synth
+    n, k1, k2 = cfg["n"], cfg["k1"], cfg["k2"]
+    A = synth.gaussian_matrix(rows, n, seed=DATA_SEED)
+    b = synth.rhs(A, "easy", seed=DATA_SEED)
+    t = time.perf_counter()
+    oracle.ms_lstsq(A, b, k1, k2, SKETCH_SEED)
+    return time.perf_counter() - t
+
+
+# ------------------------------------------------------------- reference arm
+def bench_reference(args, cfg):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    n = cfg["n"]
+    d = cfg["d"] if args.config != "c5" else cfg["d"] // max(ws, 1)
+    total_budget = 150.0
+    per_step = max(0.5, min(8.0, total_budget / max(1, args.steps + args.warmup)))
+    rows, per_row, fixed = oracle_sample_rows(n, per_step, cfg["k1"], cfg["k2"])
+    rows = min(rows, d)
+    for _ in range(args.warmup):
+        run_oracle_sample(cfg, rows)
+    times = [run_oracle_sample(cfg, rows) for _ in range(args.steps)]
+    t = statistics.mean(times)
+    gbs = rows * (n + 1) * 8 / t / 1e9
+    sample = (f"first {rows} rows of the {cfg['name']} workload (host-generated, same shape and "
+              f"distribution), full oracle ms_lstsq (codes + CountSketch + G + G-stage + Householder) per step")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["name"], "d": d, "n": n, "k1": cfg["k1"], "k2": cfg["k2"],
+                   "parallelism": "oracle (CPU, 1 thread)"},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample,
+                         "host_cores_available": cpu_cores()},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- our arm
+def bench_ours(args, cfg):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2508_14209_b200 as csk
+    import synth
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if args.variant != "auto":
+        os.environ["CSK_VARIANT"] = str(csk.csk.VARIANTS[args.variant])
+    n, k1, k2 = cfg["n"], cfg["k1"], cfg["k2"]
+    strong = args.config == "c5"
+    d_glob = cfg["d"] if strong else cfg["d"] * ws
+    d = d_glob // ws if strong else cfg["d"]
+    row0 = rank * d
+    ncols = n + 1
+    bytes_step = d * ncols * 8                        # [A b] read once per step (per rank)
+    stream = torch.cuda.current_stream(dev)
+
+    # ---- inputs: [A b] contiguous column-major (d x (n+1)), resident in HBM before timing
+    t0 = time.perf_counter()
+    buf = synth.colmajor_empty(torch, d, ncols, torch.float64, dev)
+    if cfg["kappa"]:
+        buf[:, :n] = synth.ill_conditioned_torch(d, n, cfg["kappa"], seed=DATA_SEED * 1000 + rank, device=dev)
+    else:
+        buf[:, :n] = synth.gaussian_matrix_torch(d, n, seed=DATA_SEED * 1000 + rank, device=dev)
+    buf[:, n] = synth.rhs_torch(buf[:, :n], "easy", seed=DATA_SEED * 1000 + rank)
+    A, b = buf[:, :n], buf[:, n]
+    torch.cuda.synchronize()
+    log(f"[bench] rank {rank}: inputs {bytes_step / 1e9:.2f} GB generated in {time.perf_counter() - t0:.1f}s")
+
+    # ---- plan (a1 codes; a4 G is drawn on first use and cached)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    plan = csk.cs_plan(d, k1, SKETCH_SEED, row0=row0, sort=(args.variant == "G"))
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    plan_ms = ev0.elapsed_time(ev1)
+    Z = synth.colmajor_empty(torch, k2, ncols, torch.float64, dev)
+    x = torch.empty(n, dtype=torch.float64, device=dev)
+    t = time.perf_counter()
+    csk.ms_apply(plan, k2, A, b=b, Z=Z)                 # draws and caches G (k2 x k1)
+    torch.cuda.synchronize()
+    gauss_first_ms = (time.perf_counter() - t) * 1e3
+
+    def step():
+        csk.ms_apply(plan, k2, A, b=b, Z=Z)
+        if ws > 1:
+            dist.all_reduce(Z)                           # a6: NCCL over NVLink
+        return csk.ms_solve(Z, n, x=x)[1]               # a7 (synchronises: numerical status)
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if ws == 1:
+            return v
+        t_ = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+        return float(t_.item())
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    clocks = ClockSampler(local)
+    csk.launch_count(reset=True)
+    with clocks:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        barrier()
+    launches = csk.launch_count() // max(1, args.steps) * args.steps
+    step_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    value = ws * bytes_step / (step_ms * 1e-3) / 1e9
+
+    # ---- dominant kernel (cs_apply main kernel) timed on its own stream with CUDA events
+    csk.profile_enable(True)
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
+    kern_ms_total, kern_launches = csk.profile_read()
+    csk.profile_enable(False)
+    kern_ms = kern_ms_total / max(1, kern_launches)
+    sa_bytes = k1 * ncols * 8
+    alg_bytes = bytes_step + sa_bytes                   # A read + SA write per launch
+    achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
+    peak, peak_src = hbm_peak()
+
+    # ---- phase breakdown (untimed in the main line): cs_apply alone
+    SA = synth.colmajor_empty(torch, k1, ncols, torch.float64, dev)
+    barrier()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        csk.cs_apply(plan, A, b=b, SA=SA)
+    ev1.record(stream)
+    barrier()
+    cs_ms = ev0.elapsed_time(ev1) / args.steps
+    ev0.record(stream)
+    for _ in range(args.steps):
+        csk.ms_apply(plan, k2, A, b=b, Z=Z)
+    ev1.record(stream)
+    barrier()
+    msa_ms = ev0.elapsed_time(ev1) / args.steps
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        csk.ms_solve(Z, n, x=x)
+    solve_ms = (time.perf_counter() - t) * 1e3 / args.steps
+
+    # ---- normal-equations baseline (a8) on the same [A b]
+    ne = {"gram": os.environ.get("CSK_NE_GRAM", "syrk")}
+    try:
+        for _ in range(max(1, args.warmup // 2)):
+            csk.ne_lstsq(A, b, x=x)
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            csk.ne_lstsq(A, b, x=x)
+        ev1.record(stream)
+        barrier()
+        ne["ms"] = ev0.elapsed_time(ev1) / args.steps
+        ne["status"] = "OK"
+    except csk.CskError as e:
+        ne["status"] = str(e).split(":")[1].strip()
+        ne["ms"] = None
+
+    # ---- accuracy of the step's solution (verification, untimed): ||b - A x|| / ||b||
+    step()
+    r_ms = float(torch.linalg.norm(b - A @ x) / torch.linalg.norm(b))
+    acc = {"rel_residual_ms": r_ms}
+    if ws == 1 and d * ncols * 8 <= 16e9:
+        R = torch.linalg.qr(buf, mode="r")[1]
+        acc["rel_residual_true"] = float(abs(R[n, n]) / torch.linalg.norm(b))
+        del R
+        if ne["status"] == "OK":
+            csk.ne_lstsq(A, b, x=x)
+            acc["rel_residual_ne"] = float(torch.linalg.norm(b - A @ x) / torch.linalg.norm(b))
+
+    # ---- e2e: C-ABI with HOST buffers (pinned), H2D inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        hbuf = torch.empty((ncols, d), dtype=torch.float64, pin_memory=True)
+        hbuf.copy_(buf.t())
+        hA, hb = hbuf.t()[:, :n], hbuf[n]
+        hx = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        csk.ms_lstsq(plan, k2, hA, hb, x=hx)           # warm
+        ke = max(1, min(args.steps, 3))
+        barrier()
+        t = time.perf_counter()
+        for _ in range(ke):
+            csk.ms_lstsq(plan, k2, hA, hb, x=hx)
+        barrier()
+        e2e_ms = max_over_ranks((time.perf_counter() - t) * 1e3 / ke)
+        e2e = {"value": ws * bytes_step / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": bytes_step, "d2h_bytes_per_step": n * 8 + 16, "steps": ke,
+               "path": "ms_lstsq(host A, b, x): row chunks streamed H2D on a copy stream, overlapped with the sketch"}
+        del hbuf
+
+    # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        rows, _, _ = oracle_sample_rows(n, 15.0, k1, k2)
+        rows = min(rows, d)
+        tcpu = run_oracle_sample(cfg, rows)
+        cpu = {"value": rows * ncols * 8 / tcpu / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+               "sample": f"first {rows} rows (+b) of the workload shape, oracle ms_lstsq (codes, CountSketch, G, "
+                         f"G-stage, Householder), {tcpu:.1f} s", "host_cores_available": cpu_cores()}
+
+    variant = os.environ.get("CSK_VARIANT", "auto")
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong" if strong else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["name"], "d_per_rank": d, "d_global": d_glob, "n": n, "k1": k1, "k2": k2,
+                   "rhs": "b = A e + eta, eta ~ N(0, 0.01)", "variant": variant,
+                   "l2": "inputs (%.1f GB per rank) > 126 MB L2; no flush needed" % (bytes_step / 1e9),
+                   "parallelism": f"row-partitioned dp{ws}" + (" + NCCL all-reduce of Z" if ws > 1 else "")},
+        "clocks": clocks.summary(),
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": ncu_traffic(args.config, variant), "kernel": "cs_apply main kernel",
+                     "kernel_ms": kern_ms, "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
+                     "frac_of_8TBs_nominal": achieved / NOMINAL_HBM_GBS},
+        "cpu_baseline": cpu,
+        "phases_ms": {"cs_apply": cs_ms, "g_stage": msa_ms - cs_ms, "solve": solve_ms, "plan_codes": plan_ms,
+                      "gauss_first_use": gauss_first_ms},
+        "cs_apply_gbs": bytes_step / (cs_ms * 1e-3) / 1e9,
+        "normal_equations": ne,
+        "speedup_vs_ne": (ne["ms"] / step_ms) if ne.get("ms") else None,
+        "accuracy": acc,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--variant", default="auto", choices=["auto", "L", "T", "S", "G", "B"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return bench_reference(args, cfg)
+    return bench_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,177 @@
+/*
+ * csk.h -- C-ABI of the B200 (sm_100a) CountSketch / multisketch / sketch-and-solve
+ * library (libcsk.so), the hot path of arXiv 2508.14209.
+ *
+ * Citations: P:Lx = PAPER.md line x (section / equation / algorithm).
+ *
+ * Conventions for every entry point
+ *  - Plain C linkage, no C++ exception ever crosses this boundary.
+ *  - Matrices are COLUMN-MAJOR with an explicit leading dimension (elements).
+ *  - "stream" is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *  - Device-side arguments are device pointers (or host pointers where stated);
+ *    the CALLER owns every buffer it passes.  A plan owns its codes, sort and
+ *    cached Gaussian matrices until cs_plan_destroy.
+ *  - Arguments are validated before any launch.  Errors are returned as a
+ *    csk_status; csk_last_error() gives a thread-local detail string.
+ *      null pointer / non-positive size .................. CSK_EINVAL
+ *      bad leading dimension or incompatible shapes ...... CSK_ESHAPE
+ *      unsupported dtype for the call .................... CSK_EDTYPE
+ *      allocation failure ................................ CSK_ENOMEM
+ *      CUDA / cuBLAS failure ............................. CSK_ECUDA
+ *      Cholesky pivot <= 0 (normal equations) ............ CSK_ENOTPD
+ *      |R_ii| <= 1e-14 max|R_jj| (sketched QR) ............ CSK_ESINGULAR
+ *      variant not applicable to this plan/shape ......... CSK_EUNSUPPORTED
+ *  - cs_plan*, cs_apply and ms_apply are asynchronous on the stream.
+ *    ms_solve, ms_lstsq and ne_lstsq synchronise the stream before returning
+ *    (they report a numerical status).
+ */
+#ifndef CSK_H
+#define CSK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    CSK_OK = 0,
+    CSK_EINVAL = 1,
+    CSK_ESHAPE = 2,
+    CSK_EDTYPE = 3,
+    CSK_ENOMEM = 4,
+    CSK_ECUDA = 5,
+    CSK_ENOTPD = 6,
+    CSK_ESINGULAR = 7,
+    CSK_EUNSUPPORTED = 8
+} csk_status;
+
+typedef enum { CSK_F64 = 0, CSK_F32 = 1 } csk_dtype;
+
+/* cs_apply kernel variants.  CSK_VAR_AUTO picks per
+ * (d, ncols, k1, dtype) from the measured selection table. */
+typedef enum {
+    CSK_VAR_AUTO = -1,
+    CSK_VAR_ATOMIC_COL = 0,   /* L: one L2 reduction (REDG) per element, column-major target  */
+    CSK_VAR_ATOMIC_ROW = 1,   /* T: row tiles transposed in smem, coalesced REDG into SA^T    */
+    CSK_VAR_SMEM = 2,         /* S: per-CTA shared-memory privatised buckets, one flush/CTA   */
+    CSK_VAR_SORTED = 3,       /* G: deterministic signed segmented gather over the plan sort   */
+    CSK_VAR_BULK_ROW = 4      /* B: row tiles in smem, TMA bulk reduce-add (cp.reduce.async.bulk) */
+} csk_variant;
+
+/* cs_plan flags */
+#define CSK_PLAN_SORT 0x2u    /* also build the stable counting sort (needed by CSK_VAR_SORTED) */
+
+typedef struct csk_plan_s* csk_plan_t;
+
+/* ---------------------------------------------------------------- plans --
+ * cs_plan: the CountSketch S (k1 x d) of Def 3, drawn from a
+ * counter-based hash of (seed, GLOBAL row) -- the hash-based generation the
+ * paper lists as future work.  Local row i of this plan is global row
+ * row0 + i, so the plans of a row-partitioned A are slices of one sketch
+ * (block-row distribution).  Device memory: 4*d bytes of codes
+ * (bucket | sign<<31); with CSK_PLAN_SORT also offsets (8*(k1+1)) and perm (4*d).
+ *   d      rows of the (local) block, 1 <= d <= 2^31 - 1
+ *   k1     embedding dimension, 1 <= k1 <= 2^31 - 1
+ *   seed   sketch seed (Philox key);  row0 >= 0 global index of local row 0
+ *   flags  0 or CSK_PLAN_SORT
+ *   out    receives the plan handle (NULL on failure) */
+csk_status cs_plan(int64_t d, int64_t k1, uint64_t seed, int64_t row0, uint32_t flags,
+                   void* stream, csk_plan_t* out);
+
+/* cs_plan_from_arrays: a plan with caller-chosen buckets h[i] in [0,k1) and
+ * signs s[i] in {-1,+1} (HOST arrays of length d, copied).  Used to force a
+ * sketch (identity, permutation, the worked example of S:L231). */
+csk_status cs_plan_from_arrays(int64_t d, int64_t k1, const int32_t* h, const int8_t* s,
+                               uint32_t flags, void* stream, csk_plan_t* out);
+
+/* cs_plan_export: copy the plan's codes (int32[d], bucket | sign<<31), and if the
+ * plan was built with CSK_PLAN_SORT the sort (offsets int64[k1+1], perm int32[d]).
+ * Pointers may be host or device (UVA copy); any may be NULL to skip.
+ * Synchronises the stream. */
+csk_status cs_plan_export(csk_plan_t plan, int32_t* code, int64_t* offsets, int32_t* perm,
+                          void* stream);
+
+/* cs_plan_info: d, k1, row0 of a plan (any output may be NULL). */
+csk_status cs_plan_info(csk_plan_t plan, int64_t* d, int64_t* k1, int64_t* row0);
+
+void cs_plan_destroy(csk_plan_t plan);
+
+/* ------------------------------------------------------------- sketches --
+ * cs_apply: SA = S [A b], Eq 2, Alg 2:
+ *   SA[m, c] = sum_{i : h(i) = m} s(i) A[i, c]   (c < n),   SA[m, n] = S b (if b).
+ *   dtype   CSK_F64 (A, b, SA double) or CSK_F32 (float)
+ *   n       columns of A (n >= 0; n + (b != NULL) >= 1)
+ *   A       d x n column-major, lda >= d (device pointer; may be NULL if n == 0)
+ *   b       optional extra column of length d (device pointer or NULL)
+ *   SA      k1 x (n + (b != NULL)) column-major, ldsa >= k1 (device pointer);
+ *           fully overwritten (empty buckets become exactly 0)
+ *   variant csk_variant; CSK_VAR_SORTED needs a plan built with CSK_PLAN_SORT
+ * Floating-point order is unspecified except for CSK_VAR_SORTED, which is
+ * bitwise deterministic; integer-valued inputs give exact sums in every variant. */
+csk_status cs_apply(csk_plan_t plan, csk_dtype dtype, int64_t n, const void* A, int64_t lda,
+                    const void* b, void* SA, int64_t ldsa, int variant, void* stream);
+
+/* ms_apply: the multisketch ("Count-Gauss"; Table 1)
+ *   Z = G S [A b],  G k2 x k1 with G_ij ~ N(0, 1/k2), drawn from Philox
+ *   stream 1 of the plan's seed (cached in the plan per k2, R4).
+ *   Z       k2 x (n + (b != NULL)) column-major, ldz >= k2 (device pointer).
+ *   A, b    device pointers, or HOST pointers (then streamed through the GPU in
+ *           row chunks, copies overlapped with the sketch -- P:L375 linearity).
+ *   Workspace for SA (k1 x ncols) comes from the stream-ordered allocator.
+ * For a row-partitioned A every rank calls ms_apply on its block
+ * with its row0-plan and the same seed, and the caller sums the Z's (NCCL
+ * all-reduce) before ms_solve. */
+csk_status ms_apply(csk_plan_t plan, int64_t k2, csk_dtype dtype, int64_t n, const void* A,
+                    int64_t lda, const void* b, void* Z, int64_t ldz, void* stream);
+
+/* ms_solve: the solve phase of sketch-and-solve (Alg 1 lines 2-3)
+ * on the augmented sketch Z = [G S A | G S b] (k2 x (n+1), fp64, device,
+ * not modified): R = qr(Z) by Householder, x = R[:n,:n]^-1 R[:n,n] (= R^-1 Q^T z).
+ *   x         device pointer, n doubles
+ *   sk_resid  HOST pointer or NULL: |R[n,n]| = ||G S (b - A x)||_2
+ * Requires k2 >= n + 1.  Returns CSK_ESINGULAR if some |R_ii| <= 1e-14 max|R_jj|.
+ * Synchronises the stream. */
+csk_status ms_solve(int64_t k2, int64_t n, const double* Z, int64_t ldz, double* x,
+                    double* sk_resid, void* stream);
+
+/* ms_lstsq: multisketched sketch-and-solve least squares min ||G S (A x - b)||
+ * (Alg 1 with S := G S1; "multisketch" bars of Fig 5):
+ * ms_apply(plan, k2, A, b) followed by ms_solve.  fp64.
+ *   A d x n (lda >= d), b length d: device or HOST pointers (host inputs are
+ *   streamed, see ms_apply); x: n doubles, device or HOST pointer;
+ *   sk_resid: HOST pointer or NULL.  Synchronises the stream. */
+csk_status ms_lstsq(csk_plan_t plan, int64_t k2, int64_t n, const double* A, int64_t lda,
+                    const double* b, double* x, double* sk_resid, void* stream);
+
+/* ne_lstsq: the normal-equations baseline: C = [A b]^T [A b] in one
+ * cuBLAS Gram (DSYRK or DGEMM, whichever is faster, R15), Cholesky
+ * of C[:n,:n] = R^T R, y = R^-T C[:n,n], x = R^-1 y.
+ *   A d x n (lda >= d), b length d, x n doubles: device pointers.
+ * Returns CSK_ENOTPD if a Cholesky pivot is <= 0 (the breakdown of Fig 8,
+ * P:L369).  Synchronises the stream. */
+csk_status ne_lstsq(int64_t d, int64_t n, const double* A, int64_t lda, const double* b,
+                    double* x, void* stream);
+
+/* ------------------------------------------------------------- utilities */
+const char* csk_status_str(csk_status st);
+const char* csk_last_error(void);      /* thread-local detail of the last failure */
+/* Number of device kernels this library launched on this host thread since
+ * the last reset (bench.py counts gpu_launches with it). */
+uint64_t csk_launch_count(int reset);
+/* Library version string. */
+const char* csk_version(void);
+
+/* Kernel timing for the roofline (bench.py): while enabled on this host thread,
+ * every launch of the dominant cs_apply kernel is bracketed by CUDA events on
+ * its launching stream.  csk_profile_read synchronises those events and returns
+ * the summed kernel time (ms) and the number of bracketed launches since the
+ * last enable, then clears them.  Off by default (no events recorded). */
+void csk_profile_enable(int on);
+csk_status csk_profile_read(double* total_ms, uint64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CSK_H */

@@ -1,0 +1,276 @@
+"""Thin ctypes binding over libcsk.so (include/csk.h).  Argument marshalling only:
+every step of the path runs in the library's CUDA kernels.  There is no CPU
+fallback -- loading fails loudly if the library is missing, and every call
+that needs a GPU raises if CUDA is unavailable.
+
+Tensors are torch tensors; matrices are column-major, i.e. shape (d, n) with
+stride (1, lda) -- e.g. ``torch.empty((n, d)).t()``.  Vectors are contiguous.
+Streams default to torch's current stream on the tensor's device.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+import threading
+
+from . import _build
+
+OK, EINVAL, ESHAPE, EDTYPE, ENOMEM, ECUDA, ENOTPD, ESINGULAR, EUNSUPPORTED = range(9)
+F64, F32 = 0, 1
+VAR_AUTO, VAR_ATOMIC_COL, VAR_ATOMIC_ROW, VAR_SMEM, VAR_SORTED, VAR_BULK_ROW = -1, 0, 1, 2, 3, 4
+VARIANTS = {"auto": VAR_AUTO, "L": VAR_ATOMIC_COL, "T": VAR_ATOMIC_ROW, "S": VAR_SMEM, "G": VAR_SORTED,
+            "B": VAR_BULK_ROW}
+PLAN_SORT = 0x2
+
+_lock = threading.Lock()
+_lib = None
+
+
+class CskError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str):
+        super().__init__(f"{where}: {_STATUS_NAMES.get(status, status)}: {detail}")
+        self.status = status
+
+
+_STATUS_NAMES = {OK: "CSK_OK", EINVAL: "CSK_EINVAL", ESHAPE: "CSK_ESHAPE", EDTYPE: "CSK_EDTYPE",
+                 ENOMEM: "CSK_ENOMEM", ECUDA: "CSK_ECUDA", ENOTPD: "CSK_ENOTPD", ESINGULAR: "CSK_ESINGULAR",
+                 EUNSUPPORTED: "CSK_EUNSUPPORTED"}
+
+
+def header_symbols() -> list[str]:
+    """Function names declared in include/csk.h (the boundary)."""
+    hdr = os.path.join(_build.ROOT, "include", "csk.h")
+    text = open(hdr).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b([a-z_][a-z0-9_]*)\s*\(", text)) - {"if", "sizeof"})
+
+
+def lib():
+    """Load libcsk.so (building it in-tree with nvcc if it is missing or stale)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            path = _build.LIB
+            if _build.needs_build():
+                path = _build.build()
+            L = ctypes.CDLL(path)
+            P, I64, U64, U32, I32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int
+            sigs = {
+                "cs_plan": [I64, I64, U64, I64, U32, P, P],
+                "cs_plan_from_arrays": [I64, I64, P, P, U32, P, P],
+                "cs_plan_export": [P, P, P, P, P],
+                "cs_plan_info": [P, P, P, P],
+                "cs_apply": [P, I32, I64, P, I64, P, P, I64, I32, P],
+                "ms_apply": [P, I64, I32, I64, P, I64, P, P, I64, P],
+                "ms_solve": [I64, I64, P, I64, P, P, P],
+                "ms_lstsq": [P, I64, I64, P, I64, P, P, P, P],
+                "ne_lstsq": [I64, I64, P, I64, P, P, P],
+            }
+            for name, argt in sigs.items():
+                f = getattr(L, name)
+                f.argtypes = argt
+                f.restype = ctypes.c_int
+            L.cs_plan_destroy.argtypes = [P]
+            L.cs_plan_destroy.restype = None
+            L.csk_status_str.argtypes = [ctypes.c_int]
+            L.csk_status_str.restype = ctypes.c_char_p
+            L.csk_last_error.restype = ctypes.c_char_p
+            L.csk_launch_count.argtypes = [ctypes.c_int]
+            L.csk_launch_count.restype = ctypes.c_uint64
+            L.csk_version.restype = ctypes.c_char_p
+            L.csk_profile_enable.argtypes = [ctypes.c_int]
+            L.csk_profile_enable.restype = None
+            L.csk_profile_read.argtypes = [P, P]
+            L.csk_profile_read.restype = ctypes.c_int
+            _lib = L
+    return _lib
+
+
+def _check(st: int, where: str):
+    if st != OK:
+        raise CskError(st, where, lib().csk_last_error().decode())
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2508_14209_b200 needs a CUDA GPU (no CPU fallback)")
+    return torch
+
+
+def _stream(stream, device=None):
+    if stream is None:
+        torch = _torch()
+        return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _colmajor(t, name):
+    """(pointer, ld) of a column-major (d, n) tensor; vectors have ld = len."""
+    if t is None:
+        return None, 0
+    if t.dim() == 1:
+        if t.stride(0) != 1:
+            raise ValueError(f"{name} must be contiguous")
+        return ctypes.c_void_p(t.data_ptr()), t.shape[0]
+    if t.dim() != 2 or (t.stride(0) != 1 and t.shape[0] > 1):
+        raise ValueError(f"{name} must be column-major: shape (d, n), stride (1, ld)")
+    ld = t.stride(1) if t.shape[1] > 1 else t.shape[0]
+    return ctypes.c_void_p(t.data_ptr()), max(ld, t.shape[0])
+
+
+def _dtype_code(t):
+    import torch
+    if t.dtype == torch.float64:
+        return F64
+    if t.dtype == torch.float32:
+        return F32
+    raise TypeError(f"unsupported dtype {t.dtype}")
+
+
+def launch_count(reset: bool = False) -> int:
+    return int(lib().csk_launch_count(1 if reset else 0))
+
+
+def profile_enable(on: bool = True):
+    """Bracket every dominant cs_apply kernel launch with CUDA events (roofline timing)."""
+    lib().csk_profile_enable(1 if on else 0)
+
+
+def profile_read():
+    """(summed kernel ms, number of bracketed launches) since profile_enable; clears them."""
+    ms = ctypes.c_double()
+    cnt = ctypes.c_uint64()
+    _check(lib().csk_profile_read(ctypes.byref(ms), ctypes.byref(cnt)), "csk_profile_read")
+    return ms.value, int(cnt.value)
+
+
+class Plan:
+    """Owning handle of a csk_plan_t (cs_plan / cs_plan_from_arrays)."""
+
+    def __init__(self, handle: int, d: int, k1: int, row0: int, seed: int | None, sorted_: bool):
+        self._h = ctypes.c_void_p(handle)
+        self.d, self.k1, self.row0, self.seed, self.sorted = d, k1, row0, seed, sorted_
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h and self._h.value:
+            lib().cs_plan_destroy(self._h)
+            self._h = ctypes.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def export(self, stream=None):
+        """(code int32[d], offsets int64[k1+1] | None, perm int32[d] | None) as numpy arrays."""
+        import numpy as np
+        code = np.zeros(self.d, np.int32)
+        offsets = np.zeros(self.k1 + 1, np.int64) if self.sorted else None
+        perm = np.zeros(self.d, np.int32) if self.sorted else None
+        ptr = lambda a: None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+        _check(lib().cs_plan_export(self._h, ptr(code), ptr(offsets), ptr(perm), _stream(stream)), "cs_plan_export")
+        return code, offsets, perm
+
+
+def cs_plan(d: int, k1: int, seed: int, row0: int = 0, sort: bool = False, stream=None) -> Plan:
+    _torch()
+    h = ctypes.c_void_p()
+    _check(lib().cs_plan(d, k1, seed, row0, PLAN_SORT if sort else 0, _stream(stream), ctypes.byref(h)), "cs_plan")
+    return Plan(h.value, d, k1, row0, seed, sort)
+
+
+def cs_plan_from_arrays(h, s, k1: int, sort: bool = False, stream=None) -> Plan:
+    import numpy as np
+    _torch()
+    h = np.ascontiguousarray(h, dtype=np.int32)
+    s = np.ascontiguousarray(s, dtype=np.int8)
+    out = ctypes.c_void_p()
+    _check(lib().cs_plan_from_arrays(h.shape[0], k1, h.ctypes.data_as(ctypes.c_void_p),
+                                     s.ctypes.data_as(ctypes.c_void_p), PLAN_SORT if sort else 0, _stream(stream),
+                                     ctypes.byref(out)), "cs_plan_from_arrays")
+    return Plan(out.value, h.shape[0], k1, 0, None, sort)
+
+
+def _ncols(A, b):
+    n = 0 if A is None else (A.shape[1] if A.dim() == 2 else 1)
+    return n, n + (1 if b is not None else 0)
+
+
+def cs_apply(plan: Plan, A, b=None, SA=None, variant="auto", stream=None):
+    """SA = S [A b] (k1 x ncols column-major, allocated if not given)."""
+    torch = _torch()
+    ref = A if A is not None else b
+    n, ncols = _ncols(A, b)
+    if SA is None:
+        SA = torch.empty((ncols, plan.k1), dtype=ref.dtype, device=ref.device).t()
+    pA, lda = _colmajor(A, "A") if A is not None else (None, plan.d)
+    pb, _ = _colmajor(b, "b")
+    pS, ldsa = _colmajor(SA, "SA")
+    v = VARIANTS[variant] if isinstance(variant, str) else int(variant)
+    _check(lib().cs_apply(plan.handle, _dtype_code(ref), n, pA, lda, pb, pS, ldsa, v, _stream(stream, ref.device)),
+           "cs_apply")
+    return SA
+
+
+def ms_apply(plan: Plan, k2: int, A, b=None, Z=None, stream=None):
+    """Z = G S [A b] (k2 x ncols column-major).  A, b may be CPU tensors (streamed)."""
+    torch = _torch()
+    ref = A if A is not None else b
+    n, ncols = _ncols(A, b)
+    dev = ref.device if ref.is_cuda else torch.device("cuda", torch.cuda.current_device())
+    if Z is None:
+        Z = torch.empty((ncols, k2), dtype=ref.dtype, device=dev).t()
+    pA, lda = _colmajor(A, "A") if A is not None else (None, plan.d)
+    pb, _ = _colmajor(b, "b")
+    pZ, ldz = _colmajor(Z, "Z")
+    _check(lib().ms_apply(plan.handle, k2, _dtype_code(ref), n, pA, lda, pb, pZ, ldz, _stream(stream, dev)),
+           "ms_apply")
+    return Z
+
+
+def ms_solve(Z, n: int, x=None, stream=None):
+    """(x, sketched residual) from the augmented sketch Z = [GSA | GSb] (k2 x (n+1))."""
+    torch = _torch()
+    if x is None:
+        x = torch.empty(n, dtype=torch.float64, device=Z.device)
+    pZ, ldz = _colmajor(Z, "Z")
+    r = ctypes.c_double()
+    _check(lib().ms_solve(Z.shape[0], n, pZ, ldz, ctypes.c_void_p(x.data_ptr()), ctypes.byref(r),
+                          _stream(stream, Z.device)), "ms_solve")
+    return x, r.value
+
+
+def ms_lstsq(plan: Plan, k2: int, A, b, x=None, stream=None):
+    """Multisketched sketch-and-solve: (x, sketched residual).  A, b, x may be CPU tensors."""
+    torch = _torch()
+    n = A.shape[1]
+    dev = A.device if A.is_cuda else torch.device("cuda", torch.cuda.current_device())
+    if x is None:
+        x = torch.empty(n, dtype=torch.float64, device=dev if A.is_cuda else "cpu")
+    pA, lda = _colmajor(A, "A")
+    pb, _ = _colmajor(b, "b")
+    r = ctypes.c_double()
+    _check(lib().ms_lstsq(plan.handle, k2, n, pA, lda, pb, ctypes.c_void_p(x.data_ptr()), ctypes.byref(r),
+                          _stream(stream, dev)), "ms_lstsq")
+    return x, r.value
+
+
+def ne_lstsq(A, b, x=None, stream=None):
+    """Normal-equations least squares (cuBLAS Gram + Cholesky); raises CskError(ENOTPD) on breakdown."""
+    torch = _torch()
+    d, n = A.shape
+    if x is None:
+        x = torch.empty(n, dtype=torch.float64, device=A.device)
+    pA, lda = _colmajor(A, "A")
+    pb, _ = _colmajor(b, "b")
+    _check(lib().ne_lstsq(d, n, pA, lda, pb, ctypes.c_void_p(x.data_ptr()), _stream(stream, A.device)), "ne_lstsq")
+    return x

@@ -1,0 +1,492 @@
+// countsketch.cu -- cs_apply: SA = S [A b]  (the hot kernel).
+//
+// Eq 2: Y_{m,:} = sum_{j: r_j = m} sigma_j A_{j,:}; Alg 2
+// scatters whole rows atomically.  A is column-major here (BASELINE.json; R7),
+// so a row is ncols strided elements.  Variants:
+//   L  cs_col_kernel    : each element -> one REDG.F64 into column-major SA (simplest)
+//   T  cs_row_kernel    : a warp loads a 32-row x 32-col tile (coalesced column reads),
+//                         transposes it through shared memory, and issues one coalesced
+//                         256-B REDG per row into SA^T (row-major, k1 x ldt) -- Alg 2's
+//                         "add rows atomically" with rows made contiguous on chip
+//   B  cs_row_kernel<BULK> : as T, but each row is reduced by the TMA engine with
+//                         cp.reduce.async.bulk .add.f64 (one 256-B bulk op per row)
+//   S  cs_smem_kernel   : per-CTA shared-memory privatised buckets for a group of columns;
+//                         each warp owns one column's k1 accumulators (no atomics on the
+//                         shared path, duplicates inside a warp merged with __match_any_sync),
+//                         one flush per CTA and column
+//   G  cs_sorted_kernel : deterministic signed segmented gather-sum over the plan's stable
+//                         counting sort (north_star form 1); bitwise reproducible
+// All variants accumulate in fp64 (fp32 input is widened; R12).
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "csk_internal.cuh"
+
+namespace csk {
+
+void prof_mark(cudaStream_t st, bool begin);
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ void red_add_f64(double* p, double v) {
+    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+template <typename T>
+__device__ __forceinline__ T ldg_stream(const T* p) {
+    return __ldcs(p);   // streaming: A is read exactly once
+}
+
+// ------------------------------------------------------------------ variant L
+template <typename T>
+__global__ void __launch_bounds__(256) cs_col_kernel(const uint32_t* __restrict__ code, int64_t rows, Cols<T> cols,
+                                                     int ncols, double* __restrict__ out, int64_t ldo) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows; i += stride) {
+        const uint32_t cd = __ldg(code + i);
+        double* dst = out + code_bucket(cd);
+        for (int c = 0; c < ncols; ++c) {
+            const double v = (double)ldg_stream(cols.col(c) + i);
+            red_add_f64(dst + (int64_t)c * ldo, apply_sign(v, cd));
+        }
+    }
+}
+
+// ------------------------------------------------------------- variants T / B
+constexpr int kRowWarps = 8;
+constexpr int kTileLd = 34;   // 32 columns + 2 pad doubles: rows stay 16-B aligned for bulk ops
+
+template <typename T, bool BULK>
+__global__ void __launch_bounds__(kRowWarps * 32) cs_row_kernel(const uint32_t* __restrict__ code, int64_t rows,
+                                                                Cols<T> cols, int ncols, double* __restrict__ SAt,
+                                                                int64_t ldt) {
+    extern __shared__ __align__(16) double row_smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int kBufs = BULK ? 2 : 1;
+    double* tiles = row_smem + (size_t)warp * kBufs * 32 * kTileLd;
+    const int nchunks = (ncols + 31) >> 5;
+    const int64_t ngroups = (rows + 31) >> 5;
+    const int64_t nunits = ngroups * nchunks;
+    const int64_t gwarp = blockIdx.x * (int64_t)kRowWarps + warp;
+    const int64_t nwarps = (int64_t)gridDim.x * kRowWarps;
+    int buf = 0;
+    for (int64_t u = gwarp; u < nunits; u += nwarps) {
+        const int64_t g = u / nchunks;
+        const int ch = (int)(u - g * nchunks);
+        const int c0 = ch * 32;
+        const int nc = min(32, ncols - c0);
+        const int64_t r = g * 32 + lane;
+        const bool valid = r < rows;
+        const uint32_t cd = valid ? __ldg(code + r) : 0u;
+        double* tile = tiles + buf * 32 * kTileLd;
+        if (BULK) {
+            // the bulk engine must have finished reading this buffer (issued 2 units ago)
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            __syncwarp();
+        }
+        double v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = (j < nc && valid) ? (double)ldg_stream(cols.col(c0 + j) + r) : 0.0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) tile[lane * kTileLd + j] = apply_sign(v[j], cd);
+        __syncwarp();
+        const int nrows = (int)min((int64_t)32, rows - g * 32);
+        if (!BULK) {
+            for (int j = 0; j < nrows; ++j) {
+                const uint32_t b = code_bucket(__shfl_sync(0xffffffffu, cd, j));
+                if (lane < nc) red_add_f64(SAt + (int64_t)b * ldt + c0 + lane, tile[j * kTileLd + lane]);
+            }
+            __syncwarp();
+        } else {
+            // generic-proxy smem writes -> visible to the async (bulk) proxy
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane < nrows) {
+                const uint32_t bytes = (uint32_t)(((nc + 1) & ~1) * 8);
+                double* dst = SAt + (int64_t)code_bucket(cd) * ldt + c0;
+                const uint32_t src = (uint32_t)__cvta_generic_to_shared(tile + lane * kTileLd);
+                asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(dst),
+                             "r"(src), "r"(bytes)
+                             : "memory");
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            buf ^= 1;
+        }
+    }
+    if (BULK) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// SA^T (row-major k1 x ldt, fp64) -> SA (column-major, ldsa, T)
+template <typename T>
+__global__ void transpose_out_kernel(const double* __restrict__ SAt, int64_t ldt, int64_t k1, int ncols,
+                                     T* __restrict__ SA, int64_t ldsa) {
+    __shared__ double t[32][33];
+    const int64_t m0 = blockIdx.x * 32;
+    const int c0 = blockIdx.y * 32;
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const int64_t m = m0 + j;
+        const int c = c0 + threadIdx.x;
+        t[j][threadIdx.x] = (m < k1 && c < ncols) ? SAt[m * ldt + c] : 0.0;
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const int c = c0 + j;
+        const int64_t m = m0 + threadIdx.x;
+        if (m < k1 && c < ncols) SA[m + (int64_t)c * ldsa] = (T)t[threadIdx.x][j];
+    }
+}
+
+// fp64 column-major workspace -> fp32 SA
+__global__ void narrow_kernel(const double* __restrict__ src, int64_t k1, int ncols, float* __restrict__ SA,
+                              int64_t ldsa) {
+    const int64_t total = k1 * ncols;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = e / k1, m = e - c * k1;
+        SA[m + c * ldsa] = (float)src[e];
+    }
+}
+
+// ------------------------------------------------------------------ variant S
+// One CTA per SM; CTA = `cpc` warps, warp w owns the k1 fp64 accumulators of
+// column g*cpc + w.  The linearised work space (column group g, row r) is split
+// evenly over CTAs, so a CTA touches at most a few groups and flushes once per group.
+constexpr int kSmemPrefetch = 4;   // row groups of 32 loaded ahead per warp
+
+template <typename T>
+__global__ void __launch_bounds__(1024, 1) cs_smem_kernel(const uint32_t* __restrict__ code, int64_t rows,
+                                                          Cols<T> cols, int ncols, int cpc, int k1,
+                                                          double* __restrict__ out, int64_t ldo,
+                                                          int64_t work_per_cta) {
+    extern __shared__ double acc_smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int ngroups = (ncols + cpc - 1) / cpc;
+    const int64_t total = (int64_t)ngroups * rows;
+    int64_t w = blockIdx.x * work_per_cta;
+    const int64_t w_end = min(total, w + work_per_cta);
+    double* acc = acc_smem + (size_t)warp * k1;
+    while (w < w_end) {
+        const int g = (int)(w / rows);
+        const int64_t r0 = w - (int64_t)g * rows;
+        const int64_t r1 = min(rows, r0 + (w_end - w));
+        for (int i = threadIdx.x; i < cpc * k1; i += blockDim.x) acc_smem[i] = 0.0;
+        __syncthreads();
+        const int c = g * cpc + warp;
+        if (c < ncols) {
+            const T* col = cols.col(c);
+            // software pipeline: kSmemPrefetch groups of 32 rows in registers
+            double pv[kSmemPrefetch];
+            uint32_t pc[kSmemPrefetch];
+#pragma unroll
+            for (int p = 0; p < kSmemPrefetch; ++p) {
+                const int64_t r = r0 + p * 32 + lane;
+                pv[p] = r < r1 ? (double)ldg_stream(col + r) : 0.0;
+                pc[p] = r < r1 ? __ldg(code + r) : 0u;
+            }
+            for (int64_t base = r0; base < r1; base += 32 * kSmemPrefetch) {
+#pragma unroll
+                for (int p = 0; p < kSmemPrefetch; ++p) {
+                    const int64_t r = base + p * 32 + lane;
+                    const bool valid = r < r1;
+                    const uint32_t cd = pc[p];
+                    double val = valid ? apply_sign(pv[p], cd) : 0.0;
+                    // refill this slot with the group kSmemPrefetch ahead
+                    const int64_t rn = r + 32 * kSmemPrefetch;
+                    pv[p] = rn < r1 ? (double)ldg_stream(col + rn) : 0.0;
+                    pc[p] = rn < r1 ? __ldg(code + rn) : 0u;
+                    const uint32_t key = valid ? code_bucket(cd) : 0x80000000u | lane;
+                    const uint32_t peers = __match_any_sync(0xffffffffu, key);
+                    if (peers != (1u << lane)) {
+                        // rare: lanes of this warp share a bucket -> the lowest lane sums them
+                        // in lane order (deterministic), the others drop out
+                        double sum = 0.0;
+                        for (uint32_t m = peers; m; m &= m - 1) sum += __shfl_sync(peers, val, __ffs(m) - 1);
+                        if (valid && lane == __ffs(peers) - 1) acc[code_bucket(cd)] += sum;
+                    } else if (valid) {
+                        const uint32_t b = code_bucket(cd);
+                        acc[b] += val;
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+        __syncthreads();
+        // flush this group's partial sums (REDG; skipped for exact zeros)
+        for (int i = threadIdx.x; i < cpc * k1; i += blockDim.x) {
+            const int cl = i / k1, m = i - cl * k1;
+            const int cc = g * cpc + cl;
+            const double v = acc_smem[i];
+            if (cc < ncols && v != 0.0) red_add_f64(out + m + (int64_t)cc * ldo, v);
+        }
+        __syncthreads();
+        w += r1 - r0;
+    }
+}
+
+// ------------------------------------------------------------------ variant G
+// Warp per (bucket m, column c): SA[m,c] = sum over the bucket's segment of the
+// sorted rows, lanes striding the segment, fixed-order shuffle tree at the end.
+// Bitwise deterministic (no atomics, fixed order).
+template <typename T>
+__global__ void __launch_bounds__(256) cs_sorted_kernel(const uint32_t* __restrict__ code,
+                                                        const int32_t* __restrict__ perm,
+                                                        const int64_t* __restrict__ offsets, int64_t k1,
+                                                        Cols<T> cols, int ncols, double* __restrict__ out,
+                                                        int64_t ldo) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t m = gw; m < k1; m += nw) {
+        const int64_t s0 = offsets[m], s1 = offsets[m + 1];
+        for (int c = 0; c < ncols; ++c) {
+            const T* col = cols.col(c);
+            double sum = 0.0;
+            for (int64_t p = s0 + lane; p < s1; p += 32) {
+                const int32_t i = __ldg(perm + p);
+                sum += apply_sign((double)__ldg(col + i), __ldg(code + i));
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            if (lane == 0) out[m + (int64_t)c * ldo] = sum;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ dispatch
+// Accumulation target of a variant: row-major SA^T workspace (T, B), or a
+// column-major fp64 buffer (L, S, G) which is SA itself for fp64 output.
+static bool variant_rowmajor(int v) { return v == CSK_VAR_ATOMIC_ROW || v == CSK_VAR_BULK_ROW; }
+
+static int env_variant() {
+    const char* e = std::getenv("CSK_VARIANT");
+    if (!e || !*e) return CSK_VAR_AUTO;
+    return std::atoi(e);
+}
+
+static int smem_cpc(int64_t k1, int ncols) {
+    const DeviceInfo& di = device_info();
+    const int64_t per_col = k1 * 8;
+    int cpc = (int)std::min<int64_t>((int64_t)di.smem_optin / per_col, 32);
+    return std::min(cpc, ncols);
+}
+
+// measured selection table
+static int select_variant(int64_t d, int64_t k1, int ncols, csk_dtype dtype, bool has_sort) {
+    (void)d;
+    (void)dtype;
+    (void)has_sort;
+    if (k1 * 8 * 2 <= (int64_t)device_info().smem_optin && smem_cpc(k1, ncols) >= 2) return CSK_VAR_SMEM;
+    (void)ncols;
+    return CSK_VAR_BULK_ROW;
+}
+
+template <typename T>
+static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> cols, int64_t row_begin,
+                              int64_t row_end, double* out, int64_t ldo, bool out_rowmajor, cudaStream_t st) {
+    const DeviceInfo& di = device_info();
+    const uint32_t* code = reinterpret_cast<const uint32_t*>(plan->code) + row_begin;
+    const int64_t rows = row_end - row_begin;
+    if (rows <= 0) return CSK_OK;
+    switch (variant) {
+        case CSK_VAR_ATOMIC_COL: {
+            const int64_t blocks = std::min<int64_t>(ceil_div(rows, 256), (int64_t)di.num_sms * 8);
+            cs_col_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(code, rows, cols, ncols, out, ldo);
+            CSK_LAUNCH_CHECK();
+            return CSK_OK;
+        }
+        case CSK_VAR_ATOMIC_ROW:
+        case CSK_VAR_BULK_ROW: {
+            (void)out_rowmajor;
+            const bool bulk = variant == CSK_VAR_BULK_ROW;
+            const size_t smem = (size_t)kRowWarps * (bulk ? 2 : 1) * 32 * kTileLd * sizeof(double);
+            const int64_t units = ceil_div(rows, 32) * ceil_div(ncols, 32);
+            auto kern = bulk ? cs_row_kernel<T, true> : cs_row_kernel<T, false>;
+            CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            int per_sm = 0;
+            CSK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowWarps * 32, smem));
+            per_sm = std::max(per_sm, 1);
+            const int64_t blocks = std::min<int64_t>(ceil_div(units, kRowWarps), (int64_t)di.num_sms * per_sm);
+            kern<<<(unsigned)blocks, kRowWarps * 32, smem, st>>>(code, rows, cols, ncols, out, ldo);
+            CSK_LAUNCH_CHECK();
+            return CSK_OK;
+        }
+        case CSK_VAR_SMEM: {
+            const int cpc = smem_cpc(plan->k1, ncols);
+            CSK_REQUIRE(cpc >= 1, CSK_EUNSUPPORTED, "variant S: k1=%lld buckets do not fit shared memory",
+                        (long long)plan->k1);
+            const size_t smem = (size_t)cpc * plan->k1 * sizeof(double);
+            CSK_CUDA_TRY(cudaFuncSetAttribute(cs_smem_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)smem));
+            const int ngroups = (ncols + cpc - 1) / cpc;
+            const int64_t total = (int64_t)ngroups * rows;
+            const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(di.num_sms, ceil_div(total, 32 * 64)));
+            const int64_t per_cta = ceil_div(total, grid);
+            cs_smem_kernel<T><<<(unsigned)grid, cpc * 32, smem, st>>>(code, rows, cols, ncols, cpc,
+                                                                        (int)plan->k1, out, ldo, per_cta);
+            CSK_LAUNCH_CHECK();
+            return CSK_OK;
+        }
+        case CSK_VAR_SORTED: {
+            CSK_REQUIRE(plan->perm != nullptr, CSK_EUNSUPPORTED, "variant G needs a plan built with CSK_PLAN_SORT");
+            CSK_REQUIRE(row_begin == 0 && row_end == plan->d, CSK_EUNSUPPORTED,
+                        "variant G needs the whole block resident on the device");
+            const int64_t blocks = std::min<int64_t>(ceil_div(plan->k1 * 32, 256), (int64_t)di.num_sms * 16);
+            cs_sorted_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(code, plan->perm, plan->offsets, plan->k1, cols,
+                                                                  ncols, out, ldo);
+            CSK_LAUNCH_CHECK();
+            return CSK_OK;
+        }
+        default:
+            set_error("unknown variant %d", variant);
+            return CSK_EINVAL;
+    }
+}
+
+
+struct ApplyTarget {
+    double* buf = nullptr;   // accumulation buffer
+    int64_t ld = 0;
+    bool owned = false;
+};
+
+csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void* A, int64_t lda, const void* b,
+                         void* SA, int64_t ldsa, int variant, cudaStream_t st, int64_t row_begin, int64_t row_end,
+                         bool accumulate) {
+    CSK_REQUIRE(plan != nullptr, CSK_EINVAL, "plan is NULL");
+    CSK_REQUIRE(dtype == CSK_F64 || dtype == CSK_F32, CSK_EDTYPE, "dtype %d not supported", (int)dtype);
+    CSK_REQUIRE(n >= 0, CSK_EINVAL, "n=%lld must be >= 0", (long long)n);
+    const int64_t ncols64 = n + (b ? 1 : 0);
+    CSK_REQUIRE(ncols64 >= 1 && ncols64 <= 65536, CSK_EINVAL, "n + (b != NULL) = %lld must be in [1, 65536]",
+                (long long)ncols64);
+    CSK_REQUIRE(n == 0 || A != nullptr, CSK_EINVAL, "A is NULL");
+    CSK_REQUIRE(SA != nullptr, CSK_EINVAL, "SA is NULL");
+    CSK_REQUIRE(n == 0 || lda >= plan->d, CSK_ESHAPE, "lda=%lld < d=%lld", (long long)lda, (long long)plan->d);
+    CSK_REQUIRE(ldsa >= plan->k1, CSK_ESHAPE, "ldsa=%lld < k1=%lld", (long long)ldsa, (long long)plan->k1);
+    const int ncols = (int)ncols64;
+    if (variant == CSK_VAR_AUTO) variant = env_variant();
+    if (variant == CSK_VAR_AUTO) variant = select_variant(plan->d, plan->k1, ncols, dtype, plan->perm != nullptr);
+    CSK_REQUIRE(variant >= CSK_VAR_ATOMIC_COL && variant <= CSK_VAR_BULK_ROW, CSK_EINVAL, "unknown variant %d",
+                variant);
+    if (variant == CSK_VAR_SMEM && smem_cpc(plan->k1, ncols) < 1) variant = CSK_VAR_BULK_ROW;
+    if (accumulate) {
+        // accumulating row blocks into SA (host streaming): SA itself must be the fp64 target
+        CSK_REQUIRE(dtype == CSK_F64, CSK_EDTYPE, "row-block accumulation needs fp64");
+        if (variant_rowmajor(variant) || variant == CSK_VAR_SORTED) variant = CSK_VAR_ATOMIC_COL;
+    }
+    const int64_t k1 = plan->k1;
+
+    ApplyTarget tgt;
+    if (variant_rowmajor(variant)) {
+        tgt.ld = (ncols + 3) & ~3;
+        tgt.owned = true;
+    } else if (dtype == CSK_F32) {
+        tgt.ld = k1;
+        tgt.owned = true;
+    } else {
+        tgt.buf = static_cast<double*>(SA);
+        tgt.ld = ldsa;
+    }
+    if (tgt.owned) {
+        const size_t bytes = (size_t)k1 * (variant_rowmajor(variant) ? tgt.ld : ncols) * sizeof(double);
+        CSK_CUDA_TRY(cudaMallocAsync(&tgt.buf, bytes, st));
+        CSK_CUDA_TRY(cudaMemsetAsync(tgt.buf, 0, bytes, st));
+    } else if (variant != CSK_VAR_SORTED && !accumulate) {
+        // zero SA (ldsa may exceed k1: clear the k1 x ncols window only)
+        if (ldsa == k1) {
+            CSK_CUDA_TRY(cudaMemsetAsync(tgt.buf, 0, (size_t)k1 * ncols * sizeof(double), st));
+        } else {
+            CSK_CUDA_TRY(cudaMemset2DAsync(tgt.buf, ldsa * sizeof(double), 0, k1 * sizeof(double), ncols, st));
+        }
+    }
+    csk_status s;
+    prof_mark(st, true);
+    if (dtype == CSK_F64) {
+        Cols<double> cols{static_cast<const double*>(A), static_cast<const double*>(b), lda, (int)n};
+        s = run_variant<double>(variant, plan, ncols, cols, row_begin, row_end, tgt.buf, tgt.ld,
+                                variant_rowmajor(variant), st);
+    } else {
+        Cols<float> cols{static_cast<const float*>(A), static_cast<const float*>(b), lda, (int)n};
+        s = run_variant<float>(variant, plan, ncols, cols, row_begin, row_end, tgt.buf, tgt.ld,
+                               variant_rowmajor(variant), st);
+    }
+    prof_mark(st, false);
+    if (s == CSK_OK && tgt.owned) {
+        if (variant_rowmajor(variant)) {
+            dim3 grid((unsigned)ceil_div(k1, 32), (unsigned)ceil_div(ncols, 32));
+            if (dtype == CSK_F64)
+                transpose_out_kernel<double><<<grid, dim3(32, 8), 0, st>>>(tgt.buf, tgt.ld, k1, ncols,
+                                                                           static_cast<double*>(SA), ldsa);
+            else
+                transpose_out_kernel<float><<<grid, dim3(32, 8), 0, st>>>(tgt.buf, tgt.ld, k1, ncols,
+                                                                          static_cast<float*>(SA), ldsa);
+        } else {
+            narrow_kernel<<<(unsigned)std::min<int64_t>(ceil_div(k1 * ncols, 256), 4096), 256, 0, st>>>(
+                tgt.buf, k1, ncols, static_cast<float*>(SA), ldsa);
+        }
+        count_launch();
+        if (cudaGetLastError() != cudaSuccess) {
+            set_error("cs_apply finalize launch failed");
+            s = CSK_ECUDA;
+        }
+    }
+    if (tgt.owned) cudaFreeAsync(tgt.buf, st);
+    return s;
+}
+
+}  // namespace csk
+
+extern "C" csk_status cs_apply(csk_plan_t plan, csk_dtype dtype, int64_t n, const void* A, int64_t lda,
+                               const void* b, void* SA, int64_t ldsa, int variant, void* stream) {
+    CSK_REQUIRE(plan != nullptr, CSK_EINVAL, "plan is NULL");
+    return csk::cs_apply_impl(plan, dtype, n, A, lda, b, SA, ldsa, variant, (cudaStream_t)stream, 0, plan->d,
+                              false);
+}
+
+// ------------------------------------------------------------- profiling
+namespace csk {
+static thread_local bool g_prof = false;
+static thread_local std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_prof_events;
+
+void prof_mark(cudaStream_t st, bool begin) {
+    if (!g_prof) return;
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    cudaEventRecord(e, st);
+    if (begin)
+        g_prof_events.push_back({e, nullptr});
+    else if (!g_prof_events.empty() && g_prof_events.back().second == nullptr)
+        g_prof_events.back().second = e;
+    else
+        cudaEventDestroy(e);
+}
+}  // namespace csk
+
+extern "C" void csk_profile_enable(int on) {
+    csk::g_prof = on != 0;
+    for (auto& p : csk::g_prof_events) {
+        cudaEventDestroy(p.first);
+        if (p.second) cudaEventDestroy(p.second);
+    }
+    csk::g_prof_events.clear();
+}
+
+extern "C" csk_status csk_profile_read(double* total_ms, uint64_t* launches) {
+    double sum = 0.0;
+    uint64_t cnt = 0;
+    for (auto& p : csk::g_prof_events) {
+        if (!p.second) continue;
+        CSK_CUDA_TRY(cudaEventSynchronize(p.second));
+        float ms = 0.f;
+        CSK_CUDA_TRY(cudaEventElapsedTime(&ms, p.first, p.second));
+        sum += ms;
+        ++cnt;
+    }
+    for (auto& p : csk::g_prof_events) {
+        cudaEventDestroy(p.first);
+        if (p.second) cudaEventDestroy(p.second);
+    }
+    csk::g_prof_events.clear();
+    if (total_ms) *total_ms = sum;
+    if (launches) *launches = cnt;
+    return CSK_OK;
+}

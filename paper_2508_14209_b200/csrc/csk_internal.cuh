@@ -1,0 +1,140 @@
+// csk_internal.cuh -- shared internals of libcsk.so (product side).
+// Nothing here is shared with oracle/; the Philox round below is written from
+// the generator's definition (Salmon et al. SC'11), R1/R3.
+#pragma once
+
+#include <cstdint>
+#include <cstdio>
+#include <map>
+#include <mutex>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "csk.h"
+
+namespace csk {
+
+// ------------------------------------------------------------------ errors
+void set_error(const char* fmt, ...);
+const char* last_error();
+
+#define CSK_REQUIRE(cond, status, ...)        \
+    do {                                       \
+        if (!(cond)) {                         \
+            ::csk::set_error(__VA_ARGS__);     \
+            return (status);                   \
+        }                                      \
+    } while (0)
+
+#define CSK_CUDA_TRY(call)                                                                  \
+    do {                                                                                    \
+        cudaError_t err__ = (call);                                                         \
+        if (err__ != cudaSuccess) {                                                         \
+            ::csk::set_error("%s failed: %s (%s:%d)", #call, cudaGetErrorString(err__),    \
+                             __FILE__, __LINE__);                                           \
+            return CSK_ECUDA;                                                               \
+        }                                                                                   \
+    } while (0)
+
+#define CSK_LAUNCH_CHECK()                                                                  \
+    do {                                                                                    \
+        ::csk::count_launch();                                                              \
+        cudaError_t err__ = cudaGetLastError();                                             \
+        if (err__ != cudaSuccess) {                                                         \
+            ::csk::set_error("kernel launch failed: %s (%s:%d)", cudaGetErrorString(err__), \
+                             __FILE__, __LINE__);                                           \
+            return CSK_ECUDA;                                                               \
+        }                                                                                   \
+    } while (0)
+
+void count_launch();
+
+// --------------------------------------------------------------- device info
+struct DeviceInfo {
+    int device = -1;
+    int num_sms = 0;
+    int smem_optin = 0;      // max dynamic smem per block (bytes)
+    int l2_bytes = 0;
+};
+const DeviceInfo& device_info();   // of the current device
+
+// -------------------------------------------------------------------- plan
+}  // namespace csk
+
+struct csk_plan_s {
+    int64_t d = 0, k1 = 0, row0 = 0;
+    uint64_t seed = 0;
+    int device = -1;
+    bool from_arrays = false;
+    int32_t* code = nullptr;      // d codes: bucket | sign << 31
+    int64_t* offsets = nullptr;   // k1 + 1 (CSK_PLAN_SORT)
+    int32_t* perm = nullptr;      // d      (CSK_PLAN_SORT)
+    std::mutex mu;                // guards the Gaussian caches
+    std::map<int64_t, double*> gauss64;
+    std::map<int64_t, float*> gauss32;
+};
+
+namespace csk {
+
+// ------------------------------------------------------------- Philox4x32-10
+__host__ __device__ __forceinline__ uint32_t mulhi32(uint32_t a, uint32_t b) {
+#ifdef __CUDA_ARCH__
+    return __umulhi(a, b);
+#else
+    return (uint32_t)(((uint64_t)a * b) >> 32);
+#endif
+}
+
+__host__ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r) {
+            k.x += 0x9E3779B9u;
+            k.y += 0xBB67AE85u;
+        }
+        const uint32_t hi0 = mulhi32(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+        const uint32_t hi1 = mulhi32(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    }
+    return c;
+}
+
+// code word: bucket in bits 0..30, sign (1 = negative) in bit 31
+__host__ __device__ __forceinline__ uint32_t code_bucket(uint32_t code) { return code & 0x7fffffffu; }
+__host__ __device__ __forceinline__ uint64_t code_sign_mask64(uint32_t code) {
+    return (uint64_t)(code & 0x80000000u) << 32;
+}
+__host__ __device__ __forceinline__ uint32_t code_sign_mask32(uint32_t code) { return code & 0x80000000u; }
+
+__device__ __forceinline__ double apply_sign(double v, uint32_t code) {
+    return __longlong_as_double(__double_as_longlong(v) ^ (long long)code_sign_mask64(code));
+}
+__device__ __forceinline__ float apply_sign(float v, uint32_t code) {
+    return __int_as_float(__float_as_int(v) ^ (int)code_sign_mask32(code));
+}
+
+// ------------------------------------------------------------ launch helpers
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// validated column-pointer table for [A b]: column c < n is A + c*lda, column n is b
+template <typename T>
+struct Cols {
+    const T* A;
+    const T* b;
+    int64_t lda;
+    int n;
+    __device__ __forceinline__ const T* col(int c) const { return c < n ? A + (int64_t)c * lda : b; }
+};
+
+// cs_apply implementation entry (countsketch.cu), also used by ms_apply
+csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void* A, int64_t lda,
+                         const void* b, void* SA, int64_t ldsa, int variant, cudaStream_t st,
+                         int64_t row_begin, int64_t row_end, bool accumulate);
+csk_status gauss_get(csk_plan_t plan, int64_t k2, csk_dtype dtype, cudaStream_t st, const void** G);
+struct cublasContext;
+csk_status blas_handle(cudaStream_t st, struct cublasContext** h);
+
+bool is_device_pointer(const void* p);
+
+}  // namespace csk

@@ -1,0 +1,381 @@
+// multisketch.cu -- ms_apply / ms_solve / ms_lstsq.
+//
+// a4 G:    k2 x k1 Gaussian, G_ij ~ N(0, 1/k2) ("2n x 2n^2 Gaussian"),
+//          Philox stream 1 + Box-Muller (R4), cached in the plan per k2.
+// a5 Z:    Z = G (S [A b])  -- the multisketch S2(S1 x), a plain DGEMM
+//          (fp64 DMMA tensor cores via cuBLAS; Table 1 P:L99 "n^4" term).
+// a7 solve: Householder QR of Z = [GSA | GSb] in one CTA, back substitution
+//          (Alg 1 lines 2-3; GeQRF + OrMQR + TRSV of P:L230).
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include <cublas_v2.h>
+
+#include "csk_internal.cuh"
+
+namespace csk {
+
+// --------------------------------------------------------------- cuBLAS
+csk_status blas_handle(cudaStream_t st, cublasHandle_t* out) {
+    static thread_local std::map<int, cublasHandle_t> handles;
+    int dev = 0;
+    CSK_CUDA_TRY(cudaGetDevice(&dev));
+    auto it = handles.find(dev);
+    if (it == handles.end()) {
+        cublasHandle_t h = nullptr;
+        CSK_REQUIRE(cublasCreate(&h) == CUBLAS_STATUS_SUCCESS, CSK_ECUDA, "cublasCreate failed");
+        // fp64 stays fp64; no TF32 for fp32 (tolerance 1e-5 needs full fp32 products)
+        cublasSetMathMode(h, CUBLAS_PEDANTIC_MATH);
+        it = handles.emplace(dev, h).first;
+    }
+    CSK_REQUIRE(cublasSetStream(it->second, st) == CUBLAS_STATUS_SUCCESS, CSK_ECUDA, "cublasSetStream failed");
+    *out = it->second;
+    return CSK_OK;
+}
+
+// ------------------------------------------------------------------ a4: G
+template <typename T>
+__global__ void gauss_kernel(T* __restrict__ G, int64_t total, double inv_sqrt_scale_div, uint32_t key_lo,
+                             uint32_t key_hi) {
+    const int64_t npairs = total >> 1;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < npairs; t += (int64_t)gridDim.x * blockDim.x) {
+        const uint4 x = philox4x32_10(make_uint4((uint32_t)t, (uint32_t)(t >> 32), 1u, 0u), make_uint2(key_lo, key_hi));
+        const uint64_t w1 = ((uint64_t)x.y << 32) | x.x;
+        const uint64_t w2 = ((uint64_t)x.w << 32) | x.z;
+        const double u1 = (double)((w1 >> 11) + 1) * 0x1.0p-53;
+        const double u2 = (double)(w2 >> 11) * 0x1.0p-53;
+        const double rho = sqrt(-2.0 * log(u1));
+        double s, c;
+        sincospi(2.0 * u2, &s, &c);
+        G[2 * t] = (T)((rho * c) / inv_sqrt_scale_div);
+        G[2 * t + 1] = (T)((rho * s) / inv_sqrt_scale_div);
+    }
+}
+
+csk_status gauss_get(csk_plan_t plan, int64_t k2, csk_dtype dtype, cudaStream_t st, const void** out) {
+    std::lock_guard<std::mutex> lk(plan->mu);
+    if (dtype == CSK_F64) {
+        auto it = plan->gauss64.find(k2);
+        if (it != plan->gauss64.end()) {
+            *out = it->second;
+            return CSK_OK;
+        }
+    } else {
+        auto it = plan->gauss32.find(k2);
+        if (it != plan->gauss32.end()) {
+            *out = it->second;
+            return CSK_OK;
+        }
+    }
+    const int64_t total = k2 * plan->k1;
+    const size_t esz = dtype == CSK_F64 ? 8 : 4;
+    void* G = nullptr;
+    if (cudaMalloc(&G, (size_t)total * esz) != cudaSuccess) {
+        cudaGetLastError();
+        set_error("allocation of G (%lld x %lld) failed", (long long)k2, (long long)plan->k1);
+        return CSK_ENOMEM;
+    }
+    const double div = std::sqrt((double)k2);
+    const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(std::max<int64_t>(total / 2, 1), 256), 148 * 32);
+    if (dtype == CSK_F64)
+        gauss_kernel<double><<<grid, 256, 0, st>>>((double*)G, total, div, (uint32_t)plan->seed,
+                                                    (uint32_t)(plan->seed >> 32));
+    else
+        gauss_kernel<float><<<grid, 256, 0, st>>>((float*)G, total, div, (uint32_t)plan->seed,
+                                                   (uint32_t)(plan->seed >> 32));
+    count_launch();
+    if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) {
+        cudaFree(G);
+        set_error("gauss_kernel failed");
+        return CSK_ECUDA;
+    }
+    if (total & 1) {
+        // odd total: the last element has no Box-Muller partner; draw its pair and keep the cosine
+        // half (the kernel above covers pairs only) -- recompute on the host, same formula
+        const int64_t t = total >> 1;
+        uint4 x = philox4x32_10(make_uint4((uint32_t)t, (uint32_t)(t >> 32), 1u, 0u),
+                                make_uint2((uint32_t)plan->seed, (uint32_t)(plan->seed >> 32)));
+        const uint64_t w1 = ((uint64_t)x.y << 32) | x.x;
+        const uint64_t w2 = ((uint64_t)x.w << 32) | x.z;
+        const double u1 = (double)((w1 >> 11) + 1) * 0x1.0p-53;
+        const double u2 = (double)(w2 >> 11) * 0x1.0p-53;
+        const double v = (std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586476925286766559 * u2)) / div;
+        if (dtype == CSK_F64) {
+            CSK_CUDA_TRY(cudaMemcpy((double*)G + total - 1, &v, 8, cudaMemcpyHostToDevice));
+        } else {
+            const float f = (float)v;
+            CSK_CUDA_TRY(cudaMemcpy((float*)G + total - 1, &f, 4, cudaMemcpyHostToDevice));
+        }
+    }
+    if (dtype == CSK_F64)
+        plan->gauss64[k2] = (double*)G;
+    else
+        plan->gauss32[k2] = (float*)G;
+    *out = G;
+    return CSK_OK;
+}
+
+// ---------------------------------------------------- a3 over host inputs
+// Host A/b: stream row chunks through two device staging buffers; the copy of
+// chunk i+1 overlaps the sketch of chunk i (the sketch is linear in row blocks,
+// P:L375).  Accumulates into the fp64 column-major buffer SA.
+static csk_status sketch_host_rows(csk_plan_t plan, int64_t n, const double* A, int64_t lda, const double* b,
+                                   double* SA, int64_t ldsa, cudaStream_t st) {
+    const int ncols = (int)(n + (b ? 1 : 0));
+    const int64_t d = plan->d;
+    const int64_t chunk = std::min<int64_t>(d, std::max<int64_t>(1 << 16, (int64_t)(256ll << 20) / (8 * ncols)));
+    double* stage[2] = {nullptr, nullptr};
+    cudaEvent_t copied[2], consumed[2];
+    cudaStream_t cs = nullptr;
+    CSK_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+        CSK_CUDA_TRY(cudaMallocAsync(&stage[i], (size_t)chunk * ncols * 8, st));
+        CSK_CUDA_TRY(cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming));
+        CSK_CUDA_TRY(cudaEventCreateWithFlags(&consumed[i], cudaEventDisableTiming));
+        CSK_CUDA_TRY(cudaEventRecord(consumed[i], st));
+    }
+    csk_status s = CSK_OK;
+    int k = 0;
+    for (int64_t r0 = 0; r0 < d && s == CSK_OK; r0 += chunk, k ^= 1) {
+        const int64_t rows = std::min(chunk, d - r0);
+        CSK_CUDA_TRY(cudaStreamWaitEvent(cs, consumed[k], 0));
+        for (int c = 0; c < n; ++c)
+            CSK_CUDA_TRY(cudaMemcpyAsync(stage[k] + (int64_t)c * rows, A + r0 + (int64_t)c * lda, rows * 8,
+                                         cudaMemcpyHostToDevice, cs));
+        if (b) CSK_CUDA_TRY(cudaMemcpyAsync(stage[k] + n * rows, b + r0, rows * 8, cudaMemcpyHostToDevice, cs));
+        CSK_CUDA_TRY(cudaEventRecord(copied[k], cs));
+        CSK_CUDA_TRY(cudaStreamWaitEvent(st, copied[k], 0));
+        s = cs_apply_impl(plan, CSK_F64, n, stage[k], rows, b ? stage[k] + n * rows : nullptr, SA, ldsa,
+                          CSK_VAR_AUTO, st, r0, r0 + rows, /*accumulate=*/true);
+        CSK_CUDA_TRY(cudaEventRecord(consumed[k], st));
+    }
+    CSK_CUDA_TRY(cudaStreamSynchronize(cs));
+    for (int i = 0; i < 2; ++i) {
+        cudaFreeAsync(stage[i], st);
+        cudaEventDestroy(copied[i]);
+        cudaEventDestroy(consumed[i]);
+    }
+    cudaStreamDestroy(cs);
+    (void)ncols;
+    return s;
+}
+
+// ------------------------------------------------------------- a7: ms_solve
+// One CTA.  W (m x nc, column-major, ld m) is a private copy of Z in global
+// memory (L2-resident: <= 1 MB at the BASELINE sizes) or shared memory when it fits.
+// Householder with the LAPACK sign choice R_jj = -sign(x0) ||x||.
+struct SolveStatus {
+    int status;
+    double sk_resid;
+};
+
+constexpr int kQrThreads = 1024;
+
+__device__ double block_sum(double v, double* red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double s = 0.0;
+    const int nw = blockDim.x >> 5;
+    for (int w = 0; w < nw; ++w) s += red[w];   // fixed order, every thread gets the same value
+    return s;
+}
+
+__global__ void __launch_bounds__(kQrThreads, 1) qr_solve_kernel(double* __restrict__ Wg, int m, int nc,
+                                                                 int use_smem, double* __restrict__ x,
+                                                                 SolveStatus* __restrict__ status) {
+    extern __shared__ double qsm[];
+    __shared__ double red[32];
+    __shared__ double s_alpha, s_beta;
+    __shared__ int s_fail;
+    double* v = qsm;                       // m
+    double* W = use_smem ? qsm + m : Wg;   // m x nc
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (use_smem) {
+        for (int e = threadIdx.x; e < m * nc; e += blockDim.x) W[e] = Wg[e];
+        __syncthreads();
+    }
+    for (int j = 0; j < nc; ++j) {
+        double* wj = W + (int64_t)j * m;
+        double part = 0.0;
+        for (int i = j + threadIdx.x; i < m; i += blockDim.x) part += wj[i] * wj[i];
+        const double norm2 = block_sum(part, red);
+        const double x0 = wj[j];
+        const double norm = sqrt(norm2);
+        const double alpha = norm == 0.0 ? 0.0 : (x0 >= 0.0 ? -norm : norm);
+        for (int i = j + threadIdx.x; i < m; i += blockDim.x) v[i] = (i == j) ? x0 - alpha : wj[i];
+        // v^T v = (x0 - alpha)^2 + (norm2 - x0^2); recompute exactly from v for robustness
+        __syncthreads();
+        double pv = 0.0;
+        for (int i = j + threadIdx.x; i < m; i += blockDim.x) pv += v[i] * v[i];
+        const double vtv = block_sum(pv, red);
+        if (threadIdx.x == 0) {
+            s_alpha = alpha;
+            s_beta = vtv > 0.0 ? 2.0 / vtv : 0.0;
+        }
+        __syncthreads();
+        const double beta = s_beta;
+        if (beta != 0.0) {
+            for (int c = j + 1 + warp; c < nc; c += nw) {
+                double* wc = W + (int64_t)c * m;
+                double dot = 0.0;
+                for (int i = j + lane; i < m; i += 32) dot += v[i] * wc[i];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+                const double f = beta * dot;
+                for (int i = j + lane; i < m; i += 32) wc[i] -= f * v[i];
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) wj[j] = s_alpha;
+        __syncthreads();
+    }
+    // R is the upper triangle of W.  Singularity check on R[:n,:n].
+    const int n = nc - 1;
+    if (threadIdx.x == 0) {
+        double rmax = 0.0;
+        for (int i = 0; i < n; ++i) rmax = fmax(rmax, fabs(W[i + (int64_t)i * m]));
+        int st = 0;
+        for (int i = 0; i < n; ++i)
+            if (!(fabs(W[i + (int64_t)i * m]) > 1e-14 * rmax)) st = CSK_ESINGULAR;
+        status->status = st;
+        status->sk_resid = fabs(W[n + (int64_t)n * m]);
+        s_fail = st;
+    }
+    __syncthreads();
+    if (s_fail) return;
+    // back substitution R[:n,:n] x = R[:n, n], column-oriented; y lives in v
+    for (int i = threadIdx.x; i < n; i += blockDim.x) v[i] = W[i + (int64_t)n * m];
+    __syncthreads();
+    for (int c = n - 1; c >= 0; --c) {
+        const double xc = v[c] / W[c + (int64_t)c * m];
+        __syncthreads();
+        for (int i = threadIdx.x; i < c; i += blockDim.x) v[i] -= W[i + (int64_t)c * m] * xc;
+        if (threadIdx.x == 0) x[c] = xc;
+        __syncthreads();
+    }
+}
+
+static csk_status solve_impl(int64_t k2, int64_t n, const double* Z, int64_t ldz, double* x, double* sk_resid,
+                             cudaStream_t st, bool x_host) {
+    CSK_REQUIRE(Z != nullptr && x != nullptr, CSK_EINVAL, "Z and x must be non-NULL");
+    CSK_REQUIRE(n >= 1 && n <= 65535, CSK_EINVAL, "n=%lld must be in [1, 65535]", (long long)n);
+    CSK_REQUIRE(k2 >= n + 1, CSK_ESHAPE, "k2=%lld must be >= n+1=%lld", (long long)k2, (long long)(n + 1));
+    CSK_REQUIRE(ldz >= k2, CSK_ESHAPE, "ldz=%lld < k2=%lld", (long long)ldz, (long long)k2);
+    const int m = (int)k2, nc = (int)(n + 1);
+    double* W = nullptr;
+    double* xd = nullptr;
+    SolveStatus* sd = nullptr;
+    const size_t wbytes = (size_t)m * nc * 8;
+    CSK_CUDA_TRY(cudaMallocAsync(&W, wbytes + 64 + (x_host ? n * 8 : 0), st));
+    sd = reinterpret_cast<SolveStatus*>(reinterpret_cast<char*>(W) + wbytes);
+    xd = x_host ? reinterpret_cast<double*>(reinterpret_cast<char*>(W) + wbytes + 64) : x;
+    CSK_CUDA_TRY(cudaMemcpy2DAsync(W, m * 8, Z, ldz * 8, m * 8, nc, cudaMemcpyDeviceToDevice, st));
+    const DeviceInfo& di = device_info();
+    const size_t smem_need = (size_t)(m + (size_t)m * nc) * 8;
+    const int use_smem = smem_need <= (size_t)di.smem_optin ? 1 : 0;
+    const size_t smem = use_smem ? smem_need : (size_t)m * 8;
+    CSK_CUDA_TRY(cudaFuncSetAttribute(qr_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    qr_solve_kernel<<<1, kQrThreads, smem, st>>>(W, m, nc, use_smem, xd, sd);
+    CSK_LAUNCH_CHECK();
+    SolveStatus hs;
+    CSK_CUDA_TRY(cudaMemcpyAsync(&hs, sd, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    if (x_host) CSK_CUDA_TRY(cudaMemcpyAsync(x, xd, n * 8, cudaMemcpyDeviceToHost, st));
+    CSK_CUDA_TRY(cudaFreeAsync(W, st));
+    CSK_CUDA_TRY(cudaStreamSynchronize(st));
+    if (sk_resid) *sk_resid = hs.sk_resid;
+    if (hs.status != 0) {
+        set_error("sketched R is numerically singular (|R_ii| <= 1e-14 max|R_jj|)");
+        return (csk_status)hs.status;
+    }
+    return CSK_OK;
+}
+
+static csk_status ms_apply_impl(csk_plan_t plan, int64_t k2, csk_dtype dtype, int64_t n, const void* A, int64_t lda,
+                                const void* b, void* Z, int64_t ldz, cudaStream_t st) {
+    CSK_REQUIRE(plan != nullptr, CSK_EINVAL, "plan is NULL");
+    CSK_REQUIRE(Z != nullptr, CSK_EINVAL, "Z is NULL");
+    CSK_REQUIRE(k2 >= 1 && k2 <= 1 << 20, CSK_EINVAL, "k2=%lld out of range", (long long)k2);
+    CSK_REQUIRE(ldz >= k2, CSK_ESHAPE, "ldz=%lld < k2=%lld", (long long)ldz, (long long)k2);
+    CSK_REQUIRE(dtype == CSK_F64 || dtype == CSK_F32, CSK_EDTYPE, "dtype %d not supported", (int)dtype);
+    const int64_t ncols = n + (b ? 1 : 0);
+    CSK_REQUIRE(n >= 0 && ncols >= 1, CSK_EINVAL, "n + (b != NULL) must be >= 1");
+    CSK_REQUIRE(n == 0 || A != nullptr, CSK_EINVAL, "A is NULL");
+    const bool host_in = (n > 0 && !is_device_pointer(A)) || (b && !is_device_pointer(b));
+    CSK_REQUIRE(!host_in || dtype == CSK_F64, CSK_EDTYPE, "host-resident inputs are supported for fp64 only");
+    const int64_t k1 = plan->k1;
+    const size_t esz = dtype == CSK_F64 ? 8 : 4;
+    void* SA = nullptr;
+    CSK_CUDA_TRY(cudaMallocAsync(&SA, (size_t)k1 * ncols * esz, st));
+    csk_status s;
+    if (host_in) {
+        CSK_REQUIRE(n == 0 || lda >= plan->d, CSK_ESHAPE, "lda < d");
+        CSK_CUDA_TRY(cudaMemsetAsync(SA, 0, (size_t)k1 * ncols * 8, st));
+        s = sketch_host_rows(plan, n, (const double*)A, lda, (const double*)b, (double*)SA, k1, st);
+    } else {
+        s = cs_apply_impl(plan, dtype, n, A, lda, b, SA, k1, CSK_VAR_AUTO, st, 0, plan->d, false);
+    }
+    if (s == CSK_OK) {
+        const void* G = nullptr;
+        s = gauss_get(plan, k2, dtype, st, &G);
+        if (s == CSK_OK) {
+            cublasHandle_t h;
+            s = blas_handle(st, &h);
+            if (s == CSK_OK) {
+                cublasStatus_t bs;
+                if (dtype == CSK_F64) {
+                    const double one = 1.0, zero = 0.0;
+                    bs = cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)k2, (int)ncols, (int)k1, &one, (const double*)G,
+                                     (int)k2, (const double*)SA, (int)k1, &zero, (double*)Z, (int)ldz);
+                } else {
+                    const float one = 1.0f, zero = 0.0f;
+                    bs = cublasSgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)k2, (int)ncols, (int)k1, &one, (const float*)G,
+                                     (int)k2, (const float*)SA, (int)k1, &zero, (float*)Z, (int)ldz);
+                }
+                if (bs != CUBLAS_STATUS_SUCCESS) {
+                    set_error("cuBLAS G-stage GEMM failed (%d)", (int)bs);
+                    s = CSK_ECUDA;
+                }
+            }
+        }
+    }
+    cudaFreeAsync(SA, st);
+    return s;
+}
+
+}  // namespace csk
+
+using namespace csk;
+
+extern "C" {
+
+csk_status ms_apply(csk_plan_t plan, int64_t k2, csk_dtype dtype, int64_t n, const void* A, int64_t lda,
+                    const void* b, void* Z, int64_t ldz, void* stream) {
+    return ms_apply_impl(plan, k2, dtype, n, A, lda, b, Z, ldz, (cudaStream_t)stream);
+}
+
+csk_status ms_solve(int64_t k2, int64_t n, const double* Z, int64_t ldz, double* x, double* sk_resid, void* stream) {
+    CSK_REQUIRE(x == nullptr || is_device_pointer(x), CSK_EINVAL, "x must be a device pointer");
+    return solve_impl(k2, n, Z, ldz, x, sk_resid, (cudaStream_t)stream, false);
+}
+
+csk_status ms_lstsq(csk_plan_t plan, int64_t k2, int64_t n, const double* A, int64_t lda, const double* b, double* x,
+                    double* sk_resid, void* stream) {
+    CSK_REQUIRE(plan != nullptr, CSK_EINVAL, "plan is NULL");
+    CSK_REQUIRE(b != nullptr && x != nullptr, CSK_EINVAL, "b and x must be non-NULL");
+    CSK_REQUIRE(n >= 1, CSK_EINVAL, "n must be >= 1");
+    CSK_REQUIRE(k2 >= n + 1, CSK_ESHAPE, "k2=%lld must be >= n+1", (long long)k2);
+    cudaStream_t st = (cudaStream_t)stream;
+    double* Z = nullptr;
+    CSK_CUDA_TRY(cudaMallocAsync(&Z, (size_t)k2 * (n + 1) * 8, st));
+    csk_status s = ms_apply_impl(plan, k2, CSK_F64, n, A, lda, b, Z, k2, st);
+    if (s == CSK_OK) s = solve_impl(k2, n, Z, k2, x, sk_resid, st, !is_device_pointer(x));
+    cudaFreeAsync(Z, st);
+    return s;
+}
+
+}  // extern "C"

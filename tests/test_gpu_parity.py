@@ -1,0 +1,326 @@
+"""GPU parity: the CUDA path through the C-ABI against the CPU oracle.
+
+Bit-exact: codes (hash), the counting sort, integer-valued A.  Tolerances
+(BASELINE.json north_star): fp64 |dSA| <= 1e-12 * sum|terms|, fp32 <= 1e-5;
+G within 1e-13/sqrt(k2); Z within 1e-12 |G| T; least squares
+||A (x_gpu - x_oracle)|| / ||b|| <= 1e-8 (R16).
+"""
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests._util import assert_within_T, gpu_colmajor, host, unpack
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA GPU", allow_module_level=True)
+
+import paper_2508_14209_b200 as csk  # noqa: E402
+
+VARIANTS = ["L", "T", "S", "G", "B"]
+
+
+# ------------------------------------------------------------------ codes
+@pytest.mark.parametrize("d,k1,seed,row0", [(4096, 64, 1, 0), (10007, 1000, 7, 3), (1, 1, 2, 0), (5, 8192, 1, 6),
+                                            (100003, 8192, 1, 1 << 20), (64, 3, 9, (1 << 33) + 1)])
+def test_codes_bit_exact(d, k1, seed, row0):
+    plan = csk.cs_plan(d, k1, seed, row0=row0)
+    code, _, _ = plan.export()
+    h, s = unpack(code)
+    ho, so = oracle.codes(d, k1, seed, row0)
+    assert np.array_equal(h, ho) and np.array_equal(s, so)
+
+
+def _curand_probe():
+    here = os.path.join(os.path.dirname(__file__), "helpers")
+    so = os.path.join(here, "build", "libcurand_probe.so")
+    if not os.path.exists(so):
+        os.makedirs(os.path.dirname(so), exist_ok=True)
+        subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+                               "-Xcompiler", "-fPIC", "-o", so, os.path.join(here, "curand_probe.cu")])
+    return ctypes.CDLL(so)
+
+
+def test_oracle_philox_matches_curand():
+    # library pin of the oracle's hash: cuRAND Philox4x32-10 ("cuRAND")
+    lib = _curand_probe()
+    q = np.array([0, 1, 2, 12345, (1 << 32) + 7, (1 << 40) + 3], dtype=np.uint64)
+    out = np.zeros((len(q), 4), np.uint32)
+    for seed in (1, 0xDEADBEEFCAFEF00D):
+        assert lib.curand_probe(ctypes.c_uint64(seed), q.ctypes.data_as(ctypes.c_void_p),
+                                out.ctypes.data_as(ctypes.c_void_p), len(q)) == 0
+        for i, qi in enumerate(q):
+            ctr = [int(qi) & 0xFFFFFFFF, int(qi) >> 32, 0, 0]
+            key = [seed & 0xFFFFFFFF, seed >> 32]
+            assert list(oracle.philox4x32_10(ctr, key)) == list(out[i])
+
+
+@pytest.mark.parametrize("d,k1", [(4096, 64), (100000, 8192), (3000, 1), (77777, 131072), (1 << 20, 65536)])
+def test_sort_bit_exact(d, k1):
+    plan = csk.cs_plan(d, k1, 3, sort=True)
+    code, offsets, perm = plan.export()
+    h, _ = unpack(code)
+    oo, po = oracle.count_sort(h, k1)
+    assert np.array_equal(offsets, oo)
+    assert np.array_equal(perm, po)
+
+
+# ------------------------------------------------------------- cs_apply
+def _check_apply(plan, h, s, A, b, variant, dtype=np.float64, rel=1e-12, lda_pad=0, ldsa_pad=0):
+    d = A.shape[0] if A is not None else len(b)
+    Ad = None
+    if A is not None:
+        if lda_pad:
+            big = np.zeros((d + lda_pad, A.shape[1]), dtype=dtype, order="F")
+            big[:d] = A
+            Ad = gpu_colmajor(big)[:d]
+        else:
+            Ad = gpu_colmajor(A.astype(dtype))
+    bd = None if b is None else gpu_colmajor(b.astype(dtype))
+    ncols = (0 if A is None else A.shape[1]) + (b is not None)
+    SA = None
+    if ldsa_pad:
+        SA = torch.full((ncols, plan.k1 + ldsa_pad), 7.0, dtype=Ad.dtype if Ad is not None else bd.dtype,
+                        device="cuda").t()[: plan.k1]
+    SA = csk.cs_apply(plan, Ad, b=bd, SA=SA, variant=variant)
+    torch.cuda.synchronize()
+    got = host(SA)
+    Aor = A if A is not None else np.zeros((d, 0))
+    exp, T = oracle.cs_apply(h, s, Aor.astype(dtype), plan.k1, b=None if b is None else b.astype(dtype),
+                             with_abs=True)
+    assert_within_T(got, exp, T, rel)
+    return got, exp
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("d,n,k1", [(4096, 8, 64), (10007, 37, 1000), (5000, 1, 8192), (1000, 3, 1), (777, 70, 4096),
+                                    (3000, 5, 65536)])
+def test_cs_apply_fp64(variant, d, n, k1):
+    plan = csk.cs_plan(d, k1, 1, sort=(variant == "G"))
+    h, s = oracle.codes(d, k1, 1)
+    A = synth.gaussian_matrix(d, n, seed=2)
+    _check_apply(plan, h, s, A, None, variant)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_cs_apply_with_b_and_padding(variant):
+    d, n, k1 = 9001, 12, 512
+    plan = csk.cs_plan(d, k1, 5, sort=(variant == "G"))
+    h, s = oracle.codes(d, k1, 5)
+    A = synth.gaussian_matrix(d, n, seed=3)
+    b = synth.rhs(A, "hard", seed=3)
+    _check_apply(plan, h, s, A, b, variant, lda_pad=3, ldsa_pad=5)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_cs_apply_only_b(variant):
+    d, k1 = 3333, 100
+    plan = csk.cs_plan(d, k1, 5, sort=(variant == "G"))
+    h, s = oracle.codes(d, k1, 5)
+    b = synth.gaussian_matrix(d, 1, seed=4)[:, 0]
+    _check_apply(plan, h, s, None, b, variant)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_cs_apply_integer_exact(variant):
+    d, n, k1 = 50000, 9, 2048
+    plan = csk.cs_plan(d, k1, 3, sort=(variant == "G"))
+    h, s = oracle.codes(d, k1, 3)
+    A = synth.integer_matrix(d, n, seed=5, lo=-(1 << 20), hi=1 << 20)
+    got, exp = _check_apply(plan, h, s, A, None, variant, rel=0.0)
+    assert np.array_equal(got, exp)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_cs_apply_fp32(variant):
+    d, n, k1 = 20000, 6, 1024
+    plan = csk.cs_plan(d, k1, 4, sort=(variant == "G"))
+    h, s = oracle.codes(d, k1, 4)
+    A = synth.gaussian_matrix(d, n, seed=6, dtype=np.float32)
+    _check_apply(plan, h, s, A, None, variant, dtype=np.float32, rel=1e-5)
+
+
+def test_worked_example_forced_plan():
+    # d=4, k=2, r=[0,1,0,1], s=[+,+,-,+], A=[1,2,3,4]^T -> Y=[-2, 6]^T
+    for variant in VARIANTS:
+        plan = csk.cs_plan_from_arrays([0, 1, 0, 1], [1, 1, -1, 1], 2, sort=True)
+        Y = csk.cs_apply(plan, gpu_colmajor(np.array([[1.0], [2.0], [3.0], [4.0]])), variant=variant)
+        assert host(Y)[:, 0].tolist() == [-2.0, 6.0]
+
+
+def test_identity_plan_returns_A():
+    d, n = 300, 4
+    A = synth.gaussian_matrix(d, n, seed=5)
+    plan = csk.cs_plan_from_arrays(np.arange(d), np.ones(d), d)
+    for variant in VARIANTS:
+        if variant == "G":
+            continue
+        assert np.array_equal(host(csk.cs_apply(plan, gpu_colmajor(A), variant=variant)), A)
+
+
+def test_sorted_variant_deterministic():
+    d, n, k1 = 200000, 4, 4096
+    plan = csk.cs_plan(d, k1, 9, sort=True)
+    A = gpu_colmajor(synth.gaussian_matrix(d, n, seed=9))
+    a = host(csk.cs_apply(plan, A, variant="G"))
+    b = host(csk.cs_apply(plan, A, variant="G"))
+    assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("p", [1, 2, 4, 7])
+def test_partition_invariance_on_one_gpu(p):
+    # CA = sum_i C^(i) A^(i) with row0-plans (the multi-GPU identity, one device)
+    d, n, k1 = 100001, 5, 4096
+    A = synth.integer_matrix(d, n, seed=11)
+    full = host(csk.cs_apply(csk.cs_plan(d, k1, 1), gpu_colmajor(A)))
+    bounds = np.linspace(0, d, p + 1).astype(int)
+    acc = np.zeros_like(full)
+    for g in range(p):
+        r0, r1 = bounds[g], bounds[g + 1]
+        acc += host(csk.cs_apply(csk.cs_plan(r1 - r0, k1, 1, row0=int(r0)), gpu_colmajor(A[r0:r1])))
+    assert np.array_equal(acc, full)
+
+
+def test_error_paths():
+    plan = csk.cs_plan(100, 10, 1)
+    A = torch.zeros((3, 100), dtype=torch.float64, device="cuda").t()
+    lib = csk.lib()
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    SA = torch.zeros((3, 10), dtype=torch.float64, device="cuda").t()
+    assert lib.cs_apply(plan.handle, 0, 3, ctypes.c_void_p(A.data_ptr()), 99, None,
+                        ctypes.c_void_p(SA.data_ptr()), 10, -1, st) == csk.csk.ESHAPE
+    assert lib.cs_apply(plan.handle, 0, 3, ctypes.c_void_p(A.data_ptr()), 100, None,
+                        ctypes.c_void_p(SA.data_ptr()), 9, -1, st) == csk.csk.ESHAPE
+    assert lib.cs_apply(plan.handle, 0, 3, None, 100, None, ctypes.c_void_p(SA.data_ptr()), 10, -1,
+                        st) == csk.csk.EINVAL
+    assert lib.cs_apply(plan.handle, 7, 3, ctypes.c_void_p(A.data_ptr()), 100, None,
+                        ctypes.c_void_p(SA.data_ptr()), 10, -1, st) == csk.csk.EDTYPE
+    assert lib.cs_apply(plan.handle, 0, 3, ctypes.c_void_p(A.data_ptr()), 100, None,
+                        ctypes.c_void_p(SA.data_ptr()), 10, 3, st) == csk.csk.EUNSUPPORTED  # G without sort
+    out = ctypes.c_void_p()
+    assert lib.cs_plan(0, 10, 1, 0, 0, st, ctypes.byref(out)) == csk.csk.EINVAL
+    assert lib.cs_plan(10, 1 << 31, 1, 0, 0, st, ctypes.byref(out)) == csk.csk.EINVAL
+    with pytest.raises(csk.CskError) as e:
+        csk.cs_plan_from_arrays([0, 5], [1, 1], 3)
+    assert e.value.status == csk.csk.EINVAL
+    Z = torch.zeros((5, 8), dtype=torch.float64, device="cuda").t()
+    x = torch.zeros(8, dtype=torch.float64, device="cuda")
+    assert lib.ms_solve(4, 4, ctypes.c_void_p(Z.data_ptr()), 8, ctypes.c_void_p(x.data_ptr()), None,
+                        st) == csk.csk.ESHAPE
+
+
+# ------------------------------------------------------------ multisketch
+def test_gauss_matches_oracle():
+    # identity plan (k1 = d) and A = I give S A = I, so Z = G exactly
+    for k2, k1 in [(8, 32), (3, 5), (128, 256)]:
+        plan_seeded = csk.cs_plan(k1, k1, 77)      # G is drawn from the plan's seed
+        Z = host(csk.ms_apply(plan_seeded, k2, gpu_colmajor(np.eye(k1))))
+        h, s = oracle.codes(k1, k1, 77)
+        S = np.zeros((k1, k1))
+        S[h, np.arange(k1)] = s
+        G = oracle.gauss(k2, k1, 77)
+        assert np.allclose(Z, G @ S, rtol=0, atol=1e-13 / np.sqrt(k2) * 4)
+
+
+@pytest.mark.parametrize("d,n,k1,k2", [(4096, 8, 128, 16), (20000, 16, 512, 32), (5000, 3, 18, 6)])
+def test_ms_apply_matches_oracle(d, n, k1, k2):
+    plan = csk.cs_plan(d, k1, 3)
+    A = synth.gaussian_matrix(d, n, seed=1)
+    b = synth.rhs(A, "easy", seed=1)
+    Z = host(csk.ms_apply(plan, k2, gpu_colmajor(A), b=gpu_colmajor(b)))
+    Zo, Zabs = oracle.ms_apply(A, k1, k2, seed=3, b=b, with_abs=True)
+    assert_within_T(Z, Zo, Zabs, 1e-12)
+
+
+def test_ms_solve_matches_oracle():
+    rng = np.random.default_rng(5)
+    for m, n in [(16, 8), (128, 64), (256, 128), (40, 3)]:
+        Z = rng.standard_normal((m, n + 1))
+        x, r = csk.ms_solve(gpu_colmajor(Z), n)
+        xo, ro = oracle.sketch_solve(Z, n)
+        assert np.linalg.norm(Z[:, :n] @ (host(x) - xo)) <= 1e-12 * np.linalg.norm(Z[:, n])
+        assert abs(r - ro) <= 1e-12 * np.linalg.norm(Z[:, n])
+
+
+def test_ms_solve_singular():
+    Z = np.zeros((10, 4))
+    Z[:, 0] = 1.0
+    Z[:, 3] = 1.0
+    with pytest.raises(csk.CskError) as e:
+        csk.ms_solve(gpu_colmajor(Z), 3)
+    assert e.value.status == csk.csk.ESINGULAR
+
+
+@pytest.mark.parametrize("kappa", [1e2, 1e10])
+@pytest.mark.parametrize("mode", ["easy", "hard", "consistent"])
+def test_ms_lstsq_matches_oracle(kappa, mode):
+    d, n = 1 << 15, 16
+    k1, k2 = 2 * n * n, 2 * n
+    A = synth.ill_conditioned(d, n, kappa, seed=4)
+    b = synth.rhs(A, mode, seed=4)
+    plan = csk.cs_plan(d, k1, 1)
+    x, r = csk.ms_lstsq(plan, k2, gpu_colmajor(A), gpu_colmajor(b))
+    xo, ro = oracle.ms_lstsq(A, b, k1, k2, seed=1)
+    nb = np.linalg.norm(b)
+    # R16: fitted values agree to 1e-8 relative; for kappa = 1e10 with a noisy b the
+    # problem itself amplifies O(u) input rounding by kappa * ||r|| / ||b|| (Wedin), so
+    # the bound is max(1e-8, 64 u kappa ||r|| / ||b||)
+    rr = oracle.residual_norm(A, b, xo) / nb
+    tol = max(1e-8, 64 * 2.2e-16 * kappa * rr)
+    assert np.linalg.norm(A @ (host(x) - xo)) / nb <= tol
+    assert abs(r - ro) <= 1e-8 * nb
+
+
+def test_ms_lstsq_host_inputs_streamed():
+    d, n = 300000, 8
+    k1, k2 = 2 * n * n, 2 * n
+    A = synth.gaussian_matrix(d, n, seed=8)
+    b = synth.rhs(A, "hard", seed=8)
+    plan = csk.cs_plan(d, k1, 2)
+    xd, rd = csk.ms_lstsq(plan, k2, gpu_colmajor(A), gpu_colmajor(b))
+    At = torch.from_numpy(np.ascontiguousarray(A.T)).pin_memory().t()
+    bt = torch.from_numpy(b).pin_memory()
+    xh, rh = csk.ms_lstsq(plan, k2, At, bt)
+    assert not xh.is_cuda
+    xo, ro = oracle.ms_lstsq(A, b, k1, k2, seed=2)
+    nb = np.linalg.norm(b)
+    assert np.linalg.norm(A @ (xh.numpy() - xo)) / nb <= 1e-8
+    assert np.linalg.norm(A @ (host(xd) - xo)) / nb <= 1e-8
+    # pageable host memory works too
+    xp, _ = csk.ms_lstsq(plan, k2, torch.from_numpy(np.ascontiguousarray(A.T)).t(), torch.from_numpy(b))
+    assert np.linalg.norm(A @ (xp.numpy() - xo)) / nb <= 1e-8
+
+
+# -------------------------------------------------------- normal equations
+def test_ne_lstsq_matches_oracle():
+    d, n = 1 << 15, 16
+    A = synth.ill_conditioned(d, n, 1e2, seed=2)
+    b = synth.rhs(A, "easy", seed=2)
+    xo = oracle.normal_eq(A, b)
+    nb = np.linalg.norm(b)
+    # b stored apart from A (SYRK + GEMV) and as column n of [A b] (one SYRK)
+    x1 = host(csk.ne_lstsq(gpu_colmajor(A), gpu_colmajor(b)))
+    Ab = gpu_colmajor(np.column_stack([A, b]))
+    x2 = host(csk.ne_lstsq(Ab[:, :n], Ab[:, n]))
+    for x in (x1, x2):
+        assert np.linalg.norm(A @ (x - xo)) / nb <= 1e-8
+
+
+def test_ne_lstsq_breaks_down_at_kappa_1e10():
+    # the normal equations fail for kappa(A) > 1e8 (ENOTPD or a useless x)
+    d, n = 1 << 17, 16
+    A = synth.ill_conditioned(d, n, 1e10, seed=3)
+    b = synth.rhs(A, "consistent", seed=3)
+    try:
+        x = host(csk.ne_lstsq(gpu_colmajor(A), gpu_colmajor(b)))
+    except csk.CskError as e:
+        assert e.status == csk.csk.ENOTPD
+        return
+    assert oracle.residual_norm(A, b, x) / np.linalg.norm(b) > 1e-2
