@@ -117,6 +117,79 @@ __global__ void __launch_bounds__(kRowWarps * 32) cs_row_kernel(const uint32_t* 
     if (BULK) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// ------------------------------------------------------------------ variant B
+// A warp owns 16-row x cw-column tiles (cw <= 66: all of [A b] at C2).  Lanes
+// (r, half) load column pairs (two coalesced 128-B half-warp reads per
+// instruction), write the signed values row-major into a 16-B aligned smem row,
+// and lane r hands the whole row to the TMA engine as ONE bulk reduce-add
+// (cp.reduce.async.bulk ... .add.f64, cw*8 bytes) into SA^T[h(r), c0:c0+cw].
+// Two tile buffers per warp; cp.async.bulk.wait_group.read 1 recycles them.
+constexpr int kBulkWarps = 8;
+constexpr int kBulkRows = 16;
+constexpr int kBulkMaxCols = 66;
+
+__host__ __device__ inline int bulk_chunk_width(int ncols) {
+    if (ncols <= kBulkMaxCols) return ncols;
+    const int nch = (ncols + 63) / 64;
+    return (((ncols + nch - 1) / nch) + 1) & ~1;   // even: every chunk start stays 16-B aligned
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBulkWarps * 32) cs_bulk_kernel(const uint32_t* __restrict__ code, int64_t rows,
+                                                                  Cols<T> cols, int ncols, int cw, int ldtile,
+                                                                  double* __restrict__ SAt, int64_t ldt) {
+    extern __shared__ __align__(16) double bulk_smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int half = lane >> 4, rr = lane & 15;
+    double* tiles = bulk_smem + (size_t)warp * 2 * kBulkRows * ldtile;
+    for (int e = lane; e < 2 * kBulkRows * ldtile; e += 32) tiles[e] = 0.0;
+    __syncwarp();
+    const int nchunks = (ncols + cw - 1) / cw;
+    const int64_t ngroups = (rows + kBulkRows - 1) / kBulkRows;
+    const int64_t nunits = ngroups * nchunks;
+    const int64_t gwarp = blockIdx.x * (int64_t)kBulkWarps + warp;
+    const int64_t nwarps = (int64_t)gridDim.x * kBulkWarps;
+    int buf = 0;
+    for (int64_t u = gwarp; u < nunits; u += nwarps) {
+        const int64_t g = u / nchunks;
+        const int ch = (int)(u - g * nchunks);
+        const int c0 = ch * cw;
+        const int nc = min(cw, ncols - c0);
+        const int64_t r = g * kBulkRows + rr;
+        const bool valid = r < rows;
+        const uint32_t cd = valid ? __ldg(code + r) : 0u;
+        double* tile = tiles + buf * kBulkRows * ldtile;
+        double v[kBulkMaxCols / 2];
+#pragma unroll
+        for (int j = 0; j < kBulkMaxCols / 2; ++j) {
+            const int c = 2 * j + half;
+            v[j] = (c < nc && valid) ? (double)ldg_stream(cols.col(c0 + c) + r) : 0.0;
+        }
+        // the TMA engine must be done reading this buffer (its bulk ops were committed 2 units ago)
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < kBulkMaxCols / 2; ++j) {
+            const int c = 2 * j + half;
+            if (c < nc) tile[rr * ldtile + c] = apply_sign(v[j], cd);
+        }
+        if ((nc & 1) && half == 0) tile[rr * ldtile + nc] = 0.0;   // 16-B padding column
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (half == 0 && valid) {
+            const uint32_t bytes = (uint32_t)(((nc + 1) & ~1) * 8);
+            double* dst = SAt + (int64_t)code_bucket(cd) * ldt + c0;
+            const uint32_t src = (uint32_t)__cvta_generic_to_shared(tile + rr * ldtile);
+            asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(dst),
+                         "r"(src), "r"(bytes)
+                         : "memory");
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        buf ^= 1;
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // SA^T (row-major k1 x ldt, fp64) -> SA (column-major, ldsa, T)
 template <typename T>
 __global__ void transpose_out_kernel(const double* __restrict__ SAt, int64_t ldt, int64_t k1, int ncols,
@@ -294,13 +367,27 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
             CSK_LAUNCH_CHECK();
             return CSK_OK;
         }
-        case CSK_VAR_ATOMIC_ROW:
         case CSK_VAR_BULK_ROW: {
+            const int cw = bulk_chunk_width(ncols);
+            const int ldtile = (cw + 1) & ~1;
+            const size_t smem = (size_t)kBulkWarps * 2 * kBulkRows * ldtile * sizeof(double);
+            const int64_t units = ceil_div(rows, kBulkRows) * ceil_div(ncols, cw);
+            CSK_CUDA_TRY(cudaFuncSetAttribute(cs_bulk_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            int per_sm = 0;
+            CSK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cs_bulk_kernel<T>, kBulkWarps * 32, smem));
+            per_sm = std::max(per_sm, 1);
+            const int64_t blocks = std::min<int64_t>(ceil_div(units, kBulkWarps), (int64_t)di.num_sms * per_sm);
+            cs_bulk_kernel<T><<<(unsigned)blocks, kBulkWarps * 32, smem, st>>>(code, rows, cols, ncols, cw, ldtile, out,
+                                                                            ldo);
+            CSK_LAUNCH_CHECK();
+            return CSK_OK;
+        }
+        case CSK_VAR_ATOMIC_ROW: {
             (void)out_rowmajor;
-            const bool bulk = variant == CSK_VAR_BULK_ROW;
+            const bool bulk = false;
             const size_t smem = (size_t)kRowWarps * (bulk ? 2 : 1) * 32 * kTileLd * sizeof(double);
             const int64_t units = ceil_div(rows, 32) * ceil_div(ncols, 32);
-            auto kern = bulk ? cs_row_kernel<T, true> : cs_row_kernel<T, false>;
+            auto kern = cs_row_kernel<T, false>;
             CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             int per_sm = 0;
             CSK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowWarps * 32, smem));
@@ -360,7 +447,9 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
                 (long long)ncols64);
     CSK_REQUIRE(n == 0 || A != nullptr, CSK_EINVAL, "A is NULL");
     CSK_REQUIRE(SA != nullptr, CSK_EINVAL, "SA is NULL");
-    CSK_REQUIRE(n == 0 || lda >= plan->d, CSK_ESHAPE, "lda=%lld < d=%lld", (long long)lda, (long long)plan->d);
+    CSK_REQUIRE(row_begin >= 0 && row_begin < row_end && row_end <= plan->d, CSK_EINVAL, "bad row range");
+    CSK_REQUIRE(n == 0 || lda >= row_end - row_begin, CSK_ESHAPE, "lda=%lld < rows=%lld", (long long)lda,
+                (long long)(row_end - row_begin));
     CSK_REQUIRE(ldsa >= plan->k1, CSK_ESHAPE, "ldsa=%lld < k1=%lld", (long long)ldsa, (long long)plan->k1);
     const int ncols = (int)ncols64;
     if (variant == CSK_VAR_AUTO) variant = env_variant();

@@ -39,6 +39,14 @@ const DeviceInfo& device_info() {
     cudaDeviceGetAttribute(&info.num_sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&info.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaDeviceGetAttribute(&info.l2_bytes, cudaDevAttrL2CacheSize, dev);
+    // keep freed workspaces mapped in the stream-ordered pool: per-call cudaMallocAsync /
+    // cudaFreeAsync of SA, Z and QR workspaces must not unmap and remap pages at every sync
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
     return cache.emplace(dev, info).first->second;
 }
 
