@@ -321,8 +321,10 @@ def bench_ours(args, cfg):
     solve_ms = (time.perf_counter() - t) * 1e3 / args.steps
 
     # ---- normal-equations baseline (a8) on the same [A b]
-    ne = {"gram": os.environ.get("CSK_NE_GRAM", "syrk")}
+    ne = {"gram": os.environ.get("CSK_NE_GRAM", "splitk (strided-batched DGEMM over row blocks + fixed-order reduce)")}
     try:
+        if args.no_ne:
+            raise csk.CskError(0, "ne_lstsq", "skipped (--no-ne)")
         for _ in range(max(1, args.warmup // 2)):
             csk.ne_lstsq(A, b, x=x)
         barrier()
@@ -341,7 +343,7 @@ def bench_ours(args, cfg):
     step()
     r_ms = float(torch.linalg.norm(b - A @ x) / torch.linalg.norm(b))
     acc = {"rel_residual_ms": r_ms}
-    if ws == 1 and d * ncols * 8 <= 16e9:
+    if ws == 1 and d * ncols * 8 <= 16e9 and not args.no_acc:
         R = torch.linalg.qr(buf, mode="r")[1]
         acc["rel_residual_true"] = float(abs(R[n, n]) / torch.linalg.norm(b))
         del R
@@ -417,9 +419,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--variant", default="auto", choices=["auto", "L", "T", "S", "G", "B"])
+    ap.add_argument("--variant", default="auto", choices=["auto", "L", "T", "S", "G", "B", "X"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-ne", action="store_true", help="skip the normal-equations baseline")
+    ap.add_argument("--no-acc", action="store_true", help="skip the untimed accuracy checks")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cfg = CONFIGS[args.config]

@@ -56,7 +56,10 @@ typedef enum {
     CSK_VAR_ATOMIC_ROW = 1,   /* T: row tiles transposed in smem, coalesced REDG into SA^T    */
     CSK_VAR_SMEM = 2,         /* S: per-CTA shared-memory privatised buckets, one flush/CTA   */
     CSK_VAR_SORTED = 3,       /* G: deterministic signed segmented gather over the plan sort   */
-    CSK_VAR_BULK_ROW = 4      /* B: row tiles in smem, TMA bulk reduce-add (cp.reduce.async.bulk) */
+    CSK_VAR_BULK_ROW = 4,     /* B: row tiles in smem, TMA bulk reduce-add (cp.reduce.async.bulk) */
+    CSK_VAR_TMA_ROW = 5       /* X: TMA tensor loads of 2-D [A b] tiles + coalesced REDG per row;
+                                 needs a uniform column stride (b == NULL or b == A + n*lda) with
+                                 16-B aligned columns, else it falls back to T */
 } csk_variant;
 
 /* cs_plan flags */

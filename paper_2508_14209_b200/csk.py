@@ -18,9 +18,9 @@ from . import _build
 
 OK, EINVAL, ESHAPE, EDTYPE, ENOMEM, ECUDA, ENOTPD, ESINGULAR, EUNSUPPORTED = range(9)
 F64, F32 = 0, 1
-VAR_AUTO, VAR_ATOMIC_COL, VAR_ATOMIC_ROW, VAR_SMEM, VAR_SORTED, VAR_BULK_ROW = -1, 0, 1, 2, 3, 4
+VAR_AUTO, VAR_ATOMIC_COL, VAR_ATOMIC_ROW, VAR_SMEM, VAR_SORTED, VAR_BULK_ROW, VAR_TMA_ROW = -1, 0, 1, 2, 3, 4, 5
 VARIANTS = {"auto": VAR_AUTO, "L": VAR_ATOMIC_COL, "T": VAR_ATOMIC_ROW, "S": VAR_SMEM, "G": VAR_SORTED,
-            "B": VAR_BULK_ROW}
+            "B": VAR_BULK_ROW, "X": VAR_TMA_ROW}
 PLAN_SORT = 0x2
 
 _lock = threading.Lock()

@@ -22,6 +22,9 @@
 #include <cstring>
 #include <vector>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "csk_internal.cuh"
 
 namespace csk {
@@ -53,24 +56,28 @@ __global__ void __launch_bounds__(256) cs_col_kernel(const uint32_t* __restrict_
     }
 }
 
-// ------------------------------------------------------------- variants T / B
+// ------------------------------------------------------------------ variant T
+// A warp owns a 32-row x 32-column unit: lane r loads A[r, c0..c0+31] (32 coalesced
+// 256-B column reads; rows and columns past the edge are clamped to legal addresses
+// and zeroed with a select, so the unrolled body has no branches), writes the signed
+// values into row r of a padded (odd-stride, conflict-free) smem tile, then for each
+// row j the warp issues one coalesced red.global.add.f64 of 32 lanes into
+// SA^T[h(j), c0:c0+32] -- Alg 2's "add rows atomically" with the row made contiguous on chip.
 constexpr int kRowWarps = 8;
-constexpr int kTileLd = 34;   // 32 columns + 2 pad doubles: rows stay 16-B aligned for bulk ops
+constexpr int kTileLd = 33;
 
-template <typename T, bool BULK>
+template <typename T>
 __global__ void __launch_bounds__(kRowWarps * 32) cs_row_kernel(const uint32_t* __restrict__ code, int64_t rows,
                                                                 Cols<T> cols, int ncols, double* __restrict__ SAt,
                                                                 int64_t ldt) {
-    extern __shared__ __align__(16) double row_smem[];
+    extern __shared__ double row_smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    constexpr int kBufs = BULK ? 2 : 1;
-    double* tiles = row_smem + (size_t)warp * kBufs * 32 * kTileLd;
+    double* tile = row_smem + (size_t)warp * 32 * kTileLd;
     const int nchunks = (ncols + 31) >> 5;
     const int64_t ngroups = (rows + 31) >> 5;
     const int64_t nunits = ngroups * nchunks;
     const int64_t gwarp = blockIdx.x * (int64_t)kRowWarps + warp;
     const int64_t nwarps = (int64_t)gridDim.x * kRowWarps;
-    int buf = 0;
     for (int64_t u = gwarp; u < nunits; u += nwarps) {
         const int64_t g = u / nchunks;
         const int ch = (int)(u - g * nchunks);
@@ -78,43 +85,151 @@ __global__ void __launch_bounds__(kRowWarps * 32) cs_row_kernel(const uint32_t* 
         const int nc = min(32, ncols - c0);
         const int64_t r = g * 32 + lane;
         const bool valid = r < rows;
-        const uint32_t cd = valid ? __ldg(code + r) : 0u;
-        double* tile = tiles + buf * 32 * kTileLd;
-        if (BULK) {
-            // the bulk engine must have finished reading this buffer (issued 2 units ago)
-            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-            __syncwarp();
-        }
+        const int64_t rc = valid ? r : rows - 1;
+        const uint32_t cd = __ldg(code + rc);
+        const long long smask = valid ? (long long)code_sign_mask64(cd) : 0ll;
         double v[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = (j < nc && valid) ? (double)ldg_stream(cols.col(c0 + j) + r) : 0.0;
+        for (int j = 0; j < 32; ++j) v[j] = (double)ldg_stream(cols.col(min(c0 + j, ncols - 1)) + rc);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) tile[lane * kTileLd + j] = apply_sign(v[j], cd);
+        for (int j = 0; j < 32; ++j) {
+            const double x = (j < nc && valid) ? v[j] : 0.0;
+            tile[lane * kTileLd + j] = __longlong_as_double(__double_as_longlong(x) ^ smask);
+        }
         __syncwarp();
         const int nrows = (int)min((int64_t)32, rows - g * 32);
-        if (!BULK) {
-            for (int j = 0; j < nrows; ++j) {
-                const uint32_t b = code_bucket(__shfl_sync(0xffffffffu, cd, j));
-                if (lane < nc) red_add_f64(SAt + (int64_t)b * ldt + c0 + lane, tile[j * kTileLd + lane]);
+        double* dst = SAt + c0 + lane;
+#pragma unroll 8
+        for (int j = 0; j < 32; ++j) {
+            const uint32_t b = code_bucket(__shfl_sync(0xffffffffu, cd, j));
+            const double x = tile[j * kTileLd + lane];
+            if (j < nrows && lane < nc) red_add_f64(dst + (int64_t)b * ldt, x);
+        }
+        __syncwarp();
+    }
+}
+
+// ------------------------------------------------------------------ variant X
+// TMA-fed row scatter.  [A b] must be one 2-D tensor (uniform column stride).  A warp
+// owns a ring of kTmaStages smem tiles; lane 0 issues one cp.async.bulk.tensor.2d per
+// tile (RB rows x cw columns, RB*sizeof(T) = 128 B per column, 128B swizzle, rows past d
+// zero-filled by the TMA unit) completing on a per-stage mbarrier.  For each row j the
+// warp reads SA^T's row slice straight out of the swizzled tile (lane = column) and issues
+// ceil(cw/32) coalesced red.global.add.f64 -- no register staging, no transpose, and
+// ~7 warp instructions per 32 elements (the LDG variant T needed ~65).
+constexpr int kTmaWarps = 8;
+constexpr int kTmaStages = 3;
+constexpr int kTmaMaxCols = 96;
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(dst)),
+        "l"(map), "r"(x), "r"(y), "r"((uint32_t)__cvta_generic_to_shared(bar))
+        : "memory");
+}
+
+template <typename T>
+__device__ __forceinline__ double swz_load(const uint8_t* tile, int c, int j) {
+    // 128B swizzle: the 16-B chunk index of each 128-B column row is XORed with (column & 7)
+    constexpr int kPerChunk = 16 / sizeof(T);
+    const int off = c * 128 + ((((j / kPerChunk) ^ (c & 7))) << 4) + (j % kPerChunk) * (int)sizeof(T);
+    return (double)*reinterpret_cast<const T*>(tile + off);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kTmaWarps * 32, 1) cs_tma_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                                    const uint32_t* __restrict__ code, int64_t rows,
+                                                                    int ncols, int cw, int stage_bytes,
+                                                                    double* __restrict__ SAt, int64_t ldt) {
+    constexpr int RB = 128 / sizeof(T);   // rows per tile: 16 (fp64) / 32 (fp32)
+    extern __shared__ uint8_t tma_smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)tma_smem_raw + 1023) & ~(uintptr_t)1023);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint8_t* ring = smem + (size_t)warp * kTmaStages * stage_bytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kTmaWarps * kTmaStages * stage_bytes) + warp * kTmaStages;
+    const int nchunks = (ncols + cw - 1) / cw;
+    const int64_t ngroups = (rows + RB - 1) / RB;
+    const int64_t nunits = ngroups * nchunks;
+    const int64_t gwarp = blockIdx.x * (int64_t)kTmaWarps + warp;
+    const int64_t nwarps = (int64_t)gridDim.x * kTmaWarps;
+    const uint32_t tile_bytes = (uint32_t)cw * 128u;
+    if (lane == 0) {
+        for (int s = 0; s < kTmaStages; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int s = 0; s < kTmaStages; ++s) {
+            const int64_t u = gwarp + s * nwarps;
+            if (u < nunits) {
+                mbar_expect_tx(&bars[s], tile_bytes);
+                tma_load_2d(ring + s * stage_bytes, &tmap, (int)((u / nchunks) * RB), (int)((u % nchunks) * cw),
+                            &bars[s]);
             }
-            __syncwarp();
-        } else {
-            // generic-proxy smem writes -> visible to the async (bulk) proxy
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (lane < nrows) {
-                const uint32_t bytes = (uint32_t)(((nc + 1) & ~1) * 8);
-                double* dst = SAt + (int64_t)code_bucket(cd) * ldt + c0;
-                const uint32_t src = (uint32_t)__cvta_generic_to_shared(tile + lane * kTileLd);
-                asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(dst),
-                             "r"(src), "r"(bytes)
-                             : "memory");
-            }
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            buf ^= 1;
         }
     }
-    if (BULK) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
+    for (int64_t k = 0;; ++k) {
+        const int64_t u = gwarp + k * nwarps;
+        if (u >= nunits) break;
+        const int s = (int)(k % kTmaStages);
+        const int64_t g = u / nchunks;
+        const int c0 = (int)(u - g * nchunks) * cw;
+        const int nc = min(cw, ncols - c0);
+        const int64_t r0 = g * RB;
+        const int nr = (int)min((int64_t)RB, rows - r0);
+        const uint32_t cdl = __ldg(code + min(r0 + (lane % RB), rows - 1));
+        mbar_wait(&bars[s], (uint32_t)((k / kTmaStages) & 1));
+        const uint8_t* tile = ring + s * stage_bytes;
+#pragma unroll 4
+        for (int j = 0; j < RB; ++j) {
+            const uint32_t cd = __shfl_sync(0xffffffffu, cdl, j);
+            double* dst = SAt + (int64_t)code_bucket(cd) * ldt + c0;
+            const long long smask = (long long)code_sign_mask64(cd);
+#pragma unroll
+            for (int q = 0; q < kTmaMaxCols / 32; ++q) {
+                const int c = q * 32 + lane;
+                if (q * 32 < nc && c < nc && j < nr) {
+                    const double x = swz_load<T>(tile, c, j);
+                    red_add_f64(dst + c, __longlong_as_double(__double_as_longlong(x) ^ smask));
+                }
+            }
+        }
+        // this warp's generic reads of the stage precede the next async (TMA) write into it
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+            const int64_t un = u + kTmaStages * nwarps;
+            if (un < nunits) {
+                mbar_expect_tx(&bars[s], tile_bytes);
+                tma_load_2d(ring + s * stage_bytes, &tmap, (int)((un / nchunks) * RB), (int)((un % nchunks) * cw),
+                            &bars[s]);
+            }
+        }
+    }
+}
+
+static int tma_chunk_width(int ncols) {
+    if (ncols <= kTmaMaxCols) return ncols;
+    const int nch = (ncols + 63) / 64;
+    return (ncols + nch - 1) / nch;
 }
 
 // ------------------------------------------------------------------ variant B
@@ -157,13 +272,15 @@ __global__ void __launch_bounds__(kBulkWarps * 32) cs_bulk_kernel(const uint32_t
         const int nc = min(cw, ncols - c0);
         const int64_t r = g * kBulkRows + rr;
         const bool valid = r < rows;
-        const uint32_t cd = valid ? __ldg(code + r) : 0u;
+        const int64_t rc = valid ? r : rows - 1;
+        const uint32_t cd = __ldg(code + rc);
         double* tile = tiles + buf * kBulkRows * ldtile;
         double v[kBulkMaxCols / 2];
 #pragma unroll
         for (int j = 0; j < kBulkMaxCols / 2; ++j) {
             const int c = 2 * j + half;
-            v[j] = (c < nc && valid) ? (double)ldg_stream(cols.col(c0 + c) + r) : 0.0;
+            const double x = (double)ldg_stream(cols.col(min(c0 + c, ncols - 1)) + rc);
+            v[j] = (c < nc) ? x : 0.0;
         }
         // the TMA engine must be done reading this buffer (its bulk ops were committed 2 units ago)
         asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
@@ -221,16 +338,22 @@ __global__ void narrow_kernel(const double* __restrict__ src, int64_t k1, int nc
 }
 
 // ------------------------------------------------------------------ variant S
-// One CTA per SM; CTA = `cpc` warps, warp w owns the k1 fp64 accumulators of
-// column g*cpc + w.  The linearised work space (column group g, row r) is split
-// evenly over CTAs, so a CTA touches at most a few groups and flushes once per group.
-constexpr int kSmemPrefetch = 4;   // row groups of 32 loaded ahead per warp
+// Shared-memory privatised buckets.  Warp w of a CTA owns the k1 fp64 accumulators of
+// one column for a contiguous range of rows: every update is a plain LDS/DADD/STS
+// (sm_100a has no native shared fp64 atomic; ptxas emits a CAS loop), duplicates among
+// the 32 rows of one iteration are merged in lane order with __match_any_sync, and the
+// warp-uniform common case (no duplicate, >94% at k1 = 8192) skips the merge.  The
+// arrays are warp-private, so the kernel has no block barrier at all.  Loads are
+// prefetched kPrivDepth iterations ahead in registers (kPrivDepth * 384 B in flight per
+// warp).  The (column, row) work space is split evenly over CTAs; each warp flushes its
+// array with REDG once per column it touched.
+constexpr int kPrivDepth = 24;
 
 template <typename T>
-__global__ void __launch_bounds__(1024, 1) cs_smem_kernel(const uint32_t* __restrict__ code, int64_t rows,
-                                                          Cols<T> cols, int ncols, int cpc, int k1,
-                                                          double* __restrict__ out, int64_t ldo,
-                                                          int64_t work_per_cta) {
+__global__ void __launch_bounds__(128, 1) cs_smem_kernel(const uint32_t* __restrict__ code, int64_t rows,
+                                                         Cols<T> cols, int ncols, int cpc, int k1,
+                                                         double* __restrict__ out, int64_t ldo,
+                                                         int64_t work_per_cta) {
     extern __shared__ double acc_smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int ngroups = (ncols + cpc - 1) / cpc;
@@ -242,59 +365,52 @@ __global__ void __launch_bounds__(1024, 1) cs_smem_kernel(const uint32_t* __rest
         const int g = (int)(w / rows);
         const int64_t r0 = w - (int64_t)g * rows;
         const int64_t r1 = min(rows, r0 + (w_end - w));
-        for (int i = threadIdx.x; i < cpc * k1; i += blockDim.x) acc_smem[i] = 0.0;
-        __syncthreads();
-        const int c = g * cpc + warp;
-        if (c < ncols) {
-            const T* col = cols.col(c);
-            // software pipeline: kSmemPrefetch groups of 32 rows in registers
-            double pv[kSmemPrefetch];
-            uint32_t pc[kSmemPrefetch];
-#pragma unroll
-            for (int p = 0; p < kSmemPrefetch; ++p) {
-                const int64_t r = r0 + p * 32 + lane;
-                pv[p] = r < r1 ? (double)ldg_stream(col + r) : 0.0;
-                pc[p] = r < r1 ? __ldg(code + r) : 0u;
-            }
-            for (int64_t base = r0; base < r1; base += 32 * kSmemPrefetch) {
-#pragma unroll
-                for (int p = 0; p < kSmemPrefetch; ++p) {
-                    const int64_t r = base + p * 32 + lane;
-                    const bool valid = r < r1;
-                    const uint32_t cd = pc[p];
-                    double val = valid ? apply_sign(pv[p], cd) : 0.0;
-                    // refill this slot with the group kSmemPrefetch ahead
-                    const int64_t rn = r + 32 * kSmemPrefetch;
-                    pv[p] = rn < r1 ? (double)ldg_stream(col + rn) : 0.0;
-                    pc[p] = rn < r1 ? __ldg(code + rn) : 0u;
-                    const uint32_t key = valid ? code_bucket(cd) : 0x80000000u | lane;
-                    const uint32_t peers = __match_any_sync(0xffffffffu, key);
-                    if (peers != (1u << lane)) {
-                        // rare: lanes of this warp share a bucket -> the lowest lane sums them
-                        // in lane order (deterministic), the others drop out
-                        double sum = 0.0;
-                        for (uint32_t m = peers; m; m &= m - 1) sum += __shfl_sync(peers, val, __ffs(m) - 1);
-                        if (valid && lane == __ffs(peers) - 1) acc[code_bucket(cd)] += sum;
-                    } else if (valid) {
-                        const uint32_t b = code_bucket(cd);
-                        acc[b] += val;
-                    }
-                    __syncwarp();
-                }
-            }
-        }
-        __syncthreads();
-        // flush this group's partial sums (REDG; skipped for exact zeros)
-        for (int i = threadIdx.x; i < cpc * k1; i += blockDim.x) {
-            const int cl = i / k1, m = i - cl * k1;
-            const int cc = g * cpc + cl;
-            const double v = acc_smem[i];
-            if (cc < ncols && v != 0.0) red_add_f64(out + m + (int64_t)cc * ldo, v);
-        }
-        __syncthreads();
         w += r1 - r0;
+        const int c = g * cpc + warp;
+        if (c >= ncols) continue;
+        for (int i = lane; i < k1; i += 32) acc[i] = 0.0;
+        __syncwarp();
+        const T* col = cols.col(c);
+        double pv[kPrivDepth];
+        uint32_t pc[kPrivDepth];
+#pragma unroll
+        for (int p = 0; p < kPrivDepth; ++p) {
+            const int64_t r = min(r0 + p * 32 + lane, r1 - 1);   // clamped: masked by `valid` at use
+            pv[p] = (double)ldg_stream(col + r);
+            pc[p] = __ldg(code + r);
+        }
+        for (int64_t base = r0; base < r1; base += 32 * kPrivDepth) {
+#pragma unroll
+            for (int p = 0; p < kPrivDepth; ++p) {
+                const int64_t r = base + p * 32 + lane;
+                const bool valid = r < r1;
+                const uint32_t cd = pc[p];
+                const double val = valid ? apply_sign(pv[p], cd) : 0.0;
+                const int64_t rn = min(r + 32 * kPrivDepth, r1 - 1);
+                pv[p] = (double)ldg_stream(col + rn);
+                pc[p] = __ldg(code + rn);
+                const uint32_t key = valid ? code_bucket(cd) : 0x80000000u | lane;
+                const uint32_t peers = __match_any_sync(0xffffffffu, key);
+                if (__all_sync(0xffffffffu, peers == (1u << lane))) {
+                    if (valid) acc[key] += val;
+                } else {
+                    // lanes sharing a bucket: the lowest lane adds their sum (lane order)
+                    double sum = 0.0;
+                    for (uint32_t m = peers; m; m &= m - 1) sum += __shfl_sync(peers, val, __ffs(m) - 1);
+                    if (valid && lane == __ffs(peers) - 1) acc[key] += sum;
+                }
+                __syncwarp();
+            }
+        }
+        // flush this column's partial sums (REDG; exact zeros skipped)
+        for (int i = lane; i < k1; i += 32) {
+            const double v = acc[i];
+            if (v != 0.0) red_add_f64(out + i + (int64_t)c * ldo, v);
+        }
+        __syncwarp();
     }
 }
+
 
 // ------------------------------------------------------------------ variant G
 // Warp per (bucket m, column c): SA[m,c] = sum over the bucket's segment of the
@@ -328,7 +444,33 @@ __global__ void __launch_bounds__(256) cs_sorted_kernel(const uint32_t* __restri
 // ------------------------------------------------------------------ dispatch
 // Accumulation target of a variant: row-major SA^T workspace (T, B), or a
 // column-major fp64 buffer (L, S, G) which is SA itself for fp64 output.
-static bool variant_rowmajor(int v) { return v == CSK_VAR_ATOMIC_ROW || v == CSK_VAR_BULK_ROW; }
+static bool variant_rowmajor(int v) {
+    return v == CSK_VAR_ATOMIC_ROW || v == CSK_VAR_BULK_ROW || v == CSK_VAR_TMA_ROW;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* f = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+        cudaGetLastError();
+    });
+    return fn;
+}
+
+// [A b] as one 2-D tensor for TMA: needs b == NULL or b == A + n*lda, 16-B aligned base and stride
+template <typename T>
+static bool tma_eligible(const Cols<T>& cols, int ncols) {
+    const T* base = cols.n > 0 ? cols.A : cols.b;
+    if (cols.n > 0 && cols.b != nullptr && cols.b != cols.A + (int64_t)cols.n * cols.lda) return false;
+    if (((uintptr_t)base & 15) != 0) return false;
+    if (ncols > 1 && ((cols.lda * (int64_t)sizeof(T)) & 15) != 0) return false;
+    return tensor_map_encoder() != nullptr;
+}
 
 static int env_variant() {
     const char* e = std::getenv("CSK_VARIANT");
@@ -339,7 +481,7 @@ static int env_variant() {
 static int smem_cpc(int64_t k1, int ncols) {
     const DeviceInfo& di = device_info();
     const int64_t per_col = k1 * 8;
-    int cpc = (int)std::min<int64_t>((int64_t)di.smem_optin / per_col, 32);
+    int cpc = (int)std::min<int64_t>((int64_t)di.smem_optin / per_col, 4);   // <= 4 warps (launch bounds)
     return std::min(cpc, ncols);
 }
 
@@ -348,9 +490,11 @@ static int select_variant(int64_t d, int64_t k1, int ncols, csk_dtype dtype, boo
     (void)d;
     (void)dtype;
     (void)has_sort;
-    if (k1 * 8 * 2 <= (int64_t)device_info().smem_optin && smem_cpc(k1, ncols) >= 2) return CSK_VAR_SMEM;
+    // measured at C2 (d=2^24, 65 cols, k1=8192, fp64): T 3.03 ms, B 3.34 ms,
+    // L 6.3 ms, G 25 ms, S 38 ms
     (void)ncols;
-    return CSK_VAR_BULK_ROW;
+    (void)k1;
+    return CSK_VAR_TMA_ROW;   // falls back to T when [A b] is not one uniformly strided tensor
 }
 
 template <typename T>
@@ -364,6 +508,34 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
         case CSK_VAR_ATOMIC_COL: {
             const int64_t blocks = std::min<int64_t>(ceil_div(rows, 256), (int64_t)di.num_sms * 8);
             cs_col_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(code, rows, cols, ncols, out, ldo);
+            CSK_LAUNCH_CHECK();
+            return CSK_OK;
+        }
+        case CSK_VAR_TMA_ROW: {
+            if (!tma_eligible(cols, ncols))
+                return run_variant<T>(CSK_VAR_ATOMIC_ROW, plan, ncols, cols, row_begin, row_end, out, ldo,
+                                      out_rowmajor, st);
+            constexpr int RB = 128 / sizeof(T);
+            const int cw = tma_chunk_width(ncols);
+            const T* base = cols.n > 0 ? cols.A : cols.b;
+            CUtensorMap tmap;
+            const cuuint64_t gdim[2] = {(cuuint64_t)rows, (cuuint64_t)ncols};
+            const cuuint64_t gstride[1] = {(cuuint64_t)((ncols > 1 ? cols.lda : rows) * (int64_t)sizeof(T))};
+            const cuuint32_t box[2] = {(cuuint32_t)RB, (cuuint32_t)cw};
+            const cuuint32_t estride[2] = {1, 1};
+            const CUresult cr = tensor_map_encoder()(
+                &tmap, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                const_cast<T*>(base), gdim, gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            CSK_REQUIRE(cr == CUDA_SUCCESS, CSK_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+            const int stage_bytes = (cw * 128 + 1023) & ~1023;
+            const size_t smem = (size_t)kTmaWarps * kTmaStages * stage_bytes + kTmaWarps * kTmaStages * 8 + 1024;
+            CSK_REQUIRE(smem <= (size_t)di.smem_optin, CSK_EUNSUPPORTED, "variant X: tile does not fit smem");
+            CSK_CUDA_TRY(cudaFuncSetAttribute(cs_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            const int64_t units = ceil_div(rows, RB) * ceil_div(ncols, cw);
+            const int64_t blocks = std::min<int64_t>(ceil_div(units, kTmaWarps), (int64_t)di.num_sms);
+            cs_tma_kernel<T><<<(unsigned)blocks, kTmaWarps * 32, smem, st>>>(tmap, code, rows, ncols, cw, stage_bytes,
+                                                                             out, ldo);
             CSK_LAUNCH_CHECK();
             return CSK_OK;
         }
@@ -387,7 +559,7 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
             const bool bulk = false;
             const size_t smem = (size_t)kRowWarps * (bulk ? 2 : 1) * 32 * kTileLd * sizeof(double);
             const int64_t units = ceil_div(rows, 32) * ceil_div(ncols, 32);
-            auto kern = cs_row_kernel<T, false>;
+            auto kern = cs_row_kernel<T>;
             CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             int per_sm = 0;
             CSK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowWarps * 32, smem));
@@ -406,7 +578,11 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
                                               (int)smem));
             const int ngroups = (ncols + cpc - 1) / cpc;
             const int64_t total = (int64_t)ngroups * rows;
-            const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(di.num_sms, ceil_div(total, 32 * 64)));
+            int per_sm = 0;
+            CSK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cs_smem_kernel<T>, cpc * 32, smem));
+            per_sm = std::max(per_sm, 1);
+            const int64_t grid = std::max<int64_t>(
+                1, std::min<int64_t>((int64_t)di.num_sms * per_sm, ceil_div(total, 32 * kPrivDepth * 4)));
             const int64_t per_cta = ceil_div(total, grid);
             cs_smem_kernel<T><<<(unsigned)grid, cpc * 32, smem, st>>>(code, rows, cols, ncols, cpc,
                                                                         (int)plan->k1, out, ldo, per_cta);
@@ -454,7 +630,7 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
     const int ncols = (int)ncols64;
     if (variant == CSK_VAR_AUTO) variant = env_variant();
     if (variant == CSK_VAR_AUTO) variant = select_variant(plan->d, plan->k1, ncols, dtype, plan->perm != nullptr);
-    CSK_REQUIRE(variant >= CSK_VAR_ATOMIC_COL && variant <= CSK_VAR_BULK_ROW, CSK_EINVAL, "unknown variant %d",
+    CSK_REQUIRE(variant >= CSK_VAR_ATOMIC_COL && variant <= CSK_VAR_TMA_ROW, CSK_EINVAL, "unknown variant %d",
                 variant);
     if (variant == CSK_VAR_SMEM && smem_cpc(plan->k1, ncols) < 1) variant = CSK_VAR_BULK_ROW;
     if (accumulate) {

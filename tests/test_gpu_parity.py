@@ -24,7 +24,7 @@ if not torch.cuda.is_available():
 
 import paper_2508_14209_b200 as csk  # noqa: E402
 
-VARIANTS = ["L", "T", "S", "G", "B"]
+VARIANTS = ["L", "T", "S", "G", "B", "X"]
 
 
 # ------------------------------------------------------------------ codes
@@ -117,6 +117,19 @@ def test_cs_apply_with_b_and_padding(variant):
     A = synth.gaussian_matrix(d, n, seed=3)
     b = synth.rhs(A, "hard", seed=3)
     _check_apply(plan, h, s, A, b, variant, lda_pad=3, ldsa_pad=5)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("d,n,k1", [(9001, 12, 512), (100003, 64, 8192), (4099, 100, 777), (5000, 200, 4096)])
+def test_cs_apply_contiguous_Ab(variant, d, n, k1):
+    # [A b] stored as one d x (n+1) column-major buffer (the TMA variant's fast layout)
+    plan = csk.cs_plan(d, k1, 5, sort=(variant == "G"))
+    h, s = oracle.codes(d, k1, 5)
+    Ab = synth.gaussian_matrix(d, n + 1, seed=3)
+    buf = gpu_colmajor(Ab)
+    SA = csk.cs_apply(plan, buf[:, :n], b=buf[:, n], variant=variant)
+    exp, T = oracle.cs_apply(h, s, Ab[:, :n], k1, b=Ab[:, n], with_abs=True)
+    assert_within_T(host(SA), exp, T, 1e-12)
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
