@@ -256,7 +256,7 @@ def bench_ours(args, cfg):
     def step():
         csk.ms_apply(plan, k2, A, b=b, Z=Z)
         if ws > 1:
-            dist.all_reduce(Z)                           # a6: NCCL over NVLink
+            dist.all_reduce(Z.t())                       # a6: NCCL over NVLink (contiguous view of Z)
         return csk.ms_solve(Z, n, x=x)[1]               # a7 (synchronises: numerical status)
 
     def barrier():

@@ -31,6 +31,17 @@ namespace csk {
 
 void prof_mark(cudaStream_t st, bool begin);
 
+// Row-major SA^T workspace layout: element (m, c) lives at (c / cw) * cs + m * lc + (c % cw).
+// Regular layout: one chunk of all columns (cw >= ncols), lc = ldt.  Chunk-major layout
+// (large k1 * ncols, e.g. C3): each cw-column chunk is its own k1 x lc slice (cs = k1 * lc)
+// and the kernels walk chunk by chunk, so only one slice has to stay L2-resident.
+struct RowLayout {
+    int cw = 1;
+    int64_t lc = 0, cs = 0;
+    bool chunk_major = false;
+    __host__ __device__ int64_t base(int ch, uint32_t bucket) const { return (int64_t)ch * cs + (int64_t)bucket * lc; }
+};
+
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ void red_add_f64(double* p, double v) {
     asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
@@ -156,52 +167,80 @@ __device__ __forceinline__ double swz_load(const uint8_t* tile, int c, int j) {
     return (double)*reinterpret_cast<const T*>(tile + off);
 }
 
+__device__ __forceinline__ void unit_coords(int64_t u, int nchunks, int64_t ngroups, bool chunk_major, int64_t& g,
+                                            int& ch) {
+    if (chunk_major) {
+        ch = (int)(u / ngroups);
+        g = u - (int64_t)ch * ngroups;
+    } else {
+        g = u / nchunks;
+        ch = (int)(u - g * nchunks);
+    }
+}
+
+__device__ __forceinline__ void bulk_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(dst)),
+        "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
+        : "memory");
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kTmaWarps * 32, 1) cs_tma_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                     const uint32_t* __restrict__ code, int64_t rows,
-                                                                    int ncols, int cw, int stage_bytes,
-                                                                    double* __restrict__ SAt, int64_t ldt) {
+                                                                    int ncols, int stage_bytes,
+                                                                    double* __restrict__ SAt, RowLayout L) {
     constexpr int RB = 128 / sizeof(T);   // rows per tile: 16 (fp64) / 32 (fp32)
     extern __shared__ uint8_t tma_smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)tma_smem_raw + 1023) & ~(uintptr_t)1023);
+    // 1024-B alignment for the 128B swizzle, by pointer arithmetic on the __shared__ array so
+    // the compiler keeps the shared state space (LDS/STS, not generic LD/ST)
+    uint8_t* smem = tma_smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(tma_smem_raw) & 1023u)) & 1023u);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // layout: [warps][stages] tiles | [warps][stages][RB] codes | [warps][stages] mbarriers
     uint8_t* ring = smem + (size_t)warp * kTmaStages * stage_bytes;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kTmaWarps * kTmaStages * stage_bytes) + warp * kTmaStages;
+    uint32_t* codes_all = reinterpret_cast<uint32_t*>(smem + (size_t)kTmaWarps * kTmaStages * stage_bytes);
+    uint32_t* codes = codes_all + warp * kTmaStages * RB;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(codes_all + kTmaWarps * kTmaStages * RB) + warp * kTmaStages;
+    const int cw = L.cw;
     const int nchunks = (ncols + cw - 1) / cw;
     const int64_t ngroups = (rows + RB - 1) / RB;
     const int64_t nunits = ngroups * nchunks;
     const int64_t gwarp = blockIdx.x * (int64_t)kTmaWarps + warp;
     const int64_t nwarps = (int64_t)gridDim.x * kTmaWarps;
     const uint32_t tile_bytes = (uint32_t)cw * 128u;
+    auto issue = [&](int64_t u, int s) {
+        int64_t g;
+        int ch;
+        unit_coords(u, nchunks, ngroups, L.chunk_major, g, ch);
+        mbar_expect_tx(&bars[s], tile_bytes + RB * 4);
+        tma_load_2d(ring + s * stage_bytes, &tmap, (int)(g * RB), ch * cw, &bars[s]);
+        bulk_load_1d(codes + s * RB, code + g * RB, RB * 4, &bars[s]);
+    };
     if (lane == 0) {
         for (int s = 0; s < kTmaStages; ++s) mbar_init(&bars[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int s = 0; s < kTmaStages; ++s) {
-            const int64_t u = gwarp + s * nwarps;
-            if (u < nunits) {
-                mbar_expect_tx(&bars[s], tile_bytes);
-                tma_load_2d(ring + s * stage_bytes, &tmap, (int)((u / nchunks) * RB), (int)((u % nchunks) * cw),
-                            &bars[s]);
-            }
-        }
+        for (int s = 0; s < kTmaStages; ++s)
+            if (gwarp + s * nwarps < nunits) issue(gwarp + s * nwarps, s);
     }
     __syncwarp();
     for (int64_t k = 0;; ++k) {
         const int64_t u = gwarp + k * nwarps;
         if (u >= nunits) break;
         const int s = (int)(k % kTmaStages);
-        const int64_t g = u / nchunks;
-        const int c0 = (int)(u - g * nchunks) * cw;
+        int64_t g;
+        int ch;
+        unit_coords(u, nchunks, ngroups, L.chunk_major, g, ch);
+        const int c0 = ch * cw;
         const int nc = min(cw, ncols - c0);
-        const int64_t r0 = g * RB;
-        const int nr = (int)min((int64_t)RB, rows - r0);
-        const uint32_t cdl = __ldg(code + min(r0 + (lane % RB), rows - 1));
+        const int nr = (int)min((int64_t)RB, rows - g * RB);
         mbar_wait(&bars[s], (uint32_t)((k / kTmaStages) & 1));
+        const uint32_t cdl = codes[s * RB + (lane % RB)];
         const uint8_t* tile = ring + s * stage_bytes;
 #pragma unroll 4
         for (int j = 0; j < RB; ++j) {
             const uint32_t cd = __shfl_sync(0xffffffffu, cdl, j);
-            double* dst = SAt + (int64_t)code_bucket(cd) * ldt + c0;
+            double* dst = SAt + L.base(ch, code_bucket(cd));
             const long long smask = (long long)code_sign_mask64(cd);
 #pragma unroll
             for (int q = 0; q < kTmaMaxCols / 32; ++q) {
@@ -215,14 +254,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 1) cs_tma_kernel(const __grid_
         // this warp's generic reads of the stage precede the next async (TMA) write into it
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) {
-            const int64_t un = u + kTmaStages * nwarps;
-            if (un < nunits) {
-                mbar_expect_tx(&bars[s], tile_bytes);
-                tma_load_2d(ring + s * stage_bytes, &tmap, (int)((un / nchunks) * RB), (int)((un % nchunks) * cw),
-                            &bars[s]);
-            }
-        }
+        if (lane == 0 && u + kTmaStages * nwarps < nunits) issue(u + kTmaStages * nwarps, s);
     }
 }
 
@@ -230,6 +262,129 @@ static int tma_chunk_width(int ncols) {
     if (ncols <= kTmaMaxCols) return ncols;
     const int nch = (ncols + 63) / 64;
     return (ncols + nch - 1) / nch;
+}
+
+// ------------------------------------------------------------ variant B (TMA)
+// The fastest form measured: TMA in, TMA bulk reduce-add out.  Per warp: a ring of
+// kB2Stages stages, each holding one RB-row x cw-column tile of [A b] (2-D tensor load,
+// 128B swizzle, zero-filled past d) plus the tile's RB codes (1-D bulk copy on the same
+// mbarrier), so nothing on the critical path waits on a synchronous load.  The warp
+// transposes the tile into a row-major fp64 row buffer (sign applied), and lanes
+// 0..RB-1 each hand their row to the TMA engine as ONE cp.reduce.async.bulk .add.f64 of
+// cw*8 bytes into SA^T[h(row), c0:c0+cw].  cw is even for multi-chunk [A b] (16-B aligned).
+constexpr int kB2Warps = 8;
+constexpr int kB2Stages = 2;
+constexpr int kB2MaxCols = 66;
+
+template <typename T>
+__global__ void __launch_bounds__(kB2Warps * 32, 1) cs_bulk_tma_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                                        const uint32_t* __restrict__ code,
+                                                                        int64_t rows, int ncols,
+                                                                        int stage_bytes, int ldrow,
+                                                                        double* __restrict__ SAt, RowLayout L) {
+    constexpr int RB = 128 / sizeof(T);   // rows per tile: 16 (fp64) / 32 (fp32)
+    const int cw = L.cw;
+    extern __shared__ uint8_t b2_smem_raw[];
+    uint8_t* smem = b2_smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(b2_smem_raw) & 1023u)) & 1023u);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // layout: [warps][stages] tiles | [warps] row buffers | [warps][stages][RB] codes | [warps][stages] mbarriers
+    uint8_t* ring = smem + (size_t)warp * kB2Stages * stage_bytes;
+    double* rowbuf = reinterpret_cast<double*>(smem + (size_t)kB2Warps * kB2Stages * stage_bytes) +
+                     (size_t)warp * RB * ldrow;
+    uint32_t* codes = reinterpret_cast<uint32_t*>(smem + (size_t)kB2Warps * kB2Stages * stage_bytes +
+                                                  (size_t)kB2Warps * RB * ldrow * 8) +
+                      warp * kB2Stages * RB;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(codes - warp * kB2Stages * RB) +
+                                                 (size_t)kB2Warps * kB2Stages * RB * 4) +
+                     warp * kB2Stages;
+    const int nchunks = (ncols + cw - 1) / cw;
+    const int64_t ngroups = (rows + RB - 1) / RB;
+    const int64_t nunits = ngroups * nchunks;
+    const int64_t gwarp = blockIdx.x * (int64_t)kB2Warps + warp;
+    const int64_t nwarps = (int64_t)gridDim.x * kB2Warps;
+    const uint32_t tile_bytes = (uint32_t)cw * 128u;
+    auto issue = [&](int64_t u, int s) {
+        int64_t g;
+        int ch;
+        unit_coords(u, nchunks, ngroups, L.chunk_major, g, ch);
+        mbar_expect_tx(&bars[s], tile_bytes + RB * 4);
+        tma_load_2d(ring + s * stage_bytes, &tmap, (int)(g * RB), ch * cw, &bars[s]);
+        bulk_load_1d(codes + s * RB, code + g * RB, RB * 4, &bars[s]);
+    };
+    if (lane == 0) {
+        for (int s = 0; s < kB2Stages; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int s = 0; s < kB2Stages; ++s)
+            if (gwarp + s * nwarps < nunits) issue(gwarp + s * nwarps, s);
+    }
+    for (int e = lane; e < RB * ldrow; e += 32) rowbuf[e] = 0.0;
+    __syncwarp();
+    constexpr int kLanesPerRow = 32 / RB;   // 2 (fp64) / 1 (fp32)
+    const int rr = lane % RB, part = lane / RB;
+    for (int64_t k = 0;; ++k) {
+        const int64_t u = gwarp + k * nwarps;
+        if (u >= nunits) break;
+        const int s = (int)(k % kB2Stages);
+        int64_t g;
+        int ch;
+        unit_coords(u, nchunks, ngroups, L.chunk_major, g, ch);
+        const int c0 = ch * cw;
+        const int nc = min(cw, ncols - c0);
+        const int nr = (int)min((int64_t)RB, rows - g * RB);
+        mbar_wait(&bars[s], (uint32_t)((k / kB2Stages) & 1));
+        const uint32_t cd = codes[s * RB + rr];
+        const long long smask = (long long)code_sign_mask64(cd);
+        const uint8_t* tile = ring + s * stage_bytes;
+        // Transpose tile (column c = 128-B swizzled row) -> row-major rowbuf.  Column c of this
+        // lane's row lives at c*128 + (((rr / E) ^ (c & 7)) << 4) + (rr % E)*sizeof(T), E = 16/sizeof(T);
+        // with j unrolled, c & 7 is a compile-time pattern, so the 4 (fp64) / 8 (fp32) swizzled
+        // offsets are precomputed per lane and every access uses an immediate displacement.
+        constexpr int E = 16 / (int)sizeof(T);
+        constexpr int kStep = 128 * kLanesPerRow;                 // bytes between this lane's columns
+        constexpr int kPat = 8 / kLanesPerRow;                    // distinct (c & 7) values per lane
+        int swz[kPat];
+#pragma unroll
+        for (int p = 0; p < kPat; ++p) swz[p] = (((rr / E) ^ ((p * kLanesPerRow + part) & 7)) << 4);
+        const uint8_t* tb = tile + part * 128 + (rr % E) * (int)sizeof(T);
+        double* rb = rowbuf + rr * ldrow + part;
+        // all tile loads first (independent, in flight together), then the row-buffer stores
+        constexpr int kJ = kB2MaxCols / kLanesPerRow;
+        double v[kJ];
+#pragma unroll
+        for (int j = 0; j < kJ; ++j)
+            v[j] = (j * kLanesPerRow + part < nc) ? (double)*reinterpret_cast<const T*>(tb + j * kStep + swz[j % kPat])
+                                                  : 0.0;
+        // the row buffer is free once this lane's previous bulk reduce has read it
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < kJ; ++j)
+            if (j * kLanesPerRow + part < nc) rb[j * kLanesPerRow] = __longlong_as_double(__double_as_longlong(v[j]) ^ smask);
+        if ((nc & 1) && part == 0) rowbuf[rr * ldrow + nc] = 0.0;   // 16-B padding column
+        // generic smem writes -> async proxy (bulk reduce source); tile reads -> next TMA write
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (part == 0 && rr < nr) {
+            const uint32_t bytes = (uint32_t)(((nc + 1) & ~1) * 8);
+            double* dst = SAt + L.base(ch, code_bucket(cd));
+            const uint32_t src = (uint32_t)__cvta_generic_to_shared(rowbuf + rr * ldrow);
+            asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(dst),
+                         "r"(src), "r"(bytes)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        if (lane == 0) {
+            const int64_t un = u + kB2Stages * nwarps;
+            if (un < nunits) issue(un, s);
+        }
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+static int b2_chunk_width(int ncols) {
+    if (ncols <= kB2MaxCols) return ncols;
+    const int nch = (ncols + 63) / 64;
+    return (((ncols + nch - 1) / nch) + 1) & ~1;
 }
 
 // ------------------------------------------------------------------ variant B
@@ -307,9 +462,9 @@ __global__ void __launch_bounds__(kBulkWarps * 32) cs_bulk_kernel(const uint32_t
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-// SA^T (row-major k1 x ldt, fp64) -> SA (column-major, ldsa, T)
+// SA^T (row-major workspace, fp64) -> SA (column-major, ldsa, T)
 template <typename T>
-__global__ void transpose_out_kernel(const double* __restrict__ SAt, int64_t ldt, int64_t k1, int ncols,
+__global__ void transpose_out_kernel(const double* __restrict__ SAt, RowLayout L, int64_t k1, int ncols,
                                      T* __restrict__ SA, int64_t ldsa) {
     __shared__ double t[32][33];
     const int64_t m0 = blockIdx.x * 32;
@@ -317,7 +472,7 @@ __global__ void transpose_out_kernel(const double* __restrict__ SAt, int64_t ldt
     for (int j = threadIdx.y; j < 32; j += blockDim.y) {
         const int64_t m = m0 + j;
         const int c = c0 + threadIdx.x;
-        t[j][threadIdx.x] = (m < k1 && c < ncols) ? SAt[m * ldt + c] : 0.0;
+        t[j][threadIdx.x] = (m < k1 && c < ncols) ? SAt[(int64_t)(c / L.cw) * L.cs + m * L.lc + (c % L.cw)] : 0.0;
     }
     __syncthreads();
     for (int j = threadIdx.y; j < 32; j += blockDim.y) {
@@ -497,9 +652,36 @@ static int select_variant(int64_t d, int64_t k1, int ncols, csk_dtype dtype, boo
     return CSK_VAR_TMA_ROW;   // falls back to T when [A b] is not one uniformly strided tensor
 }
 
+// 2-D tensor map of [A b] (rows x ncols, column stride lda) with a RB x cw box, 128B swizzle
+template <typename T>
+static bool make_tensor_map(CUtensorMap* tmap, const Cols<T>& cols, int64_t rows, int ncols, int cw) {
+    constexpr int RB = 128 / sizeof(T);
+    const T* base = cols.n > 0 ? cols.A : cols.b;
+    const cuuint64_t gdim[2] = {(cuuint64_t)rows, (cuuint64_t)ncols};
+    const cuuint64_t gstride[1] = {(cuuint64_t)(ncols > 1 ? cols.lda * (int64_t)sizeof(T)
+                                                          : ((rows * (int64_t)sizeof(T) + 15) & ~(int64_t)15))};
+    const cuuint32_t box[2] = {(cuuint32_t)RB, (cuuint32_t)cw};
+    const cuuint32_t estride[2] = {1, 1};
+    // L2 fetch granularity of the tile loads (CSK_L2PROMO = 0 | 64 | 128 | 256 for experiments)
+    CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    if (const char* e = std::getenv("CSK_L2PROMO")) {
+        const int v = std::atoi(e);
+        promo = v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                : v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    }
+    const CUresult cr = tensor_map_encoder()(
+        tmap, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+        const_cast<T*>(base), gdim, gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+        promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return cr == CUDA_SUCCESS;
+}
+
+// For the row-scatter variants `out` is the SA^T workspace described by L (L.cs > 0 marks
+// a TMA-eligible launch decided by cs_apply_impl); the others write column-major (out, ldo).
 template <typename T>
 static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> cols, int64_t row_begin,
-                              int64_t row_end, double* out, int64_t ldo, bool out_rowmajor, cudaStream_t st) {
+                              int64_t row_end, double* out, int64_t ldo, const RowLayout& L, cudaStream_t st) {
     const DeviceInfo& di = device_info();
     const uint32_t* code = reinterpret_cast<const uint32_t*>(plan->code) + row_begin;
     const int64_t rows = row_end - row_begin;
@@ -512,34 +694,43 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
             return CSK_OK;
         }
         case CSK_VAR_TMA_ROW: {
-            if (!tma_eligible(cols, ncols))
-                return run_variant<T>(CSK_VAR_ATOMIC_ROW, plan, ncols, cols, row_begin, row_end, out, ldo,
-                                      out_rowmajor, st);
             constexpr int RB = 128 / sizeof(T);
-            const int cw = tma_chunk_width(ncols);
-            const T* base = cols.n > 0 ? cols.A : cols.b;
+            CSK_REQUIRE(L.cs > 0, CSK_EINVAL, "variant X launched without a TMA layout");
             CUtensorMap tmap;
-            const cuuint64_t gdim[2] = {(cuuint64_t)rows, (cuuint64_t)ncols};
-            const cuuint64_t gstride[1] = {(cuuint64_t)((ncols > 1 ? cols.lda : rows) * (int64_t)sizeof(T))};
-            const cuuint32_t box[2] = {(cuuint32_t)RB, (cuuint32_t)cw};
-            const cuuint32_t estride[2] = {1, 1};
-            const CUresult cr = tensor_map_encoder()(
-                &tmap, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
-                const_cast<T*>(base), gdim, gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-            CSK_REQUIRE(cr == CUDA_SUCCESS, CSK_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
-            const int stage_bytes = (cw * 128 + 1023) & ~1023;
-            const size_t smem = (size_t)kTmaWarps * kTmaStages * stage_bytes + kTmaWarps * kTmaStages * 8 + 1024;
+            CSK_REQUIRE(make_tensor_map(&tmap, cols, rows, ncols, L.cw), CSK_ECUDA, "cuTensorMapEncodeTiled failed");
+            const int stage_bytes = (L.cw * 128 + 1023) & ~1023;
+            const size_t smem = (size_t)kTmaWarps * kTmaStages * stage_bytes + (size_t)kTmaWarps * kTmaStages * RB * 4 +
+                                (size_t)kTmaWarps * kTmaStages * 8 + 1024;
             CSK_REQUIRE(smem <= (size_t)di.smem_optin, CSK_EUNSUPPORTED, "variant X: tile does not fit smem");
             CSK_CUDA_TRY(cudaFuncSetAttribute(cs_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            const int64_t units = ceil_div(rows, RB) * ceil_div(ncols, cw);
+            const int64_t units = ceil_div(rows, RB) * ceil_div(ncols, L.cw);
             const int64_t blocks = std::min<int64_t>(ceil_div(units, kTmaWarps), (int64_t)di.num_sms);
-            cs_tma_kernel<T><<<(unsigned)blocks, kTmaWarps * 32, smem, st>>>(tmap, code, rows, ncols, cw, stage_bytes,
-                                                                             out, ldo);
+            cs_tma_kernel<T><<<(unsigned)blocks, kTmaWarps * 32, smem, st>>>(tmap, code, rows, ncols, stage_bytes, out, L);
             CSK_LAUNCH_CHECK();
             return CSK_OK;
         }
         case CSK_VAR_BULK_ROW: {
+            if (L.cs > 0) {
+                constexpr int RB = 128 / sizeof(T);
+                // even (16-B aligned rows) and == 2 mod 4: the 16 rows x 2 column-lanes of one
+                // STS hit every bank exactly twice (2 wavefronts, the minimum for 256 B)
+                int ldrow = (L.cw + 1) & ~1;
+                if (ldrow % 4 == 0) ldrow += 2;
+                CUtensorMap tmap;
+                CSK_REQUIRE(make_tensor_map(&tmap, cols, rows, ncols, L.cw), CSK_ECUDA, "cuTensorMapEncodeTiled failed");
+                const int stage_bytes = (L.cw * 128 + 1023) & ~1023;
+                const size_t smem = (size_t)kB2Warps * kB2Stages * stage_bytes + (size_t)kB2Warps * RB * ldrow * 8 +
+                                    (size_t)kB2Warps * kB2Stages * RB * 4 + (size_t)kB2Warps * kB2Stages * 8 + 1024;
+                CSK_REQUIRE(smem <= (size_t)di.smem_optin, CSK_EUNSUPPORTED, "variant B: tile does not fit smem");
+                CSK_CUDA_TRY(cudaFuncSetAttribute(cs_bulk_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)smem));
+                const int64_t units = ceil_div(rows, RB) * ceil_div(ncols, L.cw);
+                const int64_t blocks = std::min<int64_t>(ceil_div(units, kB2Warps), (int64_t)di.num_sms);
+                cs_bulk_tma_kernel<T><<<(unsigned)blocks, kB2Warps * 32, smem, st>>>(tmap, code, rows, ncols,
+                                                                                     stage_bytes, ldrow, out, L);
+                CSK_LAUNCH_CHECK();
+                return CSK_OK;
+            }
             const int cw = bulk_chunk_width(ncols);
             const int ldtile = (cw + 1) & ~1;
             const size_t smem = (size_t)kBulkWarps * 2 * kBulkRows * ldtile * sizeof(double);
@@ -555,7 +746,6 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
             return CSK_OK;
         }
         case CSK_VAR_ATOMIC_ROW: {
-            (void)out_rowmajor;
             const bool bulk = false;
             const size_t smem = (size_t)kRowWarps * (bulk ? 2 : 1) * 32 * kTileLd * sizeof(double);
             const int64_t units = ceil_div(rows, 32) * ceil_div(ncols, 32);
@@ -640,21 +830,52 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
     }
     const int64_t k1 = plan->k1;
 
+    // TMA eligibility of [A b] as one 2-D tensor (variants X and B)
+    const size_t esz = dtype == CSK_F64 ? 8 : 4;
+    const void* base = n > 0 ? A : b;
+    bool tma = variant == CSK_VAR_TMA_ROW || variant == CSK_VAR_BULK_ROW;
+    tma = tma && !std::getenv("CSK_NO_TMA") && (n == 0 || b == nullptr ||
+                                               (const char*)b == (const char*)A + (size_t)n * lda * esz);
+    tma = tma && ((uintptr_t)base & 15) == 0 && (ncols == 1 || ((lda * (int64_t)esz) & 15) == 0);
+    tma = tma && (((uintptr_t)(plan->code + row_begin)) & 15) == 0 && tensor_map_encoder() != nullptr;
+    if (variant == CSK_VAR_TMA_ROW && !tma) variant = CSK_VAR_ATOMIC_ROW;
+
     ApplyTarget tgt;
+    RowLayout L;
+    size_t ws_doubles = 0;
     if (variant_rowmajor(variant)) {
-        tgt.ld = (ncols + 3) & ~3;
+        if (tma) {
+            L.cw = variant == CSK_VAR_BULK_ROW ? b2_chunk_width(ncols) : tma_chunk_width(ncols);
+            const int nchunks = (ncols + L.cw - 1) / L.cw;
+            if (nchunks > 1 && (int64_t)k1 * ncols * 8 > (int64_t)device_info().l2_bytes / 2) {
+                L.chunk_major = true;                     // one L2-sized SA^T slice per column chunk
+                L.lc = (L.cw + 1) & ~1;
+                L.cs = k1 * L.lc;
+                ws_doubles = (size_t)nchunks * L.cs;
+            } else {
+                L.lc = (ncols + 3) & ~3;
+                L.cs = L.cw;
+                ws_doubles = (size_t)k1 * L.lc;
+            }
+        } else {
+            L.cw = ncols;
+            L.lc = (ncols + 3) & ~3;
+            L.cs = 0;
+            ws_doubles = (size_t)k1 * L.lc;
+        }
+        tgt.ld = L.lc;
         tgt.owned = true;
     } else if (dtype == CSK_F32) {
         tgt.ld = k1;
         tgt.owned = true;
+        ws_doubles = (size_t)k1 * ncols;
     } else {
         tgt.buf = static_cast<double*>(SA);
         tgt.ld = ldsa;
     }
     if (tgt.owned) {
-        const size_t bytes = (size_t)k1 * (variant_rowmajor(variant) ? tgt.ld : ncols) * sizeof(double);
-        CSK_CUDA_TRY(cudaMallocAsync(&tgt.buf, bytes, st));
-        CSK_CUDA_TRY(cudaMemsetAsync(tgt.buf, 0, bytes, st));
+        CSK_CUDA_TRY(cudaMallocAsync(&tgt.buf, ws_doubles * sizeof(double), st));
+        CSK_CUDA_TRY(cudaMemsetAsync(tgt.buf, 0, ws_doubles * sizeof(double), st));
     } else if (variant != CSK_VAR_SORTED && !accumulate) {
         // zero SA (ldsa may exceed k1: clear the k1 x ncols window only)
         if (ldsa == k1) {
@@ -667,22 +888,22 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
     prof_mark(st, true);
     if (dtype == CSK_F64) {
         Cols<double> cols{static_cast<const double*>(A), static_cast<const double*>(b), lda, (int)n};
-        s = run_variant<double>(variant, plan, ncols, cols, row_begin, row_end, tgt.buf, tgt.ld,
-                                variant_rowmajor(variant), st);
+        s = run_variant<double>(variant, plan, ncols, cols, row_begin, row_end, tgt.buf, tgt.ld, L, st);
     } else {
         Cols<float> cols{static_cast<const float*>(A), static_cast<const float*>(b), lda, (int)n};
-        s = run_variant<float>(variant, plan, ncols, cols, row_begin, row_end, tgt.buf, tgt.ld,
-                               variant_rowmajor(variant), st);
+        s = run_variant<float>(variant, plan, ncols, cols, row_begin, row_end, tgt.buf, tgt.ld, L, st);
     }
     prof_mark(st, false);
     if (s == CSK_OK && tgt.owned) {
         if (variant_rowmajor(variant)) {
+            RowLayout Lt = L;
+            if (Lt.cs == 0) Lt.cs = Lt.cw;   // regular layout of the non-TMA kernels
             dim3 grid((unsigned)ceil_div(k1, 32), (unsigned)ceil_div(ncols, 32));
             if (dtype == CSK_F64)
-                transpose_out_kernel<double><<<grid, dim3(32, 8), 0, st>>>(tgt.buf, tgt.ld, k1, ncols,
+                transpose_out_kernel<double><<<grid, dim3(32, 8), 0, st>>>(tgt.buf, Lt, k1, ncols,
                                                                            static_cast<double*>(SA), ldsa);
             else
-                transpose_out_kernel<float><<<grid, dim3(32, 8), 0, st>>>(tgt.buf, tgt.ld, k1, ncols,
+                transpose_out_kernel<float><<<grid, dim3(32, 8), 0, st>>>(tgt.buf, Lt, k1, ncols,
                                                                           static_cast<float*>(SA), ldsa);
         } else {
             narrow_kernel<<<(unsigned)std::min<int64_t>(ceil_div(k1 * ncols, 256), 4096), 256, 0, st>>>(

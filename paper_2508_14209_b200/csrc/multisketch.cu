@@ -162,103 +162,102 @@ static csk_status sketch_host_rows(csk_plan_t plan, int64_t n, const double* A, 
 }
 
 // ------------------------------------------------------------- a7: ms_solve
-// One CTA.  W (m x nc, column-major, ld m) is a private copy of Z in global
-// memory (L2-resident: <= 1 MB at the BASELINE sizes) or shared memory when it fits.
-// Householder with the LAPACK sign choice R_jj = -sign(x0) ||x||.
+// One CTA.  W (m x nc, column-major, ld m) is a private copy of Z, held in shared
+// memory when it fits (else in global memory, L2-resident: <= 1 MB at BASELINE sizes).
+// Householder with the LAPACK sign choice R_jj = -sign(x0) ||x||.  One __syncthreads
+// per column: every thread recomputes alpha and beta = 2/(v^T v) = 1/(alpha (alpha - x0))
+// from the column's norm^2, which the warp updating column j+1 accumulates during step j
+// (look-ahead).  Back substitution by one warp.
 struct SolveStatus {
     int status;
     double sk_resid;
 };
 
-constexpr int kQrThreads = 1024;
-
-__device__ double block_sum(double v, double* red) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    __syncthreads();
-    if (lane == 0) red[warp] = v;
-    __syncthreads();
-    double s = 0.0;
-    const int nw = blockDim.x >> 5;
-    for (int w = 0; w < nw; ++w) s += red[w];   // fixed order, every thread gets the same value
-    return s;
-}
+constexpr int kQrThreads = 512;
 
 __global__ void __launch_bounds__(kQrThreads, 1) qr_solve_kernel(double* __restrict__ Wg, int m, int nc,
                                                                  int use_smem, double* __restrict__ x,
                                                                  SolveStatus* __restrict__ status) {
     extern __shared__ double qsm[];
-    __shared__ double red[32];
-    __shared__ double s_alpha, s_beta;
+    __shared__ double red[kQrThreads / 32];
     __shared__ int s_fail;
-    double* v = qsm;                       // m
-    double* W = use_smem ? qsm + m : Wg;   // m x nc
+    double* norm2 = qsm;               // nc + 1
+    double* diag = norm2 + nc + 1;     // nc
+    double* y = diag + nc;             // nc
+    double* W = use_smem ? y + nc + 1 : Wg;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    if (use_smem) {
+    if (use_smem)
         for (int e = threadIdx.x; e < m * nc; e += blockDim.x) W[e] = Wg[e];
+    __syncthreads();
+    {   // norm^2 of column 0, fixed-order reduction
+        double part = 0.0;
+        for (int i = threadIdx.x; i < m; i += blockDim.x) part += W[i] * W[i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        if (lane == 0) red[warp] = part;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double s = 0.0;
+            for (int w = 0; w < nw; ++w) s += red[w];
+            norm2[0] = s;
+        }
         __syncthreads();
     }
     for (int j = 0; j < nc; ++j) {
-        double* wj = W + (int64_t)j * m;
-        double part = 0.0;
-        for (int i = j + threadIdx.x; i < m; i += blockDim.x) part += wj[i] * wj[i];
-        const double norm2 = block_sum(part, red);
+        const double* wj = W + (int64_t)j * m;
         const double x0 = wj[j];
-        const double norm = sqrt(norm2);
-        const double alpha = norm == 0.0 ? 0.0 : (x0 >= 0.0 ? -norm : norm);
-        for (int i = j + threadIdx.x; i < m; i += blockDim.x) v[i] = (i == j) ? x0 - alpha : wj[i];
-        // v^T v = (x0 - alpha)^2 + (norm2 - x0^2); recompute exactly from v for robustness
-        __syncthreads();
-        double pv = 0.0;
-        for (int i = j + threadIdx.x; i < m; i += blockDim.x) pv += v[i] * v[i];
-        const double vtv = block_sum(pv, red);
-        if (threadIdx.x == 0) {
-            s_alpha = alpha;
-            s_beta = vtv > 0.0 ? 2.0 / vtv : 0.0;
-        }
-        __syncthreads();
-        const double beta = s_beta;
-        if (beta != 0.0) {
-            for (int c = j + 1 + warp; c < nc; c += nw) {
-                double* wc = W + (int64_t)c * m;
-                double dot = 0.0;
-                for (int i = j + lane; i < m; i += 32) dot += v[i] * wc[i];
+        const double nrm = sqrt(norm2[j]);
+        const double alpha = nrm == 0.0 ? 0.0 : (x0 >= 0.0 ? -nrm : nrm);
+        const double beta = nrm == 0.0 ? 0.0 : 1.0 / (alpha * (alpha - x0));
+        const double v0 = x0 - alpha;
+        if (threadIdx.x == 0) diag[j] = alpha;
+        for (int c = j + 1 + warp; c < nc; c += nw) {
+            double* wc = W + (int64_t)c * m;
+            double dot = lane == 0 ? v0 * wc[j] : 0.0;
+            for (int i = j + 1 + lane; i < m; i += 32) dot += wj[i] * wc[i];
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-                const double f = beta * dot;
-                for (int i = j + lane; i < m; i += 32) wc[i] -= f * v[i];
+            for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+            const double f = beta * dot;
+            if (lane == 0) wc[j] -= f * v0;
+            double ss = 0.0;
+            for (int i = j + 1 + lane; i < m; i += 32) {
+                const double t = wc[i] - f * wj[i];
+                wc[i] = t;
+                ss += t * t;
+            }
+            if (c == j + 1) {   // look-ahead: norm^2 of the next pivot column below the diagonal
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+                if (lane == 0) norm2[j + 1] = ss;
             }
         }
         __syncthreads();
-        if (threadIdx.x == 0) wj[j] = s_alpha;
-        __syncthreads();
     }
-    // R is the upper triangle of W.  Singularity check on R[:n,:n].
+    // R: diagonal in diag[], strictly upper part in W.  Singularity check on R[:n,:n].
     const int n = nc - 1;
     if (threadIdx.x == 0) {
         double rmax = 0.0;
-        for (int i = 0; i < n; ++i) rmax = fmax(rmax, fabs(W[i + (int64_t)i * m]));
+        for (int i = 0; i < n; ++i) rmax = fmax(rmax, fabs(diag[i]));
         int st = 0;
         for (int i = 0; i < n; ++i)
-            if (!(fabs(W[i + (int64_t)i * m]) > 1e-14 * rmax)) st = CSK_ESINGULAR;
+            if (!(fabs(diag[i]) > 1e-14 * rmax)) st = CSK_ESINGULAR;
         status->status = st;
-        status->sk_resid = fabs(W[n + (int64_t)n * m]);
+        status->sk_resid = fabs(diag[n]);
         s_fail = st;
     }
     __syncthreads();
-    if (s_fail) return;
-    // back substitution R[:n,:n] x = R[:n, n], column-oriented; y lives in v
-    for (int i = threadIdx.x; i < n; i += blockDim.x) v[i] = W[i + (int64_t)n * m];
-    __syncthreads();
+    if (s_fail || warp != 0) return;
+    // back substitution R[:n,:n] x = R[:n, n] (= Q^T z), column-oriented, one warp
+    for (int i = lane; i < n; i += 32) y[i] = W[i + (int64_t)n * m];
+    __syncwarp();
     for (int c = n - 1; c >= 0; --c) {
-        const double xc = v[c] / W[c + (int64_t)c * m];
-        __syncthreads();
-        for (int i = threadIdx.x; i < c; i += blockDim.x) v[i] -= W[i + (int64_t)c * m] * xc;
-        if (threadIdx.x == 0) x[c] = xc;
-        __syncthreads();
+        const double xc = y[c] / diag[c];
+        for (int i = lane; i < c; i += 32) y[i] -= W[i + (int64_t)c * m] * xc;
+        if (lane == 0) x[c] = xc;
+        __syncwarp();
     }
 }
+
 
 static csk_status solve_impl(int64_t k2, int64_t n, const double* Z, int64_t ldz, double* x, double* sk_resid,
                              cudaStream_t st, bool x_host) {
@@ -276,9 +275,10 @@ static csk_status solve_impl(int64_t k2, int64_t n, const double* Z, int64_t ldz
     xd = x_host ? reinterpret_cast<double*>(reinterpret_cast<char*>(W) + wbytes + 64) : x;
     CSK_CUDA_TRY(cudaMemcpy2DAsync(W, m * 8, Z, ldz * 8, m * 8, nc, cudaMemcpyDeviceToDevice, st));
     const DeviceInfo& di = device_info();
-    const size_t smem_need = (size_t)(m + (size_t)m * nc) * 8;
+    const size_t small = (size_t)(3 * nc + 2) * 8;
+    const size_t smem_need = small + (size_t)m * nc * 8;
     const int use_smem = smem_need <= (size_t)di.smem_optin ? 1 : 0;
-    const size_t smem = use_smem ? smem_need : (size_t)m * 8;
+    const size_t smem = use_smem ? smem_need : small;
     CSK_CUDA_TRY(cudaFuncSetAttribute(qr_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     qr_solve_kernel<<<1, kQrThreads, smem, st>>>(W, m, nc, use_smem, xd, sd);
     CSK_LAUNCH_CHECK();

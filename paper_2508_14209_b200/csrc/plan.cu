@@ -268,7 +268,8 @@ static csk_status alloc_plan(int64_t d, int64_t k1, uint32_t flags, csk_plan_t* 
     plan->d = d;
     plan->k1 = k1;
     cudaGetDevice(&plan->device);
-    if (cudaMalloc(&plan->code, d * 4) != cudaSuccess ||
+    // codes are padded by 32 zero entries: 64/128-B bulk copies of a tile's codes never read past the end
+    if (cudaMalloc(&plan->code, (d + 32) * 4) != cudaSuccess || cudaMemset(plan->code + d, 0, 32 * 4) != cudaSuccess ||
         ((flags & CSK_PLAN_SORT) &&
          (cudaMalloc(&plan->offsets, (k1 + 1) * 8) != cudaSuccess || cudaMalloc(&plan->perm, d * 4) != cudaSuccess))) {
         cudaGetLastError();

@@ -132,6 +132,31 @@ def test_cs_apply_contiguous_Ab(variant, d, n, k1):
     assert_within_T(host(SA), exp, T, 1e-12)
 
 
+@pytest.mark.parametrize("variant", ["B", "X"])
+def test_cs_apply_contiguous_Ab_fp32(variant):
+    d, n, k1 = 50001, 64, 4096
+    plan = csk.cs_plan(d, k1, 6)
+    h, s = oracle.codes(d, k1, 6)
+    Ab = synth.gaussian_matrix(d, n + 1, seed=4, dtype=np.float32)
+    buf = gpu_colmajor(Ab)
+    SA = csk.cs_apply(plan, buf[:, :n], b=buf[:, n], variant=variant)
+    exp, T = oracle.cs_apply(h, s, Ab[:, :n], k1, b=Ab[:, n], with_abs=True)
+    assert_within_T(host(SA), exp, T, 1e-5)
+
+
+@pytest.mark.parametrize("variant", ["B", "X"])
+def test_cs_apply_chunk_major_layout(variant):
+    # k1 * ncols * 8 > L2/2 switches the TMA variants to one SA^T slice per column chunk (C3 regime)
+    d, n, k1 = 30011, 200, 65536
+    plan = csk.cs_plan(d, k1, 8)
+    h, s = oracle.codes(d, k1, 8)
+    Ab = synth.integer_matrix(d, n + 1, seed=8, lo=-1000, hi=1000)
+    buf = gpu_colmajor(Ab)
+    SA = csk.cs_apply(plan, buf[:, :n], b=buf[:, n], variant=variant)
+    exp = oracle.cs_apply(h, s, Ab[:, :n], k1, b=Ab[:, n])
+    assert np.array_equal(host(SA), exp)
+
+
 @pytest.mark.parametrize("variant", VARIANTS)
 def test_cs_apply_only_b(variant):
     d, k1 = 3333, 100
