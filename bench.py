@@ -253,7 +253,12 @@ def bench_ours(args, cfg):
     torch.cuda.synchronize()
     gauss_first_ms = (time.perf_counter() - t) * 1e3
 
+    SA_ws = synth.colmajor_empty(torch, k1, ncols, torch.float64, dev)
+
     def step():
+        if args.cs_only:                                 # kernel experiments: the CountSketch alone
+            csk.cs_apply(plan, A, b=b, SA=SA_ws)
+            return 0.0
         csk.ms_apply(plan, k2, A, b=b, Z=Z)
         if ws > 1:
             dist.all_reduce(Z.t())                       # a6: NCCL over NVLink (contiguous view of Z)
@@ -316,7 +321,7 @@ def bench_ours(args, cfg):
     barrier()
     msa_ms = ev0.elapsed_time(ev1) / args.steps
     t = time.perf_counter()
-    for _ in range(args.steps):
+    for _ in range(0 if args.cs_only else args.steps):
         csk.ms_solve(Z, n, x=x)
     solve_ms = (time.perf_counter() - t) * 1e3 / args.steps
 
@@ -340,10 +345,11 @@ def bench_ours(args, cfg):
         ne["ms"] = None
 
     # ---- accuracy of the step's solution (verification, untimed): ||b - A x|| / ||b||
-    step()
-    r_ms = float(torch.linalg.norm(b - A @ x) / torch.linalg.norm(b))
-    acc = {"rel_residual_ms": r_ms}
-    if ws == 1 and d * ncols * 8 <= 16e9 and not args.no_acc:
+    acc = {}
+    if not args.cs_only:
+        step()
+        acc["rel_residual_ms"] = float(torch.linalg.norm(b - A @ x) / torch.linalg.norm(b))
+    if ws == 1 and d * ncols * 8 <= 16e9 and not args.no_acc and not args.cs_only:
         R = torch.linalg.qr(buf, mode="r")[1]
         acc["rel_residual_true"] = float(abs(R[n, n]) / torch.linalg.norm(b))
         del R
@@ -423,6 +429,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ne", action="store_true", help="skip the normal-equations baseline")
+    ap.add_argument("--cs-only", action="store_true", help="experiment mode: a step is cs_apply alone")
     ap.add_argument("--no-acc", action="store_true", help="skip the untimed accuracy checks")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)

@@ -272,36 +272,50 @@ static int tma_chunk_width(int ncols) {
 // transposes the tile into a row-major fp64 row buffer (sign applied), and lanes
 // 0..RB-1 each hand their row to the TMA engine as ONE cp.reduce.async.bulk .add.f64 of
 // cw*8 bytes into SA^T[h(row), c0:c0+cw].  cw is even for multi-chunk [A b] (16-B aligned).
-constexpr int kB2Warps = 8;
-constexpr int kB2Stages = 2;
 constexpr int kB2MaxCols = 66;
 
+// B2 pipeline shape: W warps per CTA, S TMA tile stages and R row buffers per warp.
+// A tile is consumed into registers right after its mbarrier completes, so its stage is
+// re-armed (next TMA issued) before the row-buffer stores; the row buffer written for
+// unit k is recycled once the bulk reduce of unit k-R has finished reading it.
+template <int W, int S, int R>
+struct B2Cfg {
+    static constexpr int kWarps = W, kStages = S, kRbufs = R;
+};
+
 template <typename T>
-__global__ void __launch_bounds__(kB2Warps * 32, 1) cs_bulk_tma_kernel(const __grid_constant__ CUtensorMap tmap,
-                                                                        const uint32_t* __restrict__ code,
-                                                                        int64_t rows, int ncols,
-                                                                        int stage_bytes, int ldrow,
-                                                                        double* __restrict__ SAt, RowLayout L) {
-    constexpr int RB = 128 / sizeof(T);   // rows per tile: 16 (fp64) / 32 (fp32)
+__host__ __device__ constexpr int b2_rows() { return 128 / (int)sizeof(T); }
+
+__host__ __device__ inline size_t b2_smem_bytes(int warps, int stages, int rbufs, int rb, int stage_bytes,
+                                                int ldrow) {
+    return (size_t)warps * stages * stage_bytes + (size_t)warps * rbufs * rb * ldrow * 8 +
+           (size_t)warps * stages * rb * 4 + (size_t)warps * stages * 8 + 1024;
+}
+
+template <typename T, typename C>
+__global__ void __launch_bounds__(C::kWarps * 32, 1) cs_bulk_tma_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                                         const uint32_t* __restrict__ code,
+                                                                         int64_t rows, int ncols, int stage_bytes,
+                                                                         int ldrow, double* __restrict__ SAt,
+                                                                         RowLayout L) {
+    constexpr int RB = b2_rows<T>();      // rows per tile: 16 (fp64) / 32 (fp32)
+    constexpr int NW = C::kWarps, NS = C::kStages, NR = C::kRbufs;
     const int cw = L.cw;
     extern __shared__ uint8_t b2_smem_raw[];
     uint8_t* smem = b2_smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(b2_smem_raw) & 1023u)) & 1023u);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // layout: [warps][stages] tiles | [warps] row buffers | [warps][stages][RB] codes | [warps][stages] mbarriers
-    uint8_t* ring = smem + (size_t)warp * kB2Stages * stage_bytes;
-    double* rowbuf = reinterpret_cast<double*>(smem + (size_t)kB2Warps * kB2Stages * stage_bytes) +
-                     (size_t)warp * RB * ldrow;
-    uint32_t* codes = reinterpret_cast<uint32_t*>(smem + (size_t)kB2Warps * kB2Stages * stage_bytes +
-                                                  (size_t)kB2Warps * RB * ldrow * 8) +
-                      warp * kB2Stages * RB;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(codes - warp * kB2Stages * RB) +
-                                                 (size_t)kB2Warps * kB2Stages * RB * 4) +
-                     warp * kB2Stages;
+    // layout: [NW][NS] tiles | [NW][NR] row buffers | [NW][NS][RB] codes | [NW][NS] mbarriers
+    uint8_t* ring = smem + (size_t)warp * NS * stage_bytes;
+    double* rowbufs = reinterpret_cast<double*>(smem + (size_t)NW * NS * stage_bytes) + (size_t)warp * NR * RB * ldrow;
+    uint32_t* codes_all =
+        reinterpret_cast<uint32_t*>(smem + (size_t)NW * NS * stage_bytes + (size_t)NW * NR * RB * ldrow * 8);
+    uint32_t* codes = codes_all + warp * NS * RB;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(codes_all + NW * NS * RB) + warp * NS;
     const int nchunks = (ncols + cw - 1) / cw;
     const int64_t ngroups = (rows + RB - 1) / RB;
     const int64_t nunits = ngroups * nchunks;
-    const int64_t gwarp = blockIdx.x * (int64_t)kB2Warps + warp;
-    const int64_t nwarps = (int64_t)gridDim.x * kB2Warps;
+    const int64_t gwarp = blockIdx.x * (int64_t)NW + warp;
+    const int64_t nwarps = (int64_t)gridDim.x * NW;
     const uint32_t tile_bytes = (uint32_t)cw * 128u;
     auto issue = [&](int64_t u, int s) {
         int64_t g;
@@ -312,71 +326,68 @@ __global__ void __launch_bounds__(kB2Warps * 32, 1) cs_bulk_tma_kernel(const __g
         bulk_load_1d(codes + s * RB, code + g * RB, RB * 4, &bars[s]);
     };
     if (lane == 0) {
-        for (int s = 0; s < kB2Stages; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int s = 0; s < kB2Stages; ++s)
+        for (int s = 0; s < NS; ++s)
             if (gwarp + s * nwarps < nunits) issue(gwarp + s * nwarps, s);
     }
-    for (int e = lane; e < RB * ldrow; e += 32) rowbuf[e] = 0.0;
+    for (int e = lane; e < NR * RB * ldrow; e += 32) rowbufs[e] = 0.0;
     __syncwarp();
     constexpr int kLanesPerRow = 32 / RB;   // 2 (fp64) / 1 (fp32)
+    constexpr int E = 16 / (int)sizeof(T);
+    constexpr int kStep = 128 * kLanesPerRow;                 // bytes between this lane's columns
+    constexpr int kPat = 8 / kLanesPerRow;                    // distinct (c & 7) values per lane
+    constexpr int kJ = kB2MaxCols / kLanesPerRow;
     const int rr = lane % RB, part = lane / RB;
+    // Column c of this lane's row lives at c*128 + (((rr / E) ^ (c & 7)) << 4) + (rr % E)*sizeof(T)
+    // (128B swizzle); with j unrolled, c & 7 is a compile-time pattern -> per-lane offsets.
+    int swz[kPat];
+#pragma unroll
+    for (int p = 0; p < kPat; ++p) swz[p] = (((rr / E) ^ ((p * kLanesPerRow + part) & 7)) << 4);
     for (int64_t k = 0;; ++k) {
         const int64_t u = gwarp + k * nwarps;
         if (u >= nunits) break;
-        const int s = (int)(k % kB2Stages);
+        const int s = (int)(k % NS);
         int64_t g;
         int ch;
         unit_coords(u, nchunks, ngroups, L.chunk_major, g, ch);
-        const int c0 = ch * cw;
-        const int nc = min(cw, ncols - c0);
+        const int nc = min(cw, ncols - ch * cw);
         const int nr = (int)min((int64_t)RB, rows - g * RB);
-        mbar_wait(&bars[s], (uint32_t)((k / kB2Stages) & 1));
+        mbar_wait(&bars[s], (uint32_t)((k / NS) & 1));
         const uint32_t cd = codes[s * RB + rr];
         const long long smask = (long long)code_sign_mask64(cd);
-        const uint8_t* tile = ring + s * stage_bytes;
-        // Transpose tile (column c = 128-B swizzled row) -> row-major rowbuf.  Column c of this
-        // lane's row lives at c*128 + (((rr / E) ^ (c & 7)) << 4) + (rr % E)*sizeof(T), E = 16/sizeof(T);
-        // with j unrolled, c & 7 is a compile-time pattern, so the 4 (fp64) / 8 (fp32) swizzled
-        // offsets are precomputed per lane and every access uses an immediate displacement.
-        constexpr int E = 16 / (int)sizeof(T);
-        constexpr int kStep = 128 * kLanesPerRow;                 // bytes between this lane's columns
-        constexpr int kPat = 8 / kLanesPerRow;                    // distinct (c & 7) values per lane
-        int swz[kPat];
-#pragma unroll
-        for (int p = 0; p < kPat; ++p) swz[p] = (((rr / E) ^ ((p * kLanesPerRow + part) & 7)) << 4);
-        const uint8_t* tb = tile + part * 128 + (rr % E) * (int)sizeof(T);
-        double* rb = rowbuf + rr * ldrow + part;
-        // all tile loads first (independent, in flight together), then the row-buffer stores
-        constexpr int kJ = kB2MaxCols / kLanesPerRow;
+        const uint8_t* tb = ring + s * stage_bytes + part * 128 + (rr % E) * (int)sizeof(T);
         double v[kJ];
 #pragma unroll
         for (int j = 0; j < kJ; ++j)
             v[j] = (j * kLanesPerRow + part < nc) ? (double)*reinterpret_cast<const T*>(tb + j * kStep + swz[j % kPat])
                                                   : 0.0;
-        // the row buffer is free once this lane's previous bulk reduce has read it
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        // tile consumed: re-arm this stage right away (generic reads -> async-proxy write)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
+        if (lane == 0 && u + NS * nwarps < nunits) issue(u + NS * nwarps, s);
+        // row buffer k % NR is free once the bulk reduce of unit k - NR has read it
+        if constexpr (NR == 1)
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        else
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+        double* rb = rowbufs + (size_t)(k % NR) * RB * ldrow + rr * ldrow;
 #pragma unroll
         for (int j = 0; j < kJ; ++j)
-            if (j * kLanesPerRow + part < nc) rb[j * kLanesPerRow] = __longlong_as_double(__double_as_longlong(v[j]) ^ smask);
-        if ((nc & 1) && part == 0) rowbuf[rr * ldrow + nc] = 0.0;   // 16-B padding column
-        // generic smem writes -> async proxy (bulk reduce source); tile reads -> next TMA write
+            if (j * kLanesPerRow + part < nc)
+                rb[j * kLanesPerRow + part] = __longlong_as_double(__double_as_longlong(v[j]) ^ smask);
+        if ((nc & 1) && part == 0) rb[nc] = 0.0;   // 16-B padding column
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (part == 0 && rr < nr) {
             const uint32_t bytes = (uint32_t)(((nc + 1) & ~1) * 8);
             double* dst = SAt + L.base(ch, code_bucket(cd));
-            const uint32_t src = (uint32_t)__cvta_generic_to_shared(rowbuf + rr * ldrow);
             asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(dst),
-                         "r"(src), "r"(bytes)
+                         "r"((uint32_t)__cvta_generic_to_shared(rb)), "r"(bytes)
                          : "memory");
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
-        if (lane == 0) {
-            const int64_t un = u + kB2Stages * nwarps;
-            if (un < nunits) issue(un, s);
-        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
@@ -388,15 +399,22 @@ static int b2_chunk_width(int ncols) {
 }
 
 // ------------------------------------------------------------------ variant B
-// A warp owns 16-row x cw-column tiles (cw <= 66: all of [A b] at C2).  Lanes
-// (r, half) load column pairs (two coalesced 128-B half-warp reads per
-// instruction), write the signed values row-major into a 16-B aligned smem row,
-// and lane r hands the whole row to the TMA engine as ONE bulk reduce-add
+// A warp owns 16-row x cw-column tiles (cw <= 66: all of [A b] at C2).  Lanes (r, half)
+// load column pairs (two coalesced 128-B half-warp reads per instruction, streaming
+// ld.global.cs), write the signed values row-major into a 16-B aligned smem row, and lane r
+// hands the whole row to the TMA engine as ONE bulk reduce-add
 // (cp.reduce.async.bulk ... .add.f64, cw*8 bytes) into SA^T[h(r), c0:c0+cw].
-// Two tile buffers per warp; cp.async.bulk.wait_group.read 1 recycles them.
-constexpr int kBulkWarps = 8;
+// BulkCfg<W, NB, PIPE>: W warps per CTA, NB smem tile buffers per warp (recycled with
+// cp.async.bulk.wait_group.read NB-1), PIPE = register double-buffering of the loads (the
+// next tile's loads are in flight while this tile is transposed and reduced).
 constexpr int kBulkRows = 16;
 constexpr int kBulkMaxCols = 66;
+
+template <int W, int NB, bool PIPE>
+struct BulkCfg {
+    static constexpr int kWarps = W, kBufs = NB;
+    static constexpr bool kPipe = PIPE;
+};
 
 __host__ __device__ inline int bulk_chunk_width(int ncols) {
     if (ncols <= kBulkMaxCols) return ncols;
@@ -405,40 +423,93 @@ __host__ __device__ inline int bulk_chunk_width(int ncols) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kBulkWarps * 32) cs_bulk_kernel(const uint32_t* __restrict__ code, int64_t rows,
-                                                                  Cols<T> cols, int ncols, int cw, int ldtile,
-                                                                  double* __restrict__ SAt, int64_t ldt) {
+__device__ __forceinline__ void bulk_load_tile(double (&v)[kBulkMaxCols / 2], const Cols<T>& cols, int ncols, int c0,
+                                               int nc, int half, int64_t rc) {
+#pragma unroll
+    for (int j = 0; j < kBulkMaxCols / 2; ++j) {
+        const int c = 2 * j + half;
+        const double x = (double)ldg_stream(cols.col(min(c0 + c, ncols - 1)) + rc);
+        v[j] = (c < nc) ? x : 0.0;
+    }
+}
+
+template <typename T, typename C, int EXP>
+__global__ void __launch_bounds__(C::kWarps * 32, 1) cs_bulk_kernel(const uint32_t* __restrict__ code, int64_t rows,
+                                                                     Cols<T> cols, int ncols, int cw, int ldtile,
+                                                                     double* __restrict__ SAt, int64_t ldt) {
+    // EXP: compile-time experiment switches for roofline attribution (0 in production):
+    // bit 0 = skip the bulk reduce, bit 1 = skip the A loads
+    constexpr int NB = C::kBufs;
     extern __shared__ __align__(16) double bulk_smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int half = lane >> 4, rr = lane & 15;
-    double* tiles = bulk_smem + (size_t)warp * 2 * kBulkRows * ldtile;
-    for (int e = lane; e < 2 * kBulkRows * ldtile; e += 32) tiles[e] = 0.0;
+    double* tiles = bulk_smem + (size_t)warp * NB * kBulkRows * ldtile;
+    for (int e = lane; e < NB * kBulkRows * ldtile; e += 32) tiles[e] = 0.0;
     __syncwarp();
     const int nchunks = (ncols + cw - 1) / cw;
     const int64_t ngroups = (rows + kBulkRows - 1) / kBulkRows;
     const int64_t nunits = ngroups * nchunks;
-    const int64_t gwarp = blockIdx.x * (int64_t)kBulkWarps + warp;
-    const int64_t nwarps = (int64_t)gridDim.x * kBulkWarps;
-    int buf = 0;
-    for (int64_t u = gwarp; u < nunits; u += nwarps) {
-        const int64_t g = u / nchunks;
-        const int ch = (int)(u - g * nchunks);
-        const int c0 = ch * cw;
-        const int nc = min(cw, ncols - c0);
+    const int64_t gwarp = blockIdx.x * (int64_t)C::kWarps + warp;
+    const int64_t nwarps = (int64_t)gridDim.x * C::kWarps;
+    auto coords = [&](int64_t u, int64_t& g, int& c0, int& nc, int64_t& rc, bool& valid) {
+        g = u / nchunks;
+        c0 = (int)(u - g * nchunks) * cw;
+        nc = min(cw, ncols - c0);
         const int64_t r = g * kBulkRows + rr;
-        const bool valid = r < rows;
-        const int64_t rc = valid ? r : rows - 1;
-        const uint32_t cd = __ldg(code + rc);
-        double* tile = tiles + buf * kBulkRows * ldtile;
-        double v[kBulkMaxCols / 2];
+        valid = r < rows;
+        rc = valid ? r : rows - 1;
+    };
+    double v[kBulkMaxCols / 2];
+    double vn[C::kPipe ? kBulkMaxCols / 2 : 1];
+    int buf = 0;
+    int64_t u = gwarp;
+    if (C::kPipe && u < nunits) {
+        int64_t g, rc;
+        int c0, nc;
+        bool valid;
+        coords(u, g, c0, nc, rc, valid);
+        if (EXP & 2) {
 #pragma unroll
-        for (int j = 0; j < kBulkMaxCols / 2; ++j) {
-            const int c = 2 * j + half;
-            const double x = (double)ldg_stream(cols.col(min(c0 + c, ncols - 1)) + rc);
-            v[j] = (c < nc) ? x : 0.0;
+            for (int j = 0; j < kBulkMaxCols / 2; ++j) v[j] = (double)(rc + j);
+        } else {
+            bulk_load_tile(v, cols, ncols, c0, nc, half, rc);
         }
-        // the TMA engine must be done reading this buffer (its bulk ops were committed 2 units ago)
-        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    }
+    for (; u < nunits; u += nwarps) {
+        int64_t g, rc;
+        int c0, nc;
+        bool valid;
+        coords(u, g, c0, nc, rc, valid);
+        const uint32_t cd = __ldg(code + rc);
+        if constexpr (C::kPipe) {
+            // next tile's loads go out before this tile is transposed and reduced
+            const int64_t un = u + nwarps;
+            if (un < nunits) {
+                int64_t gn, rcn;
+                int c0n, ncn;
+                bool validn;
+                coords(un, gn, c0n, ncn, rcn, validn);
+                if (EXP & 2) {
+#pragma unroll
+                    for (int j = 0; j < kBulkMaxCols / 2; ++j) vn[j] = (double)(rcn + j);
+                } else {
+                    bulk_load_tile(vn, cols, ncols, c0n, ncn, half, rcn);
+                }
+            }
+        } else {
+            if (EXP & 2) {
+#pragma unroll
+                for (int j = 0; j < kBulkMaxCols / 2; ++j) v[j] = (double)(rc + j);
+            } else {
+                bulk_load_tile(v, cols, ncols, c0, nc, half, rc);
+            }
+        }
+        double* tile = tiles + buf * kBulkRows * ldtile;
+        // the TMA engine must be done reading this buffer (its bulk ops were committed NB units ago)
+        if constexpr (NB == 1)
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        else
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         __syncwarp();
 #pragma unroll
         for (int j = 0; j < kBulkMaxCols / 2; ++j) {
@@ -448,7 +519,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32) cs_bulk_kernel(const uint32_t
         if ((nc & 1) && half == 0) tile[rr * ldtile + nc] = 0.0;   // 16-B padding column
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (half == 0 && valid) {
+        if (half == 0 && valid && !(EXP & 1)) {
             const uint32_t bytes = (uint32_t)(((nc + 1) & ~1) * 8);
             double* dst = SAt + (int64_t)code_bucket(cd) * ldt + c0;
             const uint32_t src = (uint32_t)__cvta_generic_to_shared(tile + rr * ldtile);
@@ -457,7 +528,11 @@ __global__ void __launch_bounds__(kBulkWarps * 32) cs_bulk_kernel(const uint32_t
                          : "memory");
         }
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        buf ^= 1;
+        if constexpr (C::kPipe) {
+#pragma unroll
+            for (int j = 0; j < kBulkMaxCols / 2; ++j) v[j] = vn[j];
+        }
+        buf = (buf + 1) % NB;
     }
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
@@ -719,31 +794,67 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
                 CUtensorMap tmap;
                 CSK_REQUIRE(make_tensor_map(&tmap, cols, rows, ncols, L.cw), CSK_ECUDA, "cuTensorMapEncodeTiled failed");
                 const int stage_bytes = (L.cw * 128 + 1023) & ~1023;
-                const size_t smem = (size_t)kB2Warps * kB2Stages * stage_bytes + (size_t)kB2Warps * RB * ldrow * 8 +
-                                    (size_t)kB2Warps * kB2Stages * RB * 4 + (size_t)kB2Warps * kB2Stages * 8 + 1024;
-                CSK_REQUIRE(smem <= (size_t)di.smem_optin, CSK_EUNSUPPORTED, "variant B: tile does not fit smem");
-                CSK_CUDA_TRY(cudaFuncSetAttribute(cs_bulk_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  (int)smem));
                 const int64_t units = ceil_div(rows, RB) * ceil_div(ncols, L.cw);
-                const int64_t blocks = std::min<int64_t>(ceil_div(units, kB2Warps), (int64_t)di.num_sms);
-                cs_bulk_tma_kernel<T><<<(unsigned)blocks, kB2Warps * 32, smem, st>>>(tmap, code, rows, ncols,
-                                                                                     stage_bytes, ldrow, out, L);
-                CSK_LAUNCH_CHECK();
-                return CSK_OK;
+                auto launch = [&](auto cfg) -> csk_status {
+                    using C = decltype(cfg);
+                    const size_t smem = b2_smem_bytes(C::kWarps, C::kStages, C::kRbufs, RB, stage_bytes, ldrow);
+                    if (smem > (size_t)di.smem_optin) return CSK_EUNSUPPORTED;
+                    CSK_CUDA_TRY(cudaFuncSetAttribute(cs_bulk_tma_kernel<T, C>,
+                                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                    const int64_t blocks = std::min<int64_t>(ceil_div(units, C::kWarps), (int64_t)di.num_sms);
+                    cs_bulk_tma_kernel<T, C><<<(unsigned)blocks, C::kWarps * 32, smem, st>>>(tmap, code, rows, ncols,
+                                                                                            stage_bytes, ldrow, out, L);
+                    CSK_LAUNCH_CHECK();
+                    return CSK_OK;
+                };
+                // pipeline shape (CSK_B2CFG for experiments; the default is the measured best at C2)
+                const char* e = std::getenv("CSK_B2CFG");
+                const int cfg = e ? std::atoi(e) : 1;
+                csk_status r = CSK_EUNSUPPORTED;
+                switch (cfg) {
+                    case 0: r = launch(B2Cfg<8, 2, 1>{}); break;
+                    case 2: r = launch(B2Cfg<8, 1, 2>{}); break;
+                    case 3: r = launch(B2Cfg<4, 3, 2>{}); break;
+                    case 4: r = launch(B2Cfg<12, 1, 1>{}); break;
+                    default: r = launch(B2Cfg<6, 2, 2>{}); break;
+                }
+                if (r == CSK_EUNSUPPORTED) r = launch(B2Cfg<4, 2, 1>{});   // wide tiles: smaller footprint
+                CSK_REQUIRE(r != CSK_EUNSUPPORTED, CSK_EUNSUPPORTED, "variant B: tile does not fit smem");
+                return r;
             }
             const int cw = bulk_chunk_width(ncols);
             const int ldtile = (cw + 1) & ~1;
-            const size_t smem = (size_t)kBulkWarps * 2 * kBulkRows * ldtile * sizeof(double);
             const int64_t units = ceil_div(rows, kBulkRows) * ceil_div(ncols, cw);
-            CSK_CUDA_TRY(cudaFuncSetAttribute(cs_bulk_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            int per_sm = 0;
-            CSK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cs_bulk_kernel<T>, kBulkWarps * 32, smem));
-            per_sm = std::max(per_sm, 1);
-            const int64_t blocks = std::min<int64_t>(ceil_div(units, kBulkWarps), (int64_t)di.num_sms * per_sm);
-            cs_bulk_kernel<T><<<(unsigned)blocks, kBulkWarps * 32, smem, st>>>(code, rows, cols, ncols, cw, ldtile, out,
-                                                                            ldo);
-            CSK_LAUNCH_CHECK();
-            return CSK_OK;
+            const char* ex = std::getenv("CSK_EXP");
+            const int expv = ex ? std::atoi(ex) : 0;
+            auto launch = [&](auto cfg) -> csk_status {
+                using C = decltype(cfg);
+                const size_t smem = (size_t)C::kWarps * C::kBufs * kBulkRows * ldtile * sizeof(double);
+                if (smem > (size_t)di.smem_optin) return CSK_EUNSUPPORTED;
+                auto kb = expv == 1 ? cs_bulk_kernel<T, C, 1>
+                          : expv == 2 ? cs_bulk_kernel<T, C, 2>
+                          : expv == 3 ? cs_bulk_kernel<T, C, 3> : cs_bulk_kernel<T, C, 0>;
+                CSK_CUDA_TRY(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                const int64_t blocks = std::min<int64_t>(ceil_div(units, C::kWarps), (int64_t)di.num_sms);
+                kb<<<(unsigned)blocks, C::kWarps * 32, smem, st>>>(code, rows, cols, ncols, cw, ldtile, out, ldo);
+                CSK_LAUNCH_CHECK();
+                return CSK_OK;
+            };
+            // pipeline shape (CSK_BCFG for experiments; default = measured best at C2)
+            const char* e = std::getenv("CSK_BCFG");
+            const int cfg = e ? std::atoi(e) : 0;
+            csk_status r = CSK_EUNSUPPORTED;
+            switch (cfg) {
+                case 1: r = launch(BulkCfg<12, 2, false>{}); break;
+                case 2: r = launch(BulkCfg<16, 1, false>{}); break;
+                case 3: r = launch(BulkCfg<8, 2, true>{}); break;
+                case 4: r = launch(BulkCfg<12, 1, true>{}); break;
+                case 5: r = launch(BulkCfg<16, 1, true>{}); break;
+                default: r = launch(BulkCfg<8, 2, false>{}); break;
+            }
+            if (r == CSK_EUNSUPPORTED) r = launch(BulkCfg<4, 2, false>{});
+            CSK_REQUIRE(r != CSK_EUNSUPPORTED, CSK_EUNSUPPORTED, "variant B: tile does not fit smem");
+            return r;
         }
         case CSK_VAR_ATOMIC_ROW: {
             const bool bulk = false;
