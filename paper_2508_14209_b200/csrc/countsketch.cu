@@ -537,6 +537,91 @@ __global__ void __launch_bounds__(C::kWarps * 32, 1) cs_bulk_kernel(const uint32
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// ------------------------------------------------------------ variant B, 32-row tiles
+// Same dataflow as cs_bulk_kernel with 32-row tiles and 16-byte loads: lane (p, half) loads
+// rows (2p, 2p+1) of column 2j+half as one double2, so every column segment is 256 B
+// contiguous (measured: 32-row tiles stream at 6.4 TB/s where 16-row tiles reach 4.8 TB/s
+// at the same occupancy, scripts/tile_read_bench.cu).  One tile buffer per warp; lane r
+// bulk-reduces row r.  fp64, 16-B aligned columns (lda even); the ragged last tile falls
+// back to clamped scalar loads.
+constexpr int kB32Rows = 32;
+
+template <int W, int EXP>
+__global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __restrict__ code, int64_t rows,
+                                                               Cols<double> cols, int ncols, int cw, int ldtile,
+                                                               double* __restrict__ SAt, int64_t ldt) {
+    extern __shared__ __align__(16) double b32_smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int p = lane & 15, half = lane >> 4;
+    double* tile = b32_smem + (size_t)warp * kB32Rows * ldtile;
+    for (int e = lane; e < kB32Rows * ldtile; e += 32) tile[e] = 0.0;
+    __syncwarp();
+    const int nchunks = (ncols + cw - 1) / cw;
+    const int64_t ngroups = (rows + kB32Rows - 1) / kB32Rows;
+    const int64_t nunits = ngroups * nchunks;
+    const int64_t gwarp = blockIdx.x * (int64_t)W + warp;
+    const int64_t nwarps = (int64_t)gridDim.x * W;
+    constexpr int kJ = kBulkMaxCols / 2;
+    for (int64_t u = gwarp; u < nunits; u += nwarps) {
+        const int64_t g = u / nchunks;
+        const int c0 = (int)(u - g * nchunks) * cw;
+        const int nc = min(cw, ncols - c0);
+        const int64_t r0 = g * kB32Rows;
+        const bool full = r0 + kB32Rows <= rows;
+        const int64_t ra = min(r0 + 2 * p, rows - 1), rb = min(r0 + 2 * p + 1, rows - 1);
+        const uint32_t ca = __ldg(code + ra), cb = __ldg(code + rb);
+        const uint32_t crow = __ldg(code + min(r0 + lane, rows - 1));
+        double2 v[kJ];
+        if (full) {
+#pragma unroll
+            for (int j = 0; j < kJ; ++j) {
+                const int c = 2 * j + half;
+                const double2 x = (EXP & 2) ? make_double2((double)ra, (double)c)
+                                            : __ldcs(reinterpret_cast<const double2*>(cols.col(min(c0 + c, ncols - 1)) + r0 + 2 * p));
+                v[j] = (c < nc) ? x : make_double2(0.0, 0.0);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < kJ; ++j) {
+                const int c = 2 * j + half;
+                const double* col = cols.col(min(c0 + c, ncols - 1));
+                const double xa = __ldcs(col + ra), xb = __ldcs(col + rb);
+                v[j] = (c < nc) ? make_double2(xa, r0 + 2 * p + 1 < rows ? xb : 0.0) : make_double2(0.0, 0.0);
+            }
+        }
+        // the TMA engine must have finished reading this tile (bulk ops of the previous unit)
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+        double* ta = tile + (2 * p) * ldtile;
+        double* tb = ta + ldtile;
+        const long long sa = (long long)code_sign_mask64(ca), sb = (long long)code_sign_mask64(cb);
+#pragma unroll
+        for (int j = 0; j < kJ; ++j) {
+            const int c = 2 * j + half;
+            if (c < nc) {
+                ta[c] = __longlong_as_double(__double_as_longlong(v[j].x) ^ sa);
+                tb[c] = __longlong_as_double(__double_as_longlong(v[j].y) ^ sb);
+            }
+        }
+        if ((nc & 1) && half == 0) {   // 16-B padding column
+            ta[nc] = 0.0;
+            tb[nc] = 0.0;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (r0 + lane < rows && !(EXP & 1)) {
+            const uint32_t bytes = (uint32_t)(((nc + 1) & ~1) * 8);
+            double* dst = SAt + (int64_t)code_bucket(crow) * ldt + c0;
+            const uint32_t src = (uint32_t)__cvta_generic_to_shared(tile + lane * ldtile);
+            asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(dst),
+                         "r"(src), "r"(bytes)
+                         : "memory");
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // SA^T (row-major workspace, fp64) -> SA (column-major, ldsa, T)
 template <typename T>
 __global__ void transpose_out_kernel(const double* __restrict__ SAt, RowLayout L, int64_t k1, int ncols,
@@ -724,7 +809,8 @@ static int select_variant(int64_t d, int64_t k1, int ncols, csk_dtype dtype, boo
     // L 6.3 ms, G 25 ms, S 38 ms
     (void)ncols;
     (void)k1;
-    return CSK_VAR_TMA_ROW;   // falls back to T when [A b] is not one uniformly strided tensor
+    // B: register-staged 32-row tiles + TMA bulk reduce-add (1.94 ms at C2)
+    return CSK_VAR_BULK_ROW;
 }
 
 // 2-D tensor map of [A b] (rows x ncols, column stride lda) with a RB x cw box, 128B swizzle
@@ -827,6 +913,36 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
             const int64_t units = ceil_div(rows, kBulkRows) * ceil_div(ncols, cw);
             const char* ex = std::getenv("CSK_EXP");
             const int expv = ex ? std::atoi(ex) : 0;
+            if constexpr (sizeof(T) == 8) {
+                // 32-row tiles with 16-B loads need every column 16-B aligned
+                const bool al = ((uintptr_t)cols.A & 15) == 0 && (cols.n <= 1 || (cols.lda & 1) == 0) &&
+                                (cols.b == nullptr || ((uintptr_t)cols.b & 15) == 0);
+                const char* w32 = std::getenv("CSK_B32");
+                const int b32 = w32 ? std::atoi(w32) : 8;   // warps per CTA, 0 = off
+                if (al && b32 > 0 && (cols.n > 0 || cols.b != nullptr)) {
+                    const int ld32 = ldtile % 4 == 0 ? ldtile + 2 : ldtile;   // == 2 mod 4
+                    const int64_t units32 = ceil_div(rows, kB32Rows) * ceil_div(ncols, cw);
+                    auto launch32 = [&](auto kern, int W) -> csk_status {
+                        const size_t smem = (size_t)W * kB32Rows * ld32 * sizeof(double);
+                        if (smem > (size_t)di.smem_optin) return CSK_EUNSUPPORTED;
+                        CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                        const int64_t blocks = std::min<int64_t>(ceil_div(units32, W), (int64_t)di.num_sms);
+                        kern<<<(unsigned)blocks, W * 32, smem, st>>>(code, rows, cols, ncols, cw, ld32, out, ldo);
+                        CSK_LAUNCH_CHECK();
+                        return CSK_OK;
+                    };
+                    csk_status r32;
+                    if (b32 == 6)
+                        r32 = expv == 1 ? launch32(cs_bulk32_kernel<6, 1>, 6)
+                              : expv == 2 ? launch32(cs_bulk32_kernel<6, 2>, 6) : launch32(cs_bulk32_kernel<6, 0>, 6);
+                    else if (b32 == 4)
+                        r32 = launch32(cs_bulk32_kernel<4, 0>, 4);
+                    else
+                        r32 = expv == 1 ? launch32(cs_bulk32_kernel<8, 1>, 8)
+                              : expv == 2 ? launch32(cs_bulk32_kernel<8, 2>, 8) : launch32(cs_bulk32_kernel<8, 0>, 8);
+                    if (r32 != CSK_EUNSUPPORTED) return r32;
+                }
+            }
             auto launch = [&](auto cfg) -> csk_status {
                 using C = decltype(cfg);
                 const size_t smem = (size_t)C::kWarps * C::kBufs * kBulkRows * ldtile * sizeof(double);
@@ -944,7 +1060,8 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
     // TMA eligibility of [A b] as one 2-D tensor (variants X and B)
     const size_t esz = dtype == CSK_F64 ? 8 : 4;
     const void* base = n > 0 ? A : b;
-    bool tma = variant == CSK_VAR_TMA_ROW || variant == CSK_VAR_BULK_ROW;
+    // X always loads with TMA; B only on request (CSK_B_TMA=1): its register-staged loads measured faster
+    bool tma = variant == CSK_VAR_TMA_ROW || (variant == CSK_VAR_BULK_ROW && std::getenv("CSK_B_TMA"));
     tma = tma && !std::getenv("CSK_NO_TMA") && (n == 0 || b == nullptr ||
                                                (const char*)b == (const char*)A + (size_t)n * lda * esz);
     tma = tma && ((uintptr_t)base & 15) == 0 && (ncols == 1 || ((lda * (int64_t)esz) & 15) == 0);
