@@ -39,6 +39,7 @@ struct RowLayout {
     int cw = 1;
     int64_t lc = 0, cs = 0;
     bool chunk_major = false;
+    bool tma = false;   // launch marked TMA-eligible by cs_apply_impl (variants X / B-with-TMA)
     __host__ __device__ int64_t base(int ch, uint32_t bucket) const { return (int64_t)ch * cs + (int64_t)bucket * lc; }
 };
 
@@ -435,11 +436,12 @@ __device__ __forceinline__ void bulk_load_tile(double (&v)[kBulkMaxCols / 2], co
 
 template <typename T, typename C, int EXP>
 __global__ void __launch_bounds__(C::kWarps * 32, 1) cs_bulk_kernel(const uint32_t* __restrict__ code, int64_t rows,
-                                                                     Cols<T> cols, int ncols, int cw, int ldtile,
-                                                                     double* __restrict__ SAt, int64_t ldt) {
+                                                                     Cols<T> cols, int ncols, int ldtile,
+                                                                     double* __restrict__ SAt, RowLayout L) {
     // EXP: compile-time experiment switches for roofline attribution (0 in production):
     // bit 0 = skip the bulk reduce, bit 1 = skip the A loads
     constexpr int NB = C::kBufs;
+    const int cw = L.cw;
     extern __shared__ __align__(16) double bulk_smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int half = lane >> 4, rr = lane & 15;
@@ -452,8 +454,9 @@ __global__ void __launch_bounds__(C::kWarps * 32, 1) cs_bulk_kernel(const uint32
     const int64_t gwarp = blockIdx.x * (int64_t)C::kWarps + warp;
     const int64_t nwarps = (int64_t)gridDim.x * C::kWarps;
     auto coords = [&](int64_t u, int64_t& g, int& c0, int& nc, int64_t& rc, bool& valid) {
-        g = u / nchunks;
-        c0 = (int)(u - g * nchunks) * cw;
+        int ch;
+        unit_coords(u, nchunks, ngroups, L.chunk_major, g, ch);
+        c0 = ch * cw;
         nc = min(cw, ncols - c0);
         const int64_t r = g * kBulkRows + rr;
         valid = r < rows;
@@ -521,7 +524,7 @@ __global__ void __launch_bounds__(C::kWarps * 32, 1) cs_bulk_kernel(const uint32
         __syncwarp();
         if (half == 0 && valid && !(EXP & 1)) {
             const uint32_t bytes = (uint32_t)(((nc + 1) & ~1) * 8);
-            double* dst = SAt + (int64_t)code_bucket(cd) * ldt + c0;
+            double* dst = SAt + L.base((int)(c0 / cw), code_bucket(cd));
             const uint32_t src = (uint32_t)__cvta_generic_to_shared(tile + rr * ldtile);
             asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(dst),
                          "r"(src), "r"(bytes)
@@ -548,8 +551,9 @@ constexpr int kB32Rows = 32;
 
 template <int W, int EXP>
 __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __restrict__ code, int64_t rows,
-                                                               Cols<double> cols, int ncols, int cw, int ldtile,
-                                                               double* __restrict__ SAt, int64_t ldt) {
+                                                               Cols<double> cols, int ncols, int ldtile,
+                                                               double* __restrict__ SAt, RowLayout L) {
+    const int cw = L.cw;
     extern __shared__ __align__(16) double b32_smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int p = lane & 15, half = lane >> 4;
@@ -563,8 +567,10 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
     const int64_t nwarps = (int64_t)gridDim.x * W;
     constexpr int kJ = kBulkMaxCols / 2;
     for (int64_t u = gwarp; u < nunits; u += nwarps) {
-        const int64_t g = u / nchunks;
-        const int c0 = (int)(u - g * nchunks) * cw;
+        int64_t g;
+        int ch;
+        unit_coords(u, nchunks, ngroups, L.chunk_major, g, ch);
+        const int c0 = ch * cw;
         const int nc = min(cw, ncols - c0);
         const int64_t r0 = g * kB32Rows;
         const bool full = r0 + kB32Rows <= rows;
@@ -611,7 +617,7 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
         __syncwarp();
         if (r0 + lane < rows && !(EXP & 1)) {
             const uint32_t bytes = (uint32_t)(((nc + 1) & ~1) * 8);
-            double* dst = SAt + (int64_t)code_bucket(crow) * ldt + c0;
+            double* dst = SAt + L.base(ch, code_bucket(crow));
             const uint32_t src = (uint32_t)__cvta_generic_to_shared(tile + lane * ldtile);
             asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(dst),
                          "r"(src), "r"(bytes)
@@ -838,7 +844,7 @@ static bool make_tensor_map(CUtensorMap* tmap, const Cols<T>& cols, int64_t rows
     return cr == CUDA_SUCCESS;
 }
 
-// For the row-scatter variants `out` is the SA^T workspace described by L (L.cs > 0 marks
+// For the row-scatter variants `out` is the SA^T workspace described by L (L.tma marks
 // a TMA-eligible launch decided by cs_apply_impl); the others write column-major (out, ldo).
 template <typename T>
 static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> cols, int64_t row_begin,
@@ -856,7 +862,7 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
         }
         case CSK_VAR_TMA_ROW: {
             constexpr int RB = 128 / sizeof(T);
-            CSK_REQUIRE(L.cs > 0, CSK_EINVAL, "variant X launched without a TMA layout");
+            CSK_REQUIRE(L.tma, CSK_EINVAL, "variant X launched without a TMA layout");
             CUtensorMap tmap;
             CSK_REQUIRE(make_tensor_map(&tmap, cols, rows, ncols, L.cw), CSK_ECUDA, "cuTensorMapEncodeTiled failed");
             const int stage_bytes = (L.cw * 128 + 1023) & ~1023;
@@ -871,7 +877,7 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
             return CSK_OK;
         }
         case CSK_VAR_BULK_ROW: {
-            if (L.cs > 0) {
+            if (L.tma) {
                 constexpr int RB = 128 / sizeof(T);
                 // even (16-B aligned rows) and == 2 mod 4: the 16 rows x 2 column-lanes of one
                 // STS hit every bank exactly twice (2 wavefronts, the minimum for 256 B)
@@ -908,7 +914,7 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
                 CSK_REQUIRE(r != CSK_EUNSUPPORTED, CSK_EUNSUPPORTED, "variant B: tile does not fit smem");
                 return r;
             }
-            const int cw = bulk_chunk_width(ncols);
+            const int cw = L.cw;   // bulk_chunk_width(ncols), set with the layout by cs_apply_impl
             const int ldtile = (cw + 1) & ~1;
             const int64_t units = ceil_div(rows, kBulkRows) * ceil_div(ncols, cw);
             const char* ex = std::getenv("CSK_EXP");
@@ -927,7 +933,7 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
                         if (smem > (size_t)di.smem_optin) return CSK_EUNSUPPORTED;
                         CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
                         const int64_t blocks = std::min<int64_t>(ceil_div(units32, W), (int64_t)di.num_sms);
-                        kern<<<(unsigned)blocks, W * 32, smem, st>>>(code, rows, cols, ncols, cw, ld32, out, ldo);
+                        kern<<<(unsigned)blocks, W * 32, smem, st>>>(code, rows, cols, ncols, ld32, out, L);
                         CSK_LAUNCH_CHECK();
                         return CSK_OK;
                     };
@@ -938,8 +944,10 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
                     else if (b32 == 4)
                         r32 = launch32(cs_bulk32_kernel<4, 0>, 4);
                     else
-                        r32 = expv == 1 ? launch32(cs_bulk32_kernel<8, 1>, 8)
-                              : expv == 2 ? launch32(cs_bulk32_kernel<8, 2>, 8) : launch32(cs_bulk32_kernel<8, 0>, 8);
+                        r32 = expv == 1   ? launch32(cs_bulk32_kernel<8, 1>, 8)
+                              : expv == 2 ? launch32(cs_bulk32_kernel<8, 2>, 8)
+                              : expv == 3 ? launch32(cs_bulk32_kernel<8, 3>, 8)
+                                          : launch32(cs_bulk32_kernel<8, 0>, 8);
                     if (r32 != CSK_EUNSUPPORTED) return r32;
                 }
             }
@@ -952,22 +960,13 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
                           : expv == 3 ? cs_bulk_kernel<T, C, 3> : cs_bulk_kernel<T, C, 0>;
                 CSK_CUDA_TRY(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
                 const int64_t blocks = std::min<int64_t>(ceil_div(units, C::kWarps), (int64_t)di.num_sms);
-                kb<<<(unsigned)blocks, C::kWarps * 32, smem, st>>>(code, rows, cols, ncols, cw, ldtile, out, ldo);
+                kb<<<(unsigned)blocks, C::kWarps * 32, smem, st>>>(code, rows, cols, ncols, ldtile, out, L);
                 CSK_LAUNCH_CHECK();
                 return CSK_OK;
             };
-            // pipeline shape (CSK_BCFG for experiments; default = measured best at C2)
-            const char* e = std::getenv("CSK_BCFG");
-            const int cfg = e ? std::atoi(e) : 0;
-            csk_status r = CSK_EUNSUPPORTED;
-            switch (cfg) {
-                case 1: r = launch(BulkCfg<12, 2, false>{}); break;
-                case 2: r = launch(BulkCfg<16, 1, false>{}); break;
-                case 3: r = launch(BulkCfg<8, 2, true>{}); break;
-                case 4: r = launch(BulkCfg<12, 1, true>{}); break;
-                case 5: r = launch(BulkCfg<16, 1, true>{}); break;
-                default: r = launch(BulkCfg<8, 2, false>{}); break;
-            }
+            // 16-row tiles (unaligned columns or fp32).  Measured at C2: 12/16 warps
+            // and register double-buffering (BulkCfg<.., .., true>) were not faster than 8 x 2.
+            csk_status r = launch(BulkCfg<8, 2, false>{});
             if (r == CSK_EUNSUPPORTED) r = launch(BulkCfg<4, 2, false>{});
             CSK_REQUIRE(r != CSK_EUNSUPPORTED, CSK_EUNSUPPORTED, "variant B: tile does not fit smem");
             return r;
@@ -1072,8 +1071,10 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
     RowLayout L;
     size_t ws_doubles = 0;
     if (variant_rowmajor(variant)) {
-        if (tma) {
-            L.cw = variant == CSK_VAR_BULK_ROW ? b2_chunk_width(ncols) : tma_chunk_width(ncols);
+        if (tma || variant == CSK_VAR_BULK_ROW) {
+            L.tma = tma;
+            L.cw = !tma ? bulk_chunk_width(ncols) : variant == CSK_VAR_BULK_ROW ? b2_chunk_width(ncols)
+                                                                                : tma_chunk_width(ncols);
             const int nchunks = (ncols + L.cw - 1) / L.cw;
             if (nchunks > 1 && (int64_t)k1 * ncols * 8 > (int64_t)device_info().l2_bytes / 2) {
                 L.chunk_major = true;                     // one L2-sized SA^T slice per column chunk
@@ -1086,9 +1087,9 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
                 ws_doubles = (size_t)k1 * L.lc;
             }
         } else {
-            L.cw = ncols;
+            L.cw = ncols;   // T (and L/S fallbacks): its own 32-column chunks, regular layout
             L.lc = (ncols + 3) & ~3;
-            L.cs = 0;
+            L.cs = ncols;
             ws_doubles = (size_t)k1 * L.lc;
         }
         tgt.ld = L.lc;
@@ -1124,8 +1125,7 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
     prof_mark(st, false);
     if (s == CSK_OK && tgt.owned) {
         if (variant_rowmajor(variant)) {
-            RowLayout Lt = L;
-            if (Lt.cs == 0) Lt.cs = Lt.cw;   // regular layout of the non-TMA kernels
+            const RowLayout& Lt = L;
             dim3 grid((unsigned)ceil_div(k1, 32), (unsigned)ceil_div(ncols, 32));
             if (dtype == CSK_F64)
                 transpose_out_kernel<double><<<grid, dim3(32, 8), 0, st>>>(tgt.buf, Lt, k1, ncols,

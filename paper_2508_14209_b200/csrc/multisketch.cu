@@ -10,6 +10,7 @@
 #include <cmath>
 #include <vector>
 
+#include <cooperative_groups.h>
 #include <cublas_v2.h>
 
 #include "csk_internal.cuh"
@@ -259,6 +260,154 @@ __global__ void __launch_bounds__(kQrThreads, 1) qr_solve_kernel(double* __restr
 }
 
 
+// Cluster-distributed Householder QR + back substitution.  Columns of Z are dealt
+// block-cyclically to the P CTAs of one thread-block cluster (column c lives in CTA c % P,
+// in shared memory).  Step j: the owner of column j forms v and beta from the norm its own
+// look-ahead produced, writes v (and beta) into every CTA's shared memory through DSMEM,
+// one cluster barrier, then every CTA updates its own columns c > j; the warp updating
+// column j+1 also accumulates its norm below the diagonal (look-ahead for the next owner).
+// R goes to global memory; CTA 0 checks the diagonal and back-substitutes with an 8-deep
+// register prefetch of R's columns.
+constexpr int kQrcThreads = 512;
+
+__global__ void __launch_bounds__(kQrcThreads, 1) qr_cluster_kernel(const double* __restrict__ Z, int64_t ldz, int m,
+                                                                   int nc, int P, double* __restrict__ Rg, int ldr,
+                                                                   double* __restrict__ x,
+                                                                   SolveStatus* __restrict__ status) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = P > 1 ? (int)cl.block_rank() : 0;
+    extern __shared__ double qc[];
+    double* vbuf = qc;            // [2][m]  Householder vectors (double-buffered by step parity)
+    double* scal = qc + 2 * m;    // [0..1] beta per buffer, [2] norm^2 of this CTA's next pivot
+    double* Wl = qc + 2 * m + 4;  // [ncl][m] local columns
+    const int ncl = (nc - rank + P - 1) / P;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int e = threadIdx.x; e < ncl * m; e += blockDim.x) {
+        const int t = e / m, i = e - t * m;
+        Wl[e] = Z[i + (int64_t)(rank + P * t) * ldz];
+    }
+    __syncthreads();
+    if (rank == 0 && warp == 0) {
+        double ss = 0.0;
+        for (int i = lane; i < m; i += 32) ss += Wl[i] * Wl[i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        if (lane == 0) scal[2] = ss;
+    }
+    __syncthreads();
+    for (int j = 0; j < nc; ++j) {
+        const int owner = j % P, buf = j & 1;
+        if (rank == owner) {
+            const double* wj = Wl + (int64_t)(j / P) * m;
+            const double x0 = wj[j];
+            const double nrm = sqrt(scal[2]);
+            const double alpha = nrm == 0.0 ? 0.0 : (x0 >= 0.0 ? -nrm : nrm);
+            const double beta = nrm == 0.0 ? 0.0 : 1.0 / (alpha * (alpha - x0));
+            const double v0 = x0 - alpha;
+            if (threadIdx.x == 0) Rg[j + (int64_t)j * ldr] = alpha;
+            const int len = m - j;
+            for (int e = threadIdx.x; e < P * len; e += blockDim.x) {
+                const int r = e / len, i = j + (e - r * len);
+                double* dst = P > 1 ? cl.map_shared_rank(vbuf, r) : vbuf;
+                dst[buf * m + i] = i == j ? v0 : wj[i];
+            }
+            if (threadIdx.x < P) {
+                double* ds = P > 1 ? cl.map_shared_rank(scal, (int)threadIdx.x) : scal;
+                ds[buf] = beta;
+            }
+        }
+        if (P > 1)
+            cl.sync();
+        else
+            __syncthreads();
+        const double* v = vbuf + buf * m;
+        const double beta = scal[buf];
+        const int t0 = j + 1 - rank > 0 ? (j + 1 - rank + P - 1) / P : 0;
+        {
+            for (int t = t0 + warp; t < ncl; t += nw) {
+                double* wc = Wl + (int64_t)t * m;
+                double dot = 0.0;
+                for (int i = j + lane; i < m; i += 32) dot += v[i] * wc[i];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+                const double f = beta * dot;
+                double ss = 0.0;
+                for (int i = j + lane; i < m; i += 32) {
+                    const double tv = wc[i] - f * v[i];
+                    wc[i] = tv;
+                    if (i > j) ss += tv * tv;
+                }
+                if (rank + P * t == j + 1) {
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+                    if (lane == 0) scal[2] = ss;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // strictly upper part of R to global (rows < c of local column c)
+    for (int t = 0; t < ncl; ++t) {
+        const int c = rank + P * t;
+        for (int i = threadIdx.x; i < c; i += blockDim.x) Rg[i + (int64_t)c * ldr] = Wl[(int64_t)t * m + i];
+    }
+    if (P > 1)
+        cl.sync();
+    else
+        __syncthreads();
+    if (rank != 0) return;
+    const int n = nc - 1;
+    double* diag = vbuf;          // reuse: nc
+    double* y = vbuf + nc;        // n
+    __shared__ int s_fail;
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) diag[i] = Rg[i + (int64_t)i * ldr];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) y[i] = Rg[i + (int64_t)n * ldr];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double rmax = 0.0;
+        for (int i = 0; i < n; ++i) rmax = fmax(rmax, fabs(diag[i]));
+        int stt = 0;
+        for (int i = 0; i < n; ++i)
+            if (!(fabs(diag[i]) > 1e-14 * rmax)) stt = CSK_ESINGULAR;
+        status->status = stt;
+        status->sk_resid = fabs(diag[n]);
+        s_fail = stt;
+    }
+    __syncthreads();
+    if (s_fail) return;
+    const int i = threadIdx.x;
+    if (n <= (int)blockDim.x) {
+        double ring[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int c = n - 1 - k;
+            ring[k] = (c >= 0 && i < c) ? Rg[i + (int64_t)c * ldr] : 0.0;
+        }
+        for (int cb = n - 1; cb >= 0; cb -= 8) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int c = cb - k;
+                if (c >= 0) {
+                    const double xc = y[c] / diag[c];
+                    if (i < c) y[i] -= ring[k] * xc;
+                    if (i == 0) x[c] = xc;
+                    const int cn = c - 8;
+                    ring[k] = (cn >= 0 && i < cn) ? Rg[i + (int64_t)cn * ldr] : 0.0;
+                    __syncthreads();
+                }
+            }
+        }
+    } else {
+        for (int c = n - 1; c >= 0; --c) {
+            const double xc = y[c] / diag[c];
+            for (int r = threadIdx.x; r < c; r += blockDim.x) y[r] -= Rg[r + (int64_t)c * ldr] * xc;
+            if (threadIdx.x == 0) x[c] = xc;
+            __syncthreads();
+        }
+    }
+}
+
 static csk_status solve_impl(int64_t k2, int64_t n, const double* Z, int64_t ldz, double* x, double* sk_resid,
                              cudaStream_t st, bool x_host) {
     CSK_REQUIRE(Z != nullptr && x != nullptr, CSK_EINVAL, "Z and x must be non-NULL");
@@ -273,8 +422,36 @@ static csk_status solve_impl(int64_t k2, int64_t n, const double* Z, int64_t ldz
     CSK_CUDA_TRY(cudaMallocAsync(&W, wbytes + 64 + (x_host ? n * 8 : 0), st));
     sd = reinterpret_cast<SolveStatus*>(reinterpret_cast<char*>(W) + wbytes);
     xd = x_host ? reinterpret_cast<double*>(reinterpret_cast<char*>(W) + wbytes + 64) : x;
-    CSK_CUDA_TRY(cudaMemcpy2DAsync(W, m * 8, Z, ldz * 8, m * 8, nc, cudaMemcpyDeviceToDevice, st));
     const DeviceInfo& di = device_info();
+    // cluster-distributed QR when a column slice fits shared memory on <= 8 CTAs
+    int P = 0;
+    for (int p = 1; p <= 8; p *= 2) {
+        const size_t need = (size_t)(2 * m + 4 + (size_t)((nc + p - 1) / p) * m) * 8;
+        if (need <= (size_t)di.smem_optin && p <= nc) {
+            P = p;
+            break;
+        }
+    }
+    if (P > 0 && !std::getenv("CSK_QR_SINGLE")) {
+        const size_t smem = (size_t)(2 * m + 4 + (size_t)((nc + P - 1) / P) * m) * 8;
+        CSK_CUDA_TRY(cudaFuncSetAttribute(qr_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(P);
+        cfg.blockDim = dim3(kQrcThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = P;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        // W doubles as the R output (ld = nc)
+        CSK_CUDA_TRY(cudaLaunchKernelEx(&cfg, qr_cluster_kernel, Z, (int64_t)ldz, m, nc, P, W, nc, xd, sd));
+        CSK_LAUNCH_CHECK();
+    } else {
+    CSK_CUDA_TRY(cudaMemcpy2DAsync(W, m * 8, Z, ldz * 8, m * 8, nc, cudaMemcpyDeviceToDevice, st));
     const size_t small = (size_t)(3 * nc + 2) * 8;
     const size_t smem_need = small + (size_t)m * nc * 8;
     const int use_smem = smem_need <= (size_t)di.smem_optin ? 1 : 0;
@@ -282,6 +459,7 @@ static csk_status solve_impl(int64_t k2, int64_t n, const double* Z, int64_t ldz
     CSK_CUDA_TRY(cudaFuncSetAttribute(qr_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     qr_solve_kernel<<<1, kQrThreads, smem, st>>>(W, m, nc, use_smem, xd, sd);
     CSK_LAUNCH_CHECK();
+    }
     SolveStatus hs;
     CSK_CUDA_TRY(cudaMemcpyAsync(&hs, sd, sizeof(hs), cudaMemcpyDeviceToHost, st));
     if (x_host) CSK_CUDA_TRY(cudaMemcpyAsync(x, xd, n * 8, cudaMemcpyDeviceToHost, st));
