@@ -202,6 +202,60 @@ def bench_reference(args, cfg):
     return 0
 
 
+# ---------------------------------------------------------- LS comparison
+def ls_compare(args, cfg, kappa, dev, stream):
+    """Multisketch sketch-and-solve (ms_apply + ms_solve, as in the step) vs the normal
+    equations on one [A b] of the cfg shape with condition number kappa; CUDA-event times
+    over args.steps calls each, relative residuals ||b - Ax|| / ||b|| against the QR optimum."""
+    import torch
+
+    import paper_2508_14209_b200 as csk
+    import synth
+
+    d, n, k1, k2 = cfg["d"], cfg["n"], cfg["k1"], cfg["k2"]
+    buf = synth.colmajor_empty(torch, d, n + 1, torch.float64, dev)
+    buf[:, :n] = synth.ill_conditioned_torch(d, n, kappa, seed=DATA_SEED, device=dev)
+    buf[:, n] = synth.rhs_torch(buf[:, :n], "easy", seed=DATA_SEED)
+    A, b = buf[:, :n], buf[:, n]
+    plan = csk.cs_plan(d, k1, SKETCH_SEED)
+    Z = synth.colmajor_empty(torch, k2, n + 1, torch.float64, dev)
+    x = torch.empty(n, dtype=torch.float64, device=dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def ms():
+        csk.ms_apply(plan, k2, A, b=b, Z=Z)
+        return csk.ms_solve(Z, n, x=x)[1]
+
+    def ne():
+        try:
+            csk.ne_lstsq(A, b, x=x)
+            return "OK"
+        except csk.CskError as e:
+            return str(e).split(":")[1].strip()
+
+    out = {"kappa": kappa, "workload": cfg["name"]}
+    for name, fn in (("ms", ms), ("ne", ne)):
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        res = [fn() for _ in range(args.steps)]
+        e1.record(stream)
+        torch.cuda.synchronize()
+        out[f"{name}_ms"] = e0.elapsed_time(e1) / args.steps
+        if name == "ne":
+            out["ne_status"] = res[-1]
+        fn()
+        out[f"{name}_rel_residual"] = float(torch.linalg.norm(b - A @ x) / torch.linalg.norm(b)) \
+            if (name == "ms" or res[-1] == "OK") else None
+    R = torch.linalg.qr(buf, mode="r")[1]
+    out["true_rel_residual"] = float(abs(R[n, n]) / torch.linalg.norm(b))
+    out["speedup_ms_vs_ne"] = out["ne_ms"] / out["ms_ms"]
+    del R, buf, A, b, Z
+    torch.cuda.empty_cache()
+    return out
+
+
 # ---------------------------------------------------------------- our arm
 def bench_ours(args, cfg):
     import numpy as np
@@ -416,6 +470,13 @@ def bench_ours(args, cfg):
         "speedup_vs_ne": (ne["ms"] / step_ms) if ne.get("ms") else None,
         "accuracy": acc,
     }
+    if ws == 1 and not args.no_ls and args.config == "c2":
+        # the least-squares comparison on BASELINE.json's C4 ([A b], d=2^23, n=128, k1=32768,
+        # k2=256): kappa = 1e10 (the BJ config: NE breaks down) and kappa = 1e2 (the
+        # paper's timing setup: both solvers accurate -> matched-accuracy speedup)
+        del buf, A, b, SA_ws, Z, x, SA
+        torch.cuda.empty_cache()
+        line["ls_c4"] = {f"kappa_{k:.0e}": ls_compare(args, CONFIGS["c4"], k, dev, stream) for k in (1e10, 1e2)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
@@ -436,6 +497,7 @@ def main():
     ap.add_argument("--no-ne", action="store_true", help="skip the normal-equations baseline")
     ap.add_argument("--cs-only", action="store_true", help="experiment mode: a step is cs_apply alone")
     ap.add_argument("--no-acc", action="store_true", help="skip the untimed accuracy checks")
+    ap.add_argument("--no-ls", action="store_true", help="skip the C4 least-squares comparison (N=1, c2)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cfg = CONFIGS[args.config]

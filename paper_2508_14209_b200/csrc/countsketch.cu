@@ -1076,7 +1076,10 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
             L.cw = !tma ? bulk_chunk_width(ncols) : variant == CSK_VAR_BULK_ROW ? b2_chunk_width(ncols)
                                                                                 : tma_chunk_width(ncols);
             const int nchunks = (ncols + L.cw - 1) / L.cw;
-            if (nchunks > 1 && (int64_t)k1 * ncols * 8 > (int64_t)device_info().l2_bytes / 2) {
+            // chunk-major once SA^T would take more than 1/cm_div of L2 (CSK_CM_DIV, default 2)
+            const char* cmd = std::getenv("CSK_CM_DIV");
+            const int64_t cm_div = cmd ? std::max(1, std::atoi(cmd)) : 2;
+            if (nchunks > 1 && (int64_t)k1 * ncols * 8 > (int64_t)device_info().l2_bytes / cm_div) {
                 L.chunk_major = true;                     // one L2-sized SA^T slice per column chunk
                 L.lc = (L.cw + 1) & ~1;
                 L.cs = k1 * L.lc;

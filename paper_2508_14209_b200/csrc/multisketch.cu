@@ -280,12 +280,13 @@ __global__ void __launch_bounds__(kQrcThreads, 1) qr_cluster_kernel(const double
     extern __shared__ double qc[];
     double* vbuf = qc;            // [2][m]  Householder vectors (double-buffered by step parity)
     double* scal = qc + 2 * m;    // [0..1] beta per buffer, [2] norm^2 of this CTA's next pivot
-    double* Wl = qc + 2 * m + 4;  // [ncl][m] local columns
+    double* Wl = qc + 2 * m + 4;  // [ncl][ldw] local columns; odd stride so column groups hit distinct banks
+    const int ldw = m | 1;
     const int ncl = (nc - rank + P - 1) / P;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int e = threadIdx.x; e < ncl * m; e += blockDim.x) {
         const int t = e / m, i = e - t * m;
-        Wl[e] = Z[i + (int64_t)(rank + P * t) * ldz];
+        Wl[t * ldw + i] = Z[i + (int64_t)(rank + P * t) * ldz];
     }
     __syncthreads();
     if (rank == 0 && warp == 0) {
@@ -299,49 +300,68 @@ __global__ void __launch_bounds__(kQrcThreads, 1) qr_cluster_kernel(const double
     for (int j = 0; j < nc; ++j) {
         const int owner = j % P, buf = j & 1;
         if (rank == owner) {
-            const double* wj = Wl + (int64_t)(j / P) * m;
+            const double* wj = Wl + (int64_t)(j / P) * ldw;
             const double x0 = wj[j];
             const double nrm = sqrt(scal[2]);
             const double alpha = nrm == 0.0 ? 0.0 : (x0 >= 0.0 ? -nrm : nrm);
             const double beta = nrm == 0.0 ? 0.0 : 1.0 / (alpha * (alpha - x0));
             const double v0 = x0 - alpha;
-            if (threadIdx.x == 0) Rg[j + (int64_t)j * ldr] = alpha;
-            const int len = m - j;
-            for (int e = threadIdx.x; e < P * len; e += blockDim.x) {
-                const int r = e / len, i = j + (e - r * len);
-                double* dst = P > 1 ? cl.map_shared_rank(vbuf, r) : vbuf;
-                dst[buf * m + i] = i == j ? v0 : wj[i];
+            if (threadIdx.x == 0) {
+                Rg[j + (int64_t)j * ldr] = alpha;
+                scal[buf] = beta;
             }
-            if (threadIdx.x < P) {
-                double* ds = P > 1 ? cl.map_shared_rank(scal, (int)threadIdx.x) : scal;
-                ds[buf] = beta;
+            for (int i = j + threadIdx.x; i < m; i += blockDim.x) vbuf[buf * m + i] = i == j ? v0 : wj[i];
+        }
+        if (P > 1) {
+            // every CTA pulls v and beta out of the owner's shared memory (DSMEM reads run in
+            // parallel on all P SMs; a push from the owner serialises on its DSMEM port)
+            cl.sync();
+            if (rank != owner) {
+                const double* src = cl.map_shared_rank(vbuf, owner) + buf * m;
+                for (int i = j + threadIdx.x; i < m; i += blockDim.x) vbuf[buf * m + i] = src[i];
+                if (threadIdx.x == 0) scal[buf] = cl.map_shared_rank(scal, owner)[buf];
             }
         }
-        if (P > 1)
-            cl.sync();
-        else
-            __syncthreads();
+        __syncthreads();
         const double* v = vbuf + buf * m;
         const double beta = scal[buf];
         const int t0 = j + 1 - rank > 0 ? (j + 1 - rank + P - 1) / P : 0;
-        {
-            for (int t = t0 + warp; t < ncl; t += nw) {
-                double* wc = Wl + (int64_t)t * m;
-                double dot = 0.0;
-                for (int i = j + lane; i < m; i += 32) dot += v[i] * wc[i];
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        const int nact = ncl - t0;   // trailing local columns
+        if (nact > 0) {
+            // G lanes per column (power of 2, <= 32), as many column groups as the block holds;
+            // lane g of a group takes rows j + g, j + g + G, ...  (all values warp-uniform)
+            int G = 32;
+            while (G > 1 && (int)(blockDim.x / G) < nact) G >>= 1;
+            const int ngrp = blockDim.x / G;
+            const int g = lane & (G - 1);
+            for (int base = 0; base < nact; base += ngrp) {   // block-uniform trip count (shuffles below)
+                const int grp = base + (int)(threadIdx.x / G);
+                const bool act = grp < nact;
+                const int t = t0 + (act ? grp : 0);
+                double* wc = Wl + (int64_t)t * ldw;
+                double d0 = 0.0, d1 = 0.0;
+                int i = j + g;
+                if (act) {
+                    for (; i + G < m; i += 2 * G) {
+                        d0 += v[i] * wc[i];
+                        d1 += v[i + G] * wc[i + G];
+                    }
+                    if (i < m) d0 += v[i] * wc[i];
+                }
+                double dot = d0 + d1;
+                for (int o = G >> 1; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
                 const double f = beta * dot;
                 double ss = 0.0;
-                for (int i = j + lane; i < m; i += 32) {
-                    const double tv = wc[i] - f * v[i];
-                    wc[i] = tv;
-                    if (i > j) ss += tv * tv;
+                if (act) {
+                    for (int r = j + g; r < m; r += G) {
+                        const double tv = wc[r] - f * v[r];
+                        wc[r] = tv;
+                        if (r > j) ss += tv * tv;
+                    }
                 }
-                if (rank + P * t == j + 1) {
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-                    if (lane == 0) scal[2] = ss;
+                if (__any_sync(0xffffffffu, act && rank + P * t == j + 1)) {
+                    for (int o = G >> 1; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+                    if (act && rank + P * t == j + 1 && g == 0) scal[2] = ss;
                 }
             }
         }
@@ -350,7 +370,7 @@ __global__ void __launch_bounds__(kQrcThreads, 1) qr_cluster_kernel(const double
     // strictly upper part of R to global (rows < c of local column c)
     for (int t = 0; t < ncl; ++t) {
         const int c = rank + P * t;
-        for (int i = threadIdx.x; i < c; i += blockDim.x) Rg[i + (int64_t)c * ldr] = Wl[(int64_t)t * m + i];
+        for (int i = threadIdx.x; i < c; i += blockDim.x) Rg[i + (int64_t)c * ldr] = Wl[(int64_t)t * ldw + i];
     }
     if (P > 1)
         cl.sync();
@@ -408,6 +428,243 @@ __global__ void __launch_bounds__(kQrcThreads, 1) qr_cluster_kernel(const double
     }
 }
 
+// Blocked (compact-WY) Householder QR over a thread-block cluster + back substitution.
+// Panels of kQbB columns are dealt block-cyclically to the P CTAs (shared memory).  Panel k:
+//  1. its owner factors it with ONE warp (warp-synchronous Householder: no block barrier per
+//     column), writing v_i (rows >= j0, explicit v0, zeros above its pivot) and beta_i;
+//  2. the owner forms T (upper triangular, H_1..H_b = I - V T V^T) from the Gram V^T V;
+//  3. one cluster barrier; the other CTAs pull V and T out of the owner's shared memory;
+//  4. every CTA applies Q^T = I - V T^T V^T to its trailing columns (warp per column).
+// One cluster barrier per panel instead of per column.
+constexpr int kQbB = 8;
+constexpr int kQbThreads = 512;
+
+__host__ __device__ inline size_t qb_smem_doubles(int m, int nc, int P) {
+    const int npan = (nc + kQbB - 1) / kQbB;
+    const int nlp = (npan + P - 1) / P;
+    return (size_t)nlp * kQbB * (m | 1) + 2 * (size_t)kQbB * m + 2 * kQbB * kQbB + 2 * kQbB + 8;
+}
+
+__global__ void __launch_bounds__(kQbThreads, 1) qr_blocked_kernel(const double* __restrict__ Z, int64_t ldz, int m,
+                                                                   int nc, int P, double* __restrict__ Rg, int ldr,
+                                                                   double* __restrict__ x,
+                                                                   SolveStatus* __restrict__ status) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = P > 1 ? (int)cl.block_rank() : 0;
+    constexpr int B = kQbB;
+    const int ldw = m | 1;
+    const int npan = (nc + B - 1) / B;
+    const int nlp = (npan - rank + P - 1) / P;   // local panels: global panel rank + P*lp
+    const int nlp_max = (npan + P - 1) / P;      // same shared-memory layout in every CTA (DSMEM mapping)
+    extern __shared__ double qb[];
+    double* Wl = qb;                                        // [nlp_max*B][ldw]
+    double* Vpub = Wl + (size_t)nlp_max * B * ldw;          // [B][m] published by the owner
+    double* Vloc = Vpub + (size_t)B * m;                    // [B][m] pulled copy
+    double* Tpub = Vloc + (size_t)B * m;                    // [B][B] column-major, upper
+    double* Tloc = Tpub + B * B;
+    double* betas = Tloc + B * B;                           // [B]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __shared__ double s_gram[B * B];
+    for (int e = threadIdx.x; e < nlp * B * m; e += blockDim.x) {
+        const int lc = e / m, r = e - lc * m;
+        const int gcol = (rank + P * (lc / B)) * B + (lc % B);
+        Wl[(size_t)lc * ldw + r] = gcol < nc ? Z[r + (int64_t)gcol * ldz] : 0.0;
+    }
+    __syncthreads();
+    for (int k = 0; k < npan; ++k) {
+        const int owner = k % P, j0 = k * B, bw = min(B, nc - j0);
+        if (rank == owner) {
+            double* pc = Wl + (size_t)(k / P) * B * ldw;   // this panel's B local columns
+            if (warp == 0) {
+                for (int i = 0; i < bw; ++i) {
+                    double* col = pc + (size_t)i * ldw;
+                    const int j = j0 + i;
+                    double ss = 0.0;
+                    for (int r = j + lane; r < m; r += 32) ss += col[r] * col[r];
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+                    const double x0 = col[j];
+                    const double nrm = sqrt(ss);
+                    const double alpha = nrm == 0.0 ? 0.0 : (x0 >= 0.0 ? -nrm : nrm);
+                    const double beta = nrm == 0.0 ? 0.0 : 1.0 / (alpha * (alpha - x0));
+                    const double v0 = x0 - alpha;
+                    double* vp = Vpub + (size_t)i * m;
+                    for (int r = j0 + lane; r < m; r += 32) vp[r] = r < j ? 0.0 : (r == j ? v0 : col[r]);
+                    __syncwarp();
+                    // apply H_i to the panel's remaining columns (dots batched, then updates)
+                    double dot[B];
+#pragma unroll
+                    for (int c = 0; c < B; ++c) dot[c] = 0.0;
+                    for (int r = j + lane; r < m; r += 32) {
+                        const double vr = vp[r];
+#pragma unroll
+                        for (int c = 0; c < B; ++c)
+                            if (c > i && c < bw) dot[c] += vr * pc[(size_t)c * ldw + r];
+                    }
+#pragma unroll
+                    for (int c = 0; c < B; ++c) {
+                        if (c > i && c < bw) {
+#pragma unroll
+                            for (int o = 16; o > 0; o >>= 1) dot[c] += __shfl_xor_sync(0xffffffffu, dot[c], o);
+                        }
+                    }
+                    for (int r = j + lane; r < m; r += 32) {
+                        const double vr = vp[r];
+#pragma unroll
+                        for (int c = 0; c < B; ++c)
+                            if (c > i && c < bw) pc[(size_t)c * ldw + r] -= beta * dot[c] * vr;
+                    }
+                    if (lane == 0) {
+                        col[j] = alpha;   // R[j][j]
+                        betas[i] = beta;
+                        Rg[j + (int64_t)j * ldr] = alpha;
+                    }
+                    __syncwarp();
+                }
+                for (int i = bw + lane; i < B; i += 32) betas[i] = 0.0;
+                for (int e = lane; e < (B - bw) * m; e += 32) Vpub[(size_t)bw * m + e] = 0.0;
+            }
+            __syncthreads();
+            // Gram V^T V (rows >= j0), one warp per entry (i <= l)
+            for (int q = warp; q < B * B; q += nw) {
+                const int i = q % B, l = q / B;
+                if (i > l) continue;
+                double s = 0.0;
+                for (int r = j0 + lane; r < m; r += 32) s += Vpub[(size_t)i * m + r] * Vpub[(size_t)l * m + r];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                if (lane == 0) s_gram[i + l * B] = s;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                // T[:, l] = [-beta_l T[0:l,0:l] G[0:l, l] ; beta_l]   (LAPACK larft, forward, columnwise)
+                for (int l = 0; l < B; ++l) {
+                    for (int i = 0; i < B; ++i) Tpub[i + l * B] = 0.0;
+                    for (int i = 0; i < l; ++i) {
+                        double s = 0.0;
+                        for (int p = i; p < l; ++p) s += Tpub[i + p * B] * s_gram[p + l * B];
+                        Tpub[i + l * B] = -betas[l] * s;
+                    }
+                    Tpub[l + l * B] = betas[l];
+                }
+            }
+        }
+        if (P > 1) {
+            cl.sync();
+            if (rank != owner) {
+                const double* vs = cl.map_shared_rank(Vpub, owner);
+                for (int e = threadIdx.x; e < B * (m - j0); e += blockDim.x) {
+                    const int i = e / (m - j0), r = j0 + (e - i * (m - j0));
+                    Vloc[(size_t)i * m + r] = vs[(size_t)i * m + r];
+                }
+                const double* ts = cl.map_shared_rank(Tpub, owner);
+                for (int e = threadIdx.x; e < B * B; e += blockDim.x) Tloc[e] = ts[e];
+            }
+        }
+        __syncthreads();
+        const double* V = rank == owner ? Vpub : Vloc;
+        const double* T = rank == owner ? Tpub : Tloc;
+        // trailing local panels: global panel index > k
+        const int lp0 = k - rank >= 0 ? (k - rank) / P + 1 : 0;
+        const int ntrail = (nlp - lp0) * B;
+        for (int q = warp; q < ntrail; q += nw) {
+            const int lc = lp0 * B + q;
+            const int gcol = (rank + P * (lc / B)) * B + (lc % B);
+            if (gcol >= nc) continue;
+            double* C = Wl + (size_t)lc * ldw;
+            double y[B];
+#pragma unroll
+            for (int i = 0; i < B; ++i) y[i] = 0.0;
+            for (int r = j0 + lane; r < m; r += 32) {
+                const double cr = C[r];
+#pragma unroll
+                for (int i = 0; i < B; ++i) y[i] += V[(size_t)i * m + r] * cr;
+            }
+#pragma unroll
+            for (int i = 0; i < B; ++i) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) y[i] += __shfl_xor_sync(0xffffffffu, y[i], o);
+            }
+            double w[B];   // w = T^T y
+#pragma unroll
+            for (int i = 0; i < B; ++i) {
+                double s = 0.0;
+#pragma unroll
+                for (int l = 0; l <= i; ++l) s += T[l + i * B] * y[l];
+                w[i] = s;
+            }
+            for (int r = j0 + lane; r < m; r += 32) {
+                double cr = C[r];
+#pragma unroll
+                for (int i = 0; i < B; ++i) cr -= V[(size_t)i * m + r] * w[i];
+                C[r] = cr;
+            }
+        }
+        __syncthreads();
+    }
+    // R (upper part of every local column; rows < its global index, diagonal already in Rg)
+    for (int lc = 0; lc < nlp * B; ++lc) {
+        const int gcol = (rank + P * (lc / B)) * B + (lc % B);
+        if (gcol >= nc) continue;
+        for (int r = threadIdx.x; r < gcol; r += blockDim.x) Rg[r + (int64_t)gcol * ldr] = Wl[(size_t)lc * ldw + r];
+    }
+    if (P > 1)
+        cl.sync();
+    else
+        __syncthreads();
+    if (rank != 0) return;
+    const int n = nc - 1;
+    double* diag = Vpub;       // reuse: nc (<= B*m)
+    double* yv = Vloc;         // n
+    __shared__ int s_fail;
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) diag[i] = Rg[i + (int64_t)i * ldr];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) yv[i] = Rg[i + (int64_t)n * ldr];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double rmax = 0.0;
+        for (int i = 0; i < n; ++i) rmax = fmax(rmax, fabs(diag[i]));
+        int stt = 0;
+        for (int i = 0; i < n; ++i)
+            if (!(fabs(diag[i]) > 1e-14 * rmax)) stt = CSK_ESINGULAR;
+        status->status = stt;
+        status->sk_resid = fabs(diag[n]);
+        s_fail = stt;
+    }
+    __syncthreads();
+    if (s_fail) return;
+    const int i = threadIdx.x;
+    if (n <= (int)blockDim.x) {
+        double ring[8];
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            const int c = n - 1 - kk;
+            ring[kk] = (c >= 0 && i < c) ? Rg[i + (int64_t)c * ldr] : 0.0;
+        }
+        for (int cb = n - 1; cb >= 0; cb -= 8) {
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+                const int c = cb - kk;
+                if (c >= 0) {
+                    const double xc = yv[c] / diag[c];
+                    if (i < c) yv[i] -= ring[kk] * xc;
+                    if (i == 0) x[c] = xc;
+                    const int cn = c - 8;
+                    ring[kk] = (cn >= 0 && i < cn) ? Rg[i + (int64_t)cn * ldr] : 0.0;
+                    __syncthreads();
+                }
+            }
+        }
+    } else {
+        for (int c = n - 1; c >= 0; --c) {
+            const double xc = yv[c] / diag[c];
+            for (int r = threadIdx.x; r < c; r += blockDim.x) yv[r] -= Rg[r + (int64_t)c * ldr] * xc;
+            if (threadIdx.x == 0) x[c] = xc;
+            __syncthreads();
+        }
+    }
+}
+
 static csk_status solve_impl(int64_t k2, int64_t n, const double* Z, int64_t ldz, double* x, double* sk_resid,
                              cudaStream_t st, bool x_host) {
     CSK_REQUIRE(Z != nullptr && x != nullptr, CSK_EINVAL, "Z and x must be non-NULL");
@@ -423,17 +680,51 @@ static csk_status solve_impl(int64_t k2, int64_t n, const double* Z, int64_t ldz
     sd = reinterpret_cast<SolveStatus*>(reinterpret_cast<char*>(W) + wbytes);
     xd = x_host ? reinterpret_cast<double*>(reinterpret_cast<char*>(W) + wbytes + 64) : x;
     const DeviceInfo& di = device_info();
-    // cluster-distributed QR when a column slice fits shared memory on <= 8 CTAs
+    // blocked (compact-WY) cluster QR: smallest cluster (<= 16 CTAs) whose column slices fit
+    {
+        int Pb = 0;
+        for (int p = 1; p <= 16; p *= 2)
+            if (qb_smem_doubles(m, nc, p) * 8 <= (size_t)di.smem_optin) {
+                Pb = p;
+                break;
+            }
+        if (const char* e = std::getenv("CSK_QR_P")) Pb = std::max(Pb, std::atoi(e));
+        const int npan = (nc + kQbB - 1) / kQbB;
+        if (Pb > npan) Pb = 0;
+        if (Pb > 0 && !std::getenv("CSK_QR_UNBLOCKED")) {
+            const size_t smem = qb_smem_doubles(m, nc, Pb) * 8;
+            CSK_CUDA_TRY(cudaFuncSetAttribute(qr_blocked_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            if (Pb > 8)
+                CSK_CUDA_TRY(cudaFuncSetAttribute(qr_blocked_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(Pb);
+            cfg.blockDim = dim3(kQbThreads);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = Pb;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            CSK_CUDA_TRY(cudaLaunchKernelEx(&cfg, qr_blocked_kernel, Z, (int64_t)ldz, m, nc, Pb, W, nc, xd, sd));
+            CSK_LAUNCH_CHECK();
+            goto launched;
+        }
+    }
+    {
+    // cluster-distributed unblocked QR when a column slice fits shared memory on <= 8 CTAs
     int P = 0;
     for (int p = 1; p <= 8; p *= 2) {
-        const size_t need = (size_t)(2 * m + 4 + (size_t)((nc + p - 1) / p) * m) * 8;
+        const size_t need = (size_t)(2 * m + 4 + (size_t)((nc + p - 1) / p) * (m | 1)) * 8;
         if (need <= (size_t)di.smem_optin && p <= nc) {
             P = p;
             break;
         }
     }
     if (P > 0 && !std::getenv("CSK_QR_SINGLE")) {
-        const size_t smem = (size_t)(2 * m + 4 + (size_t)((nc + P - 1) / P) * m) * 8;
+        const size_t smem = (size_t)(2 * m + 4 + (size_t)((nc + P - 1) / P) * (m | 1)) * 8;
         CSK_CUDA_TRY(cudaFuncSetAttribute(qr_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(P);
@@ -460,6 +751,8 @@ static csk_status solve_impl(int64_t k2, int64_t n, const double* Z, int64_t ldz
     qr_solve_kernel<<<1, kQrThreads, smem, st>>>(W, m, nc, use_smem, xd, sd);
     CSK_LAUNCH_CHECK();
     }
+    }
+launched:
     SolveStatus hs;
     CSK_CUDA_TRY(cudaMemcpyAsync(&hs, sd, sizeof(hs), cudaMemcpyDeviceToHost, st));
     if (x_host) CSK_CUDA_TRY(cudaMemcpyAsync(x, xd, n * 8, cudaMemcpyDeviceToHost, st));
