@@ -137,4 +137,13 @@ csk_status blas_handle(cudaStream_t st, struct cublasContext** h);
 
 bool is_device_pointer(const void* p);
 
+// small-solve status written by the solve kernels (multisketch.cu, qr_wy.cu)
+struct SolveStatus {
+    int status;
+    double sk_resid;
+};
+csk_status qr_wy_launch(const double* Z, int64_t ldz, int m, int nc, double* Rg, int ldr, double* scratch,
+                        double* x, SolveStatus* status, cudaStream_t st, bool* launched);
+size_t qr_wy_scratch_doubles(int m, int nc);
+
 }  // namespace csk

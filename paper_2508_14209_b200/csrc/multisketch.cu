@@ -169,11 +169,6 @@ static csk_status sketch_host_rows(csk_plan_t plan, int64_t n, const double* A, 
 // per column: every thread recomputes alpha and beta = 2/(v^T v) = 1/(alpha (alpha - x0))
 // from the column's norm^2, which the warp updating column j+1 accumulates during step j
 // (look-ahead).  Back substitution by one warp.
-struct SolveStatus {
-    int status;
-    double sk_resid;
-};
-
 constexpr int kQrThreads = 512;
 
 __global__ void __launch_bounds__(kQrThreads, 1) qr_solve_kernel(double* __restrict__ Wg, int m, int nc,
@@ -428,243 +423,6 @@ __global__ void __launch_bounds__(kQrcThreads, 1) qr_cluster_kernel(const double
     }
 }
 
-// Blocked (compact-WY) Householder QR over a thread-block cluster + back substitution.
-// Panels of kQbB columns are dealt block-cyclically to the P CTAs (shared memory).  Panel k:
-//  1. its owner factors it with ONE warp (warp-synchronous Householder: no block barrier per
-//     column), writing v_i (rows >= j0, explicit v0, zeros above its pivot) and beta_i;
-//  2. the owner forms T (upper triangular, H_1..H_b = I - V T V^T) from the Gram V^T V;
-//  3. one cluster barrier; the other CTAs pull V and T out of the owner's shared memory;
-//  4. every CTA applies Q^T = I - V T^T V^T to its trailing columns (warp per column).
-// One cluster barrier per panel instead of per column.
-constexpr int kQbB = 8;
-constexpr int kQbThreads = 512;
-
-__host__ __device__ inline size_t qb_smem_doubles(int m, int nc, int P) {
-    const int npan = (nc + kQbB - 1) / kQbB;
-    const int nlp = (npan + P - 1) / P;
-    return (size_t)nlp * kQbB * (m | 1) + 2 * (size_t)kQbB * m + 2 * kQbB * kQbB + 2 * kQbB + 8;
-}
-
-__global__ void __launch_bounds__(kQbThreads, 1) qr_blocked_kernel(const double* __restrict__ Z, int64_t ldz, int m,
-                                                                   int nc, int P, double* __restrict__ Rg, int ldr,
-                                                                   double* __restrict__ x,
-                                                                   SolveStatus* __restrict__ status) {
-    namespace cg = cooperative_groups;
-    cg::cluster_group cl = cg::this_cluster();
-    const int rank = P > 1 ? (int)cl.block_rank() : 0;
-    constexpr int B = kQbB;
-    const int ldw = m | 1;
-    const int npan = (nc + B - 1) / B;
-    const int nlp = (npan - rank + P - 1) / P;   // local panels: global panel rank + P*lp
-    const int nlp_max = (npan + P - 1) / P;      // same shared-memory layout in every CTA (DSMEM mapping)
-    extern __shared__ double qb[];
-    double* Wl = qb;                                        // [nlp_max*B][ldw]
-    double* Vpub = Wl + (size_t)nlp_max * B * ldw;          // [B][m] published by the owner
-    double* Vloc = Vpub + (size_t)B * m;                    // [B][m] pulled copy
-    double* Tpub = Vloc + (size_t)B * m;                    // [B][B] column-major, upper
-    double* Tloc = Tpub + B * B;
-    double* betas = Tloc + B * B;                           // [B]
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    __shared__ double s_gram[B * B];
-    for (int e = threadIdx.x; e < nlp * B * m; e += blockDim.x) {
-        const int lc = e / m, r = e - lc * m;
-        const int gcol = (rank + P * (lc / B)) * B + (lc % B);
-        Wl[(size_t)lc * ldw + r] = gcol < nc ? Z[r + (int64_t)gcol * ldz] : 0.0;
-    }
-    __syncthreads();
-    for (int k = 0; k < npan; ++k) {
-        const int owner = k % P, j0 = k * B, bw = min(B, nc - j0);
-        if (rank == owner) {
-            double* pc = Wl + (size_t)(k / P) * B * ldw;   // this panel's B local columns
-            if (warp == 0) {
-                for (int i = 0; i < bw; ++i) {
-                    double* col = pc + (size_t)i * ldw;
-                    const int j = j0 + i;
-                    double ss = 0.0;
-                    for (int r = j + lane; r < m; r += 32) ss += col[r] * col[r];
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-                    const double x0 = col[j];
-                    const double nrm = sqrt(ss);
-                    const double alpha = nrm == 0.0 ? 0.0 : (x0 >= 0.0 ? -nrm : nrm);
-                    const double beta = nrm == 0.0 ? 0.0 : 1.0 / (alpha * (alpha - x0));
-                    const double v0 = x0 - alpha;
-                    double* vp = Vpub + (size_t)i * m;
-                    for (int r = j0 + lane; r < m; r += 32) vp[r] = r < j ? 0.0 : (r == j ? v0 : col[r]);
-                    __syncwarp();
-                    // apply H_i to the panel's remaining columns (dots batched, then updates)
-                    double dot[B];
-#pragma unroll
-                    for (int c = 0; c < B; ++c) dot[c] = 0.0;
-                    for (int r = j + lane; r < m; r += 32) {
-                        const double vr = vp[r];
-#pragma unroll
-                        for (int c = 0; c < B; ++c)
-                            if (c > i && c < bw) dot[c] += vr * pc[(size_t)c * ldw + r];
-                    }
-#pragma unroll
-                    for (int c = 0; c < B; ++c) {
-                        if (c > i && c < bw) {
-#pragma unroll
-                            for (int o = 16; o > 0; o >>= 1) dot[c] += __shfl_xor_sync(0xffffffffu, dot[c], o);
-                        }
-                    }
-                    for (int r = j + lane; r < m; r += 32) {
-                        const double vr = vp[r];
-#pragma unroll
-                        for (int c = 0; c < B; ++c)
-                            if (c > i && c < bw) pc[(size_t)c * ldw + r] -= beta * dot[c] * vr;
-                    }
-                    if (lane == 0) {
-                        col[j] = alpha;   // R[j][j]
-                        betas[i] = beta;
-                        Rg[j + (int64_t)j * ldr] = alpha;
-                    }
-                    __syncwarp();
-                }
-                for (int i = bw + lane; i < B; i += 32) betas[i] = 0.0;
-                for (int e = lane; e < (B - bw) * m; e += 32) Vpub[(size_t)bw * m + e] = 0.0;
-            }
-            __syncthreads();
-            // Gram V^T V (rows >= j0), one warp per entry (i <= l)
-            for (int q = warp; q < B * B; q += nw) {
-                const int i = q % B, l = q / B;
-                if (i > l) continue;
-                double s = 0.0;
-                for (int r = j0 + lane; r < m; r += 32) s += Vpub[(size_t)i * m + r] * Vpub[(size_t)l * m + r];
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-                if (lane == 0) s_gram[i + l * B] = s;
-            }
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                // T[:, l] = [-beta_l T[0:l,0:l] G[0:l, l] ; beta_l]   (LAPACK larft, forward, columnwise)
-                for (int l = 0; l < B; ++l) {
-                    for (int i = 0; i < B; ++i) Tpub[i + l * B] = 0.0;
-                    for (int i = 0; i < l; ++i) {
-                        double s = 0.0;
-                        for (int p = i; p < l; ++p) s += Tpub[i + p * B] * s_gram[p + l * B];
-                        Tpub[i + l * B] = -betas[l] * s;
-                    }
-                    Tpub[l + l * B] = betas[l];
-                }
-            }
-        }
-        if (P > 1) {
-            cl.sync();
-            if (rank != owner) {
-                const double* vs = cl.map_shared_rank(Vpub, owner);
-                for (int e = threadIdx.x; e < B * (m - j0); e += blockDim.x) {
-                    const int i = e / (m - j0), r = j0 + (e - i * (m - j0));
-                    Vloc[(size_t)i * m + r] = vs[(size_t)i * m + r];
-                }
-                const double* ts = cl.map_shared_rank(Tpub, owner);
-                for (int e = threadIdx.x; e < B * B; e += blockDim.x) Tloc[e] = ts[e];
-            }
-        }
-        __syncthreads();
-        const double* V = rank == owner ? Vpub : Vloc;
-        const double* T = rank == owner ? Tpub : Tloc;
-        // trailing local panels: global panel index > k
-        const int lp0 = k - rank >= 0 ? (k - rank) / P + 1 : 0;
-        const int ntrail = (nlp - lp0) * B;
-        for (int q = warp; q < ntrail; q += nw) {
-            const int lc = lp0 * B + q;
-            const int gcol = (rank + P * (lc / B)) * B + (lc % B);
-            if (gcol >= nc) continue;
-            double* C = Wl + (size_t)lc * ldw;
-            double y[B];
-#pragma unroll
-            for (int i = 0; i < B; ++i) y[i] = 0.0;
-            for (int r = j0 + lane; r < m; r += 32) {
-                const double cr = C[r];
-#pragma unroll
-                for (int i = 0; i < B; ++i) y[i] += V[(size_t)i * m + r] * cr;
-            }
-#pragma unroll
-            for (int i = 0; i < B; ++i) {
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) y[i] += __shfl_xor_sync(0xffffffffu, y[i], o);
-            }
-            double w[B];   // w = T^T y
-#pragma unroll
-            for (int i = 0; i < B; ++i) {
-                double s = 0.0;
-#pragma unroll
-                for (int l = 0; l <= i; ++l) s += T[l + i * B] * y[l];
-                w[i] = s;
-            }
-            for (int r = j0 + lane; r < m; r += 32) {
-                double cr = C[r];
-#pragma unroll
-                for (int i = 0; i < B; ++i) cr -= V[(size_t)i * m + r] * w[i];
-                C[r] = cr;
-            }
-        }
-        __syncthreads();
-    }
-    // R (upper part of every local column; rows < its global index, diagonal already in Rg)
-    for (int lc = 0; lc < nlp * B; ++lc) {
-        const int gcol = (rank + P * (lc / B)) * B + (lc % B);
-        if (gcol >= nc) continue;
-        for (int r = threadIdx.x; r < gcol; r += blockDim.x) Rg[r + (int64_t)gcol * ldr] = Wl[(size_t)lc * ldw + r];
-    }
-    if (P > 1)
-        cl.sync();
-    else
-        __syncthreads();
-    if (rank != 0) return;
-    const int n = nc - 1;
-    double* diag = Vpub;       // reuse: nc (<= B*m)
-    double* yv = Vloc;         // n
-    __shared__ int s_fail;
-    for (int i = threadIdx.x; i < nc; i += blockDim.x) diag[i] = Rg[i + (int64_t)i * ldr];
-    for (int i = threadIdx.x; i < n; i += blockDim.x) yv[i] = Rg[i + (int64_t)n * ldr];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double rmax = 0.0;
-        for (int i = 0; i < n; ++i) rmax = fmax(rmax, fabs(diag[i]));
-        int stt = 0;
-        for (int i = 0; i < n; ++i)
-            if (!(fabs(diag[i]) > 1e-14 * rmax)) stt = CSK_ESINGULAR;
-        status->status = stt;
-        status->sk_resid = fabs(diag[n]);
-        s_fail = stt;
-    }
-    __syncthreads();
-    if (s_fail) return;
-    const int i = threadIdx.x;
-    if (n <= (int)blockDim.x) {
-        double ring[8];
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-            const int c = n - 1 - kk;
-            ring[kk] = (c >= 0 && i < c) ? Rg[i + (int64_t)c * ldr] : 0.0;
-        }
-        for (int cb = n - 1; cb >= 0; cb -= 8) {
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-                const int c = cb - kk;
-                if (c >= 0) {
-                    const double xc = yv[c] / diag[c];
-                    if (i < c) yv[i] -= ring[kk] * xc;
-                    if (i == 0) x[c] = xc;
-                    const int cn = c - 8;
-                    ring[kk] = (cn >= 0 && i < cn) ? Rg[i + (int64_t)cn * ldr] : 0.0;
-                    __syncthreads();
-                }
-            }
-        }
-    } else {
-        for (int c = n - 1; c >= 0; --c) {
-            const double xc = yv[c] / diag[c];
-            for (int r = threadIdx.x; r < c; r += blockDim.x) yv[r] -= Rg[r + (int64_t)c * ldr] * xc;
-            if (threadIdx.x == 0) x[c] = xc;
-            __syncthreads();
-        }
-    }
-}
-
 static csk_status solve_impl(int64_t k2, int64_t n, const double* Z, int64_t ldz, double* x, double* sk_resid,
                              cudaStream_t st, bool x_host) {
     CSK_REQUIRE(Z != nullptr && x != nullptr, CSK_EINVAL, "Z and x must be non-NULL");
@@ -676,42 +434,21 @@ static csk_status solve_impl(int64_t k2, int64_t n, const double* Z, int64_t ldz
     double* xd = nullptr;
     SolveStatus* sd = nullptr;
     const size_t wbytes = (size_t)m * nc * 8;
-    CSK_CUDA_TRY(cudaMallocAsync(&W, wbytes + 64 + (x_host ? n * 8 : 0), st));
+    const size_t scratch_bytes = qr_wy_scratch_doubles(m, nc) * 8;
+    CSK_CUDA_TRY(cudaMallocAsync(&W, wbytes + 64 + (x_host ? n * 8 : 0) + scratch_bytes, st));
     sd = reinterpret_cast<SolveStatus*>(reinterpret_cast<char*>(W) + wbytes);
     xd = x_host ? reinterpret_cast<double*>(reinterpret_cast<char*>(W) + wbytes + 64) : x;
+    double* scratch = reinterpret_cast<double*>(reinterpret_cast<char*>(W) + wbytes + 64 + (x_host ? n * 8 : 0));
     const DeviceInfo& di = device_info();
-    // blocked (compact-WY) cluster QR: smallest cluster (<= 16 CTAs) whose column slices fit
+    // register-blocked compact-WY cluster QR (qr_wy.cu) when Z fits <= 16 CTAs
     {
-        int Pb = 0;
-        for (int p = 1; p <= 16; p *= 2)
-            if (qb_smem_doubles(m, nc, p) * 8 <= (size_t)di.smem_optin) {
-                Pb = p;
-                break;
-            }
-        if (const char* e = std::getenv("CSK_QR_P")) Pb = std::max(Pb, std::atoi(e));
-        const int npan = (nc + kQbB - 1) / kQbB;
-        if (Pb > npan) Pb = 0;
-        if (Pb > 0 && !std::getenv("CSK_QR_UNBLOCKED")) {
-            const size_t smem = qb_smem_doubles(m, nc, Pb) * 8;
-            CSK_CUDA_TRY(cudaFuncSetAttribute(qr_blocked_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            if (Pb > 8)
-                CSK_CUDA_TRY(cudaFuncSetAttribute(qr_blocked_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(Pb);
-            cfg.blockDim = dim3(kQbThreads);
-            cfg.dynamicSmemBytes = smem;
-            cfg.stream = st;
-            cudaLaunchAttribute attr[1];
-            attr[0].id = cudaLaunchAttributeClusterDimension;
-            attr[0].val.clusterDim.x = Pb;
-            attr[0].val.clusterDim.y = 1;
-            attr[0].val.clusterDim.z = 1;
-            cfg.attrs = attr;
-            cfg.numAttrs = 1;
-            CSK_CUDA_TRY(cudaLaunchKernelEx(&cfg, qr_blocked_kernel, Z, (int64_t)ldz, m, nc, Pb, W, nc, xd, sd));
-            CSK_LAUNCH_CHECK();
-            goto launched;
+        bool wy = false;
+        const csk_status ws = qr_wy_launch(Z, ldz, m, nc, W, nc, scratch, xd, sd, st, &wy);
+        if (ws != CSK_OK) {
+            cudaFreeAsync(W, st);
+            return ws;
         }
+        if (wy) goto launched;
     }
     {
     // cluster-distributed unblocked QR when a column slice fits shared memory on <= 8 CTAs

@@ -277,17 +277,53 @@ def test_ms_apply_matches_oracle(d, n, k1, k2):
     assert_within_T(Z, Zo, Zabs, 1e-12)
 
 
-def test_ms_solve_matches_oracle():
+# every small-solve kernel (csrc/qr_wy.cu default, forced wider clusters, and the older
+# multisketch.cu kernels kept for m > 512) against the oracle's Householder QR
+SOLVERS = {
+    "wy": {},
+    "wy_p4": {"CSK_QR_WY_P": "4"},
+    "wy_p16": {"CSK_QR_WY_P": "16"},
+    "cluster": {"CSK_QR_WY": "0"},
+    "single": {"CSK_QR_WY": "0", "CSK_QR_SINGLE": "1"},
+}
+
+
+@pytest.fixture(params=list(SOLVERS), ids=list(SOLVERS))
+def solver_env(request, monkeypatch):
+    for k, v in SOLVERS[request.param].items():
+        monkeypatch.setenv(k, v)
+    return request.param
+
+
+def test_ms_solve_matches_oracle(solver_env):
     rng = np.random.default_rng(5)
-    for m, n in [(16, 8), (128, 64), (256, 128), (40, 3)]:
+    for m, n in [(16, 8), (128, 64), (256, 128), (40, 3), (512, 256), (300, 150), (33, 32), (2, 1), (70, 9)]:
         Z = rng.standard_normal((m, n + 1))
         x, r = csk.ms_solve(gpu_colmajor(Z), n)
         xo, ro = oracle.sketch_solve(Z, n)
-        assert np.linalg.norm(Z[:, :n] @ (host(x) - xo)) <= 1e-12 * np.linalg.norm(Z[:, n])
-        assert abs(r - ro) <= 1e-12 * np.linalg.norm(Z[:, n])
+        err = np.linalg.norm(Z[:, :n] @ (host(x) - xo))
+        assert err <= 1e-12 * np.linalg.norm(Z[:, n]), (m, n, err)
+        assert abs(r - ro) <= 1e-12 * np.linalg.norm(Z[:, n]), (m, n)
 
 
-def test_ms_solve_singular():
+@pytest.mark.parametrize("kappa", [1e6, 1e12])
+def test_ms_solve_ill_conditioned(solver_env, kappa):
+    # Z1 = U diag(sigma) V^T with sigma log-spaced over [1/kappa, 1]; z = Z1 x* + noise.
+    # Backward-stable solves agree in fitted values to O(u kappa ||r||) (Wedin; R16)
+    m, n = 256, 128
+    Z1 = synth.ill_conditioned(m, n, kappa, seed=11)
+    z = synth.rhs(Z1, "hard", seed=11)
+    Z = np.column_stack([Z1, z])
+    x, r = csk.ms_solve(gpu_colmajor(Z), n)
+    xo, ro = oracle.sketch_solve(Z, n)
+    nz = np.linalg.norm(z)
+    rr = ro / nz
+    tol = max(1e-12, 64 * 2.2e-16 * kappa * rr)
+    assert np.linalg.norm(Z1 @ (host(x) - xo)) / nz <= tol
+    assert abs(r - ro) <= tol * nz
+
+
+def test_ms_solve_singular(solver_env):
     Z = np.zeros((10, 4))
     Z[:, 0] = 1.0
     Z[:, 3] = 1.0
