@@ -380,7 +380,7 @@ def bench_ours(args, cfg):
     solve_ms = (time.perf_counter() - t) * 1e3 / args.steps
 
     # ---- normal-equations baseline (a8) on the same [A b]
-    ne = {"gram": os.environ.get("CSK_NE_GRAM", "splitk (strided-batched DGEMM over row blocks + fixed-order reduce)")}
+    ne = {"gram": os.environ.get("CSK_NE_GRAM", "cuBLAS DGEMM A^T A + DGEMV A^T b + DDOT b^T b, one-CTA augmented Cholesky")}
     def ne_call():
         # the Gram + Cholesky work is done whether or not a pivot fails (ENOTPD is the
         # breakdown of Fig 8), so the time is recorded either way, with the status

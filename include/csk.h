@@ -147,8 +147,9 @@ csk_status ms_solve(int64_t k2, int64_t n, const double* Z, int64_t ldz, double*
 csk_status ms_lstsq(csk_plan_t plan, int64_t k2, int64_t n, const double* A, int64_t lda,
                     const double* b, double* x, double* sk_resid, void* stream);
 
-/* ne_lstsq: the normal-equations baseline: C = [A b]^T [A b] in one
- * cuBLAS Gram (DSYRK or DGEMM, whichever is faster, R15), Cholesky
+/* ne_lstsq: the normal-equations baseline: C = [A b]^T [A b] with
+ * cuBLAS (DGEMM A^T A + DGEMV A^T b + DDOT b^T b, the fastest form measured on
+ * B200, R15), Cholesky
  * of C[:n,:n] = R^T R, y = R^-T C[:n,n], x = R^-1 y.
  *   A d x n (lda >= d), b length d, x n doubles: device pointers.
  * Returns CSK_ENOTPD if a Cholesky pivot is <= 0 (the breakdown of Fig 8,

@@ -433,17 +433,18 @@ static csk_status solve_impl(int64_t k2, int64_t n, const double* Z, int64_t ldz
     double* W = nullptr;
     double* xd = nullptr;
     SolveStatus* sd = nullptr;
-    const size_t wbytes = (size_t)m * nc * 8;
+    const size_t wbytes = (size_t)(m + 1) * nc * 8;   // >= the R of the WY path, (nc rounded to even) x nc
     const size_t scratch_bytes = qr_wy_scratch_doubles(m, nc) * 8;
-    CSK_CUDA_TRY(cudaMallocAsync(&W, wbytes + 64 + (x_host ? n * 8 : 0) + scratch_bytes, st));
+    const size_t scratch_off = (wbytes + 64 + (x_host ? n * 8 : 0) + 255) & ~(size_t)255;   // 16-B vector loads
+    CSK_CUDA_TRY(cudaMallocAsync(&W, scratch_off + scratch_bytes, st));
     sd = reinterpret_cast<SolveStatus*>(reinterpret_cast<char*>(W) + wbytes);
     xd = x_host ? reinterpret_cast<double*>(reinterpret_cast<char*>(W) + wbytes + 64) : x;
-    double* scratch = reinterpret_cast<double*>(reinterpret_cast<char*>(W) + wbytes + 64 + (x_host ? n * 8 : 0));
+    double* scratch = reinterpret_cast<double*>(reinterpret_cast<char*>(W) + scratch_off);
     const DeviceInfo& di = device_info();
     // register-blocked compact-WY cluster QR (qr_wy.cu) when Z fits <= 16 CTAs
     {
         bool wy = false;
-        const csk_status ws = qr_wy_launch(Z, ldz, m, nc, W, nc, scratch, xd, sd, st, &wy);
+        const csk_status ws = qr_wy_launch(Z, ldz, m, nc, W, (nc + 1) & ~1, scratch, xd, sd, st, &wy);   // even ld: 16-B R reads
         if (ws != CSK_OK) {
             cudaFreeAsync(W, st);
             return ws;

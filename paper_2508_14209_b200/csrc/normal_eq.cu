@@ -2,9 +2,9 @@
 //
 // "computing the Gram matrix G = A^T A, and augmenting the right hand side
 // y = A^T b using GeMM and GeMV ... Cholesky factorization (POTRF) G = R^T R ...
-// two TRSVs: x = R^-1 (R^-T y)".  Here the Gram of the augmented [A b] is one
-// cuBLAS call (DSYRK by default, DGEMM with CSK_NE_GRAM=gemm; R15) when
-// b is stored as column n of A, else DSYRK + DGEMV.  The augmented Cholesky
+// two TRSVs: x = R^-1 (R^-T y)".  Exactly that: DGEMM for A^T A, DGEMV for A^T b,
+// DDOT for b^T b (the fastest cuBLAS form on B200, R15 / 6.3; CSK_NE_GRAM
+// selects the alternatives for measurement).  The augmented Cholesky
 // [[C11, c12], [c12^T, beta]] = [[R^T, 0], [y^T, rho]] [[R, y], [0, rho]] yields
 // y = R^-T c12 for free; one CTA then back-substitutes R x = y.
 #include <algorithm>
@@ -145,11 +145,26 @@ extern "C" csk_status ne_lstsq(int64_t d, int64_t n, const double* A, int64_t ld
     double* Sg = C + (size_t)nc * nc;
     int* sd = reinterpret_cast<int*>(Sg + (size_t)nc * nc);
     const double one = 1.0, zero = 0.0;
+    // Gram variants (measured on B200 at C2/C4): default = one DGEMM for A^T A
+    // (n x n: cuBLAS runs K = d split internally at 28-33 TF/s when n is a multiple of 64) +
+    // DGEMV for A^T b + DDOT for b^T b.  "gemm"/"syrk" = one call on [A b] (n+1 columns: the
+    // ragged 65th/129th column costs cuBLAS 2-3x), "splitk" = strided-batched DGEMM over row blocks.
     const char* gram = std::getenv("CSK_NE_GRAM");
     const bool use_gemm = gram && std::strcmp(gram, "gemm") == 0;
     const bool use_syrk = gram && std::strcmp(gram, "syrk") == 0;
+    const bool use_splitk = gram && std::strcmp(gram, "splitk") == 0;
     cublasStatus_t bs = CUBLAS_STATUS_SUCCESS;
-    if (!use_gemm && !use_syrk) {
+    if (!use_gemm && !use_syrk && !use_splitk) {
+        bs = cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)n, (int)n, (int)d, &one, A, (int)lda, A, (int)lda, &zero, C,
+                         nc);
+        if (bs == CUBLAS_STATUS_SUCCESS)
+            bs = cublasDgemv(h, CUBLAS_OP_T, (int)d, (int)n, &one, A, (int)lda, b, 1, &zero, C + (size_t)n * nc, 1);
+        if (bs == CUBLAS_STATUS_SUCCESS) {
+            cublasSetPointerMode(h, CUBLAS_POINTER_MODE_DEVICE);
+            bs = cublasDdot(h, (int)d, b, 1, b, 1, C + (size_t)n * nc + n);
+            cublasSetPointerMode(h, CUBLAS_POINTER_MODE_HOST);
+        }
+    } else if (use_splitk) {
         csk_status gs = gram_split_k(h, d, (int)n, A, lda, b, C, nc, st);
         if (gs != CSK_OK) {
             cudaFreeAsync(C, st);

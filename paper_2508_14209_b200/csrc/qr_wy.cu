@@ -82,22 +82,51 @@ constexpr int kTeam = 32 * kTeamWarps;
 
 __device__ __forceinline__ void team_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kTeam) : "memory"); }
 
-// Sum N per-thread partials over the team; every team thread gets the bit-identical total
-// (warp butterfly, then the four warp totals added in warp order).  buf: [2][kTeamWarps][16]
-// shared ring, `ph` alternates per call so one barrier per call suffices.
-template <int N>
-__device__ __forceinline__ void team_sum(double (&v)[N], double* buf, int& ph) {
-    static_assert(N <= 16, "team_sum: N <= 16");
-    warp_sum_n<N>(v);
-    const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
-    double* b = buf + ph * (kTeamWarps * 16);
-    if (lane == 0) {
+// Warp reduce-scatter of N = 2^K values (B300_MICROARCH / scripts/lat_bench.cu: a 64-bit shuffle
+// costs ~5 issue cycles, so a full 5-level butterfly of 8 values takes ~420 cycles; halving the
+// vector at each of the first K levels needs N - 1 + (5 - K) shuffles instead of 5 N).
+// Returns the warp total of value lane >> (5 - K); lanes sharing those top K bits hold
+// bit-identical totals (every add pairs the same two partials).
+template <int K>
+__device__ __forceinline__ double warp_reduce_scatter(double* v) {
+    const int lane = threadIdx.x & 31;
 #pragma unroll
-        for (int i = 0; i < N; ++i) b[q * 16 + i] = v[i];
+    for (int lev = 0; lev < K; ++lev) {
+        const int o = 16 >> lev, n = (1 << K) >> (lev + 1);
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < n; ++i) {
+            const double send = up ? v[i] : v[i + n];
+            const double keep = up ? v[i + n] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
     }
-    team_bar();
+    double r = v[0];
 #pragma unroll
-    for (int i = 0; i < N; ++i) v[i] = ((b[i] + b[16 + i]) + b[32 + i]) + b[48 + i];
+    for (int o = 16 >> K; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    return r;
+}
+
+// Sum 2^K per-thread partials over the panel team; every team thread gets the bit-identical
+// totals.  Warp reduce-scatter, one lane per value stores its warp total, named barrier, lane i
+// adds value i over the four warps (fixed order) into a per-warp slot, every lane reads all.
+// buf: [2][kTeamWarps][16] ring (ph alternates per call: one team barrier per call suffices);
+// tot: [kTeamWarps][16] per-warp totals.
+template <int K>
+__device__ __forceinline__ void team_sum(double* v, double* buf, double* tot, int& ph) {
+    constexpr int N = 1 << K;
+    static_assert(N <= 16, "team_sum: N <= 16");
+    const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
+    const double r = warp_reduce_scatter<K>(v);
+    double* b = buf + ph * (kTeamWarps * 16);
+    if ((lane & ((32 >> K) - 1)) == 0) b[q * 16 + (lane >> (5 - K))] = r;
+    team_bar();
+    double* t = tot + q * 16;
+    if (lane < N) t[lane] = ((b[lane] + b[16 + lane]) + b[32 + lane]) + b[48 + lane];
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = t[i];
+    __syncwarp();   // t is rewritten by this warp's next call
     ph ^= 1;
 }
 
@@ -106,7 +135,7 @@ __device__ __forceinline__ void team_sum(double (&v)[N], double* buf, int& ph) {
 // write R (rows <= diagonal) to global, V/T to shared memory (and to global when P > 1).
 template <int RPL>
 __device__ __forceinline__ void factor_panel(const WyArgs& a, const double* cols, int kp, double* Vout, double* Tout,
-                                             const double* Vin, const double* Tin, double* rbuf) {
+                                             const double* Vin, const double* Tin, double* rbuf, double* rtot) {
     constexpr int RPLT = (RPL + kTeamWarps - 1) / kTeamWarps;
     const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
     const int m = a.m, ldw = a.ldw, j0 = kp * kB, bw = min(kB, a.nc - j0);
@@ -136,7 +165,7 @@ __device__ __forceinline__ void factor_panel(const WyArgs& a, const double* cols
                 for (int c = 0; c < kB; ++c) y[c * kB + i] += vi * p[c][u];
             }
         }
-        team_sum<kB * kB>(y, rbuf, ph);
+        team_sum<4>(y, rbuf, rtot, ph);
         double w[kB * kB];
 #pragma unroll
         for (int c = 0; c < kB; ++c)
@@ -184,7 +213,7 @@ __device__ __forceinline__ void factor_panel(const WyArgs& a, const double* cols
                 for (int c = i + 1; c < kB; ++c) red[kB + c] = p[c][u];
             }
         }
-        team_sum<2 * kB>(red, rbuf, ph);
+        team_sum<3>(red, rbuf, rtot, ph);
         const double xj = red[kB];
         const double nrm = sqrt(red[0] + xj * xj);
         const double alpha = nrm == 0.0 ? 0.0 : (xj >= 0.0 ? -nrm : nrm);
@@ -216,9 +245,9 @@ __device__ __forceinline__ void factor_panel(const WyArgs& a, const double* cols
         beta[i] = bt;
     }
     // Gram of V and T (T[i + l kB], upper; T[:, l] = [-beta_l T[0:l,0:l] G[0:l,l]; beta_l])
-    double g[kB * (kB - 1) / 2];
+    double g[8];   // 6 Gram entries, padded to 2^3 for the reduction
 #pragma unroll
-    for (int e = 0; e < kB * (kB - 1) / 2; ++e) g[e] = 0.0;
+    for (int e = 0; e < 8; ++e) g[e] = 0.0;
 #pragma unroll
     for (int u = 0; u < RPLT; ++u) {
         int e = 0;
@@ -227,7 +256,7 @@ __device__ __forceinline__ void factor_panel(const WyArgs& a, const double* cols
 #pragma unroll
             for (int i = 0; i < l; ++i) g[e++] += p[i][u] * p[l][u];
     }
-    team_sum<kB * (kB - 1) / 2>(g, rbuf, ph);
+    team_sum<3>(g, rbuf, rtot, ph);
     double T[kB * kB];
 #pragma unroll
     for (int e = 0; e < kB * kB; ++e) T[e] = 0.0;
@@ -271,23 +300,30 @@ __device__ __forceinline__ void factor_panel(const WyArgs& a, const double* cols
     }
 }
 
-// Trailing update of one shared-memory column C (rows >= 32 t0): C -= V (T^T (V^T C)).
-template <int RPL>
-__device__ __forceinline__ void apply_wy(double* C, const double (&vr)[kB][RPL], const double (&Tr)[kB * kB], int t0,
-                                         int m) {
-    const int lane = threadIdx.x & 31;
-    double cr[RPL];
+// Trailing update of up to 4 shared-memory columns by one warp, a quarter-warp (8 lanes) per
+// column: C -= V (T^T (V^T C)) over rows >= r0 (V is zero above its pivots).  The V^T C
+// reduction is 3 shuffle levels within the quarter, shared by the 4 columns (24 shuffles per 4
+// columns instead of 40 per column for a full-warp butterfly); V rows are broadcast LDS.
+__device__ __forceinline__ void apply_wy4(double* C, bool active, const double* V, int ldw, const double* Tr, int r0,
+                                          int m) {
+    const int sub = threadIdx.x & 7;
     double y[kB];
 #pragma unroll
     for (int i = 0; i < kB; ++i) y[i] = 0.0;
+    if (active) {
+#pragma unroll 4
+        for (int r = r0 + sub; r < m; r += 8) {
+            const double c = C[r];
 #pragma unroll
-    for (int t = 0; t < RPL; ++t) {
-        const int r = lane + 32 * t;
-        cr[t] = (t >= t0 && r < m) ? C[r] : 0.0;
-#pragma unroll
-        for (int i = 0; i < kB; ++i) y[i] += vr[i][t] * cr[t];
+            for (int i = 0; i < kB; ++i) y[i] += V[i * ldw + r] * c;
+        }
     }
-    warp_sum_n<kB>(y);
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+#pragma unroll
+        for (int i = 0; i < kB; ++i) y[i] += __shfl_xor_sync(0xffffffffu, y[i], o);
+    }
+    if (!active) return;
     double w[kB];
 #pragma unroll
     for (int i = 0; i < kB; ++i) {
@@ -296,30 +332,55 @@ __device__ __forceinline__ void apply_wy(double* C, const double (&vr)[kB][RPL],
         for (int l = 0; l <= i; ++l) s += Tr[l + i * kB] * y[l];
         w[i] = s;
     }
+#pragma unroll 4
+    for (int r = r0 + sub; r < m; r += 8) {
+        double c = C[r];
 #pragma unroll
-    for (int t = 0; t < RPL; ++t) {
-        const int r = lane + 32 * t;
-        if (t >= t0 && r < m) {
-            double v = cr[t];
-#pragma unroll
-            for (int i = 0; i < kB; ++i) v -= vr[i][t] * w[i];
-            C[r] = v;
-        }
+        for (int i = 0; i < kB; ++i) c -= V[i * ldw + r] * w[i];
+        C[r] = c;
     }
 }
 
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async16(double* dst, const double* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // Back substitution R11 x = r12 by one CTA (R in global memory, column-major, ld ldr), with the
 // singularity test |R_ii| <= 1e-14 max |R_jj| and the sketched residual |R_nn|.
-// Blocked by 32 from the bottom: warp 0 solves the 32 x 32 diagonal block with the block in
-// registers (lane l holds row c0 + l; x_c = y_c * (1/R_cc) broadcast by shuffle), then every
-// thread updates one row of y above the block with the block's 32 columns (coalesced L2 reads).
-// diag, yv: shared scratch of nc and n doubles.
+// Blocked by 32 columns from the bottom.  Block column R[0:c1, c0:c1] is prefetched into shared
+// memory (cp.async, double-buffered) while the previous block is solved; warp 0 solves the
+// diagonal block (lane l owns row c0 + l; x_c = y_c * (1/R_cc) broadcast by shuffle), then each
+// thread updates one row of y above the block.
+// diag, yv: shared scratch of nc and n doubles; rbuf: shared scratch of 2 * 32 * n doubles.
 __device__ void back_substitute(const double* __restrict__ Rg, int ldr, int nc, double* __restrict__ x,
-                                SolveStatus* __restrict__ status, double* diag, double* yv) {
+                                SolveStatus* __restrict__ status, double* diag, double* yv, double* rbuf) {
     const int n = nc - 1;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     __shared__ int s_fail;
     __shared__ double s_wmax[kWarps];
+    // block column b covers columns [c0, c1) with c1 = n - 32 b; its rows [0, c1) go to
+    // rbuf[(b & 1) * 32 * n + cc * c1 + r]
+    auto prefetch = [&](int c1) {
+        const int c0 = max(0, c1 - 32), bs = c1 - c0;
+        double* dst = rbuf + (size_t)(((n - c1) / 32) & 1) * 32 * n;
+        if (((ldr | c1) & 1) == 0) {   // 16-B chunks (ldr, c1 even: Rg columns and rbuf rows 16-B aligned)
+            const int h = c1 >> 1;
+            for (int cc = warp; cc < bs; cc += kWarps)
+                for (int e = lane; e < h; e += 32) cp_async16(dst + cc * c1 + 2 * e, Rg + 2 * e + (int64_t)(c0 + cc) * ldr);
+        } else {
+            for (int cc = warp; cc < bs; cc += kWarps)
+                for (int r = lane; r < c1; r += 32) cp_async8(dst + cc * c1 + r, Rg + r + (int64_t)(c0 + cc) * ldr);
+        }
+        cp_async_commit();
+    };
+    prefetch(n);
     double mx = 0.0;
     for (int i = threadIdx.x; i < nc; i += blockDim.x) {
         const double di = Rg[i + (int64_t)i * ldr];
@@ -345,15 +406,20 @@ __device__ void back_substitute(const double* __restrict__ Rg, int ldr, int nc, 
         }
     }
     __syncthreads();
-    if (s_fail) return;
+    if (s_fail) {
+        cp_async_wait_all();
+        return;
+    }
     for (int c1 = n; c1 > 0; c1 -= 32) {
         const int c0 = max(0, c1 - 32), bs = c1 - c0;
+        const double* Rb = rbuf + (size_t)(((n - c1) / 32) & 1) * 32 * n;   // [bs][c1]
+        cp_async_wait_all();
+        __syncthreads();
+        if (c0 > 0) prefetch(c0);   // next block column streams in while this one is solved
         if (warp == 0) {
-            // diagonal block: lane l owns row c0 + l
             double rb[32];
 #pragma unroll
-            for (int cc = 0; cc < 32; ++cc)
-                rb[cc] = (cc < bs && lane < cc) ? Rg[c0 + lane + (int64_t)(c0 + cc) * ldr] : 0.0;
+            for (int cc = 0; cc < 32; ++cc) rb[cc] = (cc < bs && lane < cc) ? Rb[cc * c1 + c0 + lane] : 0.0;
             double yl = lane < bs ? yv[c0 + lane] : 0.0;
             const double rinv = lane < bs ? 1.0 / diag[c0 + lane] : 0.0;
             double xl = 0.0;
@@ -371,23 +437,37 @@ __device__ void back_substitute(const double* __restrict__ Rg, int ldr, int nc, 
             }
         }
         __syncthreads();
-        if (c0 > 0) {
-            for (int i = threadIdx.x; i < c0; i += blockDim.x) {
-                double s = yv[i];
-#pragma unroll 8
-                for (int cc = 0; cc < bs; ++cc) s -= Rg[i + (int64_t)(c0 + cc) * ldr] * yv[c0 + cc];
-                yv[i] = s;
+        for (int i = threadIdx.x; i < c0; i += blockDim.x) {
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            int cc = 0;
+            for (; cc + 4 <= bs; cc += 4) {
+                s0 += Rb[cc * c1 + i] * yv[c0 + cc];
+                s1 += Rb[(cc + 1) * c1 + i] * yv[c0 + cc + 1];
+                s2 += Rb[(cc + 2) * c1 + i] * yv[c0 + cc + 2];
+                s3 += Rb[(cc + 3) * c1 + i] * yv[c0 + cc + 3];
             }
-            __syncthreads();
+            for (; cc < bs; ++cc) s0 += Rb[cc * c1 + i] * yv[c0 + cc];
+            yv[i] -= (s0 + s1) + (s2 + s3);
         }
     }
 }
 
-__host__ __device__ inline size_t wy_smem_doubles(int m, int nc, int P) {
-    const int ldw = (m + 1) & ~1;
+// column stride: even (16-B vectors) and = 8 mod 16 doubles, so the two quarter-warps of a
+// half-warp (same rows of adjacent columns) hit disjoint shared-memory banks in apply_wy4
+__host__ __device__ inline int wy_ldw(int m) { return ((m + 15) & ~15) + 8; }
+
+// local-column region: the CTA's panels, and (CTA 0, after the factorization) the two
+// back-substitution block-column buffers of 32 x n doubles
+__host__ __device__ inline size_t wy_local_doubles(int m, int nc, int P) {
+    const int ldw = wy_ldw(m);
     const int npan = (nc + kB - 1) / kB;
     const int nlp = (npan + P - 1) / P;
-    return (size_t)nlp * kB * ldw + 2 * (size_t)kB * ldw + 2 * kB * kB;
+    const size_t cols = (size_t)nlp * kB * ldw, bsub = (size_t)2 * 32 * (nc - 1);
+    return cols > bsub ? cols : bsub;
+}
+__host__ __device__ inline size_t wy_smem_doubles(int m, int nc, int P) {
+    const int ldw = wy_ldw(m);
+    return wy_local_doubles(m, nc, P) + 2 * (size_t)kB * ldw + 2 * kB * kB;
 }
 
 template <int RPL>
@@ -397,13 +477,13 @@ __global__ void __launch_bounds__(kThreads, 1) qr_wy_kernel(WyArgs a) {
     const int m = a.m, nc = a.nc, npan = a.npan, ldw = a.ldw;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nlp = (npan - rank + P - 1) / P;   // local panels: global panel rank + P*lp
-    const int nlp_max = (npan + P - 1) / P;      // identical layout in every CTA
     extern __shared__ __align__(16) double sm[];
-    double* Wl = sm;                                     // [nlp_max*kB][ldw] local columns
-    double* Vst = Wl + (size_t)nlp_max * kB * ldw;       // [2][kB][ldw] V of the current/next panel
-    double* Tst = Vst + 2 * (size_t)kB * ldw;            // [2][kB*kB]
-    __shared__ double s_rbuf[2 * kTeamWarps * 16];       // team reduction ring
-    __shared__ int s_ctr[2];                             // trailing-column work counters (per step parity)
+    double* Wl = sm;                                             // [nlp_max*kB][ldw] local columns
+    double* Vst = Wl + wy_local_doubles(m, nc, P);               // [2][kB][ldw] V of the current/next panel
+    double* Tst = Vst + 2 * (size_t)kB * ldw;                    // [2][kB*kB]
+    __shared__ __align__(16) double s_rbuf[2 * kTeamWarps * 16];   // team reduction ring
+    __shared__ __align__(16) double s_rtot[kTeamWarps * 16];       // team totals (per warp)
+    __shared__ int s_ctr[2];                                     // trailing-panel work counters (step parity)
     if (threadIdx.x == 0) QPROF(npan, 0);
     // local columns (zero padding past nc); one column per warp iteration, RPL loads in flight
     for (int lc = warp; lc < nlp * kB; lc += kWarps) {
@@ -423,23 +503,25 @@ __global__ void __launch_bounds__(kThreads, 1) qr_wy_kernel(WyArgs a) {
     if (threadIdx.x == 0) s_ctr[0] = 0;
     __syncthreads();
     if (threadIdx.x == 0) QPROF(npan, 1);
-    if (rank == 0 && warp < kTeamWarps) factor_panel<RPL>(a, Wl, 0, Vst, Tst, nullptr, nullptr, s_rbuf);
+    if (rank == 0 && warp < kTeamWarps) factor_panel<RPL>(a, Wl, 0, Vst, Tst, nullptr, nullptr, s_rbuf, s_rtot);
     if (threadIdx.x == 0) QPROF(npan, 2);
     for (int k = 0; k < npan; ++k) {
         sync_all(P);   // panel k factored and published
         if (threadIdx.x == 0) QPROF(k, 0);
         if (threadIdx.x == kThreads - 1) QPROF(k, 4);
         if (threadIdx.x == kThreads - 1) s_ctr[(k + 1) & 1] = 0;   // last used in step k-1
-        const int owner = k % P, j0 = k * kB, buf = k & 1, t0 = j0 >> 5;
+        const int owner = k % P, j0 = k * kB, buf = k & 1;
         double* V = Vst + (size_t)buf * kB * ldw;
         double* T = Tst + buf * kB * kB;
         if (rank != owner) {
+            // V rows >= 32*(j0/32) of the 4 columns (16-B vectors; ldw and the row start are even)
             const double* Vgk = a.Vg + (size_t)k * kB * ldw;
-            const int r0 = t0 * 32;
-            const int len = m - r0;
-            for (int e = threadIdx.x; e < kB * len; e += kThreads) {
-                const int c = e / len, r = r0 + (e - c * len);
-                V[c * ldw + r] = __ldcg(Vgk + c * ldw + r);
+            const int r0 = (j0 >> 5) * 32, h = (m - r0 + 1) >> 1;
+#pragma unroll
+            for (int c = 0; c < kB; ++c) {
+                const double2* src = reinterpret_cast<const double2*>(Vgk + (size_t)c * ldw + r0);
+                double2* dst = reinterpret_cast<double2*>(V + (size_t)c * ldw + r0);
+                for (int e = threadIdx.x; e < h; e += kThreads) dst[e] = __ldcg(src + e);
             }
             if (threadIdx.x < kB * kB) T[threadIdx.x] = __ldcg(a.Tg + (size_t)k * kB * kB + threadIdx.x);
             __syncthreads();
@@ -450,44 +532,30 @@ __global__ void __launch_bounds__(kThreads, 1) qr_wy_kernel(WyArgs a) {
         if (la && warp < kTeamWarps) {
             const int nb = (k + 1) & 1;
             factor_panel<RPL>(a, Wl + (size_t)lp_next * kB * ldw, k + 1, Vst + (size_t)nb * kB * ldw,
-                              Tst + nb * kB * kB, V, T, s_rbuf);
+                              Tst + nb * kB * kB, V, T, s_rbuf, s_rtot);
             if (threadIdx.x == 0) QPROF(k, 2);
         }
-        // trailing local columns (global panel index > k, panel k+1 excluded when la), handed out
-        // one at a time; the panel team joins when it is done
+        // trailing local panels (global index > k; panel k+1 excluded when la), one panel of 4
+        // columns per warp at a time (quarter-warp per column), handed out by a shared counter;
+        // the panel team joins when it is done
         const int lp0 = k - rank >= 0 ? (k - rank) / P + 1 : 0;
-        const int ncols = (nlp - lp0) * kB;
-        if (ncols <= 0) {
-            if (threadIdx.x == 0) QPROF(k, 3);
-            if (threadIdx.x == kThreads - 1) QPROF(k, 5);
-            continue;
-        }
-        bool have_v = false;
-        double vr[kB][RPL];
-        double Tr[kB * kB];
-        for (;;) {
-            int q = 0;
-            if (lane == 0) q = atomicAdd(&s_ctr[k & 1], 1);
-            q = __shfl_sync(0xffffffffu, q, 0);
-            if (q >= ncols) break;
-            const int lc = lp0 * kB + q;
-            const int lp = lc / kB;
-            if (lp == lp_next) continue;
-            const int gcol = (rank + P * lp) * kB + (lc % kB);
-            if (gcol >= nc) continue;
-            if (!have_v) {
+        const int npl = nlp - lp0;
+        if (npl > 0) {
+            double Tr[kB * kB];
 #pragma unroll
-                for (int i = 0; i < kB; ++i)
-#pragma unroll
-                    for (int t = 0; t < RPL; ++t) {
-                        const int r = lane + 32 * t;
-                        vr[i][t] = (t >= t0 && r < m) ? V[i * ldw + r] : 0.0;
-                    }
-#pragma unroll
-                for (int e = 0; e < kB * kB; ++e) Tr[e] = T[e];
-                have_v = true;
+            for (int e = 0; e < kB * kB; ++e) Tr[e] = T[e];
+            const int r0 = j0 & ~7;
+            for (;;) {
+                int q = 0;
+                if (lane == 0) q = atomicAdd(&s_ctr[k & 1], 1);
+                q = __shfl_sync(0xffffffffu, q, 0);
+                if (q >= npl) break;
+                const int lp = lp0 + q;
+                if (lp == lp_next) continue;
+                const int g = lane >> 3;
+                const int gcol = (rank + P * lp) * kB + g;
+                apply_wy4(Wl + (size_t)(lp * kB + g) * ldw, gcol < nc, V, ldw, Tr, r0, m);
             }
-            apply_wy<RPL>(Wl + (size_t)lc * ldw, vr, Tr, t0, m);
         }
         if (threadIdx.x == 0) QPROF(k, 3);
         if (threadIdx.x == kThreads - 1) QPROF(k, 5);
@@ -495,7 +563,7 @@ __global__ void __launch_bounds__(kThreads, 1) qr_wy_kernel(WyArgs a) {
     sync_all(P);   // all of R written
     if (threadIdx.x == 0) QPROF(npan, 3);
     if (rank != 0) return;
-    back_substitute(a.Rg, a.ldr, nc, a.x, a.status, Vst, Vst + nc);
+    back_substitute(a.Rg, a.ldr, nc, a.x, a.status, Vst, Vst + nc, Wl);
     if (threadIdx.x == 0) QPROF(npan, 4);
 }
 
@@ -532,7 +600,7 @@ csk_status qr_wy_launch(const double* Z, int64_t ldz, int m, int nc, double* Rg,
     a.nc = nc;
     a.P = P;
     a.npan = npan;
-    a.ldw = (m + 1) & ~1;
+    a.ldw = wy_ldw(m);
     a.Vg = scratch;
     a.Tg = scratch + (size_t)npan * kB * a.ldw;
     a.Rg = Rg;
@@ -565,7 +633,7 @@ csk_status qr_wy_launch(const double* Z, int64_t ldz, int m, int nc, double* Rg,
 
 size_t qr_wy_scratch_doubles(int m, int nc) {
     const int npan = (nc + kB - 1) / kB;
-    return (size_t)npan * kB * ((m + 1) & ~1) + (size_t)npan * kB * kB;
+    return (size_t)npan * kB * wy_ldw(m) + (size_t)npan * kB * kB;
 }
 
 }  // namespace csk

@@ -23,7 +23,7 @@ int main(int argc, char** argv) {
     long long* dp;
     const size_t profn = (size_t)16 * (npan + 1) * 8;
     cudaMalloc(&dZ, Z.size() * 8);
-    cudaMalloc(&dR, (size_t)nc * nc * 8);
+    cudaMalloc(&dR, (size_t)(nc + 1) * nc * 8);
     cudaMalloc(&dS, csk::qr_wy_scratch_doubles(m, nc) * 8);
     cudaMalloc(&dx, n * 8);
     cudaMalloc(&dst, sizeof(csk::SolveStatus));
@@ -37,7 +37,7 @@ int main(int argc, char** argv) {
     for (int it = 0; it < 4; ++it) {
         cudaMemset(dp, 0, profn * 8);
         cudaEventRecord(e0);
-        csk::qr_wy_launch(dZ, m, m, nc, dR, nc, dS, dx, dst, 0, &launched);
+        csk::qr_wy_launch(dZ, m, m, nc, dR, (nc + 1) & ~1, dS, dx, dst, 0, &launched);
         cudaEventRecord(e1);
         cudaDeviceSynchronize();
     }
