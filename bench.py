@@ -233,7 +233,7 @@ def ls_compare(args, cfg, kappa, dev, stream):
         except csk.CskError as e:
             return str(e).split(":")[1].strip()
 
-    out = {"kappa": kappa, "workload": cfg["name"]}
+    out = {"kappa": kappa, "workload": cfg["name"].replace("kappa(A)=1e10", f"kappa(A)={kappa:.0e}")}
     for name, fn in (("ms", ms), ("ne", ne)):
         for _ in range(args.warmup):
             fn()
@@ -335,22 +335,29 @@ def bench_ours(args, cfg):
     barrier()
     clocks = ClockSampler(local)
     csk.launch_count(reset=True)
+    # the dominant kernel (cs_apply main kernel) is timed inside the timed region: the library
+    # records a pooled CUDA event on its launching stream right before the launch and one right
+    # after it (csk_profile_enable); per-step times come from events around each step
+    csk.profile_enable(True)
+    step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
     with clocks:
         barrier()
+        torch.cuda.nvtx.range_push("csk_timed")   # ncu --nvtx --nvtx-include csk_timed/ (launch list)
         ev0.record(stream)
-        for _ in range(args.steps):
+        for i in range(args.steps):
+            step_ev[i][0].record(stream)
             step()
+            step_ev[i][1].record(stream)
         ev1.record(stream)
         barrier()
+        torch.cuda.nvtx.range_pop()
     launches = csk.launch_count() // max(1, args.steps) * args.steps
     step_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     value = ws * bytes_step / (step_ms * 1e-3) / 1e9
-
-    # ---- dominant kernel (cs_apply main kernel) timed on its own stream with CUDA events
-    csk.profile_enable(True)
-    for _ in range(args.steps):
-        step()
-    torch.cuda.synchronize()
+    per_step = sorted(a.elapsed_time(b_) for a, b_ in step_ev)
+    step_stats = {"median": per_step[len(per_step) // 2], "mean": sum(per_step) / len(per_step),
+                  "min": per_step[0], "max": per_step[-1]}
     kern_ms_total, kern_launches = csk.profile_read()
     csk.profile_enable(False)
     kern_ms = kern_ms_total / max(1, kern_launches)
@@ -378,6 +385,36 @@ def bench_ours(args, cfg):
     for _ in range(0 if args.cs_only else args.steps):
         csk.ms_solve(Z, n, x=x)
     solve_ms = (time.perf_counter() - t) * 1e3 / args.steps
+
+    # ---- SURVEY 8(d) "both input families" + the fp32 path: the CountSketch alone on kappa = 1e10 A
+    # of the same shape (its speed must not depend on the values) and on the fp32 copy of [A b]
+    families = None
+    if ws == 1 and not args.no_extra and not args.cs_only and args.config in ("c2", "c3"):
+        def time_cs(Ax, bx, SAx):
+            for _ in range(2):
+                csk.cs_apply(plan, Ax, b=bx, SA=SAx)
+            barrier()
+            ev0.record(stream)
+            for _ in range(args.steps):
+                csk.cs_apply(plan, Ax, b=bx, SA=SAx)
+            ev1.record(stream)
+            barrier()
+            return ev0.elapsed_time(ev1) / args.steps
+
+        families = {"gaussian_f64": {"ms": cs_ms, "gbs": bytes_step / (cs_ms * 1e-3) / 1e9}}
+        buf2 = synth.colmajor_empty(torch, d, ncols, torch.float64, dev)
+        buf2[:, :n] = synth.ill_conditioned_torch(d, n, 1e10, seed=DATA_SEED, device=dev)
+        buf2[:, n] = b
+        t_ill = time_cs(buf2[:, :n], buf2[:, n], SA)
+        families["kappa1e10_f64"] = {"ms": t_ill, "gbs": bytes_step / (t_ill * 1e-3) / 1e9}
+        del buf2
+        buf32 = synth.colmajor_empty(torch, d, ncols, torch.float32, dev)
+        buf32.copy_(buf)
+        SA32 = synth.colmajor_empty(torch, k1, ncols, torch.float32, dev)
+        t32 = time_cs(buf32[:, :n], buf32[:, n], SA32)
+        families["gaussian_f32"] = {"ms": t32, "gbs": bytes_step / 2 / (t32 * 1e-3) / 1e9}
+        del buf32, SA32
+        torch.cuda.empty_cache()
 
     # ---- normal-equations baseline (a8) on the same [A b]
     ne = {"gram": os.environ.get("CSK_NE_GRAM", "cuBLAS DGEMM A^T A + DGEMV A^T b + DDOT b^T b, one-CTA augmented Cholesky")}
@@ -450,7 +487,7 @@ def bench_ours(args, cfg):
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong" if strong else "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "step_ms_stats": step_stats,
         "config": {"workload": cfg["name"], "d_per_rank": d, "d_global": d_glob, "n": n, "k1": k1, "k2": k2,
                    "rhs": "b = A e + eta, eta ~ N(0, 0.01)", "variant": variant,
                    "l2": "inputs (%.1f GB per rank) > 126 MB L2; no flush needed" % (bytes_step / 1e9),
@@ -460,12 +497,14 @@ def bench_ours(args, cfg):
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic(args.config, variant), "kernel": "cs_apply main kernel",
-                     "kernel_ms": kern_ms, "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
+                     "kernel_ms": kern_ms, "kernel_share_of_step": kern_ms / step_ms,
+                     "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
                      "frac_of_8TBs_nominal": achieved / NOMINAL_HBM_GBS},
         "cpu_baseline": cpu,
         "phases_ms": {"cs_apply": cs_ms, "g_stage": msa_ms - cs_ms, "solve": solve_ms, "plan_codes": plan_ms,
                       "gauss_first_use": gauss_first_ms},
         "cs_apply_gbs": bytes_step / (cs_ms * 1e-3) / 1e9,
+        "cs_apply_input_families": families,
         "normal_equations": ne,
         "speedup_vs_ne": (ne["ms"] / step_ms) if ne.get("ms") else None,
         "accuracy": acc,
@@ -498,6 +537,7 @@ def main():
     ap.add_argument("--cs-only", action="store_true", help="experiment mode: a step is cs_apply alone")
     ap.add_argument("--no-acc", action="store_true", help="skip the untimed accuracy checks")
     ap.add_argument("--no-ls", action="store_true", help="skip the C4 least-squares comparison (N=1, c2)")
+    ap.add_argument("--no-extra", action="store_true", help="skip the kappa=1e10 / fp32 CountSketch lines")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cfg = CONFIGS[args.config]

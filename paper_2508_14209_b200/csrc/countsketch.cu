@@ -856,6 +856,7 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
     switch (variant) {
         case CSK_VAR_ATOMIC_COL: {
             const int64_t blocks = std::min<int64_t>(ceil_div(rows, 256), (int64_t)di.num_sms * 8);
+            prof_mark(st, true);   // right before the launch: host prep is not timed
             cs_col_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(code, rows, cols, ncols, out, ldo);
             CSK_LAUNCH_CHECK();
             return CSK_OK;
@@ -872,6 +873,7 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
             CSK_CUDA_TRY(cudaFuncSetAttribute(cs_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             const int64_t units = ceil_div(rows, RB) * ceil_div(ncols, L.cw);
             const int64_t blocks = std::min<int64_t>(ceil_div(units, kTmaWarps), (int64_t)di.num_sms);
+            prof_mark(st, true);   // right before the launch: host prep is not timed
             cs_tma_kernel<T><<<(unsigned)blocks, kTmaWarps * 32, smem, st>>>(tmap, code, rows, ncols, stage_bytes, out, L);
             CSK_LAUNCH_CHECK();
             return CSK_OK;
@@ -894,6 +896,7 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
                     CSK_CUDA_TRY(cudaFuncSetAttribute(cs_bulk_tma_kernel<T, C>,
                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
                     const int64_t blocks = std::min<int64_t>(ceil_div(units, C::kWarps), (int64_t)di.num_sms);
+                    prof_mark(st, true);   // right before the launch: host prep is not timed
                     cs_bulk_tma_kernel<T, C><<<(unsigned)blocks, C::kWarps * 32, smem, st>>>(tmap, code, rows, ncols,
                                                                                             stage_bytes, ldrow, out, L);
                     CSK_LAUNCH_CHECK();
@@ -933,6 +936,7 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
                         if (smem > (size_t)di.smem_optin) return CSK_EUNSUPPORTED;
                         CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
                         const int64_t blocks = std::min<int64_t>(ceil_div(units32, W), (int64_t)di.num_sms);
+                        prof_mark(st, true);   // right before the launch: host prep is not timed
                         kern<<<(unsigned)blocks, W * 32, smem, st>>>(code, rows, cols, ncols, ld32, out, L);
                         CSK_LAUNCH_CHECK();
                         return CSK_OK;
@@ -960,6 +964,7 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
                           : expv == 3 ? cs_bulk_kernel<T, C, 3> : cs_bulk_kernel<T, C, 0>;
                 CSK_CUDA_TRY(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
                 const int64_t blocks = std::min<int64_t>(ceil_div(units, C::kWarps), (int64_t)di.num_sms);
+                prof_mark(st, true);   // right before the launch: host prep is not timed
                 kb<<<(unsigned)blocks, C::kWarps * 32, smem, st>>>(code, rows, cols, ncols, ldtile, out, L);
                 CSK_LAUNCH_CHECK();
                 return CSK_OK;
@@ -981,6 +986,7 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
             CSK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowWarps * 32, smem));
             per_sm = std::max(per_sm, 1);
             const int64_t blocks = std::min<int64_t>(ceil_div(units, kRowWarps), (int64_t)di.num_sms * per_sm);
+            prof_mark(st, true);   // right before the launch: host prep is not timed
             kern<<<(unsigned)blocks, kRowWarps * 32, smem, st>>>(code, rows, cols, ncols, out, ldo);
             CSK_LAUNCH_CHECK();
             return CSK_OK;
@@ -1000,6 +1006,7 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
             const int64_t grid = std::max<int64_t>(
                 1, std::min<int64_t>((int64_t)di.num_sms * per_sm, ceil_div(total, 32 * kPrivDepth * 4)));
             const int64_t per_cta = ceil_div(total, grid);
+            prof_mark(st, true);   // right before the launch: host prep is not timed
             cs_smem_kernel<T><<<(unsigned)grid, cpc * 32, smem, st>>>(code, rows, cols, ncols, cpc,
                                                                         (int)plan->k1, out, ldo, per_cta);
             CSK_LAUNCH_CHECK();
@@ -1010,6 +1017,7 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
             CSK_REQUIRE(row_begin == 0 && row_end == plan->d, CSK_EUNSUPPORTED,
                         "variant G needs the whole block resident on the device");
             const int64_t blocks = std::min<int64_t>(ceil_div(plan->k1 * 32, 256), (int64_t)di.num_sms * 16);
+            prof_mark(st, true);   // right before the launch: host prep is not timed
             cs_sorted_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(code, plan->perm, plan->offsets, plan->k1, cols,
                                                                   ncols, out, ldo);
             CSK_LAUNCH_CHECK();
@@ -1117,7 +1125,6 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
         }
     }
     csk_status s;
-    prof_mark(st, true);
     if (dtype == CSK_F64) {
         Cols<double> cols{static_cast<const double*>(A), static_cast<const double*>(b), lda, (int)n};
         s = run_variant<double>(variant, plan, ncols, cols, row_begin, row_end, tgt.buf, tgt.ld, L, st);
@@ -1162,47 +1169,53 @@ extern "C" csk_status cs_apply(csk_plan_t plan, csk_dtype dtype, int64_t n, cons
 // ------------------------------------------------------------- profiling
 namespace csk {
 static thread_local bool g_prof = false;
-static thread_local std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_prof_events;
+// pool of events created by csk_profile_enable (no cudaEventCreate on the launch path);
+// g_prof_pairs[i] = (begin, end) indices of the i-th profiled launch
+static thread_local std::vector<cudaEvent_t> g_prof_pool;
+static thread_local size_t g_prof_next = 0;
+static thread_local std::vector<std::pair<int, int>> g_prof_pairs;
+constexpr size_t kProfPool = 4096;
 
 void prof_mark(cudaStream_t st, bool begin) {
-    if (!g_prof) return;
-    cudaEvent_t e;
-    if (cudaEventCreate(&e) != cudaSuccess) return;
-    cudaEventRecord(e, st);
-    if (begin)
-        g_prof_events.push_back({e, nullptr});
-    else if (!g_prof_events.empty() && g_prof_events.back().second == nullptr)
-        g_prof_events.back().second = e;
-    else
-        cudaEventDestroy(e);
+    if (!g_prof || g_prof_next >= g_prof_pool.size()) return;
+    if (begin) {
+        if (!g_prof_pairs.empty() && g_prof_pairs.back().second < 0) return;   // one open interval
+        cudaEventRecord(g_prof_pool[g_prof_next], st);
+        g_prof_pairs.push_back({(int)g_prof_next++, -1});
+    } else if (!g_prof_pairs.empty() && g_prof_pairs.back().second < 0) {
+        cudaEventRecord(g_prof_pool[g_prof_next], st);
+        g_prof_pairs.back().second = (int)g_prof_next++;
+    }
 }
 }  // namespace csk
 
 extern "C" void csk_profile_enable(int on) {
     csk::g_prof = on != 0;
-    for (auto& p : csk::g_prof_events) {
-        cudaEventDestroy(p.first);
-        if (p.second) cudaEventDestroy(p.second);
+    if (csk::g_prof && csk::g_prof_pool.empty()) {
+        csk::g_prof_pool.resize(csk::kProfPool);
+        for (auto& e : csk::g_prof_pool)
+            if (cudaEventCreate(&e) != cudaSuccess) {
+                csk::g_prof = false;
+                break;
+            }
     }
-    csk::g_prof_events.clear();
+    csk::g_prof_next = 0;
+    csk::g_prof_pairs.clear();
 }
 
 extern "C" csk_status csk_profile_read(double* total_ms, uint64_t* launches) {
     double sum = 0.0;
     uint64_t cnt = 0;
-    for (auto& p : csk::g_prof_events) {
-        if (!p.second) continue;
-        CSK_CUDA_TRY(cudaEventSynchronize(p.second));
+    for (auto& p : csk::g_prof_pairs) {
+        if (p.second < 0) continue;
+        CSK_CUDA_TRY(cudaEventSynchronize(csk::g_prof_pool[p.second]));
         float ms = 0.f;
-        CSK_CUDA_TRY(cudaEventElapsedTime(&ms, p.first, p.second));
+        CSK_CUDA_TRY(cudaEventElapsedTime(&ms, csk::g_prof_pool[p.first], csk::g_prof_pool[p.second]));
         sum += ms;
         ++cnt;
     }
-    for (auto& p : csk::g_prof_events) {
-        cudaEventDestroy(p.first);
-        if (p.second) cudaEventDestroy(p.second);
-    }
-    csk::g_prof_events.clear();
+    csk::g_prof_next = 0;
+    csk::g_prof_pairs.clear();
     if (total_ms) *total_ms = sum;
     if (launches) *launches = cnt;
     return CSK_OK;

@@ -11,8 +11,9 @@ fi
 timeout 900 python bench.py > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
 timeout 900 python bench.py --config c4 --no-cpu > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err
 timeout 900 python bench.py --config c3 --no-cpu --no-e2e > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file gpurun_out/launches_c2.csv python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu --no-acc > gpurun_out/ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'cs_(bulk|tma|row)' -c 1 -o gpurun_out/prof_c2_main python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-ne --no-acc --cs-only > gpurun_out/ncu_main.log 2>&1
-timeout 900 ncu --set full --clock-control none -k regex:'gemm|Kernel2' -c 1 -o gpurun_out/prof_c3_gstage python bench.py --config c3 --steps 1 --warmup 3 --no-e2e --no-cpu --no-ne --no-acc > gpurun_out/ncu_gstage.log 2>&1
+timeout 600 ncu --nvtx --nvtx-include "csk_timed/" --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2.csv python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu --no-acc --no-ne --no-ls --no-extra > gpurun_out/ncu_launch.log 2>&1
+python scripts/launch_share.py gpurun_out/launches_c2.csv 5 > gpurun_out/launch_share_c2.txt 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'cs_(bulk|tma|row)' -c 1 -o gpurun_out/prof_c2_main python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-ne --no-acc --no-ls --no-extra --cs-only > gpurun_out/ncu_main.log 2>&1
+timeout 900 ncu --set full --clock-control none -k regex:'gemm|Kernel2' -c 1 -o gpurun_out/prof_c3_gstage python bench.py --config c3 --steps 1 --warmup 3 --no-e2e --no-cpu --no-ne --no-acc --no-extra > gpurun_out/ncu_gstage.log 2>&1
 tail -2 gpurun_out/pytest_gpu.log; tail -1 gpurun_out/smoke.log
 for f in c2 c4 c3; do python -c "import json; d=json.load(open('gpurun_out/bench_$f.json')); print('$f', round(d['value'],1), d['unit'], 'step', round(d['ms_per_step'],3), 'cs', round(d['roofline']['kernel_ms'],3), 'frac', round(d['roofline']['frac'],3), 'ne', d['normal_equations'].get('ms'), d['normal_equations'].get('status'), 'speedup', d['speedup_vs_ne'], d['phases_ms'], d['accuracy'])" 2>&1 | tail -1; done

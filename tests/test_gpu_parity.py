@@ -398,3 +398,18 @@ def test_ne_lstsq_breaks_down_at_kappa_1e10():
         assert e.status == csk.csk.ENOTPD
         return
     assert oracle.residual_norm(A, b, x) / np.linalg.norm(b) > 1e-2
+
+
+def test_profile_hooks_time_the_main_kernel():
+    d, n, k1 = 1 << 16, 8, 64
+    A = synth.gaussian_matrix(d, n, seed=2)
+    plan = csk.cs_plan(d, k1, 1)
+    Ad = gpu_colmajor(A)
+    csk.profile_enable(True)
+    for _ in range(3):
+        csk.cs_apply(plan, Ad)
+    ms, launches = csk.profile_read()
+    csk.profile_enable(False)
+    assert launches == 3 and ms > 0.0
+    csk.cs_apply(plan, Ad)                    # disabled: nothing recorded
+    assert csk.profile_read() == (0.0, 0)
