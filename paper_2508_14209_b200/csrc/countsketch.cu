@@ -53,6 +53,26 @@ __device__ __forceinline__ T ldg_stream(const T* p) {
     return __ldcs(p);   // streaming: A is read exactly once
 }
 
+// Predicated streaming loads (branch-free; a lane with pred == false fetches nothing and
+// returns 0).  The address must still be legal: callers clamp it.
+__device__ __forceinline__ double ldcs_pred(const double* p, bool pred) {
+    double v = 0.0;
+    asm("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q ld.global.cs.f64 %0, [%1]; }" : "+d"(v) : "l"(p), "r"((int)pred));
+    return v;
+}
+__device__ __forceinline__ double ldcs_pred(const float* p, bool pred) {
+    float v = 0.0f;
+    asm("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q ld.global.cs.f32 %0, [%1]; }" : "+f"(v) : "l"(p), "r"((int)pred));
+    return (double)v;
+}
+__device__ __forceinline__ double2 ldcs2_pred(const double* p, bool pred) {
+    double2 v = make_double2(0.0, 0.0);
+    asm("{ .reg .pred q; setp.ne.b32 q, %3, 0; @q ld.global.cs.v2.f64 {%0, %1}, [%2]; }"
+        : "+d"(v.x), "+d"(v.y)
+        : "l"(p), "r"((int)pred));
+    return v;
+}
+
 // ------------------------------------------------------------------ variant L
 template <typename T>
 __global__ void __launch_bounds__(256) cs_col_kernel(const uint32_t* __restrict__ code, int64_t rows, Cols<T> cols,
@@ -419,7 +439,7 @@ struct BulkCfg {
 
 __host__ __device__ inline int bulk_chunk_width(int ncols) {
     if (ncols <= kBulkMaxCols) return ncols;
-    const int nch = (ncols + 63) / 64;
+    const int nch = (ncols + kBulkMaxCols - 1) / kBulkMaxCols;   // fewest chunks: each re-reads the codes
     return (((ncols + nch - 1) / nch) + 1) & ~1;   // even: every chunk start stays 16-B aligned
 }
 
@@ -429,8 +449,8 @@ __device__ __forceinline__ void bulk_load_tile(double (&v)[kBulkMaxCols / 2], co
 #pragma unroll
     for (int j = 0; j < kBulkMaxCols / 2; ++j) {
         const int c = 2 * j + half;
-        const double x = (double)ldg_stream(cols.col(min(c0 + c, ncols - 1)) + rc);
-        v[j] = (c < nc) ? x : 0.0;
+        // predicated: lanes past the chunk's last column fetch nothing (clamped legal address)
+        v[j] = ldcs_pred(cols.col(min(c0 + c, ncols - 1)) + rc, c < nc);
     }
 }
 
@@ -582,17 +602,16 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
 #pragma unroll
             for (int j = 0; j < kJ; ++j) {
                 const int c = 2 * j + half;
-                const double2 x = (EXP & 2) ? make_double2((double)ra, (double)c)
-                                            : __ldcs(reinterpret_cast<const double2*>(cols.col(min(c0 + c, ncols - 1)) + r0 + 2 * p));
-                v[j] = (c < nc) ? x : make_double2(0.0, 0.0);
+                // predicated loads: lanes past the chunk's last column fetch nothing
+                v[j] = (EXP & 2) ? make_double2((double)ra, (double)c)
+                                 : ldcs2_pred(cols.col(min(c0 + c, ncols - 1)) + r0 + 2 * p, c < nc);
             }
         } else {
 #pragma unroll
             for (int j = 0; j < kJ; ++j) {
                 const int c = 2 * j + half;
                 const double* col = cols.col(min(c0 + c, ncols - 1));
-                const double xa = __ldcs(col + ra), xb = __ldcs(col + rb);
-                v[j] = (c < nc) ? make_double2(xa, r0 + 2 * p + 1 < rows ? xb : 0.0) : make_double2(0.0, 0.0);
+                v[j] = make_double2(ldcs_pred(col + ra, c < nc), ldcs_pred(col + rb, c < nc && r0 + 2 * p + 1 < rows));
             }
         }
         // the TMA engine must have finished reading this tile (bulk ops of the previous unit)
@@ -935,7 +954,8 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
                         const size_t smem = (size_t)W * kB32Rows * ld32 * sizeof(double);
                         if (smem > (size_t)di.smem_optin) return CSK_EUNSUPPORTED;
                         CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                        const int64_t blocks = std::min<int64_t>(ceil_div(units32, W), (int64_t)di.num_sms);
+                        int64_t blocks = std::min<int64_t>(ceil_div(units32, W), (int64_t)di.num_sms);
+                        if (const char* g = std::getenv("CSK_GRID")) blocks = std::max(1, std::atoi(g));   // experiment
                         prof_mark(st, true);   // right before the launch: host prep is not timed
                         kern<<<(unsigned)blocks, W * 32, smem, st>>>(code, rows, cols, ncols, ld32, out, L);
                         CSK_LAUNCH_CHECK();
@@ -1083,6 +1103,18 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
             L.tma = tma;
             L.cw = !tma ? bulk_chunk_width(ncols) : variant == CSK_VAR_BULK_ROW ? b2_chunk_width(ncols)
                                                                                 : tma_chunk_width(ncols);
+            if (!tma && (int64_t)k1 * ncols * 8 > (int64_t)device_info().l2_bytes / 2) {
+                // Each chunk's SA^T slice must stay L2-resident (C3: 66-column slices of 69 MB
+                // ran at 53% of HBM, 52-column slices of 54 MB at 65%): the fewest
+                // chunks whose slice fits half of L2.
+                const int64_t fit = std::max<int64_t>(2, ((int64_t)device_info().l2_bytes / 2 / (8 * k1)) & ~1);
+                const int nch = (int)std::max<int64_t>(ceil_div(ncols, kBulkMaxCols), ceil_div(ncols, fit));
+                L.cw = std::min(kBulkMaxCols, (((ncols + nch - 1) / nch) + 1) & ~1);
+            }
+            if (const char* e = std::getenv("CSK_CW")) {   // experiment: force the chunk width (even, <= 66)
+                const int f = std::atoi(e) & ~1;
+                if (f >= 2 && f <= kBulkMaxCols && !tma) L.cw = std::min(f, (ncols + 1) & ~1);
+            }
             const int nchunks = (ncols + L.cw - 1) / L.cw;
             // chunk-major once SA^T would take more than 1/cm_div of L2 (CSK_CM_DIV, default 2)
             const char* cmd = std::getenv("CSK_CM_DIV");
@@ -1093,8 +1125,10 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
                 L.cs = k1 * L.lc;
                 ws_doubles = (size_t)nchunks * L.cs;
             } else {
-                L.lc = (ncols + 3) & ~3;
-                L.cs = L.cw;
+                // chunks start on 32-B sector boundaries inside a row (cw is even, cs a multiple of 4)
+                L.cs = nchunks > 1 ? (L.cw + 3) & ~3 : L.cw;
+                L.lc = std::max<int64_t>((ncols + 3) & ~3, nchunks * L.cs);
+                if (const char* e = std::getenv("CSK_LC")) L.lc = std::max<int64_t>(L.lc, std::atoi(e) & ~3);   // experiment
                 ws_doubles = (size_t)k1 * L.lc;
             }
         } else {
