@@ -22,6 +22,10 @@ Functions and the passage each follows (P:Lx = PAPER.md line x):
   ms_lstsq        the whole multisketch sketch-and-solve (Alg 1 with S = G S1)
   normal_eq       normal equations, ENOTPD on a non-positive pivot
   residual_norm   ||b - Ax|| (P:L338)
+  rand_cholqr_lstsq  rand_cholQR least squares, Alg 5, in the paper's order
+  srht_draws      the SRHT's D signs and sampled rows (Readings R16-R17)
+  fwht_rad4       Alg 3 radix-4 FWHT
+  srht_apply      SRHT S = k^-1/2 P H D (Def) applied to [A b]
 No function here is "parity unpinned"; each pin is listed in oracle.c's header.
 """
 from __future__ import annotations
@@ -77,6 +81,10 @@ def _load():
             lib.or_normal_eq.argtypes = [I64, I64, P, I64, P, P]
             lib.or_residual_norm.argtypes = [I64, I64, P, I64, P, P]
             lib.or_residual_norm.restype = ctypes.c_double
+            lib.or_rand_cholqr_lstsq.argtypes = [I64, I64, P, I64, P, P, I64, I64, P, P, I64]
+            lib.or_srht_draws.argtypes = [I64, I64, ctypes.c_uint64, P, P]
+            lib.or_fwht_rad4.argtypes = [I64, P]
+            lib.or_srht_apply.argtypes = [I64, I64, I64, ctypes.c_uint64, P, I64, P, P, I64]
             _lib = lib
     return _lib
 
@@ -218,3 +226,44 @@ def residual_norm(A, b, x) -> float:
     bb = np.ascontiguousarray(b, dtype=np.float64)
     xx = np.ascontiguousarray(x, dtype=np.float64)
     return float(_load().or_residual_norm(d, n, _ptr(A), d, _ptr(bb), _ptr(xx)))
+
+
+def rand_cholqr_lstsq(A, b, Y, return_R: bool = False):
+    """rand_cholQR least squares (Alg 5) given the sketch Y = S A (k x n)."""
+    A = _fortran(A, np.float64)
+    d, n = A.shape
+    Yf = _fortran(Y, np.float64)
+    k = Yf.shape[0]
+    assert Yf.shape[1] == n
+    bb = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.zeros(n, dtype=np.float64)
+    R = np.zeros((n, n), dtype=np.float64, order="F")
+    _check(_load().or_rand_cholqr_lstsq(d, n, _ptr(A), d, _ptr(bb), _ptr(Yf), k, k, _ptr(x), _ptr(R), n),
+           "rand_cholqr_lstsq")
+    return (x, R) if return_R else x
+
+
+def srht_draws(d: int, k: int, seed: int):
+    """(D signs int8[d], sampled rows int64[k]) of the SRHT."""
+    D = np.zeros(d, dtype=np.int8)
+    p = np.zeros(k, dtype=np.int64)
+    _check(_load().or_srht_draws(d, k, seed, _ptr(D), _ptr(p)), "srht_draws")
+    return D, p
+
+
+def fwht_rad4(a) -> np.ndarray:
+    v = np.array(a, dtype=np.float64, copy=True)
+    _check(_load().or_fwht_rad4(v.shape[0], _ptr(v)), "fwht_rad4")
+    return v
+
+
+def srht_apply(A, k: int, seed: int, b=None) -> np.ndarray:
+    """Y = k^-1/2 P H D [A b] (k x ncols)."""
+    A = _fortran(A, np.float64)
+    if A.ndim == 1:
+        A = A.reshape(-1, 1, order="F")
+    d, n = A.shape
+    bb = None if b is None else np.ascontiguousarray(b, dtype=np.float64)
+    Y = np.zeros((k, n + (b is not None)), dtype=np.float64, order="F")
+    _check(_load().or_srht_apply(d, n, k, seed, _ptr(A), d, _ptr(bb), _ptr(Y), k), "srht_apply")
+    return Y

@@ -29,6 +29,12 @@
  *   or_sketch_solve   numpy.linalg.lstsq on the oracle's Z (library);
  *                     identity sketch == QR least squares
  *   or_normal_eq      scipy.linalg.cho_solve (library); NOT_PD past kappa~1e8
+ *   or_rand_cholqr_lstsq  numpy.linalg.lstsq on A itself (library: rand_cholQR has no
+ *                     distortion); R^T R = A^T A and |R| = |qr(A).R|; identity sketch;
+ *                     stability at kappa = 1e10 where the normal equations fail
+ *   or_srht_draws     sign balance, uniform samples (chi-square)
+ *   or_fwht_rad4      scipy.linalg.hadamard (Sylvester) brute force; H H = d I; Parseval
+ *   or_srht_apply     dense (1/sqrt k) P H D A brute force; E||Sx||^2 = ||x||^2
  */
 #include <math.h>
 #include <stdint.h>
@@ -339,6 +345,177 @@ int or_normal_eq(int64_t d, int64_t n, const double* A, int64_t lda, const doubl
     }
     back_subst(n, C, n, z, x);
     free(C); free(y); free(z);
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------
+ * NEXT-1. rand_cholQR least squares, Alg 5 (Alg 4),
+ * written in the paper's order and notation:
+ *   1  Y = S A                      (given: the k x n sketch, here the multisketch G S1 A)
+ *   2  [~, R0] = qr(Y, 0)           (Householder, or_householder_qr)
+ *   3  Q0 = A R0^-1                 (row-wise forward substitution: q R0 = a, i.e. TRSM)
+ *   4  G = Q0^T Q0,  z = Q0^T b     (plain loops)
+ *   5  R1 = chol(G)                 (upper, ENOTPD on a non-positive pivot)
+ *   6  R = R1 R0
+ *   7  y = R1^-T z
+ *   8  x = R^-1 y
+ * R (nullable, n x n column-major, ldr) receives line 6's R.  Returns ESINGULAR if
+ * some |R0_ii| <= 1e-14 max|R0_jj| (as for sketch-and-solve).
+ * ---------------------------------------------------------------------- */
+int or_rand_cholqr_lstsq(int64_t d, int64_t n, const double* A, int64_t lda, const double* b,
+                         const double* Y, int64_t k, int64_t ldy, double* x, double* R, int64_t ldr) {
+    if (n < 1 || d < n || k < n || lda < d || ldy < k || !A || !b || !Y || !x || (R && ldr < n))
+        return OR_EINVAL;
+    double* W = (double*)malloc((size_t)(k * n) * sizeof(double));
+    double* R0 = (double*)malloc((size_t)(n * n) * sizeof(double));
+    double* Q0 = (double*)malloc((size_t)(d * n) * sizeof(double));
+    double* G = (double*)calloc((size_t)(n * n), sizeof(double));
+    double* z = (double*)calloc((size_t)n, sizeof(double));
+    double* Rf = (double*)calloc((size_t)(n * n), sizeof(double));
+    double* y = (double*)calloc((size_t)n, sizeof(double));
+    int st = OR_OK;
+    if (!W || !R0 || !Q0 || !G || !z || !Rf || !y) { st = OR_EINVAL; goto done; }
+    /* line 2 */
+    for (int64_t c = 0; c < n; ++c)
+        for (int64_t r = 0; r < k; ++r) W[r + c * k] = Y[r + c * ldy];
+    st = or_householder_qr(k, n, W, k, R0, n);
+    if (st != OR_OK) goto done;
+    {
+        double rmax = 0.0;
+        for (int64_t i = 0; i < n; ++i) rmax = fmax(rmax, fabs(R0[i + i * n]));
+        for (int64_t i = 0; i < n; ++i)
+            if (!(fabs(R0[i + i * n]) > 1e-14 * rmax)) { st = OR_ESINGULAR; goto done; }
+    }
+    /* line 3: for every row r, q R0 = a  =>  q_j = (a_j - sum_{l<j} q_l R0[l,j]) / R0[j,j] */
+    for (int64_t r = 0; r < d; ++r)
+        for (int64_t j = 0; j < n; ++j) {
+            double acc = A[r + j * lda];
+            for (int64_t l = 0; l < j; ++l) acc -= Q0[r + l * d] * R0[l + j * n];
+            Q0[r + j * d] = acc / R0[j + j * n];
+        }
+    /* line 4 */
+    for (int64_t j = 0; j < n; ++j) {
+        for (int64_t i = 0; i <= j; ++i) {
+            double acc = 0.0;
+            for (int64_t r = 0; r < d; ++r) acc += Q0[r + i * d] * Q0[r + j * d];
+            G[i + j * n] = acc;
+            G[j + i * n] = acc;
+        }
+        double acc = 0.0;
+        for (int64_t r = 0; r < d; ++r) acc += Q0[r + j * d] * b[r];
+        z[j] = acc;
+    }
+    /* line 5: upper Cholesky G = R1^T R1, R1 stored in the upper triangle of G */
+    for (int64_t j = 0; j < n; ++j) {
+        double piv = G[j + j * n];
+        for (int64_t l = 0; l < j; ++l) piv -= G[l + j * n] * G[l + j * n];
+        if (!(piv > 0.0)) { st = OR_ENOTPD; goto done; }
+        double rjj = sqrt(piv);
+        G[j + j * n] = rjj;
+        for (int64_t i = j + 1; i < n; ++i) {
+            double v = G[j + i * n];
+            for (int64_t l = 0; l < j; ++l) v -= G[l + j * n] * G[l + i * n];
+            G[j + i * n] = v / rjj;
+        }
+    }
+    /* line 6: R = R1 R0 (both upper) */
+    for (int64_t j = 0; j < n; ++j)
+        for (int64_t i = 0; i <= j; ++i) {
+            double acc = 0.0;
+            for (int64_t l = i; l <= j; ++l) acc += G[i + l * n] * R0[l + j * n];
+            Rf[i + j * n] = acc;
+        }
+    /* line 7: R1^T y = z (forward) */
+    for (int64_t i = 0; i < n; ++i) {
+        double acc = z[i];
+        for (int64_t l = 0; l < i; ++l) acc -= G[l + i * n] * y[l];
+        y[i] = acc / G[i + i * n];
+    }
+    /* line 8: R x = y (back) */
+    back_subst(n, Rf, n, y, x);
+    if (R)
+        for (int64_t j = 0; j < n; ++j)
+            for (int64_t i = 0; i < n; ++i) R[i + j * ldr] = Rf[i + j * n];
+done:
+    free(W); free(R0); free(Q0); free(G); free(z); free(Rf); free(y);
+    return st;
+}
+
+/* ------------------------------------------------------------------------
+ * NEXT-3. SRHT (Def): S = k^-1/2 P H_d D, d = 2^q.
+ *   D = diag(d_i), d_i = +-1: bit 0 of w_i, w_i = word (i & 3) of
+ *       Philox(ctr = (lo32(i>>2), hi32(i>>2), 6, 0), key = seed)      (stream 6, Reading R17)
+ *   P: k sampled rows p_j = mulhi32(v_j, d) (Lemire), v_j = word (j & 3) of
+ *       Philox(ctr = (lo32(j>>2), hi32(j>>2), 7, 0), key = seed)      (stream 7; i.i.d.
+ *       uniform row sampling with replacement, Reading R16)
+ *   H_d: Sylvester-ordered Hadamard, applied by Alg 3: radix-4 stages
+ *       at stride d/4, d/16, ..., with one radix-2 stage at stride 1 when q is odd
+ *       (Reading R18); 0-based indices i0 = b + k (the paper's b + k + 1 is 1-based).
+ * ---------------------------------------------------------------------- */
+static uint32_t stream_word(uint64_t seed, uint64_t i, uint32_t stream) {
+    uint32_t ctr[4] = {(uint32_t)(i >> 2), (uint32_t)(i >> 34), stream, 0u};
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    uint32_t x[4];
+    or_philox4x32_10(ctr, key, x);
+    return x[i & 3];
+}
+
+int or_srht_draws(int64_t d, int64_t k, uint64_t seed, int8_t* D, int64_t* p) {
+    if (d < 1 || k < 1 || (d & (d - 1)) || !D || !p) return OR_EINVAL;
+    for (int64_t i = 0; i < d; ++i) D[i] = (stream_word(seed, (uint64_t)i, 6u) & 1u) ? -1 : 1;
+    for (int64_t j = 0; j < k; ++j)
+        p[j] = (int64_t)(((uint64_t)stream_word(seed, (uint64_t)j, 7u) * (uint64_t)d) >> 32);
+    return OR_OK;
+}
+
+/* Alg 3, in place on a (length d = 2^q). */
+int or_fwht_rad4(int64_t d, double* a) {
+    if (d < 1 || (d & (d - 1)) || !a) return OR_EINVAL;
+    int64_t stride = d / 4;
+    while (stride >= 1) {
+        int64_t s4 = stride * 4;
+        for (int64_t b = 0; b <= d - s4; b += s4)
+            for (int64_t kk = 0; kk < stride; ++kk) {
+                int64_t i0 = b + kk, i1 = i0 + stride, i2 = i0 + 2 * stride, i3 = i0 + 3 * stride;
+                double x = a[i0], y = a[i1], zz = a[i2], t = a[i3];
+                double X = x + zz, Y = y + t, Z = x - zz, T = y - t;
+                a[i0] = X + Y; a[i1] = X - Y; a[i2] = Z + T; a[i3] = Z - T;
+            }
+        stride /= 4;
+    }
+    /* odd q: the radix-4 sweep ended at stride 2 (it covered bits q-1..1); bit 0 remains */
+    int q = 0;
+    while (((int64_t)1 << q) < d) ++q;
+    if (q & 1)
+        for (int64_t i0 = 0; i0 < d; i0 += 2) {
+            double x = a[i0], y = a[i0 + 1];
+            a[i0] = x + y; a[i0 + 1] = x - y;
+        }
+    return OR_OK;
+}
+
+/* Y = S [A b] (k x ncols, column-major, ldy): per column, v = D a; v = H v (Alg 3);
+ * Y[j, c] = v[p_j] / sqrt(k). */
+int or_srht_apply(int64_t d, int64_t n, int64_t k, uint64_t seed, const double* A, int64_t lda,
+                  const double* b, double* Y, int64_t ldy) {
+    int64_t ncols = n + (b ? 1 : 0);
+    if (d < 1 || (d & (d - 1)) || k < 1 || ncols < 1 || ldy < k || (n > 0 && (!A || lda < d)) || !Y)
+        return OR_EINVAL;
+    int8_t* D = (int8_t*)malloc((size_t)d);
+    int64_t* p = (int64_t*)malloc((size_t)k * sizeof(int64_t));
+    double* v = (double*)malloc((size_t)d * sizeof(double));
+    if (!D || !p || !v) { free(D); free(p); free(v); return OR_EINVAL; }
+    or_srht_draws(d, k, seed, D, p);
+    double scale = 1.0 / sqrt((double)k);
+    for (int64_t c = 0; c < ncols; ++c) {
+        for (int64_t i = 0; i < d; ++i) {
+            double a = (c < n) ? A[i + c * lda] : b[i];
+            v[i] = D[i] > 0 ? a : -a;
+        }
+        or_fwht_rad4(d, v);
+        for (int64_t j = 0; j < k; ++j) Y[j + c * ldy] = v[p[j]] * scale;
+    }
+    free(D); free(p); free(v);
     return OR_OK;
 }
 
