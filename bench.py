@@ -233,8 +233,15 @@ def ls_compare(args, cfg, kappa, dev, stream):
         except csk.CskError as e:
             return str(e).split(":")[1].strip()
 
+    def rc():
+        try:
+            csk.rc_lstsq(plan, k2, A, b, x=x)
+            return "OK"
+        except csk.CskError as e:
+            return str(e).split(":")[1].strip()
+
     out = {"kappa": kappa, "workload": cfg["name"].replace("kappa(A)=1e10", f"kappa(A)={kappa:.0e}")}
-    for name, fn in (("ms", ms), ("ne", ne)):
+    for name, fn in (("ms", ms), ("ne", ne), ("rc", rc)):
         for _ in range(args.warmup):
             fn()
         torch.cuda.synchronize()
@@ -243,14 +250,16 @@ def ls_compare(args, cfg, kappa, dev, stream):
         e1.record(stream)
         torch.cuda.synchronize()
         out[f"{name}_ms"] = e0.elapsed_time(e1) / args.steps
-        if name == "ne":
-            out["ne_status"] = res[-1]
+        if name in ("ne", "rc"):
+            out[f"{name}_status"] = res[-1]
         fn()
         out[f"{name}_rel_residual"] = float(torch.linalg.norm(b - A @ x) / torch.linalg.norm(b)) \
             if (name == "ms" or res[-1] == "OK") else None
     R = torch.linalg.qr(buf, mode="r")[1]
     out["true_rel_residual"] = float(abs(R[n, n]) / torch.linalg.norm(b))
     out["speedup_ms_vs_ne"] = out["ne_ms"] / out["ms_ms"]
+    # rand_cholQR: the true LS solution; its pass over A is TRSM d n^2 + Gram 2 d n^2 flops
+    out["rc_pass_gflop"] = 3.0 * d * n * n / 1e9
     del R, buf, A, b, Z
     torch.cuda.empty_cache()
     return out

@@ -157,6 +157,21 @@ csk_status ms_lstsq(csk_plan_t plan, int64_t k2, int64_t n, const double* A, int
 csk_status ne_lstsq(int64_t d, int64_t n, const double* A, int64_t lda, const double* b,
                     double* x, void* stream);
 
+/* rc_lstsq: rand_cholQR least squares, Alg 5 (Alg 4): the TRUE
+ * least-squares solution min ||A x - b|| (no sketch distortion), stable for kappa(A) < u^-1
+ * (P:L314-318).  Y = G S [A b] (ms_apply with this plan and k2), R0 = qr(Y)[:n,:n],
+ * Q0 = A R0^-1 by a row-chunked triangular solve, G = Q0^T Q0 and z = Q0^T b in the same pass,
+ * R1 = chol(G), x = R^-1 R1^-T z with R = R1 R0 (R23-R24).
+ *   A d x n (lda >= d), b length d, x n doubles: DEVICE pointers (d = the plan's d)
+ *   R  nullable DEVICE pointer: n x n column-major (ldr >= n) receives R = R1 R0, the R factor
+ *      of A (A = Q R with Q = A R^-1 orthonormal)
+ * Requires k2 >= n + 1 and k2 <= 512 (the cluster QR of ms_solve); n <= 1024.
+ * Returns CSK_ESINGULAR if the sketched R0 is numerically singular, CSK_ENOTPD if the Cholesky
+ * of Q0^T Q0 breaks down.  Workspace: k2*(n+1) + 3(n+1)^2 + (L2/4 bytes) doubles, stream-ordered.
+ * Synchronises the stream. */
+csk_status rc_lstsq(csk_plan_t plan, int64_t k2, int64_t n, const double* A, int64_t lda, const double* b,
+                    double* x, double* R, int64_t ldr, void* stream);
+
 /* ------------------------------------------------------------- utilities */
 const char* csk_status_str(csk_status st);
 const char* csk_last_error(void);      /* thread-local detail of the last failure */

@@ -66,6 +66,7 @@ def lib():
                 "ms_solve": [I64, I64, P, I64, P, P, P],
                 "ms_lstsq": [P, I64, I64, P, I64, P, P, P, P],
                 "ne_lstsq": [I64, I64, P, I64, P, P, P],
+                "rc_lstsq": [P, I64, I64, P, I64, P, P, P, I64, P],
             }
             for name, argt in sigs.items():
                 f = getattr(L, name)
@@ -274,3 +275,18 @@ def ne_lstsq(A, b, x=None, stream=None):
     pb, _ = _colmajor(b, "b")
     _check(lib().ne_lstsq(d, n, pA, lda, pb, ctypes.c_void_p(x.data_ptr()), _stream(stream, A.device)), "ne_lstsq")
     return x
+
+
+def rc_lstsq(plan: Plan, k2: int, A, b, x=None, want_R: bool = False, stream=None):
+    """rand_cholQR least squares (Alg 5): the true LS solution x (and R = R1 R0 if want_R)."""
+    torch = _torch()
+    d, n = A.shape
+    if x is None:
+        x = torch.empty(n, dtype=torch.float64, device=A.device)
+    R = torch.empty((n, n), dtype=torch.float64, device=A.device).t() if want_R else None
+    pA, lda = _colmajor(A, "A")
+    pb, _ = _colmajor(b, "b")
+    pR, ldr = _colmajor(R, "R") if want_R else (None, n)
+    _check(lib().rc_lstsq(plan.handle, k2, n, pA, lda, pb, ctypes.c_void_p(x.data_ptr()), pR, ldr,
+                          _stream(stream, A.device)), "rc_lstsq")
+    return (x, R) if want_R else x

@@ -9,6 +9,7 @@
 #include <mutex>
 #include <string>
 
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include "csk.h"
@@ -145,5 +146,17 @@ struct SolveStatus {
 csk_status qr_wy_launch(const double* Z, int64_t ldz, int m, int nc, double* Rg, int ldr, double* scratch,
                         double* x, SolveStatus* status, cudaStream_t st, bool* launched);
 size_t qr_wy_scratch_doubles(int m, int nc);
+// multisketch.cu: Z = G S [A b] (ms_apply) and the sketched QR solve (ms_solve).  solve_impl
+// optionally exports R (nc x nc upper, ld nc, device) for rand_cholQR's R0.
+csk_status ms_apply_impl(csk_plan_t plan, int64_t k2, csk_dtype dtype, int64_t n, const void* A, int64_t lda,
+                         const void* b, void* Z, int64_t ldz, cudaStream_t st);
+csk_status solve_impl(int64_t k2, int64_t n, const double* Z, int64_t ldz, double* x, double* sk_resid,
+                      cudaStream_t st, bool x_host, double* R_out);
+csk_status blas_handle(cudaStream_t st, cublasHandle_t* out);
+// normal_eq.cu: upper Cholesky of the augmented Gram C (nc x nc, upper part read) in S (ld nc);
+// x = R^-1 R^-T C[:n, n]; *status = CSK_ENOTPD on a non-positive pivot.
+__global__ void __launch_bounds__(1024, 1) chol_solve_kernel(const double* __restrict__ Cg, int nc, int use_smem,
+                                                             double* __restrict__ Sg,
+                                  double* __restrict__ x, int* __restrict__ status);
 
 }  // namespace csk

@@ -423,8 +423,8 @@ __global__ void __launch_bounds__(kQrcThreads, 1) qr_cluster_kernel(const double
     }
 }
 
-static csk_status solve_impl(int64_t k2, int64_t n, const double* Z, int64_t ldz, double* x, double* sk_resid,
-                             cudaStream_t st, bool x_host) {
+csk_status solve_impl(int64_t k2, int64_t n, const double* Z, int64_t ldz, double* x, double* sk_resid,
+                      cudaStream_t st, bool x_host, double* R_out) {
     CSK_REQUIRE(Z != nullptr && x != nullptr, CSK_EINVAL, "Z and x must be non-NULL");
     CSK_REQUIRE(n >= 1 && n <= 65535, CSK_EINVAL, "n=%lld must be in [1, 65535]", (long long)n);
     CSK_REQUIRE(k2 >= n + 1, CSK_ESHAPE, "k2=%lld must be >= n+1=%lld", (long long)k2, (long long)(n + 1));
@@ -449,7 +449,12 @@ static csk_status solve_impl(int64_t k2, int64_t n, const double* Z, int64_t ldz
             cudaFreeAsync(W, st);
             return ws;
         }
-        if (wy) goto launched;
+        if (wy) {
+            if (R_out)   // R (nc x nc, upper) -> caller's buffer, ld nc
+                CSK_CUDA_TRY(cudaMemcpy2DAsync(R_out, nc * 8, W, ((nc + 1) & ~1) * 8, nc * 8, nc,
+                                               cudaMemcpyDeviceToDevice, st));
+            goto launched;
+        }
     }
     {
     // cluster-distributed unblocked QR when a column slice fits shared memory on <= 8 CTAs
@@ -479,7 +484,13 @@ static csk_status solve_impl(int64_t k2, int64_t n, const double* Z, int64_t ldz
         // W doubles as the R output (ld = nc)
         CSK_CUDA_TRY(cudaLaunchKernelEx(&cfg, qr_cluster_kernel, Z, (int64_t)ldz, m, nc, P, W, nc, xd, sd));
         CSK_LAUNCH_CHECK();
+        if (R_out) CSK_CUDA_TRY(cudaMemcpyAsync(R_out, W, (size_t)nc * nc * 8, cudaMemcpyDeviceToDevice, st));
     } else {
+    if (R_out) {
+        cudaFreeAsync(W, st);
+        set_error("R export needs the cluster QR paths (k2=%lld, n=%lld too large)", (long long)k2, (long long)n);
+        return CSK_EUNSUPPORTED;
+    }
     CSK_CUDA_TRY(cudaMemcpy2DAsync(W, m * 8, Z, ldz * 8, m * 8, nc, cudaMemcpyDeviceToDevice, st));
     const size_t small = (size_t)(3 * nc + 2) * 8;
     const size_t smem_need = small + (size_t)m * nc * 8;
@@ -504,7 +515,7 @@ launched:
     return CSK_OK;
 }
 
-static csk_status ms_apply_impl(csk_plan_t plan, int64_t k2, csk_dtype dtype, int64_t n, const void* A, int64_t lda,
+csk_status ms_apply_impl(csk_plan_t plan, int64_t k2, csk_dtype dtype, int64_t n, const void* A, int64_t lda,
                                 const void* b, void* Z, int64_t ldz, cudaStream_t st) {
     CSK_REQUIRE(plan != nullptr, CSK_EINVAL, "plan is NULL");
     CSK_REQUIRE(Z != nullptr, CSK_EINVAL, "Z is NULL");
@@ -569,7 +580,7 @@ csk_status ms_apply(csk_plan_t plan, int64_t k2, csk_dtype dtype, int64_t n, con
 
 csk_status ms_solve(int64_t k2, int64_t n, const double* Z, int64_t ldz, double* x, double* sk_resid, void* stream) {
     CSK_REQUIRE(x == nullptr || is_device_pointer(x), CSK_EINVAL, "x must be a device pointer");
-    return solve_impl(k2, n, Z, ldz, x, sk_resid, (cudaStream_t)stream, false);
+    return solve_impl(k2, n, Z, ldz, x, sk_resid, (cudaStream_t)stream, false, nullptr);
 }
 
 csk_status ms_lstsq(csk_plan_t plan, int64_t k2, int64_t n, const double* A, int64_t lda, const double* b, double* x,
@@ -582,7 +593,7 @@ csk_status ms_lstsq(csk_plan_t plan, int64_t k2, int64_t n, const double* A, int
     double* Z = nullptr;
     CSK_CUDA_TRY(cudaMallocAsync(&Z, (size_t)k2 * (n + 1) * 8, st));
     csk_status s = ms_apply_impl(plan, k2, CSK_F64, n, A, lda, b, Z, k2, st);
-    if (s == CSK_OK) s = solve_impl(k2, n, Z, k2, x, sk_resid, st, !is_device_pointer(x));
+    if (s == CSK_OK) s = solve_impl(k2, n, Z, k2, x, sk_resid, st, !is_device_pointer(x), nullptr);
     cudaFreeAsync(Z, st);
     return s;
 }

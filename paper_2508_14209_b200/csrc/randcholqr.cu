@@ -1,0 +1,313 @@
+// randcholqr.cu -- rc_lstsq: rand_cholQR least squares, Alg 5.
+//
+//   1  Y = S A                    ms_apply_impl on [A b] (the multisketch G S1 of this path, R23)
+//   2  [~, R0] = qr(Y, 0)         the cluster Householder QR of ms_solve (R0 = R[:n,:n] of [Y | Sb])
+//   3  Q0 = A R0^-1               row-chunked TRSM (R24: a triangular solve, not an explicit inverse)
+//   4  G = Q0^T Q0, z = Q0^T b    accumulated chunk by chunk while the chunk is L2-resident
+//   5  R1 = chol(G)               chol_solve_kernel (normal_eq.cu), which also returns u = R1^-1 R1^-T z
+//   6  R = R1 R0                  rc_finish_kernel (only when the caller asks for R)
+//   7-8 x = R^-1 R1^-T z          = R0^-1 u (R23), rc_finish_kernel
+//
+// Lines 3-4 are the single pass over A: each chunk of rows is copied into an
+// L2-sized workspace, solved in place against R0 (cuBLAS DTRSM), and folded into the Gram with
+// DGEMM (Q0^T Q0, n x n: the K = rows split keeps it at the DMMA roofline when n is a multiple of
+// 64) and DGEMV (Q0^T b); Q0 never reaches HBM as a whole.
+#include <algorithm>
+#include <cstdlib>
+
+#include <cublas_v2.h>
+
+#include "csk_internal.cuh"
+
+namespace csk {
+
+// x = R0^-1 u (back substitution, R0 upper n x n, ld ldr0), and optionally R = R1 R0 with R1 the
+// upper Cholesky factor left in S (ld nc).  One CTA.
+__global__ void __launch_bounds__(1024, 1) rc_finish_kernel(const double* __restrict__ R0, int ldr0,
+                                                            const double* __restrict__ S, int nc, int n,
+                                                            const double* __restrict__ u, double* __restrict__ x,
+                                                            double* __restrict__ R, int ldr,
+                                                            const int* __restrict__ chol_status) {
+    if (*chol_status != 0) return;
+    extern __shared__ double fsm[];
+    double* y = fsm;   // n
+    for (int i = threadIdx.x; i < n; i += blockDim.x) y[i] = u[i];
+    __syncthreads();
+    for (int c = n - 1; c >= 0; --c) {
+        const double xc = y[c] / R0[c + (int64_t)c * ldr0];
+        __syncthreads();
+        for (int i = threadIdx.x; i < c; i += blockDim.x) y[i] -= R0[i + (int64_t)c * ldr0] * xc;
+        if (threadIdx.x == 0) x[c] = xc;
+        __syncthreads();
+    }
+    if (R != nullptr) {
+        // R[i,j] = sum_{l=i..j} R1[i,l] R0[l,j]
+        for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+            const int i = e % n, j = e / n;
+            double acc = 0.0;
+            for (int l = i; l <= j; ++l) acc += S[i + (int64_t)l * nc] * R0[l + (int64_t)j * ldr0];
+            R[i + (int64_t)j * ldr] = i <= j ? acc : 0.0;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- fused pass (lines 3-4)
+// One persistent CTA per SM walks 64-row tiles of A.  fp64 tensor cores (DMMA 8x8x4, the native
+// fp64 MMA of sm_100a: every f64 mma.sync shape lowers to it) do both halves:
+//  * TRSM (line 3): warp w owns rows 8w..8w+7 of the tile and solves them alone (rows are
+//    independent): for each 8-column block J, T = A[:, J] - Q[:, <J] R0[<J, J] (2J DMMAs with
+//    the warp's own Q rows as the A operand, R0 from shared memory as B), then the 8x8 diagonal
+//    block by substitution inside each 4-lane row group (shuffles, true division as in Alg 5);
+//    Q rows go to shared memory.  No CTA barrier inside the solve.
+//  * Gram (line 4): after one barrier the 8 warps accumulate Q^T Q over the tile into the upper
+//    8x8 blocks of C (block (I,J), I <= J, dealt round-robin to warps; accumulators stay in
+//    registers for the whole kernel) and z = Q^T b with plain FMAs.
+// Each CTA writes its partial [C | z] once; rc_reduce_kernel sums the partials in a fixed order.
+// Shared memory: R0 as [j][k] with ld = NP + 4 and Q as [row][col] with ld = NP + 4 (both
+// == 4 mod 16 doubles: the fragment loads of a half-warp touch 16 distinct bank pairs).
+constexpr int kRcRows = 64;     // rows per tile (8 per warp)
+constexpr int kRcWarps = 8;
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+template <int NB>   // NP = 8 * NB padded columns (n <= NP)
+__global__ void __launch_bounds__(kRcWarps * 32, 1) rc_pass_kernel(const double* __restrict__ A, int64_t lda,
+                                                                   const double* __restrict__ b, int64_t d, int n,
+                                                                   const double* __restrict__ R0g, int ldr0g,
+                                                                   double* __restrict__ part, int nc) {
+    constexpr int NP = 8 * NB, LD = NP + 4;
+    constexpr int NBLK = NB * (NB + 1) / 2;
+    constexpr int PER = (NBLK + kRcWarps - 1) / kRcWarps;
+    extern __shared__ __align__(16) double rsm[];
+    double* R0s = rsm;                       // [NP][LD]: R0s[j * LD + k] = R0[k][j]
+    double* Qs = R0s + NP * LD;              // [kRcRows][LD]
+    double* bs = Qs + kRcRows * LD;          // [kRcRows]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;   // fragment row group / thread in group
+    for (int e = threadIdx.x; e < NP * NP; e += blockDim.x) {
+        const int k = e % NP, j = e / NP;
+        double v = (k < n && j < n) ? R0g[k + (int64_t)j * ldr0g] : (k == j ? 1.0 : 0.0);
+        R0s[j * LD + k] = (k <= j) ? v : 0.0;
+    }
+    double acc[PER][2];
+#pragma unroll
+    for (int p = 0; p < PER; ++p) acc[p][0] = acc[p][1] = 0.0;
+    double zacc = 0.0;   // thread i < NP: z[i]
+    __syncthreads();
+    const int64_t ntiles = (d + kRcRows - 1) / kRcRows;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t r0 = tile * kRcRows;
+        const int64_t row = r0 + 8 * warp + g;            // this lane's row in the solve
+        const bool rv = row < d;
+        const double* arow = A + (rv ? row : 0);
+        for (int e = threadIdx.x; e < kRcRows; e += blockDim.x) bs[e] = (r0 + e < d) ? b[r0 + e] : 0.0;
+        // ---- TRSM: rows 8*warp .. +8, column blocks J = 0 .. NB-1
+        double* qrow = Qs + (8 * warp + g) * LD;
+        double nx0, nx1;   // prefetched A[row, 8J + 2t + {0,1}]
+        {
+            const int c0 = 2 * t, c1 = 2 * t + 1;
+            nx0 = (rv && c0 < n) ? __ldcs(arow + (int64_t)c0 * lda) : 0.0;
+            nx1 = (rv && c1 < n) ? __ldcs(arow + (int64_t)c1 * lda) : 0.0;
+        }
+#pragma unroll 1
+        for (int J = 0; J < NB; ++J) {
+            double t0 = nx0, t1 = nx1;
+            if (J + 1 < NB) {
+                const int c0 = 8 * (J + 1) + 2 * t, c1 = c0 + 1;
+                nx0 = (rv && c0 < n) ? __ldcs(arow + (int64_t)c0 * lda) : 0.0;
+                nx1 = (rv && c1 < n) ? __ldcs(arow + (int64_t)c1 * lda) : 0.0;
+            }
+            // two interleaved accumulation chains over k = 0 .. 8J
+            double u0 = 0.0, u1 = 0.0, v0 = 0.0, v1 = 0.0;
+            const double* qa = Qs + (8 * warp + g) * LD + t;      // A operand: Q[8w + g][k + t]
+            const double* rb = R0s + (8 * J + g) * LD + t;        // B operand: R0[k + t][8J + g]
+            for (int k = 0; k < 8 * J; k += 8) {
+                dmma884(u0, u1, qa[k], rb[k]);
+                dmma884(v0, v1, qa[k + 4], rb[k + 4]);
+            }
+            t0 -= u0 + v0;
+            t1 -= u1 + v1;
+            // 8x8 diagonal block: substitution inside the row group (lane holds cols 2t, 2t+1)
+            const double* rd = R0s + (8 * J) * LD + 8 * J;          // rd[c' * LD + c] = R0[8J+c][8J+c']
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const double own = (c & 1) ? t1 : t0;
+                const double qc_own = own / rd[c * LD + c];
+                const double qc = __shfl_sync(0xffffffffu, qc_own, (lane & ~3) | (c >> 1));
+                if (2 * t == c) t0 = qc;
+                if (2 * t + 1 == c) t1 = qc;
+                if (2 * t > c) t0 -= qc * rd[(2 * t) * LD + c];
+                if (2 * t + 1 > c) t1 -= qc * rd[(2 * t + 1) * LD + c];
+            }
+            *reinterpret_cast<double2*>(qrow + 8 * J + 2 * t) = make_double2(t0, t1);
+            __syncwarp();
+        }
+        __syncthreads();
+        // ---- Gram: C[8I.., 8J..] += Q[:, I-block]^T Q[:, J-block] over the 64 tile rows
+#pragma unroll
+        for (int p = 0; p < PER; ++p) {
+            const int blk = warp + p * kRcWarps;
+            if (blk < NBLK) {
+                // blk -> (I, J), I <= J, column-major over the upper triangle
+                int J = 0;
+                while ((J + 1) * (J + 2) / 2 <= blk) ++J;
+                const int I = blk - J * (J + 1) / 2;
+                const double* qa = Qs + t * LD + 8 * I + g;   // A operand: Q^T[8I + g][k + t] = Q[k + t][8I + g]
+                const double* qb = Qs + t * LD + 8 * J + g;   // B operand: Q[k + t][8J + g]
+                double w0 = 0.0, w1 = 0.0;
+#pragma unroll 4
+                for (int k = 0; k < kRcRows; k += 8) {
+                    dmma884(acc[p][0], acc[p][1], qa[k * LD], qb[k * LD]);
+                    dmma884(w0, w1, qa[(k + 4) * LD], qb[(k + 4) * LD]);
+                }
+                acc[p][0] += w0;
+                acc[p][1] += w1;
+            }
+        }
+        if (threadIdx.x < NP) {
+            double s = 0.0;
+            for (int r = 0; r < kRcRows; ++r) s += Qs[r * LD + threadIdx.x] * bs[r];
+            zacc += s;
+        }
+        __syncthreads();   // Qs and bs are rewritten by the next tile
+    }
+    // ---- this CTA's partial [C | z] (nc x nc column-major, upper blocks + column n)
+    double* P = part + (size_t)blockIdx.x * nc * nc;
+#pragma unroll
+    for (int p = 0; p < PER; ++p) {
+        const int blk = warp + p * kRcWarps;
+        if (blk < NBLK) {
+            int J = 0;
+            while ((J + 1) * (J + 2) / 2 <= blk) ++J;
+            const int I = blk - J * (J + 1) / 2;
+            const int i = 8 * I + g, j0 = 8 * J + 2 * t;
+            if (i < n && j0 < n) P[i + (int64_t)j0 * nc] = acc[p][0];
+            if (i < n && j0 + 1 < n) P[i + (int64_t)(j0 + 1) * nc] = acc[p][1];
+        }
+    }
+    if (threadIdx.x < n) P[threadIdx.x + (int64_t)(nc - 1) * nc] = zacc;
+}
+
+// C[e] = sum_p part[p][e], fixed order (deterministic for a given grid)
+__global__ void rc_reduce_kernel(const double* __restrict__ part, int parts, int64_t elems, double* __restrict__ C) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < elems; e += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int p = 0; p < parts; ++p) s += part[(size_t)p * elems + e];
+        C[e] = s;
+    }
+}
+
+static csk_status rc_impl(csk_plan_t plan, int64_t k2, int64_t n, const double* A, int64_t lda, const double* b,
+                          double* x, double* R, int64_t ldr, cudaStream_t st) {
+    CSK_REQUIRE(plan != nullptr, CSK_EINVAL, "plan is NULL");
+    CSK_REQUIRE(A != nullptr && b != nullptr && x != nullptr, CSK_EINVAL, "A, b, x must be non-NULL");
+    CSK_REQUIRE(n >= 1 && n <= 1024, CSK_EINVAL, "n=%lld must be in [1, 1024]", (long long)n);
+    CSK_REQUIRE(k2 >= n + 1, CSK_ESHAPE, "k2=%lld must be >= n+1=%lld", (long long)k2, (long long)(n + 1));
+    const int64_t d = plan->d;
+    CSK_REQUIRE(d >= n, CSK_ESHAPE, "d=%lld < n=%lld", (long long)d, (long long)n);
+    CSK_REQUIRE(lda >= d, CSK_ESHAPE, "lda=%lld < d=%lld", (long long)lda, (long long)d);
+    CSK_REQUIRE(R == nullptr || ldr >= n, CSK_ESHAPE, "ldr=%lld < n", (long long)ldr);
+    CSK_REQUIRE(is_device_pointer(A) && is_device_pointer(b) && is_device_pointer(x) &&
+                    (R == nullptr || is_device_pointer(R)),
+                CSK_EINVAL, "rc_lstsq takes device pointers");
+    const int nc = (int)n + 1;
+    // chunk rows: the chunk's Q0 (rows x n doubles) stays L2-resident between TRSM and GEMM
+    int64_t mc = (int64_t)device_info().l2_bytes / 4 / (8 * n);
+    if (const char* e = std::getenv("CSK_RC_CHUNK")) mc = std::max<int64_t>(256, std::atoll(e));
+    mc = std::max<int64_t>(1024, mc & ~(int64_t)255);
+    mc = std::min(mc, d);
+    cublasHandle_t h;
+    csk_status s = blas_handle(st, &h);
+    if (s != CSK_OK) return s;
+    // workspace: Z (k2 x nc) | R0aug (nc x nc) | xs (nc) | C (nc x nc) | S (nc x nc) | u (nc) | Wk (mc x n) | status
+    auto pad = [](size_t cnt) { return (cnt + 31) & ~(size_t)31; };   // 256-B aligned regions
+    const size_t zd = pad((size_t)k2 * nc), rd = pad((size_t)nc * nc), vd = pad(nc);
+    const size_t total = zd + 3 * rd + 2 * vd + pad((size_t)mc * n) + 32;
+    double* ws = nullptr;
+    CSK_CUDA_TRY(cudaMallocAsync(&ws, total * 8, st));
+    double* Z = ws;
+    double* R0 = Z + zd;
+    double* xs = R0 + rd;
+    double* C = xs + vd;
+    double* S = C + rd;
+    double* u = S + rd;
+    double* Wk = u + vd;
+    int* sd = reinterpret_cast<int*>(Wk + pad((size_t)mc * n));
+    // lines 1-2
+    s = ms_apply_impl(plan, k2, CSK_F64, n, A, lda, b, Z, k2, st);
+    if (s == CSK_OK) s = solve_impl(k2, n, Z, k2, xs, nullptr, st, false, R0);
+    if (s != CSK_OK) {
+        cudaFreeAsync(ws, st);
+        return s;
+    }
+    // lines 3-4
+    const char* pe = std::getenv("CSK_RC_PATH");
+    const bool fused = n <= 128 && !(pe && std::atoi(pe) == 0);
+    if (fused) {
+        const int nb = n <= 16 ? 2 : n <= 32 ? 4 : n <= 64 ? 8 : 16;
+        const int NP = 8 * nb, LD = NP + 4;
+        const size_t smem = ((size_t)NP * LD + (size_t)kRcRows * LD + kRcRows) * 8;
+        const DeviceInfo& di = device_info();
+        const int64_t tiles = ceil_div(d, kRcRows);
+        const int grid = (int)std::min<int64_t>(tiles, di.num_sms);
+        double* part = nullptr;
+        CSK_CUDA_TRY(cudaMallocAsync(&part, (size_t)grid * nc * nc * 8, st));
+        CSK_CUDA_TRY(cudaMemsetAsync(part, 0, (size_t)grid * nc * nc * 8, st));
+        auto kern = nb == 2 ? rc_pass_kernel<2> : nb == 4 ? rc_pass_kernel<4> : nb == 8 ? rc_pass_kernel<8>
+                                                                                          : rc_pass_kernel<16>;
+        CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<grid, kRcWarps * 32, smem, st>>>(A, lda, b, d, (int)n, R0, nc, part, nc);
+        CSK_LAUNCH_CHECK();
+        rc_reduce_kernel<<<(unsigned)std::min<int64_t>(ceil_div((int64_t)nc * nc, 256), 1024), 256, 0, st>>>(
+            part, grid, (int64_t)nc * nc, C);
+        CSK_LAUNCH_CHECK();
+        CSK_CUDA_TRY(cudaFreeAsync(part, st));
+    }
+    const double one = 1.0, zero = 0.0;
+    cublasStatus_t bs = CUBLAS_STATUS_SUCCESS;
+    for (int64_t r0 = 0; !fused && r0 < d && bs == CUBLAS_STATUS_SUCCESS; r0 += mc) {
+        const int64_t m = std::min(mc, d - r0);
+        const double* beta = r0 == 0 ? &zero : &one;
+        CSK_CUDA_TRY(cudaMemcpy2DAsync(Wk, m * 8, A + r0, lda * 8, m * 8, n, cudaMemcpyDeviceToDevice, st));
+        bs = cublasDtrsm(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)m, (int)n,
+                         &one, R0, nc, Wk, (int)m);
+        if (bs == CUBLAS_STATUS_SUCCESS)
+            bs = cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)n, (int)n, (int)m, &one, Wk, (int)m, Wk, (int)m, beta,
+                             C, nc);
+        if (bs == CUBLAS_STATUS_SUCCESS)
+            bs = cublasDgemv(h, CUBLAS_OP_T, (int)m, (int)n, &one, Wk, (int)m, b + r0, 1, beta, C + (size_t)n * nc, 1);
+    }
+    if (bs != CUBLAS_STATUS_SUCCESS) {
+        cudaFreeAsync(ws, st);
+        set_error("cuBLAS rand_cholQR pass failed (%d)", (int)bs);
+        return CSK_ECUDA;
+    }
+    CSK_CUDA_TRY(cudaMemsetAsync(C + (size_t)n * nc + n, 0, 8, st));   // b^T b is not needed for x
+    // line 5 (+ R1^-T z and R1^-1 of it)
+    CSK_CUDA_TRY(cudaFuncSetAttribute(chol_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 0));
+    chol_solve_kernel<<<1, 1024, 0, st>>>(C, nc, 0, S, u, sd);
+    CSK_LAUNCH_CHECK();
+    // lines 6-8
+    rc_finish_kernel<<<1, 1024, (size_t)n * 8, st>>>(R0, nc, S, nc, (int)n, u, x, R, (int)ldr, sd);
+    CSK_LAUNCH_CHECK();
+    int hs = 0;
+    CSK_CUDA_TRY(cudaMemcpyAsync(&hs, sd, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CSK_CUDA_TRY(cudaFreeAsync(ws, st));
+    CSK_CUDA_TRY(cudaStreamSynchronize(st));
+    if (hs != 0) {
+        set_error("rand_cholQR: Cholesky of Q0^T Q0 failed (pivot <= 0)");
+        return (csk_status)hs;
+    }
+    return CSK_OK;
+}
+
+}  // namespace csk
+
+extern "C" csk_status rc_lstsq(csk_plan_t plan, int64_t k2, int64_t n, const double* A, int64_t lda, const double* b,
+                               double* x, double* R, int64_t ldr, void* stream) {
+    return csk::rc_impl(plan, k2, n, A, lda, b, x, R, ldr, (cudaStream_t)stream);
+}
