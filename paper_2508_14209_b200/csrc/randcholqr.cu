@@ -63,8 +63,9 @@ __global__ void __launch_bounds__(1024, 1) rc_finish_kernel(const double* __rest
 //    8x8 blocks of C (block (I,J), I <= J, dealt round-robin to warps; accumulators stay in
 //    registers for the whole kernel) and z = Q^T b with plain FMAs.
 // Each CTA writes its partial [C | z] once; rc_reduce_kernel sums the partials in a fixed order.
-// Shared memory: R0 as [j][k] with ld = NP + 4 and Q as [row][col] with ld = NP + 4 (both
-// == 4 mod 16 doubles: the fragment loads of a half-warp touch 16 distinct bank pairs).
+// Shared memory: packed upper R0 (8-column blocks), Q as [row][col] with ld = NP + 4 (== 4 mod 16
+// doubles: the fragment loads of a half-warp touch 16 distinct bank pairs), the A tile staged by
+// cp.async (the next tile's copy overlaps this tile's Gram) and b.
 constexpr int kRcRows = 64;     // rows per tile (8 per warp)
 constexpr int kRcWarps = 8;
 
@@ -74,120 +75,157 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
                  : "d"(a), "d"(b));
 }
 
+__device__ __forceinline__ void rc_cp_async(double* dst, const double* src, int bytes, int src_bytes) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+    if (bytes == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
+}
+
+// Packed upper R0: 8-column block J holds rows 0 .. 8J+7 of its columns with ld 8J + 12
+// (== 4 or 12 mod 16: conflict-free fragment loads), at offset 32 J (J-1) + 96 J.
+__host__ __device__ constexpr int rc_r0_off(int J) { return 32 * J * (J - 1) + 96 * J; }
+
 template <int NB>   // NP = 8 * NB padded columns (n <= NP)
 __global__ void __launch_bounds__(kRcWarps * 32, 1) rc_pass_kernel(const double* __restrict__ A, int64_t lda,
                                                                    const double* __restrict__ b, int64_t d, int n,
                                                                    const double* __restrict__ R0g, int ldr0g,
-                                                                   double* __restrict__ part, int nc) {
-    constexpr int NP = 8 * NB, LD = NP + 4;
-    constexpr int NBLK = NB * (NB + 1) / 2;
-    constexpr int PER = (NBLK + kRcWarps - 1) / kRcWarps;
+                                                                   double* __restrict__ part, int nc, int al16) {
+    constexpr int NP = 8 * NB, LD = NP + 4, LDA = kRcRows + 4;
+    constexpr int NPAIR = NB / 2, KS = kRcWarps / NPAIR, GK = kRcRows / KS;   // k split of the Gram
     extern __shared__ __align__(16) double rsm[];
-    double* R0s = rsm;                       // [NP][LD]: R0s[j * LD + k] = R0[k][j]
-    double* Qs = R0s + NP * LD;              // [kRcRows][LD]
-    double* bs = Qs + kRcRows * LD;          // [kRcRows]
+    double* R0p = rsm;                           // packed upper R0 (rc_r0_off(NB) doubles)
+    double* Qs = R0p + rc_r0_off(NB);            // [kRcRows][LD]   Q rows of the tile
+    double* As = Qs + kRcRows * LD;              // [NP][LDA]       A tile, column-major (cp.async-staged)
+    double* bs = As + NP * LDA;                  // [2][kRcRows]    b tiles (double-buffered)
+    double* invd = bs + 2 * kRcRows;             // [NP]            1 / R0[j][j]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t = lane & 3;   // fragment row group / thread in group
-    for (int e = threadIdx.x; e < NP * NP; e += blockDim.x) {
-        const int k = e % NP, j = e / NP;
-        double v = (k < n && j < n) ? R0g[k + (int64_t)j * ldr0g] : (k == j ? 1.0 : 0.0);
-        R0s[j * LD + k] = (k <= j) ? v : 0.0;
-    }
-    double acc[PER][2];
-#pragma unroll
-    for (int p = 0; p < PER; ++p) acc[p][0] = acc[p][1] = 0.0;
-    double zacc = 0.0;   // thread i < NP: z[i]
-    __syncthreads();
-    const int64_t ntiles = (d + kRcRows - 1) / kRcRows;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t r0 = tile * kRcRows;
-        const int64_t row = r0 + 8 * warp + g;            // this lane's row in the solve
-        const bool rv = row < d;
-        const double* arow = A + (rv ? row : 0);
-        for (int e = threadIdx.x; e < kRcRows; e += blockDim.x) bs[e] = (r0 + e < d) ? b[r0 + e] : 0.0;
-        // ---- TRSM: rows 8*warp .. +8, column blocks J = 0 .. NB-1
-        double* qrow = Qs + (8 * warp + g) * LD;
-        double nx0, nx1;   // prefetched A[row, 8J + 2t + {0,1}]
-        {
-            const int c0 = 2 * t, c1 = 2 * t + 1;
-            nx0 = (rv && c0 < n) ? __ldcs(arow + (int64_t)c0 * lda) : 0.0;
-            nx1 = (rv && c1 < n) ? __ldcs(arow + (int64_t)c1 * lda) : 0.0;
+    for (int J = 0; J < NB; ++J)
+        for (int e = threadIdx.x; e < 8 * (8 * J + 8); e += blockDim.x) {
+            const int k = e % (8 * J + 8), j = 8 * J + e / (8 * J + 8);
+            const double v = (k < n && j < n) ? R0g[k + (int64_t)j * ldr0g] : (k == j ? 1.0 : 0.0);
+            R0p[rc_r0_off(J) + (j - 8 * J) * (8 * J + 12) + k] = (k <= j) ? v : 0.0;
+            if (k == j) invd[j] = 1.0 / v;
         }
+    const int J1 = warp % NPAIR, J2 = NB - 1 - J1, gk0 = (warp / NPAIR) * GK;
+    double acc[NB + 1][2];
+#pragma unroll
+    for (int p = 0; p <= NB; ++p) acc[p][0] = acc[p][1] = 0.0;
+    double zacc = 0.0;   // thread i < NP: z[i]
+    const int64_t ntiles = (d + kRcRows - 1) / kRcRows;
+    // stage a tile's A (n columns x 64 rows) and b into shared memory; rows >= d are zero-filled
+    auto stage = [&](int64_t tile, double* bdst) {
+        const int64_t r0 = tile * kRcRows;
+        if (al16) {
+            for (int e = threadIdx.x; e < (n + 1) * (kRcRows / 2); e += blockDim.x) {
+                const int c = e / (kRcRows / 2), r = 2 * (e % (kRcRows / 2));
+                const int64_t row = r0 + r;
+                const int src = row + 1 < d ? 16 : (row < d ? 8 : 0);
+                const double* gp = c < n ? A + (int64_t)c * lda : b;
+                rc_cp_async(c < n ? As + c * LDA + r : bdst + r, gp + (src ? row : 0), 16, src);
+            }
+        } else {
+            for (int e = threadIdx.x; e < (n + 1) * kRcRows; e += blockDim.x) {
+                const int c = e / kRcRows, r = e % kRcRows;
+                const int64_t row = r0 + r;
+                const double* gp = c < n ? A + (int64_t)c * lda : b;
+                rc_cp_async(c < n ? As + c * LDA + r : bdst + r, gp + (row < d ? row : 0), 8, row < d ? 8 : 0);
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    int buf = 0;
+    if (blockIdx.x < ntiles) stage(blockIdx.x, bs);
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        // ---- TRSM: rows 8*warp .. +8, column blocks J = 0 .. NB-1 (warp-local)
+        const double* arow = As + 8 * warp + g;
+        double* qrow = Qs + (8 * warp + g) * LD;
 #pragma unroll 1
         for (int J = 0; J < NB; ++J) {
-            double t0 = nx0, t1 = nx1;
-            if (J + 1 < NB) {
-                const int c0 = 8 * (J + 1) + 2 * t, c1 = c0 + 1;
-                nx0 = (rv && c0 < n) ? __ldcs(arow + (int64_t)c0 * lda) : 0.0;
-                nx1 = (rv && c1 < n) ? __ldcs(arow + (int64_t)c1 * lda) : 0.0;
+            const int c0 = 8 * J + 2 * t;
+            double t0 = c0 < n ? arow[c0 * LDA] : 0.0;
+            double t1 = c0 + 1 < n ? arow[(c0 + 1) * LDA] : 0.0;
+            // four interleaved accumulation chains over k = 0 .. 8J (DMMA latency, not issue, binds)
+            double u0 = 0.0, u1 = 0.0, v0 = 0.0, v1 = 0.0, w0 = 0.0, w1 = 0.0, y0 = 0.0, y1 = 0.0;
+            const double* qa = Qs + (8 * warp + g) * LD + t;                  // A operand: Q[8w + g][k + t]
+            const double* rb = R0p + rc_r0_off(J) + g * (8 * J + 12) + t;     // B operand: R0[k + t][8J + g]
+            int k = 0;
+            for (; k + 16 <= 8 * J; k += 16) {
+                dmma884(u0, u1, qa[k], rb[k]);
+                dmma884(v0, v1, qa[k + 4], rb[k + 4]);
+                dmma884(w0, w1, qa[k + 8], rb[k + 8]);
+                dmma884(y0, y1, qa[k + 12], rb[k + 12]);
             }
-            // two interleaved accumulation chains over k = 0 .. 8J
-            double u0 = 0.0, u1 = 0.0, v0 = 0.0, v1 = 0.0;
-            const double* qa = Qs + (8 * warp + g) * LD + t;      // A operand: Q[8w + g][k + t]
-            const double* rb = R0s + (8 * J + g) * LD + t;        // B operand: R0[k + t][8J + g]
-            for (int k = 0; k < 8 * J; k += 8) {
+            if (k < 8 * J) {
                 dmma884(u0, u1, qa[k], rb[k]);
                 dmma884(v0, v1, qa[k + 4], rb[k + 4]);
             }
-            t0 -= u0 + v0;
-            t1 -= u1 + v1;
-            // 8x8 diagonal block: substitution inside the row group (lane holds cols 2t, 2t+1)
-            const double* rd = R0s + (8 * J) * LD + 8 * J;          // rd[c' * LD + c] = R0[8J+c][8J+c']
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                const double own = (c & 1) ? t1 : t0;
-                const double qc_own = own / rd[c * LD + c];
-                const double qc = __shfl_sync(0xffffffffu, qc_own, (lane & ~3) | (c >> 1));
-                if (2 * t == c) t0 = qc;
-                if (2 * t + 1 == c) t1 = qc;
-                if (2 * t > c) t0 -= qc * rd[(2 * t) * LD + c];
-                if (2 * t + 1 > c) t1 -= qc * rd[(2 * t + 1) * LD + c];
-            }
+            t0 -= (u0 + v0) + (w0 + y0);
+            t1 -= (u1 + v1) + (w1 + y1);
+            // 8x8 diagonal block: lanes 0..7 each solve one row in registers (a shuffle chain
+            // across the 4-lane row group cost ~1400 cycles per block; this ~200)
             *reinterpret_cast<double2*>(qrow + 8 * J + 2 * t) = make_double2(t0, t1);
+            __syncwarp();
+            if (lane < 8) {
+                double* q = Qs + (8 * warp + lane) * LD + 8 * J;
+                const double* rd = R0p + rc_r0_off(J) + 8 * J;      // rd[c' * ldJ + c] = R0[8J+c][8J+c']
+                double v[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) v[c] = q[c];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    v[c] *= invd[8 * J + c];                       // q_c = t_c / R_cc (R19: times 1/R_cc)
+#pragma unroll
+                    for (int c2 = c + 1; c2 < 8; ++c2) v[c2] -= v[c] * rd[c2 * (8 * J + 12) + c];
+                }
+#pragma unroll
+                for (int c = 0; c < 8; c += 2) *reinterpret_cast<double2*>(q + c) = make_double2(v[c], v[c + 1]);
+            }
             __syncwarp();
         }
         __syncthreads();
-        // ---- Gram: C[8I.., 8J..] += Q[:, I-block]^T Q[:, J-block] over the 64 tile rows
-#pragma unroll
-        for (int p = 0; p < PER; ++p) {
-            const int blk = warp + p * kRcWarps;
-            if (blk < NBLK) {
-                // blk -> (I, J), I <= J, column-major over the upper triangle
-                int J = 0;
-                while ((J + 1) * (J + 2) / 2 <= blk) ++J;
-                const int I = blk - J * (J + 1) / 2;
-                const double* qa = Qs + t * LD + 8 * I + g;   // A operand: Q^T[8I + g][k + t] = Q[k + t][8I + g]
-                const double* qb = Qs + t * LD + 8 * J + g;   // B operand: Q[k + t][8J + g]
-                double w0 = 0.0, w1 = 0.0;
-#pragma unroll 4
-                for (int k = 0; k < kRcRows; k += 8) {
-                    dmma884(acc[p][0], acc[p][1], qa[k * LD], qb[k * LD]);
-                    dmma884(w0, w1, qa[(k + 4) * LD], qb[(k + 4) * LD]);
-                }
-                acc[p][0] += w0;
-                acc[p][1] += w1;
-            }
-        }
+        // z = Q^T b for this tile, then the next tile's A and b go out while the Gram runs
         if (threadIdx.x < NP) {
+            const double* bt = bs + buf * kRcRows;
             double s = 0.0;
-            for (int r = 0; r < kRcRows; ++r) s += Qs[r * LD + threadIdx.x] * bs[r];
+            for (int r = 0; r < kRcRows; ++r) s += Qs[r * LD + threadIdx.x] * bt[r];
             zacc += s;
         }
-        __syncthreads();   // Qs and bs are rewritten by the next tile
+        if (tile + gridDim.x < ntiles) stage(tile + gridDim.x, bs + (buf ^ 1) * kRcRows);
+        // ---- Gram: C[8I.., 8J..] += Q[:, I-block]^T Q[:, J-block] over this warp's k rows.
+        // Warp = (column pair, k split): block columns J1 = pair and J2 = NB-1-pair together hold
+        // NB+1 upper blocks (slot s <= J1: (s, J1); else (s-J1-1, J2)), so every warp carries
+        // NB+1 independent accumulation chains and the work is balanced.
+        {
+            const double* qk = Qs + (gk0 + t) * LD + g;
+#pragma unroll 2
+            for (int k = 0; k < GK; k += 4, qk += 4 * LD) {
+                const double b1 = qk[8 * J1], b2 = qk[8 * J2];
+#pragma unroll
+                for (int s2 = 0; s2 <= NB; ++s2) {
+                    const bool first = s2 <= J1;
+                    const int I = first ? s2 : s2 - J1 - 1;
+                    dmma884(acc[s2][0], acc[s2][1], qk[8 * I], first ? b1 : b2);
+                }
+            }
+        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();   // Qs, As and bs[buf] are rewritten by the next tile
+        buf ^= 1;
     }
     // ---- this CTA's partial [C | z] (nc x nc column-major, upper blocks + column n)
-    double* P = part + (size_t)blockIdx.x * nc * nc;
+    double* P = part + (size_t)blockIdx.x * nc * nc;   // zeroed by the host; KS warps add into each block
 #pragma unroll
-    for (int p = 0; p < PER; ++p) {
-        const int blk = warp + p * kRcWarps;
-        if (blk < NBLK) {
-            int J = 0;
-            while ((J + 1) * (J + 2) / 2 <= blk) ++J;
-            const int I = blk - J * (J + 1) / 2;
-            const int i = 8 * I + g, j0 = 8 * J + 2 * t;
-            if (i < n && j0 < n) P[i + (int64_t)j0 * nc] = acc[p][0];
-            if (i < n && j0 + 1 < n) P[i + (int64_t)(j0 + 1) * nc] = acc[p][1];
-        }
+    for (int s2 = 0; s2 <= NB; ++s2) {
+        const bool first = s2 <= J1;
+        const int I = first ? s2 : s2 - J1 - 1, J = first ? J1 : J2;
+        const int i = 8 * I + g, j0 = 8 * J + 2 * t;
+        if (i < n && j0 < n) atomicAdd(P + i + (int64_t)j0 * nc, acc[s2][0]);
+        if (i < n && j0 + 1 < n) atomicAdd(P + i + (int64_t)(j0 + 1) * nc, acc[s2][1]);
     }
     if (threadIdx.x < n) P[threadIdx.x + (int64_t)(nc - 1) * nc] = zacc;
 }
@@ -250,7 +288,9 @@ static csk_status rc_impl(csk_plan_t plan, int64_t k2, int64_t n, const double* 
     if (fused) {
         const int nb = n <= 16 ? 2 : n <= 32 ? 4 : n <= 64 ? 8 : 16;
         const int NP = 8 * nb, LD = NP + 4;
-        const size_t smem = ((size_t)NP * LD + (size_t)kRcRows * LD + kRcRows) * 8;
+        const size_t smem =
+            ((size_t)rc_r0_off(nb) + (size_t)kRcRows * LD + (size_t)NP * (kRcRows + 4) + 2 * kRcRows + NP) * 8;
+        const int al16 = ((uintptr_t)A & 15) == 0 && ((uintptr_t)b & 15) == 0 && (lda & 1) == 0;
         const DeviceInfo& di = device_info();
         const int64_t tiles = ceil_div(d, kRcRows);
         const int grid = (int)std::min<int64_t>(tiles, di.num_sms);
@@ -260,7 +300,7 @@ static csk_status rc_impl(csk_plan_t plan, int64_t k2, int64_t n, const double* 
         auto kern = nb == 2 ? rc_pass_kernel<2> : nb == 4 ? rc_pass_kernel<4> : nb == 8 ? rc_pass_kernel<8>
                                                                                           : rc_pass_kernel<16>;
         CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kern<<<grid, kRcWarps * 32, smem, st>>>(A, lda, b, d, (int)n, R0, nc, part, nc);
+        kern<<<grid, kRcWarps * 32, smem, st>>>(A, lda, b, d, (int)n, R0, nc, part, nc, al16);
         CSK_LAUNCH_CHECK();
         rc_reduce_kernel<<<(unsigned)std::min<int64_t>(ceil_div((int64_t)nc * nc, 256), 1024), 256, 0, st>>>(
             part, grid, (int64_t)nc * nc, C);
