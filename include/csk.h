@@ -172,6 +172,21 @@ csk_status ne_lstsq(int64_t d, int64_t n, const double* A, int64_t lda, const do
 csk_status rc_lstsq(csk_plan_t plan, int64_t k2, int64_t n, const double* A, int64_t lda, const double* b,
                     double* x, double* R, int64_t ldr, void* stream);
 
+/* srht_apply: the SRHT S = k^-1/2 P H_d D (Def) applied to
+ * [A b]:  Y[j, c] = k^-1/2 (H_d D [A b][:, c])[p_j],  fp64.
+ *   D_ii = +-1 and the k sampled rows p_j (i.i.d. uniform, with replacement) come from Philox
+ *   streams 6 and 7 of seed over GLOBAL rows (R20-R21); H_d is the Sylvester
+ *   Hadamard matrix, H[p, i] = (-1)^popcount(p & i) (Alg 3 computes it; R22).
+ *   dglob  global row count, a power of two, <= 2^32
+ *   d, row0  this block's rows [row0, row0 + d) of the global matrix: a row-partitioned A sums
+ *          the Y of its blocks (linearity).  For dglob >= 4096, row0 and d must be
+ *          multiples of 4096; for dglob < 4096 the block is the whole matrix.
+ *   A      d x n column-major (lda >= d), b optional extra column, Y k x (n + (b != NULL))
+ *          column-major (ldy >= k): DEVICE pointers; Y is overwritten.  k <= 1024.
+ * Asynchronous on the stream.  Workspace: d/8 + 4k bytes, stream-ordered. */
+csk_status srht_apply(int64_t d, int64_t dglob, int64_t row0, int64_t k, uint64_t seed, int64_t n,
+                      const double* A, int64_t lda, const double* b, double* Y, int64_t ldy, void* stream);
+
 /* ------------------------------------------------------------- utilities */
 const char* csk_status_str(csk_status st);
 const char* csk_last_error(void);      /* thread-local detail of the last failure */

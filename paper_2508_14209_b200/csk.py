@@ -67,6 +67,7 @@ def lib():
                 "ms_lstsq": [P, I64, I64, P, I64, P, P, P, P],
                 "ne_lstsq": [I64, I64, P, I64, P, P, P],
                 "rc_lstsq": [P, I64, I64, P, I64, P, P, P, I64, P],
+                "srht_apply": [I64, I64, I64, I64, U64, I64, P, I64, P, P, I64, P],
             }
             for name, argt in sigs.items():
                 f = getattr(L, name)
@@ -290,3 +291,20 @@ def rc_lstsq(plan: Plan, k2: int, A, b, x=None, want_R: bool = False, stream=Non
     _check(lib().rc_lstsq(plan.handle, k2, n, pA, lda, pb, ctypes.c_void_p(x.data_ptr()), pR, ldr,
                           _stream(stream, A.device)), "rc_lstsq")
     return (x, R) if want_R else x
+
+
+def srht_apply(A, k: int, seed: int, b=None, Y=None, dglob: int | None = None, row0: int = 0, stream=None):
+    """SRHT Y = k^-1/2 P H D [A b] (k x ncols) of the rows [row0, row0 + d) of a dglob-row matrix."""
+    torch = _torch()
+    d = A.shape[0] if A is not None else b.shape[0]
+    n = A.shape[1] if A is not None else 0
+    ncols = n + (b is not None)
+    dev = A.device if A is not None else b.device
+    if Y is None:
+        Y = torch.empty((ncols, k), dtype=torch.float64, device=dev).t()
+    pA, lda = _colmajor(A, "A") if A is not None else (None, max(d, 1))
+    pb, _ = _colmajor(b, "b")
+    pY, ldy = _colmajor(Y, "Y")
+    _check(lib().srht_apply(d, dglob if dglob is not None else d, row0, k, seed, n, pA, lda, pb, pY, ldy,
+                            _stream(stream, dev)), "srht_apply")
+    return Y

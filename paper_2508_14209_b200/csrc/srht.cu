@@ -1,0 +1,248 @@
+// srht.cu -- srht_apply: the SRHT S = k^-1/2 P H_d D (Def)
+// applied to [A b], column-major, fp64.
+//
+// B200 design (not the paper's multi-pass FWHT): only k of the d rows of H D a are
+// kept, and H_d = H_{d/L} (x) H_L (Sylvester order: H[p, i] = (-1)^popcount(p & i)), so with
+// i = hi*L + lo and p_j = ph_j*L + pl_j
+//     y_j = k^-1/2 sum_hi (-1)^popcount(ph_j & hi) * (H_L (D a)[hi-block])[pl_j].
+// One pass over A: a CTA takes (column, L-row block) units, applies D while loading the block
+// (coalesced, L = 4096 rows = 32 KB), runs the length-L FWHT on chip (three radix-16 phases in
+// registers with two padded shared-memory exchanges), and adds the k sampled entries, signed by
+// the block's hi index, into per-thread accumulators that are flushed to Y once per column.
+// HBM traffic = d * ncols * 8 bytes read (+ d/8 bytes of D bits); the paper's implementation
+// reads and writes A O(log k) times.  Alg 3's radix-4 butterfly order
+// becomes radix-16 in registers; every stage is the same Sylvester factor, so the result is
+// H_L regardless of stage order (R22).
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+
+#include "csk_internal.cuh"
+
+namespace csk {
+
+void prof_mark(cudaStream_t st, bool begin);
+
+constexpr int kHL = 4096;            // FWHT block length on chip
+constexpr int kHThreads = 256;       // 16 elements per thread
+constexpr int kHPad = kHL + kHL / 16;
+
+__device__ __forceinline__ int hpad(int i) { return i + (i >> 4); }
+
+// D as packed bits: bit (i & 31) of dbits[i >> 5] = 1 iff D_ii = -1, local row i = global row0 + i
+// (Reading R21: bit 0 of word (g & 3) of Philox(ctr = (lo32(g>>2), hi32(g>>2), 6, 0), key = seed)).
+__global__ void srht_dbits_kernel(uint32_t* __restrict__ dbits, int64_t nwords, int64_t row0, uint32_t key0,
+                                  uint32_t key1) {
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nwords; w += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t bits = 0;
+        const uint64_t g0 = (uint64_t)row0 + (uint64_t)w * 32;   // multiple of 4
+        for (int q = 0; q < 8; ++q) {
+            const uint64_t blk = (g0 >> 2) + q;
+            const uint4 x = philox4x32_10(make_uint4((uint32_t)blk, (uint32_t)(blk >> 32), 6u, 0u), make_uint2(key0, key1));
+            bits |= ((x.x & 1u) | ((x.y & 1u) << 1) | ((x.z & 1u) << 2) | ((x.w & 1u) << 3)) << (4 * q);
+        }
+        dbits[w] = bits;
+    }
+}
+
+// sampled rows p_j = floor(w_j * dglob / 2^32) (dglob <= 2^32), w_j from stream 7
+__global__ void srht_samples_kernel(uint32_t* __restrict__ p, int64_t k, uint64_t dglob, uint32_t key0, uint32_t key1) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < k; j += (int64_t)gridDim.x * blockDim.x) {
+        const uint4 x = philox4x32_10(make_uint4((uint32_t)(j >> 2), (uint32_t)(j >> 34), 7u, 0u), make_uint2(key0, key1));
+        const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+        p[j] = (uint32_t)(((uint64_t)w[j & 3] * dglob) >> 32);
+    }
+}
+
+__device__ __forceinline__ void fwht16(double (&x)[16]) {
+#pragma unroll
+    for (int h = 1; h < 16; h <<= 1)
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            if ((i & h) == 0) {
+                const double a = x[i], b = x[i + h];
+                x[i] = a + b;
+                x[i + h] = a - b;
+            }
+}
+
+// Units u = c * nblk + blk (column-major), CTA b takes the contiguous range [u0, u1).
+template <int R>   // samples per thread: k <= 256 R
+__global__ void __launch_bounds__(kHThreads) srht_kernel(const double* __restrict__ A, int64_t lda,
+                                                         const double* __restrict__ bvec, int n, int ncols,
+                                                         int64_t nblk, int64_t hb0, const uint32_t* __restrict__ dbits,
+                                                         const uint32_t* __restrict__ psamp, int k, double scale,
+                                                         double* __restrict__ Y, int64_t ldy) {
+    __shared__ double xs[kHPad];
+    const int t = threadIdx.x;
+    const int64_t total = nblk * ncols;
+    const int64_t per = (total + gridDim.x - 1) / gridDim.x;
+    const int64_t u0 = blockIdx.x * per, u1 = min(total, u0 + per);
+    if (u0 >= u1) return;
+    // this thread's samples: pl (in-block row), ph (block index)
+    int pl[R];
+    uint32_t ph[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int j = t + r * kHThreads;
+        const uint32_t pj = j < k ? psamp[j] : 0u;
+        pl[r] = (int)(pj & (kHL - 1));
+        ph[r] = pj / kHL;
+    }
+    double acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+    int cur = (int)(u0 / nblk);
+    for (int64_t u = u0; u < u1; ++u) {
+        const int c = (int)(u / nblk);
+        const int64_t blk = u - (int64_t)c * nblk;
+        if (c != cur) {   // flush the previous column
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int j = t + r * kHThreads;
+                if (j < k) atomicAdd(Y + j + (int64_t)cur * ldy, acc[r] * scale);
+                acc[r] = 0.0;
+            }
+            cur = c;
+        }
+        const double* col = (c < n ? A + (int64_t)c * lda : bvec) + blk * kHL;
+        const uint32_t* db = dbits + blk * (kHL / 32);
+        // phase A: elements e*256 + t, D applied as a sign flip; FWHT over bits 8..11
+        double x[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) x[e] = __ldcs(col + e * kHThreads + t);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int i = e * kHThreads + t;
+            const uint32_t bit = (__ldg(db + (i >> 5)) >> (i & 31)) & 1u;
+            x[e] = __longlong_as_double(__double_as_longlong(x[e]) ^ ((long long)bit << 63));
+        }
+        fwht16(x);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) xs[hpad(e * kHThreads + t)] = x[e];
+        __syncthreads();
+        // phase B: bits 4..7 (thread = bits 0..3 and 8..11)
+        {
+            const int base = (t >> 4) * 256 + (t & 15);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) x[e] = xs[hpad(base + e * 16)];
+            fwht16(x);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) xs[hpad(base + e * 16)] = x[e];
+        }
+        __syncthreads();
+        // phase C: bits 0..3 (thread = bits 4..11)
+        {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) x[e] = xs[hpad(t * 16 + e)];
+            fwht16(x);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) xs[hpad(t * 16 + e)] = x[e];
+        }
+        __syncthreads();
+        // samples: acc_j += (-1)^popcount(ph_j & hi) X[pl_j], hi = global block index
+        const uint32_t hi = (uint32_t)(hb0 + blk);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const double v = xs[hpad(pl[r])];
+            acc[r] += (__popc(ph[r] & hi) & 1) ? -v : v;
+        }
+        __syncthreads();   // xs is rewritten by the next unit
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int j = t + r * kHThreads;
+        if (j < k) atomicAdd(Y + j + (int64_t)cur * ldy, acc[r] * scale);
+    }
+}
+
+// d < 4096: one CTA per column, the whole vector in shared memory, radix-2 stages (Alg 3's
+// butterflies, one barrier per stage).
+__global__ void __launch_bounds__(256) srht_small_kernel(const double* __restrict__ A, int64_t lda,
+                                                         const double* __restrict__ bvec, int n, int d,
+                                                         const uint32_t* __restrict__ dbits,
+                                                         const uint32_t* __restrict__ psamp, int k, double scale,
+                                                         double* __restrict__ Y, int64_t ldy) {
+    __shared__ double v[kHL];
+    const int c = blockIdx.x;
+    const double* col = c < n ? A + (int64_t)c * lda : bvec;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+        const uint32_t bit = (dbits[i >> 5] >> (i & 31)) & 1u;
+        v[i] = bit ? -col[i] : col[i];
+    }
+    __syncthreads();
+    for (int h = 1; h < d; h <<= 1) {
+        for (int q = threadIdx.x; q < d / 2; q += blockDim.x) {
+            const int i = (q / h) * 2 * h + (q % h);
+            const double a = v[i], b = v[i + h];
+            v[i] = a + b;
+            v[i + h] = a - b;
+        }
+        __syncthreads();
+    }
+    for (int j = threadIdx.x; j < k; j += blockDim.x) Y[j + (int64_t)c * ldy] = v[psamp[j]] * scale;
+}
+
+static csk_status srht_impl(int64_t d, int64_t dglob, int64_t row0, int64_t k, uint64_t seed, int64_t n,
+                            const double* A, int64_t lda, const double* b, double* Y, int64_t ldy, cudaStream_t st) {
+    const int64_t ncols = n + (b ? 1 : 0);
+    CSK_REQUIRE(d >= 1 && k >= 1 && n >= 0 && ncols >= 1 && Y != nullptr, CSK_EINVAL, "bad SRHT arguments");
+    CSK_REQUIRE(n == 0 || A != nullptr, CSK_EINVAL, "A is NULL");
+    CSK_REQUIRE(dglob >= 1 && (dglob & (dglob - 1)) == 0 && dglob <= (1LL << 32), CSK_ESHAPE,
+                "dglob=%lld must be a power of two <= 2^32 (P:L165: log2 d integer)", (long long)dglob);
+    CSK_REQUIRE(row0 >= 0 && row0 + d <= dglob, CSK_ESHAPE, "rows [row0, row0+d) outside [0, dglob)");
+    CSK_REQUIRE(n == 0 || lda >= d, CSK_ESHAPE, "lda=%lld < d=%lld", (long long)lda, (long long)d);
+    CSK_REQUIRE(ldy >= k, CSK_ESHAPE, "ldy=%lld < k=%lld", (long long)ldy, (long long)k);
+    CSK_REQUIRE(k <= 1024, CSK_EUNSUPPORTED, "k=%lld > 1024 sampled rows", (long long)k);
+    CSK_REQUIRE(ncols <= 1 << 20, CSK_EINVAL, "too many columns");
+    const bool small = dglob < kHL;
+    if (small) CSK_REQUIRE(row0 == 0 && d == dglob, CSK_ESHAPE, "dglob < 4096 cannot be row-partitioned");
+    else
+        CSK_REQUIRE(row0 % kHL == 0 && d % kHL == 0, CSK_ESHAPE,
+                    "row blocks must be multiples of 4096 rows (row0=%lld, d=%lld)", (long long)row0, (long long)d);
+    CSK_REQUIRE((n == 0 || is_device_pointer(A)) && (!b || is_device_pointer(b)) && is_device_pointer(Y), CSK_EINVAL,
+                "srht_apply takes device pointers");
+    const int64_t nwords = (d + 31) / 32;
+    uint32_t* ws = nullptr;
+    CSK_CUDA_TRY(cudaMallocAsync(&ws, (size_t)(nwords + k) * 4, st));
+    uint32_t* dbits = ws;
+    uint32_t* psamp = ws + nwords;
+    const uint32_t key0 = (uint32_t)seed, key1 = (uint32_t)(seed >> 32);
+    srht_dbits_kernel<<<(unsigned)std::min<int64_t>(ceil_div(nwords, 256), 4096), 256, 0, st>>>(dbits, nwords, row0,
+                                                                                               key0, key1);
+    CSK_LAUNCH_CHECK();
+    srht_samples_kernel<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(psamp, k, (uint64_t)dglob, key0, key1);
+    CSK_LAUNCH_CHECK();
+    const double scale = 1.0 / std::sqrt((double)k);
+    if (small) {
+        srht_small_kernel<<<(unsigned)ncols, 256, 0, st>>>(A, lda, b, (int)n, (int)d, dbits, psamp, (int)k, scale, Y,
+                                                           ldy);
+        CSK_LAUNCH_CHECK();
+    } else {
+        if (ldy == k) {
+            CSK_CUDA_TRY(cudaMemsetAsync(Y, 0, (size_t)k * ncols * 8, st));
+        } else {
+            CSK_CUDA_TRY(cudaMemset2DAsync(Y, ldy * 8, 0, k * 8, ncols, st));
+        }
+        const int64_t nblk = d / kHL, total = nblk * ncols;
+        const DeviceInfo& di = device_info();
+        int per_sm = 0;
+        auto kern = k <= 256 ? srht_kernel<1> : k <= 512 ? srht_kernel<2> : srht_kernel<4>;
+        CSK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kHThreads, 0));
+        const int64_t grid = std::min<int64_t>(total, (int64_t)di.num_sms * std::max(per_sm, 1));
+        prof_mark(st, true);
+        kern<<<(unsigned)grid, kHThreads, 0, st>>>(A, lda, b, (int)n, (int)ncols, nblk, row0 / kHL, dbits, psamp,
+                                                   (int)k, scale, Y, ldy);
+        CSK_LAUNCH_CHECK();
+        prof_mark(st, false);
+    }
+    CSK_CUDA_TRY(cudaFreeAsync(ws, st));
+    return CSK_OK;
+}
+
+}  // namespace csk
+
+extern "C" csk_status srht_apply(int64_t d, int64_t dglob, int64_t row0, int64_t k, uint64_t seed, int64_t n,
+                                 const double* A, int64_t lda, const double* b, double* Y, int64_t ldy, void* stream) {
+    return csk::srht_impl(d, dglob, row0, k, seed, n, A, lda, b, Y, ldy, (cudaStream_t)stream);
+}

@@ -13,7 +13,8 @@ WANT = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum
         'l1tex__m_l1tex2xbar_write_bytes_mem_global_op_tma_red.sum.pct_of_peak_sustained_elapsed',
         'sm__cycles_elapsed.avg.per_second', 'launch__registers_per_thread', 'launch__grid_size',
         'launch__block_size', 'sm__pipe_tensor_op_dmma_cycles_active.avg.pct_of_peak_sustained_active',
-        'sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active']
+        'sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active',
+        'sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active']
 
 
 def summary(path):
