@@ -156,6 +156,226 @@ __global__ void __launch_bounds__(kHThreads) srht_kernel(const double* __restric
     }
 }
 
+// TMA-fed variant: the unit's 32 KB column segment arrives by one cp.async.bulk into a 2-stage
+// ring (unit i+2 is in flight while unit i is transformed), so HBM reads no longer wait on the
+// warps reaching their load instructions.  Needs 16-B aligned columns (A aligned, lda even).
+constexpr int kHStages = 2;
+
+template <int R>
+__global__ void __launch_bounds__(kHThreads, 2) srht_tma_kernel(const double* __restrict__ A, int64_t lda,
+                                                                const double* __restrict__ bvec, int n, int ncols,
+                                                                int64_t nblk, int64_t hb0,
+                                                                const uint32_t* __restrict__ dbits,
+                                                                const uint32_t* __restrict__ psamp, int k, double scale,
+                                                                double* __restrict__ Y, int64_t ldy) {
+    extern __shared__ __align__(128) double hsm[];
+    double* stage = hsm;                          // [kHStages][kHL]
+    double* xs = stage + kHStages * kHL;          // [kHPad]
+    __shared__ __align__(8) uint64_t bar[kHStages];
+    const int t = threadIdx.x;
+    const int64_t total = nblk * ncols;
+    const int64_t per = (total + gridDim.x - 1) / gridDim.x;
+    const int64_t u0 = blockIdx.x * per, u1 = min(total, u0 + per);
+    if (u0 >= u1) return;
+    auto src_of = [&](int64_t u) {
+        const int c = (int)(u / nblk);
+        const int64_t blk = u - (int64_t)c * nblk;
+        return (c < n ? A + (int64_t)c * lda : bvec) + blk * kHL;
+    };
+    if (t == 0) {
+        for (int s = 0; s < kHStages; ++s) mbar_init(&bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int s = 0; s < kHStages && u0 + s < u1; ++s) {
+            mbar_expect_tx(&bar[s], kHL * 8);
+            bulk_load_1d(stage + s * kHL, src_of(u0 + s), kHL * 8, &bar[s]);
+        }
+    }
+    __syncthreads();
+    int pl[R];
+    uint32_t ph[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int j = t + r * kHThreads;
+        const uint32_t pj = j < k ? psamp[j] : 0u;
+        pl[r] = (int)(pj & (kHL - 1));
+        ph[r] = pj / kHL;
+    }
+    double acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+    int cur = (int)(u0 / nblk);
+    for (int64_t u = u0; u < u1; ++u) {
+        const int64_t i = u - u0;
+        const int s = (int)(i % kHStages);
+        const uint32_t parity = (uint32_t)((i / kHStages) & 1);
+        const int c = (int)(u / nblk);
+        const int64_t blk = u - (int64_t)c * nblk;
+        if (c != cur) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int j = t + r * kHThreads;
+                if (j < k) atomicAdd(Y + j + (int64_t)cur * ldy, acc[r] * scale);
+                acc[r] = 0.0;
+            }
+            cur = c;
+        }
+        const uint32_t* db = dbits + blk * (kHL / 32);
+        uint32_t dw[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) dw[e] = __ldg(db + ((e * kHThreads + t) >> 5));
+        mbar_wait(&bar[s], parity);
+        const double* st = stage + s * kHL;
+        double x[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int ii = e * kHThreads + t;
+            const uint32_t bit = (dw[e] >> (ii & 31)) & 1u;
+            x[e] = __longlong_as_double(__double_as_longlong(st[ii]) ^ ((long long)bit << 63));
+        }
+        fwht16(x);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) xs[hpad(e * kHThreads + t)] = x[e];
+        __syncthreads();   // every thread is done reading stage s: refill it with unit u + kHStages
+        if (t == 0 && u + kHStages < u1) {
+            mbar_expect_tx(&bar[s], kHL * 8);
+            bulk_load_1d(stage + s * kHL, src_of(u + kHStages), kHL * 8, &bar[s]);
+        }
+        {
+            const int base = (t >> 4) * 256 + (t & 15);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) x[e] = xs[hpad(base + e * 16)];
+            fwht16(x);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) xs[hpad(base + e * 16)] = x[e];
+        }
+        __syncthreads();
+        {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) x[e] = xs[hpad(t * 16 + e)];
+            fwht16(x);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) xs[hpad(t * 16 + e)] = x[e];
+        }
+        __syncthreads();
+        const uint32_t hi = (uint32_t)(hb0 + blk);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const double v = xs[hpad(pl[r])];
+            acc[r] += (__popc(ph[r] & hi) & 1) ? -v : v;
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int j = t + r * kHThreads;
+        if (j < k) atomicAdd(Y + j + (int64_t)cur * ldy, acc[r] * scale);
+    }
+}
+
+// Shared-memory-lean variant (default): 64 threads per block of L = 4096 rows, 64 elements per
+// thread, so H_L = two radix-64 register phases with ONE padded shared-memory exchange, and only
+// the k sampled positions are written back for the gather (a 4096-bit sample map).  Per 32 KB of
+// A this moves ~68 KB through shared memory (the 3-phase kernels move ~200-260 KB: shared-memory
+// bandwidth, not HBM, bounded them at ~3.6 TB/s).  Loads go straight to registers, coalesced.
+constexpr int kH64Threads = 64;
+constexpr int kH64Pad = kHL + kHL / 64;
+__device__ __forceinline__ int hpad64(int i) { return i + (i >> 6); }
+
+__device__ __forceinline__ void fwht64(double (&x)[64]) {
+#pragma unroll
+    for (int h = 1; h < 64; h <<= 1)
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+            if ((i & h) == 0) {
+                const double a = x[i], b = x[i + h];
+                x[i] = a + b;
+                x[i + h] = a - b;
+            }
+}
+
+template <int R>   // samples per thread: k <= 64 R
+__global__ void __launch_bounds__(kH64Threads) srht_r64_kernel(const double* __restrict__ A, int64_t lda,
+                                                               const double* __restrict__ bvec, int n, int ncols,
+                                                               int64_t nblk, int64_t hb0,
+                                                               const uint32_t* __restrict__ dbits,
+                                                               const uint32_t* __restrict__ psamp, int k, double scale,
+                                                               double* __restrict__ Y, int64_t ldy) {
+    __shared__ double xs[kH64Pad];
+    __shared__ uint32_t smap[kHL / 32];   // bit pos set iff some sample has in-block row pos
+    const int t = threadIdx.x;
+    const int64_t total = nblk * ncols;
+    const int64_t per = (total + gridDim.x - 1) / gridDim.x;
+    const int64_t u0 = blockIdx.x * per, u1 = min(total, u0 + per);
+    if (u0 >= u1) return;
+    for (int w = t; w < kHL / 32; w += kH64Threads) smap[w] = 0u;
+    __syncthreads();
+    int pl[R];
+    uint32_t ph[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int j = t + r * kH64Threads;
+        const uint32_t pj = j < k ? psamp[j] : 0u;
+        pl[r] = (int)(pj & (kHL - 1));
+        ph[r] = pj / kHL;
+        if (j < k) atomicOr(&smap[pl[r] >> 5], 1u << (pl[r] & 31));
+    }
+    __syncthreads();
+    const uint32_t m0 = smap[2 * t], m1 = smap[2 * t + 1];   // samples among this thread's phase-2 rows t*64 + e
+    double acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+    int cur = (int)(u0 / nblk);
+    for (int64_t u = u0; u < u1; ++u) {
+        const int c = (int)(u / nblk);
+        const int64_t blk = u - (int64_t)c * nblk;
+        if (c != cur) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int j = t + r * kH64Threads;
+                if (j < k) atomicAdd(Y + j + (int64_t)cur * ldy, acc[r] * scale);
+                acc[r] = 0.0;
+            }
+            cur = c;
+        }
+        const double* col = (c < n ? A + (int64_t)c * lda : bvec) + blk * kHL;
+        const uint32_t* db = dbits + blk * (kHL / 32);
+        // phase 1: rows e*64 + t (coalesced), D as a sign flip; FWHT over bits 6..11
+        double x[64];
+#pragma unroll
+        for (int e = 0; e < 64; ++e) x[e] = __ldcs(col + e * kH64Threads + t);
+#pragma unroll
+        for (int e = 0; e < 64; ++e) {
+            const uint32_t bit = (__ldg(db + 2 * e + (t >> 5)) >> (t & 31)) & 1u;
+            x[e] = __longlong_as_double(__double_as_longlong(x[e]) ^ ((long long)bit << 63));
+        }
+        fwht64(x);
+#pragma unroll
+        for (int e = 0; e < 64; ++e) xs[hpad64(e * kH64Threads + t)] = x[e];
+        __syncthreads();
+        // phase 2: rows t*64 + e; FWHT over bits 0..5; write back only the sampled rows
+#pragma unroll
+        for (int e = 0; e < 64; ++e) x[e] = xs[hpad64(t * 64 + e)];
+        fwht64(x);
+        __syncthreads();   // every thread has read its rows before the sampled ones are rewritten
+#pragma unroll
+        for (int e = 0; e < 64; ++e)
+            if (((e < 32 ? m0 : m1) >> (e & 31)) & 1u) xs[hpad64(t * 64 + e)] = x[e];
+        __syncthreads();
+        const uint32_t hi = (uint32_t)(hb0 + blk);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const double v = xs[hpad64(pl[r])];
+            acc[r] += (__popc(ph[r] & hi) & 1) ? -v : v;
+        }
+        __syncthreads();   // xs is rewritten by the next unit
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int j = t + r * kH64Threads;
+        if (j < k) atomicAdd(Y + j + (int64_t)cur * ldy, acc[r] * scale);
+    }
+}
+
 // d < 4096: one CTA per column, the whole vector in shared memory, radix-2 stages (Alg 3's
 // butterflies, one barrier per stage).
 __global__ void __launch_bounds__(256) srht_small_kernel(const double* __restrict__ A, int64_t lda,
@@ -227,13 +447,36 @@ static csk_status srht_impl(int64_t d, int64_t dglob, int64_t row0, int64_t k, u
         const int64_t nblk = d / kHL, total = nblk * ncols;
         const DeviceInfo& di = device_info();
         int per_sm = 0;
-        auto kern = k <= 256 ? srht_kernel<1> : k <= 512 ? srht_kernel<2> : srht_kernel<4>;
-        CSK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kHThreads, 0));
-        const int64_t grid = std::min<int64_t>(total, (int64_t)di.num_sms * std::max(per_sm, 1));
-        prof_mark(st, true);
-        kern<<<(unsigned)grid, kHThreads, 0, st>>>(A, lda, b, (int)n, (int)ncols, nblk, row0 / kHL, dbits, psamp,
-                                                   (int)k, scale, Y, ldy);
-        CSK_LAUNCH_CHECK();
+        const bool al = (n == 0 || (((uintptr_t)A & 15) == 0 && (lda & 1) == 0)) && (!b || ((uintptr_t)b & 15) == 0);
+        const char* e = std::getenv("CSK_SRHT_TMA");
+        const char* v = std::getenv("CSK_SRHT_KERNEL");   // experiment: 1 = 3-phase kernels
+        if (!(v && std::atoi(v) == 1)) {
+            auto kern = k <= 256 ? srht_r64_kernel<4> : k <= 512 ? srht_r64_kernel<8> : srht_r64_kernel<16>;
+            CSK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kH64Threads, 0));
+            const int64_t grid = std::min<int64_t>(total, (int64_t)di.num_sms * std::max(per_sm, 1));
+            prof_mark(st, true);
+            kern<<<(unsigned)grid, kH64Threads, 0, st>>>(A, lda, b, (int)n, (int)ncols, nblk, row0 / kHL, dbits,
+                                                         psamp, (int)k, scale, Y, ldy);
+            CSK_LAUNCH_CHECK();
+        } else if (al && !(e && std::atoi(e) == 0)) {
+            auto kern = k <= 256 ? srht_tma_kernel<1> : k <= 512 ? srht_tma_kernel<2> : srht_tma_kernel<4>;
+            const size_t smem = ((size_t)kHStages * kHL + kHPad) * 8;
+            CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            CSK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kHThreads, smem));
+            const int64_t grid = std::min<int64_t>(total, (int64_t)di.num_sms * std::max(per_sm, 1));
+            prof_mark(st, true);
+            kern<<<(unsigned)grid, kHThreads, smem, st>>>(A, lda, b, (int)n, (int)ncols, nblk, row0 / kHL, dbits,
+                                                          psamp, (int)k, scale, Y, ldy);
+            CSK_LAUNCH_CHECK();
+        } else {
+            auto kern = k <= 256 ? srht_kernel<1> : k <= 512 ? srht_kernel<2> : srht_kernel<4>;
+            CSK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kHThreads, 0));
+            const int64_t grid = std::min<int64_t>(total, (int64_t)di.num_sms * std::max(per_sm, 1));
+            prof_mark(st, true);
+            kern<<<(unsigned)grid, kHThreads, 0, st>>>(A, lda, b, (int)n, (int)ncols, nblk, row0 / kHL, dbits, psamp,
+                                                       (int)k, scale, Y, ldy);
+            CSK_LAUNCH_CHECK();
+        }
         prof_mark(st, false);
     }
     CSK_CUDA_TRY(cudaFreeAsync(ws, st));

@@ -82,3 +82,21 @@ def test_srht_errors():
     with pytest.raises(csk.CskError) as e:
         csk.srht_apply(A2, 2000, seed=1)
     assert e.value.status == csk.csk.EUNSUPPORTED
+
+
+@pytest.mark.parametrize("path", ["r64", "tma", "ldg"])
+@pytest.mark.parametrize("lda_pad", [0, 1])
+def test_srht_kernel_paths(monkeypatch, path, lda_pad):
+    # default radix-64 kernel; the 3-phase kernels: TMA-fed ring (16-B aligned columns) and the
+    # register-load kernel (forced, or odd lda)
+    if path != "r64":
+        monkeypatch.setenv("CSK_SRHT_KERNEL", "1")
+    if path == "ldg":
+        monkeypatch.setenv("CSK_SRHT_TMA", "0")
+    d, n, k = 1 << 15, 7, 130
+    A = synth.gaussian_matrix(d, n, seed=8)
+    big = np.zeros((d + lda_pad, n), order="F")
+    big[:d] = A
+    Y = host(csk.srht_apply(gpu_colmajor(big)[:d], k, seed=5))
+    Yo = oracle.srht_apply(A, k, seed=5)
+    assert np.all(np.abs(Y - Yo) <= 1e-12 * _T(A, k))
