@@ -376,6 +376,110 @@ __global__ void __launch_bounds__(kH64Threads) srht_r64_kernel(const double* __r
     }
 }
 
+// Warp-block variant (default for k <= 512): every WARP owns whole 1024-row blocks, 32 rows per
+// lane, so H_1024 = two radix-32 register phases with one warp-private padded exchange and no CTA
+// barrier at all; 16 resident warps per SM keep ~130 KB of loads in flight.  Samples: lane l
+// takes j = l + 32 r; the block's sampled rows are the only ones written back.
+constexpr int kHW = 1024;                       // rows per warp block
+constexpr int kHWWarps = 4;                     // warps per CTA (independent)
+constexpr int kHWPad = kHW + kHW / 32;
+__device__ __forceinline__ int hpadw(int i) { return i + (i >> 5); }
+
+__device__ __forceinline__ void fwht32(double (&x)[32]) {
+#pragma unroll
+    for (int h = 1; h < 32; h <<= 1)
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+            if ((i & h) == 0) {
+                const double a = x[i], b = x[i + h];
+                x[i] = a + b;
+                x[i + h] = a - b;
+            }
+}
+
+template <int R>   // samples per lane: k <= 32 R
+__global__ void __launch_bounds__(kHWWarps * 32) srht_warp_kernel(const double* __restrict__ A, int64_t lda,
+                                                                  const double* __restrict__ bvec, int n, int ncols,
+                                                                  int64_t nblk, int64_t hb0,
+                                                                  const uint32_t* __restrict__ dbits,
+                                                                  const uint32_t* __restrict__ psamp, int k,
+                                                                  double scale, double* __restrict__ Y, int64_t ldy) {
+    __shared__ double xsall[kHWWarps][kHWPad];
+    __shared__ uint32_t smap[kHW / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* xs = xsall[warp];
+    for (int w = threadIdx.x; w < kHW / 32; w += blockDim.x) smap[w] = 0u;
+    __syncthreads();
+    int pl[R];
+    uint32_t ph[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int j = lane + 32 * r;
+        const uint32_t pj = j < k ? psamp[j] : 0u;
+        pl[r] = (int)(pj & (kHW - 1));
+        ph[r] = pj / kHW;
+        if (j < k && warp == 0) atomicOr(&smap[pl[r] >> 5], 1u << (pl[r] & 31));
+    }
+    __syncthreads();
+    const uint32_t mymap = smap[lane];   // sampled rows among this lane's phase-2 rows lane*32 + e
+    const int64_t total = nblk * ncols;
+    const int64_t nw = (int64_t)gridDim.x * kHWWarps, gw = (int64_t)blockIdx.x * kHWWarps + warp;
+    const int64_t per = (total + nw - 1) / nw;
+    const int64_t u0 = gw * per, u1 = min(total, u0 + per);
+    if (u0 >= u1) return;
+    double acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+    int cur = (int)(u0 / nblk);
+    for (int64_t u = u0; u < u1; ++u) {
+        const int c = (int)(u / nblk);
+        const int64_t blk = u - (int64_t)c * nblk;
+        if (c != cur) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int j = lane + 32 * r;
+                if (j < k) atomicAdd(Y + j + (int64_t)cur * ldy, acc[r] * scale);
+                acc[r] = 0.0;
+            }
+            cur = c;
+        }
+        const double* col = (c < n ? A + (int64_t)c * lda : bvec) + blk * kHW;
+        const uint32_t* db = dbits + blk * (kHW / 32);
+        double x[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) x[e] = __ldcs(col + e * 32 + lane);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+            const uint32_t bit = (__ldg(db + e) >> lane) & 1u;
+            x[e] = __longlong_as_double(__double_as_longlong(x[e]) ^ ((long long)bit << 63));
+        }
+        fwht32(x);   // bits 5..9
+#pragma unroll
+        for (int e = 0; e < 32; ++e) xs[hpadw(e * 32 + lane)] = x[e];
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < 32; ++e) x[e] = xs[hpadw(lane * 32 + e)];
+        fwht32(x);   // bits 0..4
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+            if ((mymap >> e) & 1u) xs[hpadw(lane * 32 + e)] = x[e];
+        __syncwarp();
+        const uint32_t hi = (uint32_t)(hb0 + blk);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const double v = xs[hpadw(pl[r])];
+            acc[r] += (__popc(ph[r] & hi) & 1) ? -v : v;
+        }
+        __syncwarp();
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int j = lane + 32 * r;
+        if (j < k) atomicAdd(Y + j + (int64_t)cur * ldy, acc[r] * scale);
+    }
+}
+
 // d < 4096: one CTA per column, the whole vector in shared memory, radix-2 stages (Alg 3's
 // butterflies, one barrier per stage).
 __global__ void __launch_bounds__(256) srht_small_kernel(const double* __restrict__ A, int64_t lda,
@@ -449,8 +553,19 @@ static csk_status srht_impl(int64_t d, int64_t dglob, int64_t row0, int64_t k, u
         int per_sm = 0;
         const bool al = (n == 0 || (((uintptr_t)A & 15) == 0 && (lda & 1) == 0)) && (!b || ((uintptr_t)b & 15) == 0);
         const char* e = std::getenv("CSK_SRHT_TMA");
-        const char* v = std::getenv("CSK_SRHT_KERNEL");   // experiment: 1 = 3-phase kernels
-        if (!(v && std::atoi(v) == 1)) {
+        const char* v = std::getenv("CSK_SRHT_KERNEL");   // experiment: 1 = 3-phase, 2 = radix-64 blocks
+        const int kv = v ? std::atoi(v) : 0;
+        if (kv == 0 && k <= 512) {
+            auto kern = k <= 128 ? srht_warp_kernel<4> : k <= 256 ? srht_warp_kernel<8> : srht_warp_kernel<16>;
+            CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+            CSK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kHWWarps * 32, 0));
+            const int64_t nblk1 = d / kHW, total1 = nblk1 * ncols;
+            const int64_t grid = std::min<int64_t>(ceil_div(total1, kHWWarps), (int64_t)di.num_sms * std::max(per_sm, 1));
+            prof_mark(st, true);
+            kern<<<(unsigned)grid, kHWWarps * 32, 0, st>>>(A, lda, b, (int)n, (int)ncols, nblk1, row0 / kHW, dbits,
+                                                           psamp, (int)k, scale, Y, ldy);
+            CSK_LAUNCH_CHECK();
+        } else if (kv != 1) {
             auto kern = k <= 256 ? srht_r64_kernel<4> : k <= 512 ? srht_r64_kernel<8> : srht_r64_kernel<16>;
             CSK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kH64Threads, 0));
             const int64_t grid = std::min<int64_t>(total, (int64_t)di.num_sms * std::max(per_sm, 1));

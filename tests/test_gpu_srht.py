@@ -84,12 +84,14 @@ def test_srht_errors():
     assert e.value.status == csk.csk.EUNSUPPORTED
 
 
-@pytest.mark.parametrize("path", ["r64", "tma", "ldg"])
+@pytest.mark.parametrize("path", ["warp", "r64", "tma", "ldg"])
 @pytest.mark.parametrize("lda_pad", [0, 1])
 def test_srht_kernel_paths(monkeypatch, path, lda_pad):
-    # default radix-64 kernel; the 3-phase kernels: TMA-fed ring (16-B aligned columns) and the
-    # register-load kernel (forced, or odd lda)
-    if path != "r64":
+    # default warp-block kernel; the radix-64 CTA kernel; the 3-phase kernels: TMA-fed ring
+    # (16-B aligned columns) and the register-load kernel (forced, or odd lda)
+    if path == "r64":
+        monkeypatch.setenv("CSK_SRHT_KERNEL", "2")
+    elif path != "warp":
         monkeypatch.setenv("CSK_SRHT_KERNEL", "1")
     if path == "ldg":
         monkeypatch.setenv("CSK_SRHT_TMA", "0")
