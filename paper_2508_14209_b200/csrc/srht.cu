@@ -557,7 +557,11 @@ static csk_status srht_impl(int64_t d, int64_t dglob, int64_t row0, int64_t k, u
         const int kv = v ? std::atoi(v) : 0;
         if (kv == 0 && k <= 512) {
             auto kern = k <= 128 ? srht_warp_kernel<4> : k <= 256 ? srht_warp_kernel<8> : srht_warp_kernel<16>;
-            CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+            // experiment: shared-memory carveout %.  The driver default measured best (1.49 ms at
+            // d=2^24 x 65, k=128): a larger carveout shrinks L1, which stages the in-flight loads.
+            const char* cv = std::getenv("CSK_SRHT_CARVE");
+            if (cv && *cv)
+                CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(cv)));
             CSK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kHWWarps * 32, 0));
             const int64_t nblk1 = d / kHW, total1 = nblk1 * ncols;
             const int64_t grid = std::min<int64_t>(ceil_div(total1, kHWWarps), (int64_t)di.num_sms * std::max(per_sm, 1));
