@@ -240,8 +240,20 @@ def ls_compare(args, cfg, kappa, dev, stream):
         except csk.CskError as e:
             return str(e).split(":")[1].strip()
 
+    def gs():      # Gaussian sketch-and-solve, k = 2n (Fig 5 "Gaussian" bars)
+        return csk.gs_lstsq(A, b, k2, SKETCH_SEED, x=x)[1]
+
+    def cs():      # CountSketch-only sketch-and-solve, k1 = 2n^2 (GEQRF on k1 x (n+1))
+        return csk.cs_lstsq(plan, A, b, x=x)[1]
+
+    def msh():     # Count+SRHT multisketch
+        return csk.msh_lstsq(plan, k2, A, b, x=x)[1]
+
     out = {"kappa": kappa, "workload": cfg["name"].replace("kappa(A)=1e10", f"kappa(A)={kappa:.0e}")}
-    for name, fn in (("ms", ms), ("ne", ne), ("rc", rc)):
+    solvers = [("ms", ms), ("ne", ne), ("rc", rc)]
+    if not getattr(args, "no_ls_extra", False):
+        solvers += [("gs", gs), ("cs", cs), ("msh", msh)]
+    for name, fn in solvers:
         for _ in range(args.warmup):
             fn()
         torch.cuda.synchronize()
@@ -254,7 +266,7 @@ def ls_compare(args, cfg, kappa, dev, stream):
             out[f"{name}_status"] = res[-1]
         fn()
         out[f"{name}_rel_residual"] = float(torch.linalg.norm(b - A @ x) / torch.linalg.norm(b)) \
-            if (name == "ms" or res[-1] == "OK") else None
+            if (name not in ("ne", "rc") or res[-1] == "OK") else None
     R = torch.linalg.qr(buf, mode="r")[1]
     out["true_rel_residual"] = float(abs(R[n, n]) / torch.linalg.norm(b))
     out["speedup_ms_vs_ne"] = out["ne_ms"] / out["ms_ms"]
@@ -547,6 +559,8 @@ def main():
     ap.add_argument("--no-acc", action="store_true", help="skip the untimed accuracy checks")
     ap.add_argument("--no-ls", action="store_true", help="skip the C4 least-squares comparison (N=1, c2)")
     ap.add_argument("--no-extra", action="store_true", help="skip the kappa=1e10 / fp32 CountSketch lines")
+    ap.add_argument("--no-ls-extra", action="store_true",
+                    help="LS comparison without the Gaussian / CountSketch-only / Count+SRHT solvers")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cfg = CONFIGS[args.config]

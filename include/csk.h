@@ -187,6 +187,35 @@ csk_status rc_lstsq(csk_plan_t plan, int64_t k2, int64_t n, const double* A, int
 csk_status srht_apply(int64_t d, int64_t dglob, int64_t row0, int64_t k, uint64_t seed, int64_t n,
                       const double* A, int64_t lda, const double* b, double* Y, int64_t ldy, void* stream);
 
+/* ------------------------------------------- other sketch-and-solve operators (Fig 5)
+ * gs_apply: Gaussian sketch Z = G[:, row0 .. row0+d) [A b], G k x dglob with G_ij ~ N(0, 1/k)
+ *    from Philox stream 1 of seed, element e = r + (global row) * k (R4's
+ *   generator over a k x d matrix).  The k x d matrix is never stored: each row chunk's slice
+ *   is generated and multiplied in (DGEMM) while L2-resident.  k even.  A (lda >= d), b
+ *   (nullable), Z k x (n + (b != NULL)) (ldz >= k): DEVICE pointers.  Asynchronous. */
+csk_status gs_apply(int64_t d, int64_t row0, int64_t k, uint64_t seed, int64_t n, const double* A, int64_t lda,
+                    const double* b, double* Z, int64_t ldz, void* stream);
+/* gs_lstsq: Gaussian sketch-and-solve (Alg 1 with S = G, k = 2n in the paper): gs_apply on
+ *   [A b] followed by the ms_solve Householder solve.  x: device or host; sk_resid: host or
+ *   NULL.  Requires n + 1 <= k <= 512.  Synchronises the stream. */
+csk_status gs_lstsq(int64_t d, int64_t k, uint64_t seed, int64_t n, const double* A, int64_t lda, const double* b,
+                    double* x, double* sk_resid, void* stream);
+/* cs_lstsq: CountSketch-only sketch-and-solve (Alg 1 with S = S1, k1 = 2n^2): QR of the
+ *   k1 x (n+1) sketch [S1 A | S1 b] by cuSOLVER GEQRF (the paper's GeQRF, whose cost
+ *   dominates this variant), x = R11^-1 r12 on the GPU, sk_resid = |R_nn|.
+ *   A, b, x: DEVICE pointers; sk_resid host or NULL.  ESINGULAR as for ms_solve.  Synchronises. */
+csk_status cs_lstsq(csk_plan_t plan, int64_t n, const double* A, int64_t lda, const double* b, double* x,
+                    double* sk_resid, void* stream);
+/* msh_apply / msh_lstsq: the Count+SRHT multisketch the paper lists as future work:
+ *   Z = SRHT_k2(S1 [A b]) with the SRHT of srht_apply over the k1 rows of the CountSketch
+ *   output (k1 must be a power of two, seed = the plan's).  msh_lstsq adds the ms_solve solve
+ *   (k2 >= n + 1).  DEVICE A, b, Z; x device or host.  msh_apply is asynchronous, msh_lstsq
+ *   synchronises. */
+csk_status msh_apply(csk_plan_t plan, int64_t k2, int64_t n, const double* A, int64_t lda, const double* b, double* Z,
+                     int64_t ldz, void* stream);
+csk_status msh_lstsq(csk_plan_t plan, int64_t k2, int64_t n, const double* A, int64_t lda, const double* b, double* x,
+                     double* sk_resid, void* stream);
+
 /* ------------------------------------------------------------- utilities */
 const char* csk_status_str(csk_status st);
 const char* csk_last_error(void);      /* thread-local detail of the last failure */

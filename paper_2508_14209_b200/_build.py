@@ -56,7 +56,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         for log in logs:
             sys.stderr.write(log)
     tmp = LIB + f".tmp{os.getpid()}"
-    run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcublas",
+    run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcublas", "-lcusolver",
          "-Xlinker", "-rpath=/usr/local/cuda/lib64"])
     os.replace(tmp, LIB)
     return LIB

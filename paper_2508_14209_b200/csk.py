@@ -68,6 +68,11 @@ def lib():
                 "ne_lstsq": [I64, I64, P, I64, P, P, P],
                 "rc_lstsq": [P, I64, I64, P, I64, P, P, P, I64, P],
                 "srht_apply": [I64, I64, I64, I64, U64, I64, P, I64, P, P, I64, P],
+                "gs_apply": [I64, I64, I64, U64, I64, P, I64, P, P, I64, P],
+                "gs_lstsq": [I64, I64, U64, I64, P, I64, P, P, P, P],
+                "cs_lstsq": [P, I64, P, I64, P, P, P, P],
+                "msh_apply": [P, I64, I64, P, I64, P, P, I64, P],
+                "msh_lstsq": [P, I64, I64, P, I64, P, P, P, P],
             }
             for name, argt in sigs.items():
                 f = getattr(L, name)
@@ -308,3 +313,72 @@ def srht_apply(A, k: int, seed: int, b=None, Y=None, dglob: int | None = None, r
     _check(lib().srht_apply(d, dglob if dglob is not None else d, row0, k, seed, n, pA, lda, pb, pY, ldy,
                             _stream(stream, dev)), "srht_apply")
     return Y
+
+
+def gs_apply(A, k: int, seed: int, b=None, Z=None, row0: int = 0, stream=None):
+    """Gaussian sketch Z = G [A b] (k x ncols), G k x d ~ N(0, 1/k) generated by row chunks."""
+    torch = _torch()
+    d = A.shape[0] if A is not None else b.shape[0]
+    n = A.shape[1] if A is not None else 0
+    dev = A.device if A is not None else b.device
+    if Z is None:
+        Z = torch.empty((n + (b is not None), k), dtype=torch.float64, device=dev).t()
+    pA, lda = _colmajor(A, "A") if A is not None else (None, max(d, 1))
+    pb, _ = _colmajor(b, "b")
+    pZ, ldz = _colmajor(Z, "Z")
+    _check(lib().gs_apply(d, row0, k, seed, n, pA, lda, pb, pZ, ldz, _stream(stream, dev)), "gs_apply")
+    return Z
+
+
+def _solve_out(n, dev, x):
+    torch = _torch()
+    return torch.empty(n, dtype=torch.float64, device=dev) if x is None else x
+
+
+def gs_lstsq(A, b, k: int, seed: int, x=None, stream=None):
+    """Gaussian sketch-and-solve: (x, sketched residual)."""
+    d, n = A.shape
+    x = _solve_out(n, A.device, x)
+    pA, lda = _colmajor(A, "A")
+    pb, _ = _colmajor(b, "b")
+    r = ctypes.c_double()
+    _check(lib().gs_lstsq(d, k, seed, n, pA, lda, pb, ctypes.c_void_p(x.data_ptr()), ctypes.byref(r),
+                          _stream(stream, A.device)), "gs_lstsq")
+    return x, r.value
+
+
+def cs_lstsq(plan: Plan, A, b, x=None, stream=None):
+    """CountSketch-only sketch-and-solve (GEQRF of the k1 x (n+1) sketch): (x, sketched residual)."""
+    n = A.shape[1]
+    x = _solve_out(n, A.device, x)
+    pA, lda = _colmajor(A, "A")
+    pb, _ = _colmajor(b, "b")
+    r = ctypes.c_double()
+    _check(lib().cs_lstsq(plan.handle, n, pA, lda, pb, ctypes.c_void_p(x.data_ptr()), ctypes.byref(r),
+                          _stream(stream, A.device)), "cs_lstsq")
+    return x, r.value
+
+
+def msh_apply(plan: Plan, k2: int, A, b=None, Z=None, stream=None):
+    """Count+SRHT multisketch Z = SRHT_k2 (S1 [A b])."""
+    torch = _torch()
+    n = A.shape[1]
+    if Z is None:
+        Z = torch.empty((n + (b is not None), k2), dtype=torch.float64, device=A.device).t()
+    pA, lda = _colmajor(A, "A")
+    pb, _ = _colmajor(b, "b")
+    pZ, ldz = _colmajor(Z, "Z")
+    _check(lib().msh_apply(plan.handle, k2, n, pA, lda, pb, pZ, ldz, _stream(stream, A.device)), "msh_apply")
+    return Z
+
+
+def msh_lstsq(plan: Plan, k2: int, A, b, x=None, stream=None):
+    """Count+SRHT multisketch sketch-and-solve: (x, sketched residual)."""
+    n = A.shape[1]
+    x = _solve_out(n, A.device, x)
+    pA, lda = _colmajor(A, "A")
+    pb, _ = _colmajor(b, "b")
+    r = ctypes.c_double()
+    _check(lib().msh_lstsq(plan.handle, k2, n, pA, lda, pb, ctypes.c_void_p(x.data_ptr()), ctypes.byref(r),
+                           _stream(stream, A.device)), "msh_lstsq")
+    return x, r.value

@@ -181,6 +181,19 @@ csk_status ms_apply_impl(csk_plan_t plan, int64_t k2, csk_dtype dtype, int64_t n
 csk_status solve_impl(int64_t k2, int64_t n, const double* Z, int64_t ldz, double* x, double* sk_resid,
                       cudaStream_t st, bool x_host, double* R_out);
 csk_status blas_handle(cudaStream_t st, cublasHandle_t* out);
+// multisketch.cu: N(0,1) pairs of Philox stream 1 divided by div, starting at pair t_off
+template <typename T>
+__global__ void gauss_kernel(T* __restrict__ G, int64_t total, double div, uint32_t key_lo, uint32_t key_hi,
+                             int64_t t_off);
+// randcholqr.cu: x = R0^-1 u (+ R = R1 R0 when R != NULL), one CTA; skipped if *chol_status != 0
+__global__ void __launch_bounds__(1024, 1) rc_finish_kernel(const double* __restrict__ R0, int ldr0,
+                                                            const double* __restrict__ S, int nc, int n,
+                                                            const double* __restrict__ u, double* __restrict__ x,
+                                                            double* __restrict__ R, int ldr,
+                                                            const int* __restrict__ chol_status);
+// srht.cu
+csk_status srht_impl(int64_t d, int64_t dglob, int64_t row0, int64_t k, uint64_t seed, int64_t n, const double* A,
+                     int64_t lda, const double* b, double* Y, int64_t ldy, cudaStream_t st);
 // normal_eq.cu: upper Cholesky of the augmented Gram C (nc x nc, upper part read) in S (ld nc);
 // x = R^-1 R^-T C[:n, n]; *status = CSK_ENOTPD on a non-positive pivot.
 __global__ void __launch_bounds__(1024, 1) chol_solve_kernel(const double* __restrict__ Cg, int nc, int use_smem,

@@ -38,9 +38,11 @@ csk_status blas_handle(cudaStream_t st, cublasHandle_t* out) {
 // ------------------------------------------------------------------ a4: G
 template <typename T>
 __global__ void gauss_kernel(T* __restrict__ G, int64_t total, double inv_sqrt_scale_div, uint32_t key_lo,
-                             uint32_t key_hi) {
+                             uint32_t key_hi, int64_t t_off) {
+    // element e of the stream is G[e - 2 t_off] (t_off: first pair, for row-chunked Gaussian sketches)
     const int64_t npairs = total >> 1;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < npairs; t += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t tl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; tl < npairs; tl += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = tl + t_off;
         const uint4 x = philox4x32_10(make_uint4((uint32_t)t, (uint32_t)(t >> 32), 1u, 0u), make_uint2(key_lo, key_hi));
         const uint64_t w1 = ((uint64_t)x.y << 32) | x.x;
         const uint64_t w2 = ((uint64_t)x.w << 32) | x.z;
@@ -49,8 +51,8 @@ __global__ void gauss_kernel(T* __restrict__ G, int64_t total, double inv_sqrt_s
         const double rho = sqrt(-2.0 * log(u1));
         double s, c;
         sincospi(2.0 * u2, &s, &c);
-        G[2 * t] = (T)((rho * c) / inv_sqrt_scale_div);
-        G[2 * t + 1] = (T)((rho * s) / inv_sqrt_scale_div);
+        G[2 * tl] = (T)((rho * c) / inv_sqrt_scale_div);
+        G[2 * tl + 1] = (T)((rho * s) / inv_sqrt_scale_div);
     }
 }
 
@@ -81,10 +83,10 @@ csk_status gauss_get(csk_plan_t plan, int64_t k2, csk_dtype dtype, cudaStream_t 
     const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(std::max<int64_t>(total / 2, 1), 256), 148 * 32);
     if (dtype == CSK_F64)
         gauss_kernel<double><<<grid, 256, 0, st>>>((double*)G, total, div, (uint32_t)plan->seed,
-                                                    (uint32_t)(plan->seed >> 32));
+                                                    (uint32_t)(plan->seed >> 32), 0);
     else
         gauss_kernel<float><<<grid, 256, 0, st>>>((float*)G, total, div, (uint32_t)plan->seed,
-                                                   (uint32_t)(plan->seed >> 32));
+                                                   (uint32_t)(plan->seed >> 32), 0);
     count_launch();
     if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) {
         cudaFree(G);
@@ -116,6 +118,9 @@ csk_status gauss_get(csk_plan_t plan, int64_t k2, csk_dtype dtype, cudaStream_t 
     *out = G;
     return CSK_OK;
 }
+
+template __global__ void gauss_kernel<double>(double*, int64_t, double, uint32_t, uint32_t, int64_t);
+template __global__ void gauss_kernel<float>(float*, int64_t, double, uint32_t, uint32_t, int64_t);
 
 // ---------------------------------------------------- a3 over host inputs
 // Host A/b: stream row chunks through two device staging buffers; the copy of

@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(256) srht_small_kernel(const double* __restric
     for (int j = threadIdx.x; j < k; j += blockDim.x) Y[j + (int64_t)c * ldy] = v[psamp[j]] * scale;
 }
 
-static csk_status srht_impl(int64_t d, int64_t dglob, int64_t row0, int64_t k, uint64_t seed, int64_t n,
+csk_status srht_impl(int64_t d, int64_t dglob, int64_t row0, int64_t k, uint64_t seed, int64_t n,
                             const double* A, int64_t lda, const double* b, double* Y, int64_t ldy, cudaStream_t st) {
     const int64_t ncols = n + (b ? 1 : 0);
     CSK_REQUIRE(d >= 1 && k >= 1 && n >= 0 && ncols >= 1 && Y != nullptr, CSK_EINVAL, "bad SRHT arguments");
