@@ -437,6 +437,53 @@ def bench_ours(args, cfg):
         del buf32, SA32
         torch.cuda.empty_cache()
 
+    # ---- roofline attribution of the dominant kernel (N = 1): the same launch with its A loads
+    # skipped (reduce path alone) and with its reductions skipped (HBM read path alone), via the
+    # library's compile-time experiment variants (CSK_EXP, DESIGN.md 6.1/6.1b).  If the full
+    # kernel runs at the reduce-only time, the L2 fp64 reduction rate -- not HBM -- bounds it.
+    attribution = None
+    if ws == 1 and not args.no_extra and args.variant in ("auto", "B"):
+        def time_exp(e):
+            os.environ["CSK_EXP"] = str(e)
+            try:
+                for _ in range(2):
+                    csk.cs_apply(plan, A, b=b, SA=SA)
+                barrier()
+                ev0.record(stream)
+                for _ in range(args.steps):
+                    csk.cs_apply(plan, A, b=b, SA=SA)
+                ev1.record(stream)
+                barrier()
+                return ev0.elapsed_time(ev1) / args.steps
+            finally:
+                del os.environ["CSK_EXP"]
+        red_ms, load_ms = time_exp(2), time_exp(1)
+        attribution = {"cs_apply_ms": cs_ms, "reduce_path_only_ms": red_ms, "load_path_only_ms": load_ms,
+                       "load_path_gbs": bytes_step / (load_ms * 1e-3) / 1e9,
+                       "kernel_over_reduce_path": kern_ms / red_ms,
+                       "note": "reduce path alone = every row's bulk reduce-add into the L2-resident SA^T with the "
+                               "A loads skipped; the kernel is bound by whichever path is slower"}
+
+    # ---- the Count+SRHT multisketch step on the same [A b], for comparison
+    msh = None
+    if ws == 1 and not args.no_extra and not args.cs_only and (k1 & (k1 - 1)) == 0:
+        Zh = synth.colmajor_empty(torch, k2, ncols, torch.float64, dev)
+        def msh_step():
+            csk.msh_apply(plan, k2, A, b=b, Z=Zh)
+            csk.ms_solve(Zh, n, x=x)
+        for _ in range(2):
+            msh_step()
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            msh_step()
+        ev1.record(stream)
+        barrier()
+        msh = {"step_ms": ev0.elapsed_time(ev1) / args.steps,
+               "rel_residual": float(torch.linalg.norm(b - A @ x) / torch.linalg.norm(b)),
+               "what": "msh_apply (CountSketch + SRHT_k2 over the k1 sketch rows) + ms_solve"}
+        del Zh
+
     # ---- normal-equations baseline (a8) on the same [A b]
     ne = {"gram": os.environ.get("CSK_NE_GRAM", "cuBLAS DGEMM A^T A + DGEMV A^T b + DDOT b^T b, one-CTA augmented Cholesky")}
     def ne_call():
@@ -520,12 +567,13 @@ def bench_ours(args, cfg):
                      "traffic": ncu_traffic(args.config, variant), "kernel": "cs_apply main kernel",
                      "kernel_ms": kern_ms, "kernel_share_of_step": kern_ms / step_ms,
                      "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
-                     "frac_of_8TBs_nominal": achieved / NOMINAL_HBM_GBS},
+                     "frac_of_8TBs_nominal": achieved / NOMINAL_HBM_GBS, "attribution": attribution},
         "cpu_baseline": cpu,
         "phases_ms": {"cs_apply": cs_ms, "g_stage": msa_ms - cs_ms, "solve": solve_ms, "plan_codes": plan_ms,
                       "gauss_first_use": gauss_first_ms},
         "cs_apply_gbs": bytes_step / (cs_ms * 1e-3) / 1e9,
         "cs_apply_input_families": families,
+        "count_srht_multisketch": msh,
         "normal_equations": ne,
         "speedup_vs_ne": (ne["ms"] / step_ms) if ne.get("ms") else None,
         "accuracy": acc,

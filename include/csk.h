@@ -172,6 +172,23 @@ csk_status ne_lstsq(int64_t d, int64_t n, const double* A, int64_t lda, const do
 csk_status rc_lstsq(csk_plan_t plan, int64_t k2, int64_t n, const double* A, int64_t lda, const double* b,
                     double* x, double* R, int64_t ldr, void* stream);
 
+/* The phases of rc_lstsq, for a row-partitioned A: every rank calls ms_apply on
+ * its block (sum the Z's: all-reduce 1), rc_r0 on the summed Z, rc_gram on its block (sum the
+ * C's: all-reduce 2), then rc_finish.  rc_lstsq == these four calls on one GPU.
+ * rc_r0:     R0 = R[:n,:n] of the Householder QR of Z = [G S A | G S b] (k2 x (n+1), ldz);
+ *            R0 n x n upper, ld ldr0 >= n.  k2 <= 512.  ESINGULAR as ms_solve.  Synchronises.
+ * rc_gram:   C = [Q0^T Q0 | Q0^T b] over this block's d rows, Q0 = A R0^-1 (R24) computed tile by
+ *            tile and never stored; C (n+1) x (n+1), ld ldc >= n+1: the upper triangle of
+ *            C[:n,:n] and column n are written (C[n,n] = 0, the rest unspecified).  Asynchronous.
+ * rc_finish: R1 = chol(C[:n,:n]) (ENOTPD on breakdown), x = R0^-1 R1^-1 R1^-T C[:n,n];
+ *            R (nullable) = R1 R0, n x n, ld ldr.  Synchronises.
+ * All pointers are DEVICE pointers. */
+csk_status rc_r0(int64_t k2, int64_t n, const double* Z, int64_t ldz, double* R0, int64_t ldr0, void* stream);
+csk_status rc_gram(int64_t d, int64_t n, const double* A, int64_t lda, const double* b, const double* R0, int64_t ldr0,
+                   double* C, int64_t ldc, void* stream);
+csk_status rc_finish(int64_t n, const double* C, int64_t ldc, const double* R0, int64_t ldr0, double* x, double* R,
+                     int64_t ldr, void* stream);
+
 /* srht_apply: the SRHT S = k^-1/2 P H_d D (Def) applied to
  * [A b]:  Y[j, c] = k^-1/2 (H_d D [A b][:, c])[p_j],  fp64.
  *   D_ii = +-1 and the k sampled rows p_j (i.i.d. uniform, with replacement) come from Philox

@@ -68,6 +68,9 @@ def lib():
                 "ne_lstsq": [I64, I64, P, I64, P, P, P],
                 "rc_lstsq": [P, I64, I64, P, I64, P, P, P, I64, P],
                 "srht_apply": [I64, I64, I64, I64, U64, I64, P, I64, P, P, I64, P],
+                "rc_r0": [I64, I64, P, I64, P, I64, P],
+                "rc_gram": [I64, I64, P, I64, P, P, I64, P, I64, P],
+                "rc_finish": [I64, P, I64, P, I64, P, P, I64, P],
                 "gs_apply": [I64, I64, I64, U64, I64, P, I64, P, P, I64, P],
                 "gs_lstsq": [I64, I64, U64, I64, P, I64, P, P, P, P],
                 "cs_lstsq": [P, I64, P, I64, P, P, P, P],
@@ -382,3 +385,39 @@ def msh_lstsq(plan: Plan, k2: int, A, b, x=None, stream=None):
     _check(lib().msh_lstsq(plan.handle, k2, n, pA, lda, pb, ctypes.c_void_p(x.data_ptr()), ctypes.byref(r),
                            _stream(stream, A.device)), "msh_lstsq")
     return x, r.value
+
+
+def rc_r0(Z, n: int, stream=None):
+    """R0 (n x n, upper) of the Householder QR of the (all-reduced) sketch Z = [GSA | GSb]."""
+    torch = _torch()
+    R0 = torch.zeros((n, n), dtype=torch.float64, device=Z.device).t()
+    pZ, ldz = _colmajor(Z, "Z")
+    _check(lib().rc_r0(Z.shape[0], n, pZ, ldz, ctypes.c_void_p(R0.data_ptr()), n, _stream(stream, Z.device)), "rc_r0")
+    return R0
+
+
+def rc_gram(A, b, R0, stream=None):
+    """[Q0^T Q0 | Q0^T b] ((n+1) x (n+1); upper triangle + column n) over this block's rows, Q0 = A R0^-1."""
+    torch = _torch()
+    d, n = A.shape
+    C = torch.zeros((n + 1, n + 1), dtype=torch.float64, device=A.device).t()
+    pA, lda = _colmajor(A, "A")
+    pb, _ = _colmajor(b, "b")
+    pR, ldr0 = _colmajor(R0, "R0")
+    _check(lib().rc_gram(d, n, pA, lda, pb, pR, ldr0, ctypes.c_void_p(C.data_ptr()), n + 1,
+                         _stream(stream, A.device)), "rc_gram")
+    return C
+
+
+def rc_finish(C, R0, want_R: bool = False, stream=None):
+    """x (and R = R1 R0) from the (all-reduced) C and R0."""
+    torch = _torch()
+    n = R0.shape[0]
+    x = torch.empty(n, dtype=torch.float64, device=C.device)
+    R = torch.empty((n, n), dtype=torch.float64, device=C.device).t() if want_R else None
+    pC, ldc = _colmajor(C, "C")
+    pR0, ldr0 = _colmajor(R0, "R0")
+    pR, ldr = _colmajor(R, "R") if want_R else (None, n)
+    _check(lib().rc_finish(n, pC, ldc, pR0, ldr0, ctypes.c_void_p(x.data_ptr()), pR, ldr, _stream(stream, C.device)),
+           "rc_finish")
+    return (x, R) if want_R else x

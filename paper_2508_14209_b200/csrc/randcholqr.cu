@@ -456,52 +456,22 @@ __global__ void rc_reduce_kernel(const double* __restrict__ part, int parts, int
     }
 }
 
-static csk_status rc_impl(csk_plan_t plan, int64_t k2, int64_t n, const double* A, int64_t lda, const double* b,
-                          double* x, double* R, int64_t ldr, cudaStream_t st) {
-    CSK_REQUIRE(plan != nullptr, CSK_EINVAL, "plan is NULL");
-    CSK_REQUIRE(A != nullptr && b != nullptr && x != nullptr, CSK_EINVAL, "A, b, x must be non-NULL");
-    CSK_REQUIRE(n >= 1 && n <= 1024, CSK_EINVAL, "n=%lld must be in [1, 1024]", (long long)n);
-    CSK_REQUIRE(k2 >= n + 1, CSK_ESHAPE, "k2=%lld must be >= n+1=%lld", (long long)k2, (long long)(n + 1));
-    const int64_t d = plan->d;
-    CSK_REQUIRE(d >= n, CSK_ESHAPE, "d=%lld < n=%lld", (long long)d, (long long)n);
-    CSK_REQUIRE(lda >= d, CSK_ESHAPE, "lda=%lld < d=%lld", (long long)lda, (long long)d);
-    CSK_REQUIRE(R == nullptr || ldr >= n, CSK_ESHAPE, "ldr=%lld < n", (long long)ldr);
-    CSK_REQUIRE(is_device_pointer(A) && is_device_pointer(b) && is_device_pointer(x) &&
-                    (R == nullptr || is_device_pointer(R)),
-                CSK_EINVAL, "rc_lstsq takes device pointers");
+// Alg 5 lines 3-4 over this block's rows: C (nc x nc, ld ldc) = [Q0^T Q0 (upper) | Q0^T b],
+// Q0 = A R0^-1, R0 upper n x n (ld ldr0).  Row-partitioned callers sum the C's.
+static csk_status rc_gram_impl(int64_t d, int64_t n, const double* A, int64_t lda, const double* b, const double* R0,
+                               int64_t ldr0, double* C, int64_t ldc, cudaStream_t st) {
+    CSK_REQUIRE(A != nullptr && b != nullptr && R0 != nullptr && C != nullptr, CSK_EINVAL, "NULL argument");
+    CSK_REQUIRE(n >= 1 && n <= 1024 && d >= 1, CSK_EINVAL, "n=%lld must be in [1, 1024], d >= 1", (long long)n);
+    CSK_REQUIRE(lda >= d && ldr0 >= n && ldc >= n + 1, CSK_ESHAPE, "bad leading dimension");
+    CSK_REQUIRE(is_device_pointer(A) && is_device_pointer(b) && is_device_pointer(R0) && is_device_pointer(C),
+                CSK_EINVAL, "rc_gram takes device pointers");
     const int nc = (int)n + 1;
-    // chunk rows: the chunk's Q0 (rows x n doubles) stays L2-resident between TRSM and GEMM
-    int64_t mc = (int64_t)device_info().l2_bytes / 4 / (8 * n);
-    if (const char* e = std::getenv("CSK_RC_CHUNK")) mc = std::max<int64_t>(256, std::atoll(e));
-    mc = std::max<int64_t>(1024, mc & ~(int64_t)255);
-    mc = std::min(mc, d);
-    cublasHandle_t h;
-    csk_status s = blas_handle(st, &h);
-    if (s != CSK_OK) return s;
-    // workspace: Z (k2 x nc) | R0aug (nc x nc) | xs (nc) | C (nc x nc) | S (nc x nc) | u (nc) | Wk (mc x n) | status
-    auto pad = [](size_t cnt) { return (cnt + 31) & ~(size_t)31; };   // 256-B aligned regions
-    const size_t zd = pad((size_t)k2 * nc), rd = pad((size_t)nc * nc), vd = pad(nc);
-    const size_t total = zd + 3 * rd + 2 * vd + pad((size_t)mc * n) + 32;
-    double* ws = nullptr;
-    CSK_CUDA_TRY(cudaMallocAsync(&ws, total * 8, st));
-    double* Z = ws;
-    double* R0 = Z + zd;
-    double* xs = R0 + rd;
-    double* C = xs + vd;
-    double* S = C + rd;
-    double* u = S + rd;
-    double* Wk = u + vd;
-    int* sd = reinterpret_cast<int*>(Wk + pad((size_t)mc * n));
-    // lines 1-2
-    s = ms_apply_impl(plan, k2, CSK_F64, n, A, lda, b, Z, k2, st);
-    if (s == CSK_OK) s = solve_impl(k2, n, Z, k2, xs, nullptr, st, false, R0);
-    if (s != CSK_OK) {
-        cudaFreeAsync(ws, st);
-        return s;
-    }
-    // lines 3-4
     const char* pe = std::getenv("CSK_RC_PATH");
     const bool fused = n <= 128 && !(pe && std::atoi(pe) == 0);
+    // the fused kernels and the reduction write an nc x nc C with ld nc; copy out when ldc differs
+    double* Cw = C;
+    if (ldc != nc) CSK_CUDA_TRY(cudaMallocAsync(&Cw, (size_t)nc * nc * 8, st));
+    csk_status s = CSK_OK;
     if (fused) {
         const int nb = n <= 16 ? 2 : n <= 32 ? 4 : n <= 64 ? 8 : 16;
         const int NP = 8 * nb, LD = NP + 4;
@@ -519,7 +489,7 @@ static csk_status rc_impl(csk_plan_t plan, int64_t k2, int64_t n, const double* 
             auto kern = nb == 2 ? rc_pass_kernel<2> : nb == 4 ? rc_pass_kernel<4> : nb == 8 ? rc_pass_kernel<8>
                                                                                               : rc_pass_kernel<16>;
             CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            kern<<<grid, kRcWarps * 32, smem, st>>>(A, lda, b, d, (int)n, R0, nc, part, nc, al16);
+            kern<<<grid, kRcWarps * 32, smem, st>>>(A, lda, b, d, (int)n, R0, (int)ldr0, part, nc, al16);
         } else {
             const size_t smem_ws = ((size_t)rc_r0_off(nb) + 2 * (size_t)kWsRows * LD + 2 * (size_t)NP * (kWsRows + 4) +
                                     4 * kWsRows + NP + (size_t)nb * 96) * 8;
@@ -530,40 +500,77 @@ static csk_status rc_impl(csk_plan_t plan, int64_t k2, int64_t n, const double* 
                             : (nb == 2 ? rc_pass_ws_kernel<2, false> : nb == 4 ? rc_pass_ws_kernel<4, false>
                                : nb == 8 ? rc_pass_ws_kernel<8, false> : rc_pass_ws_kernel<16, false>);
             CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ws));
-            kern<<<grid, (kWsSolve + kWsGram) * 32, smem_ws, st>>>(A, lda, b, d, (int)n, R0, nc, part, nc, al16);
+            kern<<<grid, (kWsSolve + kWsGram) * 32, smem_ws, st>>>(A, lda, b, d, (int)n, R0, (int)ldr0, part, nc,
+                                                                   al16);
         }
         CSK_LAUNCH_CHECK();
         rc_reduce_kernel<<<(unsigned)std::min<int64_t>(ceil_div((int64_t)nc * nc, 256), 1024), 256, 0, st>>>(
-            part, grid, (int64_t)nc * nc, C);
+            part, grid, (int64_t)nc * nc, Cw);
         CSK_LAUNCH_CHECK();
         CSK_CUDA_TRY(cudaFreeAsync(part, st));
+    } else {
+        // row-chunked cuBLAS: chunk copy -> DTRSM in place -> DGEMM (Q0^T Q0) + DGEMV (Q0^T b); the chunk's Q0
+        // (rows x n doubles) stays L2-resident between the calls
+        int64_t mc = (int64_t)device_info().l2_bytes / 4 / (8 * n);
+        if (const char* e = std::getenv("CSK_RC_CHUNK")) mc = std::max<int64_t>(256, std::atoll(e));
+        mc = std::min(std::max<int64_t>(1024, mc & ~(int64_t)255), d);
+        cublasHandle_t h;
+        s = blas_handle(st, &h);
+        double* Wk = nullptr;
+        if (s == CSK_OK) CSK_CUDA_TRY(cudaMallocAsync(&Wk, (size_t)mc * n * 8, st));
+        const double one = 1.0, zero = 0.0;
+        cublasStatus_t bs = CUBLAS_STATUS_SUCCESS;
+        for (int64_t r0 = 0; s == CSK_OK && r0 < d && bs == CUBLAS_STATUS_SUCCESS; r0 += mc) {
+            const int64_t m = std::min(mc, d - r0);
+            const double* beta = r0 == 0 ? &zero : &one;
+            CSK_CUDA_TRY(cudaMemcpy2DAsync(Wk, m * 8, A + r0, lda * 8, m * 8, n, cudaMemcpyDeviceToDevice, st));
+            bs = cublasDtrsm(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)m,
+                             (int)n, &one, R0, (int)ldr0, Wk, (int)m);
+            if (bs == CUBLAS_STATUS_SUCCESS)
+                bs = cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)n, (int)n, (int)m, &one, Wk, (int)m, Wk, (int)m,
+                                 beta, Cw, nc);
+            if (bs == CUBLAS_STATUS_SUCCESS)
+                bs = cublasDgemv(h, CUBLAS_OP_T, (int)m, (int)n, &one, Wk, (int)m, b + r0, 1, beta,
+                                 Cw + (size_t)n * nc, 1);
+        }
+        if (Wk) cudaFreeAsync(Wk, st);
+        if (s == CSK_OK && bs != CUBLAS_STATUS_SUCCESS) {
+            set_error("cuBLAS rand_cholQR pass failed (%d)", (int)bs);
+            s = CSK_ECUDA;
+        }
+        if (s == CSK_OK) CSK_CUDA_TRY(cudaMemsetAsync(Cw + (size_t)n * nc + n, 0, 8, st));
     }
-    const double one = 1.0, zero = 0.0;
-    cublasStatus_t bs = CUBLAS_STATUS_SUCCESS;
-    for (int64_t r0 = 0; !fused && r0 < d && bs == CUBLAS_STATUS_SUCCESS; r0 += mc) {
-        const int64_t m = std::min(mc, d - r0);
-        const double* beta = r0 == 0 ? &zero : &one;
-        CSK_CUDA_TRY(cudaMemcpy2DAsync(Wk, m * 8, A + r0, lda * 8, m * 8, n, cudaMemcpyDeviceToDevice, st));
-        bs = cublasDtrsm(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)m, (int)n,
-                         &one, R0, nc, Wk, (int)m);
-        if (bs == CUBLAS_STATUS_SUCCESS)
-            bs = cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)n, (int)n, (int)m, &one, Wk, (int)m, Wk, (int)m, beta,
-                             C, nc);
-        if (bs == CUBLAS_STATUS_SUCCESS)
-            bs = cublasDgemv(h, CUBLAS_OP_T, (int)m, (int)n, &one, Wk, (int)m, b + r0, 1, beta, C + (size_t)n * nc, 1);
+    if (Cw != C) {
+        if (s == CSK_OK)
+            CSK_CUDA_TRY(cudaMemcpy2DAsync(C, ldc * 8, Cw, nc * 8, nc * 8, nc, cudaMemcpyDeviceToDevice, st));
+        cudaFreeAsync(Cw, st);
     }
-    if (bs != CUBLAS_STATUS_SUCCESS) {
-        cudaFreeAsync(ws, st);
-        set_error("cuBLAS rand_cholQR pass failed (%d)", (int)bs);
-        return CSK_ECUDA;
-    }
-    CSK_CUDA_TRY(cudaMemsetAsync(C + (size_t)n * nc + n, 0, 8, st));   // b^T b is not needed for x
-    // line 5 (+ R1^-T z and R1^-1 of it)
+    return s;
+}
+
+// Alg 5 lines 5-8 from the (all-reduced) C: R1 = chol(C11), u = R1^-1 R1^-T z, x = R0^-1 u, R = R1 R0
+static csk_status rc_finish_impl(int64_t n, const double* C, int64_t ldc, const double* R0, int64_t ldr0, double* x,
+                                 double* R, int64_t ldr, cudaStream_t st) {
+    CSK_REQUIRE(C != nullptr && R0 != nullptr && x != nullptr, CSK_EINVAL, "NULL argument");
+    CSK_REQUIRE(n >= 1 && n <= 1024, CSK_EINVAL, "n out of range");
+    CSK_REQUIRE(ldc >= n + 1 && ldr0 >= n && (R == nullptr || ldr >= n), CSK_ESHAPE, "bad leading dimension");
+    CSK_REQUIRE(is_device_pointer(C) && is_device_pointer(R0) && is_device_pointer(x) &&
+                    (R == nullptr || is_device_pointer(R)),
+                CSK_EINVAL, "rc_finish takes device pointers");
+    const int nc = (int)n + 1;
+    auto pad = [](size_t cnt) { return (cnt + 31) & ~(size_t)31; };
+    double* ws = nullptr;
+    CSK_CUDA_TRY(cudaMallocAsync(&ws, (2 * pad((size_t)nc * nc) + pad(nc) + 32) * 8, st));
+    double* Cc = ws;
+    double* S = Cc + pad((size_t)nc * nc);
+    double* u = S + pad((size_t)nc * nc);
+    int* sd = reinterpret_cast<int*>(u + pad(nc));
+    CSK_CUDA_TRY(cudaMemcpy2DAsync(Cc, nc * 8, C, ldc * 8, nc * 8, nc, cudaMemcpyDeviceToDevice, st));
+    CSK_CUDA_TRY(cudaMemsetAsync(Cc + (size_t)n * nc + n, 0, 8, st));   // b^T b is not needed for x
     CSK_CUDA_TRY(cudaFuncSetAttribute(chol_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 0));
-    chol_solve_kernel<<<1, 1024, 0, st>>>(C, nc, 0, S, u, sd);
+    chol_solve_kernel<<<1, 1024, 0, st>>>(Cc, nc, 0, S, u, sd);
     CSK_LAUNCH_CHECK();
-    // lines 6-8
-    rc_finish_kernel<<<1, 1024, (size_t)n * 8, st>>>(R0, nc, S, nc, (int)n, u, x, R, (int)ldr, sd);
+    rc_finish_kernel<<<1, 1024, (size_t)n * 8, st>>>(R0, (int)ldr0, S, nc, (int)n, u, x, R, (int)ldr, sd);
     CSK_LAUNCH_CHECK();
     int hs = 0;
     CSK_CUDA_TRY(cudaMemcpyAsync(&hs, sd, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -576,9 +583,70 @@ static csk_status rc_impl(csk_plan_t plan, int64_t k2, int64_t n, const double* 
     return CSK_OK;
 }
 
+// Alg 5 line 2 from the (all-reduced) sketch Z = [G S A | G S b]: R0 = R[:n, :n] of qr(Z) (ld ldr0).
+static csk_status rc_r0_impl(int64_t k2, int64_t n, const double* Z, int64_t ldz, double* R0, int64_t ldr0,
+                             cudaStream_t st) {
+    CSK_REQUIRE(R0 != nullptr && is_device_pointer(R0), CSK_EINVAL, "R0 must be a device pointer");
+    CSK_REQUIRE(ldr0 >= n, CSK_ESHAPE, "ldr0 < n");
+    const int nc = (int)n + 1;
+    double* ws = nullptr;
+    CSK_CUDA_TRY(cudaMallocAsync(&ws, ((size_t)nc * nc + nc) * 8, st));
+    csk_status s = solve_impl(k2, n, Z, ldz, ws + (size_t)nc * nc, nullptr, st, false, ws);
+    if (s == CSK_OK)
+        CSK_CUDA_TRY(cudaMemcpy2DAsync(R0, ldr0 * 8, ws, nc * 8, n * 8, n, cudaMemcpyDeviceToDevice, st));
+    cudaFreeAsync(ws, st);
+    return s;
+}
+
+static csk_status rc_impl(csk_plan_t plan, int64_t k2, int64_t n, const double* A, int64_t lda, const double* b,
+                          double* x, double* R, int64_t ldr, cudaStream_t st) {
+    CSK_REQUIRE(plan != nullptr, CSK_EINVAL, "plan is NULL");
+    CSK_REQUIRE(A != nullptr && b != nullptr && x != nullptr, CSK_EINVAL, "A, b, x must be non-NULL");
+    CSK_REQUIRE(n >= 1 && n <= 1024, CSK_EINVAL, "n=%lld must be in [1, 1024]", (long long)n);
+    CSK_REQUIRE(k2 >= n + 1, CSK_ESHAPE, "k2=%lld must be >= n+1=%lld", (long long)k2, (long long)(n + 1));
+    const int64_t d = plan->d;
+    CSK_REQUIRE(d >= n, CSK_ESHAPE, "d=%lld < n=%lld", (long long)d, (long long)n);
+    CSK_REQUIRE(lda >= d, CSK_ESHAPE, "lda=%lld < d=%lld", (long long)lda, (long long)d);
+    CSK_REQUIRE(R == nullptr || ldr >= n, CSK_ESHAPE, "ldr=%lld < n", (long long)ldr);
+    CSK_REQUIRE(is_device_pointer(A) && is_device_pointer(b) && is_device_pointer(x) &&
+                    (R == nullptr || is_device_pointer(R)),
+                CSK_EINVAL, "rc_lstsq takes device pointers");
+    const int nc = (int)n + 1;
+    auto pad = [](size_t cnt) { return (cnt + 31) & ~(size_t)31; };
+    double* ws = nullptr;
+    CSK_CUDA_TRY(cudaMallocAsync(&ws, (pad((size_t)k2 * nc) + 2 * pad((size_t)nc * nc)) * 8, st));
+    double* Z = ws;
+    double* R0 = Z + pad((size_t)k2 * nc);      // n x n, ld nc
+    double* C = R0 + pad((size_t)nc * nc);      // nc x nc
+    csk_status s = ms_apply_impl(plan, k2, CSK_F64, n, A, lda, b, Z, k2, st);   // line 1
+    if (s == CSK_OK) s = rc_r0_impl(k2, n, Z, k2, R0, nc, st);                   // line 2
+    if (s == CSK_OK) s = rc_gram_impl(d, n, A, lda, b, R0, nc, C, nc, st);       // lines 3-4
+    if (s == CSK_OK) s = rc_finish_impl(n, C, nc, R0, nc, x, R, ldr, st);        // lines 5-8
+    cudaFreeAsync(ws, st);
+    return s;
+}
+
 }  // namespace csk
 
-extern "C" csk_status rc_lstsq(csk_plan_t plan, int64_t k2, int64_t n, const double* A, int64_t lda, const double* b,
-                               double* x, double* R, int64_t ldr, void* stream) {
+extern "C" {
+
+csk_status rc_lstsq(csk_plan_t plan, int64_t k2, int64_t n, const double* A, int64_t lda, const double* b, double* x,
+                    double* R, int64_t ldr, void* stream) {
     return csk::rc_impl(plan, k2, n, A, lda, b, x, R, ldr, (cudaStream_t)stream);
 }
+
+csk_status rc_r0(int64_t k2, int64_t n, const double* Z, int64_t ldz, double* R0, int64_t ldr0, void* stream) {
+    return csk::rc_r0_impl(k2, n, Z, ldz, R0, ldr0, (cudaStream_t)stream);
+}
+
+csk_status rc_gram(int64_t d, int64_t n, const double* A, int64_t lda, const double* b, const double* R0, int64_t ldr0,
+                   double* C, int64_t ldc, void* stream) {
+    return csk::rc_gram_impl(d, n, A, lda, b, R0, ldr0, C, ldc, (cudaStream_t)stream);
+}
+
+csk_status rc_finish(int64_t n, const double* C, int64_t ldc, const double* R0, int64_t ldr0, double* x, double* R,
+                     int64_t ldr, void* stream) {
+    return csk::rc_finish_impl(n, C, ldc, R0, ldr0, x, R, ldr, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -51,3 +51,48 @@ def ms_lstsq_distributed(A_local, b_local, row0: int, k1: int, k2: int, seed: in
             Z = Z.contiguous()
             dist.all_reduce(Z, op=dist.ReduceOp.SUM, group=group)
     return solve_(Z, A_local.shape[1])
+
+
+def _all_reduce_colmajor(M, group):
+    """SUM all-reduce of a column-major (m, k) tensor in place (or of a contiguous copy)."""
+    import torch.distributed as dist
+    if not (dist.is_initialized() and dist.get_world_size(group) > 1):
+        return M
+    if M.t().is_contiguous():
+        dist.all_reduce(M.t(), op=dist.ReduceOp.SUM, group=group)
+        return M
+    M = M.contiguous()
+    dist.all_reduce(M, op=dist.ReduceOp.SUM, group=group)
+    return M
+
+
+def _cuda_rc_r0(Z, n):
+    from . import csk
+    return csk.rc_r0(Z, n)
+
+
+def _cuda_rc_gram(A_local, b_local, R0):
+    from . import csk
+    return csk.rc_gram(A_local, b_local, R0)
+
+
+def _cuda_rc_finish(C, R0):
+    from . import csk
+    return csk.rc_finish(C, R0)
+
+
+def rc_lstsq_distributed(A_local, b_local, row0: int, k1: int, k2: int, seed: int, group=None,
+                         local_apply=None, local_r0=None, local_gram=None, local_finish=None):
+    """rand_cholQR least squares (Alg 5) on a row-partitioned [A b]: the exact LS
+    solution x on every rank.  Two SUM all-reduces: the k2 x (n+1) sketch Z (as in
+    ms_lstsq_distributed) and the (n+1) x (n+1) Gram [Q0^T Q0 | Q0^T b] of the preconditioned
+    blocks Q0^(g) = A^(g) R0^-1 (every rank holds the same R0).  Collective over ``group``."""
+    apply_ = local_apply or _cuda_apply
+    r0_ = local_r0 or _cuda_rc_r0
+    gram_ = local_gram or _cuda_rc_gram
+    finish_ = local_finish or _cuda_rc_finish
+    n = A_local.shape[1]
+    Z = _all_reduce_colmajor(apply_(A_local, b_local, row0, k1, k2, seed), group)   # lines 1: G S [A b]
+    R0 = r0_(Z, n)                                                                  # line 2 (redundant per rank)
+    C = _all_reduce_colmajor(gram_(A_local, b_local, R0), group)                    # lines 3-4
+    return finish_(C, R0)                                                           # lines 5-8

@@ -132,3 +132,29 @@ def test_rc_lstsq_paths_and_shapes(monkeypatch, path, d, n):
     Rg = host(R)
     AtA = A.T @ A
     assert np.abs(Rg.T @ Rg - AtA).max() <= 1e-11 * np.abs(AtA).max()
+
+
+@pytest.mark.parametrize("p", [1, 3])
+def test_rc_phases_row_partitioned(p):
+    # the distributed form on one GPU: sum_g Z_g -> rc_r0 -> sum_g rc_gram(A_g) -> rc_finish
+    # must reproduce rc_lstsq (and the oracle) -- P:L373-381 linearity of both reductions
+    d, n = 30011, 20
+    k1, k2 = 2 * n * n, 2 * n
+    A, b = _case(d, n, 1e8, "hard", seed=9)
+    Ad, bd = gpu_colmajor(A), gpu_colmajor(b)
+    bounds = [g * d // p for g in range(p + 1)]
+    Z = None
+    for g in range(p):
+        r0, r1 = bounds[g], bounds[g + 1]
+        plan = csk.cs_plan(r1 - r0, k1, 2, row0=r0)
+        Zg = csk.ms_apply(plan, k2, Ad[r0:r1], b=bd[r0:r1])
+        Z = Zg if Z is None else Z + Zg
+    R0 = csk.rc_r0(Z, n)
+    C = sum(csk.rc_gram(Ad[bounds[g]:bounds[g + 1]], bd[bounds[g]:bounds[g + 1]], R0) for g in range(p))
+    x, R = csk.rc_finish(C, R0, want_R=True)
+    xo, Ro = _oracle(A, b, k1, k2, seed=2)
+    nb = np.linalg.norm(b)
+    rr = oracle.residual_norm(A, b, xo) / nb
+    assert np.linalg.norm(A @ (host(x) - xo)) / nb <= max(1e-8, 64 * U * 1e8 * rr)
+    x1 = host(csk.rc_lstsq(csk.cs_plan(d, k1, 2), k2, Ad, bd))
+    assert np.linalg.norm(A @ (host(x) - x1)) / nb <= max(1e-8, 64 * U * 1e8 * rr)
