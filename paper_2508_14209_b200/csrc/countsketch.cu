@@ -40,6 +40,7 @@ struct RowLayout {
     int64_t lc = 0, cs = 0;
     bool chunk_major = false;
     bool tma = false;   // launch marked TMA-eligible by cs_apply_impl (variants X / B-with-TMA)
+    int64_t sep = -1;   // >= 0: the last column is accumulated apart (B32 "split"), k1 doubles at SAt + sep
     __host__ __device__ int64_t base(int ch, uint32_t bucket) const { return (int64_t)ch * cs + (int64_t)bucket * lc; }
 };
 
@@ -545,13 +546,23 @@ constexpr int kB32Rows = 32;
 template <int W, int EXP>
 __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __restrict__ code, int64_t rows,
                                                                Cols<double> cols, int ncols, int ldtile,
-                                                               double* __restrict__ SAt, RowLayout L) {
+                                                               double* __restrict__ SAt, RowLayout L, int k1) {
+    // Split mode (L.sep >= 0): columns [0, ncols) go through the row bulk reductions and column
+    // ncols (the odd last one, b at C2) is accumulated per CTA in shared memory (k1 doubles) and
+    // flushed once: a 64-column row is 512 B = 16 L2 sectors, a 65-column row 17 -- the L2 fp64
+    // reduction rate bounds this kernel, so one sector fewer per row is ~6%.
     const int cw = L.cw;
     extern __shared__ __align__(16) double b32_smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int p = lane & 15, half = lane >> 4;
     double* tile = b32_smem + (size_t)warp * kB32Rows * ldtile;
+    const bool split = L.sep >= 0;
+    double* sb = b32_smem + (size_t)W * kB32Rows * ldtile;   // split: k1 bucket sums of column ncols
     for (int e = lane; e < kB32Rows * ldtile; e += 32) tile[e] = 0.0;
+    if (split) {
+        for (int e = threadIdx.x; e < k1; e += blockDim.x) sb[e] = 0.0;
+        __syncthreads();
+    }
     __syncwarp();
     const int nchunks = (ncols + cw - 1) / cw;
     const int64_t ngroups = (rows + kB32Rows - 1) / kB32Rows;
@@ -570,6 +581,10 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
         const int64_t ra = min(r0 + 2 * p, rows - 1), rb = min(r0 + 2 * p + 1, rows - 1);
         const uint32_t ca = __ldg(code + ra), cb = __ldg(code + rb);
         const uint32_t crow = __ldg(code + min(r0 + lane, rows - 1));
+        if (split) {   // row r0 + lane of the split column into this CTA's shared buckets
+            const double bv = ldcs_pred(cols.col(ncols) + min(r0 + lane, rows - 1), r0 + lane < rows);
+            if (r0 + lane < rows) atomicAdd(sb + code_bucket(crow), apply_sign(bv, crow));
+        }
         double2 v[kJ];
         if (full) {
 #pragma unroll
@@ -617,6 +632,17 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
         }
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
+    if (split) {   // one bulk reduce-add of this CTA's k1 sums into the separate column
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            const uint32_t src = (uint32_t)__cvta_generic_to_shared(sb);
+            asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(SAt + L.sep),
+                         "r"(src), "r"((uint32_t)(k1 * 8))
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+    }
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
@@ -630,7 +656,10 @@ __global__ void transpose_out_kernel(const double* __restrict__ SAt, RowLayout L
     for (int j = threadIdx.y; j < 32; j += blockDim.y) {
         const int64_t m = m0 + j;
         const int c = c0 + threadIdx.x;
-        t[j][threadIdx.x] = (m < k1 && c < ncols) ? SAt[(int64_t)(c / L.cw) * L.cs + m * L.lc + (c % L.cw)] : 0.0;
+        t[j][threadIdx.x] = (m < k1 && c < ncols)
+                                ? ((L.sep >= 0 && c == ncols - 1) ? SAt[L.sep + m]
+                                                                  : SAt[(int64_t)(c / L.cw) * L.cs + m * L.lc + (c % L.cw)])
+                                : 0.0;
     }
     __syncthreads();
     for (int j = threadIdx.y; j < 32; j += blockDim.y) {
@@ -922,15 +951,18 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
                 const int b32 = w32 ? std::atoi(w32) : 8;   // warps per CTA, 0 = off
                 if (al && b32 > 0 && (cols.n > 0 || cols.b != nullptr)) {
                     const int ld32 = ldtile % 4 == 0 ? ldtile + 2 : ldtile;   // == 2 mod 4
-                    const int64_t units32 = ceil_div(rows, kB32Rows) * ceil_div(ncols, cw);
+                    const int nbulk = L.sep >= 0 ? ncols - 1 : ncols;   // split: the last column goes apart
+                    const int64_t units32 = ceil_div(rows, kB32Rows) * ceil_div(nbulk, cw);
                     auto launch32 = [&](auto kern, int W) -> csk_status {
-                        const size_t smem = (size_t)W * kB32Rows * ld32 * sizeof(double);
+                        const size_t smem = (size_t)W * kB32Rows * ld32 * sizeof(double) +
+                                            (L.sep >= 0 ? (size_t)plan->k1 * sizeof(double) : 0);
                         if (smem > (size_t)di.smem_optin) return CSK_EUNSUPPORTED;
                         CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
                         int64_t blocks = std::min<int64_t>(ceil_div(units32, W), (int64_t)di.num_sms);
                         if (const char* g = std::getenv("CSK_GRID")) blocks = std::max(1, std::atoi(g));   // experiment
                         prof_mark(st, true);   // right before the launch: host prep is not timed
-                        kern<<<(unsigned)blocks, W * 32, smem, st>>>(code, rows, cols, ncols, ld32, out, L);
+                        kern<<<(unsigned)blocks, W * 32, smem, st>>>(code, rows, cols, nbulk, ld32, out, L,
+                                                                     (int)plan->k1);
                         CSK_LAUNCH_CHECK();
                         return CSK_OK;
                     };
@@ -1103,6 +1135,24 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
                 L.lc = std::max<int64_t>((ncols + 3) & ~3, nchunks * L.cs);
                 if (const char* e = std::getenv("CSK_LC")) L.lc = std::max<int64_t>(L.lc, std::atoi(e) & ~3);   // experiment
                 ws_doubles = (size_t)k1 * L.lc;
+                // B32 split, opt-in (CSK_SPLIT=1): one odd trailing column of a
+                // single-chunk fp64 [A b] is summed in shared memory per CTA, so the bulk rows are
+                // (ncols-1)*8 B (C2: 512 B = 16 sectors instead of 17).  Measured slower at C2 (2.32 vs
+                // 2.04 ms): the 64 KB of bucket sums take L1 capacity from the in-flight loads and the
+                // fp64 shared atomics are CAS loops (ATOMS.CAST.SPIN.64).
+                const bool al32 = dtype == CSK_F64 && ((uintptr_t)A & 15) == 0 && (n <= 1 || (lda & 1) == 0) &&
+                                  (b == nullptr || ((uintptr_t)b & 15) == 0);
+                const char* b32e = std::getenv("CSK_B32");
+                const char* spe = std::getenv("CSK_SPLIT");
+                if (!tma && variant == CSK_VAR_BULK_ROW && al32 && !(b32e && std::atoi(b32e) == 0) &&
+                    spe && std::atoi(spe) == 1 && nchunks == 1 && (ncols & 1) && ncols >= 5 &&
+                    (k1 & 1) == 0 && k1 <= 10240 && n > 0 && (b != nullptr || n >= 5)) {
+                    L.cw = ncols - 1;
+                    L.cs = L.cw;
+                    L.lc = (L.cw + 3) & ~3;
+                    L.sep = k1 * L.lc;
+                    ws_doubles = (size_t)k1 * L.lc + (size_t)k1;
+                }
             }
         } else {
             L.cw = ncols;   // T (and L/S fallbacks): its own 32-column chunks, regular layout

@@ -1,0 +1,8 @@
+#!/bin/bash
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out
+for rep in 1 2; do
+for w in 8 6 4; do for sp in 0 1; do
+  CSK_B32=$w CSK_SPLIT=$sp timeout 300 python bench.py --config c2 --cs-only --no-cpu --no-e2e --no-ne --no-acc --no-ls --no-extra --steps 10 > gpurun_out/x.json 2> gpurun_out/x.err
+  python -c "import json; d=json.load(open('gpurun_out/x.json')); r=d['roofline']; print('W=$w split=$sp', 'kernel_ms', round(r['kernel_ms'],4), 'frac', round(r['frac'],4))" || tail -n 3 gpurun_out/x.err
+done; done; done

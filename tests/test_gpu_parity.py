@@ -413,3 +413,30 @@ def test_profile_hooks_time_the_main_kernel():
     assert launches == 3 and ms > 0.0
     csk.cs_apply(plan, Ad)                    # disabled: nothing recorded
     assert csk.profile_read() == (0.0, 0)
+
+
+# ------------------------------------------------ B32 split of the odd last column
+@pytest.mark.parametrize("split", ["1", "0"])
+@pytest.mark.parametrize("d,n,with_b,k1", [(100003, 64, True, 8192), (50000, 4, True, 2048), (40961, 5, False, 64),
+                                           (9999, 64, True, 10240), (3000, 64, True, 16384)])
+def test_cs_apply_split_last_column(monkeypatch, split, d, n, with_b, k1):
+    # ncols odd and one chunk: the last column is summed in shared memory per CTA (C2's b),
+    # the other columns by the row bulk reductions; both parts and the fallback must match
+    monkeypatch.setenv("CSK_SPLIT", split)
+    A = synth.gaussian_matrix(d, n, seed=3)
+    b = synth.rhs(A, "hard", seed=3) if with_b else None
+    plan = csk.cs_plan(d, k1, 7)
+    h, s = oracle.codes(d, k1, 7)
+    for variant in ("auto", "B"):
+        _check_apply(plan, h, s, A, b, variant)
+
+
+def test_cs_apply_split_integer_exact(monkeypatch):
+    d, n, k1 = 70001, 64, 8192
+    A = synth.integer_matrix(d, n, seed=4)
+    b = synth.integer_matrix(d, 1, seed=5)[:, 0]
+    plan = csk.cs_plan(d, k1, 2)
+    h, s = oracle.codes(d, k1, 2)
+    got = host(csk.cs_apply(plan, gpu_colmajor(A), b=gpu_colmajor(b)))
+    exp = oracle.cs_apply(h, s, A, k1, b=b)
+    assert np.array_equal(got, exp)
