@@ -592,12 +592,145 @@ def bench_ours(args, cfg):
     return 0
 
 
+# ------------------------------------------------- NEXT rows: SRHT and rand_cholQR
+NEXT_CONFIGS = {
+    "srht": dict(d=1 << 24, n=64, k=128,
+                 name="NEXT-3 SRHT (P:L164-173) of [A b], d=2^24, n=64 (+b), k=2n=128, fp64 col-major, Gaussian A"),
+    "rc": dict(d=1 << 23, n=128, k1=32768, k2=256, kappa=1e10,
+               name="NEXT-1 rand_cholQR LS (Alg 5) on C4's [A b]: d=2^23, n=128, kappa(A)=1e10, k1=2n^2, k2=2n"),
+}
+DGEMM_TFS_MEASURED = 35.41   # profiles/r01_measured_b200.json: cuBLAS DGEMM 8192^3 on this pool's B200
+
+
+def _timed(fn, steps, warmup, stream):
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def bench_next(args, cfg):
+    """One JSON line for a NEXT row, N = 1 (N > 1: rank 0 runs, the others exit; these rows are
+    measured on one GPU).  Same contract keys as the main line."""
+    import torch
+    import paper_2508_14209_b200 as csk
+    import synth
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    d, n = cfg["d"], cfg["n"]
+    ncols = n + 1
+    buf = synth.colmajor_empty(torch, d, ncols, torch.float64, dev)
+    if args.config == "rc":
+        buf[:, :n] = synth.ill_conditioned_torch(d, n, cfg["kappa"], seed=DATA_SEED, device=dev)
+        buf[:, n] = synth.rhs_torch(buf[:, :n], "easy", seed=DATA_SEED)
+    else:
+        buf.copy_(synth.gaussian_matrix_torch(d, ncols, seed=DATA_SEED, device=dev))
+    A, b = buf[:, :n], buf[:, n]
+    nbytes = d * ncols * 8
+    peak, peak_src = hbm_peak()
+    csk.launch_count(reset=True)
+    if args.config == "srht":
+        k = cfg["k"]
+        Y = torch.empty((ncols, k), dtype=torch.float64, device=dev).t()
+        step = lambda: csk.srht_apply(A, k, SKETCH_SEED, b=b, Y=Y)   # noqa: E731
+        for _ in range(args.warmup):
+            step()
+        launches0 = csk.launch_count(reset=True)
+        with ClockSampler(local) as clocks:
+            csk.profile_enable(True)
+            ms = _timed(step, args.steps, 0, stream)
+            kms, kl = csk.profile_read()
+            csk.profile_enable(False)
+        launches = csk.launch_count() // max(1, args.steps)
+        kern_ms = kms / max(1, kl)
+        achieved = nbytes / (kern_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": None, "kernel": "srht_warp_kernel", "kernel_ms": kern_ms,
+                "kernel_share_of_step": kern_ms / ms, "alg_bytes_per_launch": nbytes, "peak_source": peak_src,
+                "note": "algorithmic bytes = d*(n+1)*8 (A and b read once; D bits d/8 B and Y k*(n+1)*8 B not counted)"}
+        # e2e: host [A b] -> device -> SRHT -> Y back to the host
+        hbuf = torch.empty((ncols, d), dtype=torch.float64).pin_memory().t()
+        hbuf.copy_(buf)
+        hY = torch.empty((ncols, k), dtype=torch.float64).pin_memory().t()
+        def e2e_step():
+            buf.copy_(hbuf, non_blocking=True)
+            csk.srht_apply(A, k, SKETCH_SEED, b=b, Y=Y)
+            hY.copy_(Y, non_blocking=True)
+        e2e_ms = _timed(e2e_step, 3, 1, stream)
+        e2e = {"value": nbytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "h2d_bytes_per_step": nbytes,
+               "d2h_bytes_per_step": k * ncols * 8, "ms_per_step": e2e_ms}
+        # the oracle on a bounded sample (2^16 rows of the same shape)
+        import oracle
+        rows = 1 << 16
+        sample = buf[:rows].cpu().numpy()
+        t = time.perf_counter()
+        oracle.srht_apply(sample[:, :n], k, SKETCH_SEED, b=sample[:, n])
+        tcpu = time.perf_counter() - t
+        cpu = {"value": rows * ncols * 8 / tcpu / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+               "sample": f"first {rows} rows of the workload (d=2^16 SRHT, radix-4 FWHT per column), {tcpu:.2f} s"}
+        value, unit, metric = nbytes / (ms * 1e-3) / 1e9, "GB/s", "SRHT apply GB/s (% HBM peak)"
+        extra = {}
+    else:
+        k1, k2 = cfg["k1"], cfg["k2"]
+        plan = csk.cs_plan(d, k1, SKETCH_SEED)
+        x = torch.empty(n, dtype=torch.float64, device=dev)
+        step = lambda: csk.rc_lstsq(plan, k2, A, b, x=x)   # noqa: E731
+        for _ in range(args.warmup):
+            step()
+        csk.launch_count(reset=True)
+        with ClockSampler(local) as clocks:
+            ms = _timed(step, args.steps, 0, stream)
+        launches = csk.launch_count() // max(1, args.steps)
+        # the dominant kernel: the fused TRSM + Gram pass (rc_gram), timed alone on the same inputs
+        Z = csk.ms_apply(plan, k2, A, b=b)
+        R0 = csk.rc_r0(Z, n)
+        gram_ms = _timed(lambda: csk.rc_gram(A, b, R0), args.steps, 2, stream)
+        flops = 2.0 * d * n * n        # TRSM d n^2 + SYRK-form Gram d n^2 (SURVEY NEXT-1)
+        achieved = flops / (gram_ms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": DGEMM_TFS_MEASURED, "unit": "TFLOP/s",
+                "frac": achieved / DGEMM_TFS_MEASURED, "traffic": None, "kernel": "rc_pass_ws_kernel (rc_gram)",
+                "kernel_ms": gram_ms, "kernel_share_of_step": gram_ms / ms,
+                "alg_flops_per_launch": flops,
+                "peak_source": "fp64 DMMA: measured cuBLAS DGEMM 8192^3 (profiles/r01_measured_b200.json); "
+                               "MEASURED_PEAKS.json has no fp64 figure"}
+        rel = float(torch.linalg.norm(b - A @ x) / torch.linalg.norm(b))
+        Rq = torch.linalg.qr(buf, mode="r")[1]
+        extra = {"rel_residual": rel, "true_rel_residual": float(abs(Rq[n, n]) / torch.linalg.norm(b))}
+        del Rq
+        try:
+            ne_ms = _timed(lambda: csk.ne_lstsq(A, b, x=x), args.steps, 1, stream)
+            extra["ne_ms"], extra["ne_status"] = ne_ms, "OK"
+        except csk.CskError as e:
+            extra["ne_status"] = str(e).split(":")[1].strip()
+        e2e, cpu = None, None
+        value, unit, metric = nbytes / (ms * 1e-3) / 1e9, "GB/s", "rand_cholQR LS: [A b] GB/s through rc_lstsq"
+        extra["ms_lstsq_distortion_free"] = True
+    line = {"metric": metric, "value": value, "unit": unit, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": cfg["name"], "l2": "inputs > 126 MB L2; no flush needed"},
+            "clocks": clocks.summary(), "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu}
+    line.update(extra)
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + sorted(NEXT_CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--variant", default="auto", choices=["auto", "L", "T", "S", "G", "B", "X"])
     ap.add_argument("--no-e2e", action="store_true")
@@ -611,6 +744,12 @@ def main():
                     help="LS comparison without the Gaussian / CountSketch-only / Count+SRHT solvers")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.config in NEXT_CONFIGS:
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "NEXT rows are measured against the oracle inside "
+                                                                  "the line's cpu_baseline"}))
+            return 0
+        return bench_next(args, NEXT_CONFIGS[args.config])
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return bench_reference(args, cfg)
