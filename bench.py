@@ -8,6 +8,7 @@ G (a4) live in the plan (timed separately as plan_ms); the normal-equations
 baseline (a8) is timed beside it on the same [A b].
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+  python bench.py --config srht | rc       # the NEXT rows (SRHT, rand_cholQR), one GPU
 
 Rank 0 prints ONE JSON line.  value = whole-job GB/s of [A b] sketched and solved
 (sum over ranks of d*(n+1)*8 bytes / max-over-ranks step time).  Weak scaling:
