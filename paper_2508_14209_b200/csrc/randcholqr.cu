@@ -69,6 +69,12 @@ __global__ void __launch_bounds__(1024, 1) rc_finish_kernel(const double* __rest
 constexpr int kRcRows = 64;     // rows per tile (8 per warp)
 constexpr int kRcWarps = 8;
 
+__device__ __forceinline__ double ldcs_pred_rc(const double* p, bool pred) {
+    double v = 0.0;
+    asm("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q ld.global.cs.f64 %0, [%1]; }" : "+d"(v) : "l"(p), "r"((int)pred));
+    return v;
+}
+
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                  : "+d"(c0), "+d"(c1)
@@ -447,6 +453,195 @@ __global__ void __launch_bounds__((kWsSolve + kWsGram) * 32, 1)
     }
 }
 
+// ----------------------------------------------------- v3: two row groups per TRSM warp
+// As rc_pass_ws_kernel, but each TRSM warp solves 16 rows of a 64-row tile as two independent
+// 8-row groups (twice the DMMA chains per warp: the TRSM was the limiter), the R0 B-fragment is
+// shared by both groups, and A is not staged in shared memory: every lane keeps a ring of P
+// prefetched column blocks in registers (the TRSM warps have the Gram warps' register budget).
+// Shared memory: packed R0, 2 x 64-row Q buffers, the 8x8 diagonal inverses, b.
+constexpr int kV3Rows = 64;
+
+template <int NB>
+__global__ void __launch_bounds__((kWsSolve + kWsGram) * 32, 1)
+    rc_pass_v3_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ b, int64_t d, int n,
+                      const double* __restrict__ R0g, int ldr0g, double* __restrict__ part, int nc) {
+    constexpr int NP = 8 * NB, LD = NP + 4;
+    constexpr int P = NB < 8 ? NB : 8;                                   // prefetch distance (column blocks)
+    constexpr int NPAIR = NB / 2;
+    constexpr int PPW = NPAIR >= kWsGram ? NPAIR / kWsGram : 1;
+    constexpr int KS = NPAIR >= kWsGram ? 1 : kWsGram / NPAIR;
+    constexpr int GK = kV3Rows / KS;
+    constexpr int NSLOT = PPW * (NB + 1);
+    extern __shared__ __align__(16) double rsm[];
+    double* R0p = rsm;                                   // packed upper R0
+    double* Qs = R0p + rc_r0_off(NB);                    // [2][kV3Rows][LD]
+    double* bs = Qs + 2 * kV3Rows * LD;                  // [2][kV3Rows]
+    double* invd = bs + 2 * kV3Rows;                     // [NP]
+    double* Wd = invd + NP;                              // [NB][8][12]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    for (int J = 0; J < NB; ++J)
+        for (int e = threadIdx.x; e < 8 * (8 * J + 8); e += blockDim.x) {
+            const int k = e % (8 * J + 8), j = 8 * J + e / (8 * J + 8);
+            const double v = (k < n && j < n) ? R0g[k + (int64_t)j * ldr0g] : (k == j ? 1.0 : 0.0);
+            R0p[rc_r0_off(J) + (j - 8 * J) * (8 * J + 12) + k] = (k <= j) ? v : 0.0;
+            if (k == j) invd[j] = 1.0 / v;
+        }
+    __syncthreads();
+    for (int e = threadIdx.x; e < NB * 8; e += blockDim.x) {
+        const int J = e >> 3, c = e & 7;
+        const double* rd = R0p + rc_r0_off(J) + 8 * J;
+        const int ldJ = 8 * J + 12;
+        double w[8];
+#pragma unroll
+        for (int r = 7; r >= 0; --r) {
+            double acc = (r == c) ? 1.0 : 0.0;
+#pragma unroll
+            for (int l = r + 1; l < 8; ++l) acc -= rd[l * ldJ + r] * w[l];
+            w[r] = acc * invd[8 * J + r];
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) Wd[J * 96 + c * 12 + r] = w[r];
+    }
+    __syncthreads();
+    const int64_t ntiles = (d + kV3Rows - 1) / kV3Rows;
+    const int64_t my = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    if (warp < kWsSolve) {
+        // ================================================================ TRSM warps
+        // prefetch ring: slot J % P holds A[rowA/rowB, 8J + 2t + {0,1}] of the step being prefetched
+        double pa0[P], pa1[P], pb0[P], pb1[P];
+        auto load_step = [&](int64_t i, int J, double& a0, double& a1, double& b0, double& b1) {
+            const int64_t r0 = (blockIdx.x + i * gridDim.x) * kV3Rows + 16 * warp + g;
+            const int c0 = 8 * J + 2 * t;
+            const bool ok = i < my;
+            const bool va = ok && r0 < d, vb = ok && r0 + 8 < d;
+            const double* p0 = A + (int64_t)min(c0, n - 1) * lda;
+            const double* p1 = A + (int64_t)min(c0 + 1, n - 1) * lda;
+            const int64_t ra = va ? r0 : 0, rb = vb ? r0 + 8 : 0;
+            a0 = ldcs_pred_rc(p0 + ra, va && c0 < n);
+            a1 = ldcs_pred_rc(p1 + ra, va && c0 + 1 < n);
+            b0 = ldcs_pred_rc(p0 + rb, vb && c0 < n);
+            b1 = ldcs_pred_rc(p1 + rb, vb && c0 + 1 < n);
+        };
+#pragma unroll
+        for (int J = 0; J < P; ++J) load_step(0, J, pa0[J], pa1[J], pb0[J], pb1[J]);
+        double bnext = 0.0;   // b of this lane's row (lanes 0..15: rows 16w + lane) for tile i
+        {
+            const int64_t r = (int64_t)blockIdx.x * kV3Rows + 16 * warp + lane;
+            bnext = (lane < 16 && my > 0 && r < d) ? __ldcs(b + r) : 0.0;
+        }
+        for (int64_t i = 0; i < my; ++i) {
+            const int q = (int)(i & 1);
+            const double bcur = bnext;
+            {
+                const int64_t r = (blockIdx.x + (i + 1) * gridDim.x) * kV3Rows + 16 * warp + lane;
+                bnext = (lane < 16 && i + 1 < my && r < d) ? __ldcs(b + r) : 0.0;
+            }
+            if (i >= 2) nbar_sync(3 + q, 256);                 // EMPTY[q]
+            double* qs = Qs + q * kV3Rows * LD;
+            double* qrowA = qs + (16 * warp + g) * LD;
+            double* qrowB = qrowA + 8 * LD;
+#pragma unroll
+            for (int J = 0; J < NB; ++J) {
+                constexpr int dummy = 0;
+                (void)dummy;
+                double tA0 = pa0[J % P], tA1 = pa1[J % P], tB0 = pb0[J % P], tB1 = pb1[J % P];
+                if (J + P < NB)
+                    load_step(i, J + P, pa0[J % P], pa1[J % P], pb0[J % P], pb1[J % P]);
+                else
+                    load_step(i + 1, J + P - NB, pa0[J % P], pa1[J % P], pb0[J % P], pb1[J % P]);
+                double a00 = 0.0, a01 = 0.0, a10 = 0.0, a11 = 0.0, b00 = 0.0, b01 = 0.0, b10 = 0.0, b11 = 0.0;
+                const double* qa = qrowA + t;
+                const double* qb = qrowB + t;
+                const double* rb = R0p + rc_r0_off(J) + g * (8 * J + 12) + t;
+#pragma unroll
+                for (int k = 0; k < 8 * J; k += 8) {
+                    const double r0v = rb[k], r1v = rb[k + 4];
+                    dmma884(a00, a01, qa[k], r0v);
+                    dmma884(b00, b01, qb[k], r0v);
+                    dmma884(a10, a11, qa[k + 4], r1v);
+                    dmma884(b10, b11, qb[k + 4], r1v);
+                }
+                tA0 -= a00 + a10;
+                tA1 -= a01 + a11;
+                tB0 -= b00 + b10;
+                tB1 -= b01 + b11;
+                // Q[:, J] = T W_J (W_J = R_JJ^-1; A operand T[g][t], T[g][t+4] by shuffles)
+                const int src0 = (lane & ~3) | (t >> 1), src1 = (lane & ~3) | (2 + (t >> 1));
+                const double xa00 = __shfl_sync(0xffffffffu, tA0, src0), xa01 = __shfl_sync(0xffffffffu, tA1, src0);
+                const double xa10 = __shfl_sync(0xffffffffu, tA0, src1), xa11 = __shfl_sync(0xffffffffu, tA1, src1);
+                const double xb00 = __shfl_sync(0xffffffffu, tB0, src0), xb01 = __shfl_sync(0xffffffffu, tB1, src0);
+                const double xb10 = __shfl_sync(0xffffffffu, tB0, src1), xb11 = __shfl_sync(0xffffffffu, tB1, src1);
+                const double* wb = Wd + J * 96 + g * 12 + t;
+                const double w0 = wb[0], w1 = wb[4];
+                double qa0 = 0.0, qa1 = 0.0, qb0 = 0.0, qb1 = 0.0;
+                dmma884(qa0, qa1, (t & 1) ? xa01 : xa00, w0);
+                dmma884(qb0, qb1, (t & 1) ? xb01 : xb00, w0);
+                dmma884(qa0, qa1, (t & 1) ? xa11 : xa10, w1);
+                dmma884(qb0, qb1, (t & 1) ? xb11 : xb10, w1);
+                *reinterpret_cast<double2*>(qrowA + 8 * J + 2 * t) = make_double2(qa0, qa1);
+                *reinterpret_cast<double2*>(qrowB + 8 * J + 2 * t) = make_double2(qb0, qb1);
+                __syncwarp();
+            }
+            if (lane < 16) bs[q * kV3Rows + 16 * warp + lane] = bcur;
+            __threadfence_block();
+            nbar_arrive(1 + q, 256);                           // FULL[q]
+        }
+        for (int64_t i = (my >= 2 ? my - 2 : 0); i < my; ++i) nbar_sync(3 + (int)(i & 1), 256);   // drain EMPTY
+    } else {
+        // ================================================================ Gram warps
+        const int gw = warp - kWsSolve;
+        const int pair0 = (gw % (kWsGram / KS)) * PPW, gk0 = (gw / (kWsGram / KS)) * GK;
+        double acc[NSLOT][2];
+#pragma unroll
+        for (int p = 0; p < NSLOT; ++p) acc[p][0] = acc[p][1] = 0.0;
+        double zacc0 = 0.0;
+        const int gtid = threadIdx.x - kWsSolve * 32;
+        for (int64_t i = 0; i < my; ++i) {
+            const int q = (int)(i & 1);
+            nbar_sync(1 + q, 256);                             // FULL[q]
+            const double* qs = Qs + q * kV3Rows * LD;
+            const double* qk = qs + (gk0 + t) * LD + g;
+#pragma unroll 2
+            for (int k = 0; k < GK; k += 4, qk += 4 * LD) {
+#pragma unroll
+                for (int pp = 0; pp < PPW; ++pp) {
+                    const int J1 = pair0 + pp, J2 = NB - 1 - J1;
+                    const double b1 = qk[8 * J1], b2 = qk[8 * J2];
+#pragma unroll
+                    for (int s2 = 0; s2 <= NB; ++s2) {
+                        const bool first = s2 <= J1;
+                        const int I = first ? s2 : s2 - J1 - 1;
+                        dmma884(acc[pp * (NB + 1) + s2][0], acc[pp * (NB + 1) + s2][1], qk[8 * I], first ? b1 : b2);
+                    }
+                }
+            }
+            if (gtid < NP) {
+                const double* bt = bs + q * kV3Rows;
+                double sz = 0.0;
+#pragma unroll 4
+                for (int r = 0; r < kV3Rows; ++r) sz += qs[r * LD + gtid] * bt[r];
+                zacc0 += sz;
+            }
+            nbar_arrive(3 + q, 256);                           // EMPTY[q]
+        }
+        double* Pp = part + (size_t)blockIdx.x * nc * nc;
+#pragma unroll
+        for (int pp = 0; pp < PPW; ++pp) {
+            const int J1 = pair0 + pp, J2 = NB - 1 - J1;
+#pragma unroll
+            for (int s2 = 0; s2 <= NB; ++s2) {
+                const bool first = s2 <= J1;
+                const int I = first ? s2 : s2 - J1 - 1, J = first ? J1 : J2;
+                const int ii = 8 * I + g, j0 = 8 * J + 2 * t;
+                if (ii < n && j0 < n) atomicAdd(Pp + ii + (int64_t)j0 * nc, acc[pp * (NB + 1) + s2][0]);
+                if (ii < n && j0 + 1 < n) atomicAdd(Pp + ii + (int64_t)(j0 + 1) * nc, acc[pp * (NB + 1) + s2][1]);
+            }
+        }
+        if (gtid < n) atomicAdd(Pp + gtid + (int64_t)(nc - 1) * nc, zacc0);
+    }
+}
+
 // C[e] = sum_p part[p][e], fixed order (deterministic for a given grid)
 __global__ void rc_reduce_kernel(const double* __restrict__ part, int parts, int64_t elems, double* __restrict__ C) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < elems; e += (int64_t)gridDim.x * blockDim.x) {
@@ -484,8 +679,16 @@ static csk_status rc_gram_impl(int64_t d, int64_t n, const double* A, int64_t ld
         double* part = nullptr;
         CSK_CUDA_TRY(cudaMallocAsync(&part, (size_t)grid * nc * nc * 8, st));
         CSK_CUDA_TRY(cudaMemsetAsync(part, 0, (size_t)grid * nc * nc * 8, st));
-        const char* ke = std::getenv("CSK_RC_KERNEL");   // 1 = the unpipelined kernel (measured alternative)
-        if (ke && std::atoi(ke) == 1) {
+        const char* ke = std::getenv("CSK_RC_KERNEL");   // 1 = unpipelined, 2 = 32-row pipeline (alternatives)
+        const int kv = ke ? std::atoi(ke) : 0;
+        if (kv == 0) {
+            const size_t smem_v3 = ((size_t)rc_r0_off(nb) + 2 * (size_t)kV3Rows * LD + 2 * kV3Rows + NP +
+                                    (size_t)nb * 96) * 8;
+            auto kern = nb == 2 ? rc_pass_v3_kernel<2> : nb == 4 ? rc_pass_v3_kernel<4>
+                      : nb == 8 ? rc_pass_v3_kernel<8> : rc_pass_v3_kernel<16>;
+            CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_v3));
+            kern<<<grid, (kWsSolve + kWsGram) * 32, smem_v3, st>>>(A, lda, b, d, (int)n, R0, (int)ldr0, part, nc);
+        } else if (kv == 1) {
             auto kern = nb == 2 ? rc_pass_kernel<2> : nb == 4 ? rc_pass_kernel<4> : nb == 8 ? rc_pass_kernel<8>
                                                                                               : rc_pass_kernel<16>;
             CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
