@@ -52,7 +52,9 @@ def lib():
     with _lock:
         if _lib is None:
             path = _build.LIB
-            if _build.needs_build():
+            if os.environ.get("CSK_LIB_OVERRIDE"):   # experiments: A/B against another build of the library
+                path = os.environ["CSK_LIB_OVERRIDE"]
+            elif _build.needs_build():
                 path = _build.build()
             L = ctypes.CDLL(path)
             P, I64, U64, U32, I32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int
@@ -78,6 +80,8 @@ def lib():
                 "msh_lstsq": [P, I64, I64, P, I64, P, P, P, P],
             }
             for name, argt in sigs.items():
+                if os.environ.get("CSK_LIB_OVERRIDE") and not hasattr(L, name):
+                    continue   # an older build under A/B: only its own entry points are bound
                 f = getattr(L, name)
                 f.argtypes = argt
                 f.restype = ctypes.c_int

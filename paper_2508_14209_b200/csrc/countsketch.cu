@@ -423,8 +423,8 @@ __device__ __forceinline__ void bulk_load_tile(double (&v)[kBulkMaxCols / 2], co
 #pragma unroll
     for (int j = 0; j < kBulkMaxCols / 2; ++j) {
         const int c = 2 * j + half;
-        // predicated: lanes past the chunk's last column fetch nothing (clamped legal address)
-        v[j] = ldcs_pred(cols.col(min(c0 + c, ncols - 1)) + rc, c < nc);
+        const double x = (double)ldg_stream(cols.col(c0 + min(c, nc - 1)) + rc);   // re-read the last column
+        v[j] = (c < nc) ? x : 0.0;
     }
 }
 
@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(C::kWarps * 32, 1) cs_bulk_kernel(const uint32
 // back to clamped scalar loads.
 constexpr int kB32Rows = 32;
 
-template <int W, int EXP>
+template <int W, int EXP, bool SPLIT = false, bool PRED = false>
 __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __restrict__ code, int64_t rows,
                                                                Cols<double> cols, int ncols, int ldtile,
                                                                double* __restrict__ SAt, RowLayout L, int k1) {
@@ -556,10 +556,10 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int p = lane & 15, half = lane >> 4;
     double* tile = b32_smem + (size_t)warp * kB32Rows * ldtile;
-    const bool split = L.sep >= 0;
+    constexpr bool split = SPLIT;   // compile-time: the default kernel carries none of the split code
     double* sb = b32_smem + (size_t)W * kB32Rows * ldtile;   // split: k1 bucket sums of column ncols
     for (int e = lane; e < kB32Rows * ldtile; e += 32) tile[e] = 0.0;
-    if (split) {
+    if constexpr (split) {
         for (int e = threadIdx.x; e < k1; e += blockDim.x) sb[e] = 0.0;
         __syncthreads();
     }
@@ -581,25 +581,40 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
         const int64_t ra = min(r0 + 2 * p, rows - 1), rb = min(r0 + 2 * p + 1, rows - 1);
         const uint32_t ca = __ldg(code + ra), cb = __ldg(code + rb);
         const uint32_t crow = __ldg(code + min(r0 + lane, rows - 1));
-        if (split) {   // row r0 + lane of the split column into this CTA's shared buckets
+        if constexpr (split) {   // row r0 + lane of the split column into this CTA's shared buckets
             const double bv = ldcs_pred(cols.col(ncols) + min(r0 + lane, rows - 1), r0 + lane < rows);
             if (r0 + lane < rows) atomicAdd(sb + code_bucket(crow), apply_sign(bv, crow));
         }
         double2 v[kJ];
-        if (full) {
+        if (full && !PRED) {
+            // (nearly) full-width chunk (C2, C4): lanes past the chunk's last column re-read that
+            // column (an L1 hit, no DRAM bytes) and drop the value.  Plain loads schedule better
+            // than predicated inline PTX (1.5% at C2, same-box A/B).
 #pragma unroll
             for (int j = 0; j < kJ; ++j) {
                 const int c = 2 * j + half;
-                // predicated loads: lanes past the chunk's last column fetch nothing
+                const double2 x = (EXP & 2) ? make_double2((double)ra, (double)c)
+                                            : __ldcs(reinterpret_cast<const double2*>(
+                                                  cols.col(c0 + min(c, nc - 1)) + r0 + 2 * p));
+                v[j] = (c < nc) ? x : make_double2(0.0, 0.0);
+            }
+        } else if (full) {
+            // PRED (narrow chunks, C3: 52 of 66 slots): predicated loads -- the idle lanes issue
+            // nothing (re-reading would add 27% load instructions; measured 2.22 vs 2.11 ms at C3).
+            // A separate instantiation: one kernel holding both paths ran C2 1.5% slower.
+#pragma unroll
+            for (int j = 0; j < kJ; ++j) {
+                const int c = 2 * j + half;
                 v[j] = (EXP & 2) ? make_double2((double)ra, (double)c)
-                                 : ldcs2_pred(cols.col(min(c0 + c, ncols - 1)) + r0 + 2 * p, c < nc);
+                                 : ldcs2_pred(cols.col(c0 + min(c, nc - 1)) + r0 + 2 * p, c < nc);
             }
         } else {
 #pragma unroll
             for (int j = 0; j < kJ; ++j) {
                 const int c = 2 * j + half;
-                const double* col = cols.col(min(c0 + c, ncols - 1));
-                v[j] = make_double2(ldcs_pred(col + ra, c < nc), ldcs_pred(col + rb, c < nc && r0 + 2 * p + 1 < rows));
+                const double* col = cols.col(c0 + min(c, nc - 1));
+                const double xa = __ldcs(col + ra), xb = __ldcs(col + rb);
+                v[j] = (c < nc) ? make_double2(xa, r0 + 2 * p + 1 < rows ? xb : 0.0) : make_double2(0.0, 0.0);
             }
         }
         // the TMA engine must have finished reading this tile (bulk ops of the previous unit)
@@ -632,7 +647,7 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
         }
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
-    if (split) {   // one bulk reduce-add of this CTA's k1 sums into the separate column
+    if constexpr (split) {   // one bulk reduce-add of this CTA's k1 sums into the separate column
         __syncthreads();
         if (threadIdx.x == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -967,7 +982,11 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
                         return CSK_OK;
                     };
                     csk_status r32;
-                    if (b32 == 6)
+                    if (L.sep >= 0)
+                        r32 = launch32(cs_bulk32_kernel<8, 0, true>, 8);
+                    else if (cw < kBulkMaxCols - 3 && expv == 0 && b32 == 8)
+                        r32 = launch32(cs_bulk32_kernel<8, 0, false, true>, 8);   // narrow chunks (C3)
+                    else if (b32 == 6)
                         r32 = expv == 1 ? launch32(cs_bulk32_kernel<6, 1>, 6)
                               : expv == 2 ? launch32(cs_bulk32_kernel<6, 2>, 6) : launch32(cs_bulk32_kernel<6, 0>, 6);
                     else if (b32 == 4)

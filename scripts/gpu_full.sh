@@ -18,8 +18,14 @@ timeout 900 ncu --set full --clock-control none -k regex:'gemm|Kernel2' -c 1 -o 
 tail -2 gpurun_out/pytest_gpu.log; tail -1 gpurun_out/smoke.log
 for f in c2 c4 c3; do python -c "import json; d=json.load(open('gpurun_out/bench_$f.json')); print('$f', round(d['value'],1), d['unit'], 'step', round(d['ms_per_step'],3), 'cs', round(d['roofline']['kernel_ms'],3), 'frac', round(d['roofline']['frac'],3), 'ne', d['normal_equations'].get('ms'), d['normal_equations'].get('status'), 'speedup', d['speedup_vs_ne'], d['phases_ms'], d['accuracy'])" 2>&1 | tail -1; done
 # NEXT items: rand_cholQR fused pass (C4) and the SRHT (k = 2n on C4's [A b])
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:rc_pass -c 1 -o gpurun_out/prof_rc env REPS=1 python scripts/rc_once.py > gpurun_out/ncu_rc.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:rc_pass_v3 -c 1 -o gpurun_out/prof_rc env REPS=1 python scripts/rc_once.py > gpurun_out/ncu_rc.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:srht_warp -c 1 -o gpurun_out/prof_srht env REPS=1 python scripts/srht_once.py > gpurun_out/ncu_srht.log 2>&1
 timeout 300 python scripts/srht_once.py > gpurun_out/srht_c4.txt 2>&1; N=64 LOGD=24 timeout 300 python scripts/srht_once.py >> gpurun_out/srht_c4.txt 2>&1
 timeout 300 python scripts/rc_once.py > gpurun_out/rc_c4.txt 2>&1; N=64 LOGD=24 timeout 300 python scripts/rc_once.py >> gpurun_out/rc_c4.txt 2>&1
 cat gpurun_out/srht_c4.txt gpurun_out/rc_c4.txt
+timeout 600 python bench.py --config srht > gpurun_out/bench_srht.json 2> gpurun_out/bench_srht.err
+timeout 900 python bench.py --config rc --steps 10 > gpurun_out/bench_rc.json 2> gpurun_out/bench_rc.err
+python -c "
+import json
+for f in ('srht','rc'):
+    d=json.load(open('gpurun_out/bench_%s.json' % f)); r=d['roofline']; print(f, round(d['value'],1), d['unit'], 'step', round(d['ms_per_step'],3), 'kernel', round(r['kernel_ms'],3), 'frac', round(r['frac'],3))"
