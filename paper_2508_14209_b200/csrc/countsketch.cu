@@ -1082,7 +1082,7 @@ struct ApplyTarget {
 
 csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void* A, int64_t lda, const void* b,
                          void* SA, int64_t ldsa, int variant, cudaStream_t st, int64_t row_begin, int64_t row_end,
-                         bool accumulate) {
+                         bool accumulate, RowOut* rowout) {
     CSK_REQUIRE(plan != nullptr, CSK_EINVAL, "plan is NULL");
     CSK_REQUIRE(dtype == CSK_F64 || dtype == CSK_F32, CSK_EDTYPE, "dtype %d not supported", (int)dtype);
     CSK_REQUIRE(n >= 0, CSK_EINVAL, "n=%lld must be >= 0", (long long)n);
@@ -1209,6 +1209,16 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
         s = run_variant<float>(variant, plan, ncols, cols, row_begin, row_end, tgt.buf, tgt.ld, L, st);
     }
     prof_mark(st, false);
+    if (rowout != nullptr) rowout->ws = nullptr;
+    if (s == CSK_OK && tgt.owned && rowout != nullptr && variant_rowmajor(variant) && dtype == CSK_F64 && L.sep < 0) {
+        // the caller (ms_apply) consumes the row-major SA^T directly (Z^T = Y^T G^T, no transpose)
+        rowout->ws = tgt.buf;
+        rowout->cw = L.cw;
+        rowout->lc = L.lc;
+        rowout->cs = L.cs;
+        rowout->ncols = ncols;
+        return CSK_OK;
+    }
     if (s == CSK_OK && tgt.owned) {
         if (variant_rowmajor(variant)) {
             const RowLayout& Lt = L;

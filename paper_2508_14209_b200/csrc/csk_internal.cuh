@@ -157,9 +157,17 @@ __device__ __forceinline__ void bulk_load_1d(void* dst, const void* src, uint32_
 }
 
 // cs_apply implementation entry (countsketch.cu), also used by ms_apply
+// RowOut (nullable): when the row-scatter variants ran, hand the caller the row-major SA^T workspace
+// instead of transposing it (the caller cudaFreeAsync's rowout->ws): element (m, c) at
+// (c / cw) * cs + m * lc + (c % cw).  rowout->ws == NULL means SA was written as usual.
+struct RowOut {
+    double* ws = nullptr;
+    int cw = 0, ncols = 0;
+    int64_t lc = 0, cs = 0;
+};
 csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void* A, int64_t lda,
                          const void* b, void* SA, int64_t ldsa, int variant, cudaStream_t st,
-                         int64_t row_begin, int64_t row_end, bool accumulate);
+                         int64_t row_begin, int64_t row_end, bool accumulate, RowOut* rowout = nullptr);
 csk_status gauss_get(csk_plan_t plan, int64_t k2, csk_dtype dtype, cudaStream_t st, const void** G);
 struct cublasContext;
 csk_status blas_handle(cudaStream_t st, struct cublasContext** h);

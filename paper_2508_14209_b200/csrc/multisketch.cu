@@ -535,14 +535,46 @@ csk_status ms_apply_impl(csk_plan_t plan, int64_t k2, csk_dtype dtype, int64_t n
     const int64_t k1 = plan->k1;
     const size_t esz = dtype == CSK_F64 ? 8 : 4;
     void* SA = nullptr;
-    CSK_CUDA_TRY(cudaMallocAsync(&SA, (size_t)k1 * ncols * esz, st));
     csk_status s;
+    RowOut ro;
+    // fp64 device inputs: take the CountSketch's row-major SA^T and run the G-stage as
+    // Z^T-style transposed products on it -- P:L228's "interpreted Y stored in row-major as the
+    // transpose ... computed Z^T = Y^T G^T" -- so the k1 x ncols transpose is never done
+    // (CSK_MS_TRANSPOSE=1 restores the transpose + NN GEMM for measurement).
+    const char* te = std::getenv("CSK_MS_TRANSPOSE");
+    const bool rowmajor = dtype == CSK_F64 && !host_in && !(te && std::atoi(te) == 1);
     if (host_in) {
         CSK_REQUIRE(n == 0 || lda >= plan->d, CSK_ESHAPE, "lda < d");
+        CSK_CUDA_TRY(cudaMallocAsync(&SA, (size_t)k1 * ncols * esz, st));
         CSK_CUDA_TRY(cudaMemsetAsync(SA, 0, (size_t)k1 * ncols * 8, st));
         s = sketch_host_rows(plan, n, (const double*)A, lda, (const double*)b, (double*)SA, k1, st);
     } else {
-        s = cs_apply_impl(plan, dtype, n, A, lda, b, SA, k1, CSK_VAR_AUTO, st, 0, plan->d, false);
+        CSK_CUDA_TRY(cudaMallocAsync(&SA, (size_t)k1 * ncols * esz, st));
+        s = cs_apply_impl(plan, dtype, n, A, lda, b, SA, k1, CSK_VAR_AUTO, st, 0, plan->d, false,
+                          rowmajor ? &ro : nullptr);
+    }
+    if (s == CSK_OK && ro.ws != nullptr) {
+        const void* G = nullptr;
+        s = gauss_get(plan, k2, dtype, st, &G);
+        cublasHandle_t h;
+        if (s == CSK_OK) s = blas_handle(st, &h);
+        const double one = 1.0, zero = 0.0;
+        for (int c0 = 0; s == CSK_OK && c0 < ro.ncols; c0 += ro.cw) {
+            // chunk columns c0 .. c0+nc of SA are rows of SA^T: as a column-major (nc x k1) matrix
+            // with ld lc starting at chunk * cs, it is SA[:, chunk]^T
+            const int nc = std::min(ro.cw, ro.ncols - c0);
+            const double* Bt = ro.ws + (int64_t)(c0 / ro.cw) * ro.cs;
+            const cublasStatus_t bs = cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, (int)k2, nc, (int)k1, &one,
+                                                  (const double*)G, (int)k2, Bt, (int)ro.lc, &zero,
+                                                  (double*)Z + (int64_t)c0 * ldz, (int)ldz);
+            if (bs != CUBLAS_STATUS_SUCCESS) {
+                set_error("cuBLAS G-stage GEMM failed (%d)", (int)bs);
+                s = CSK_ECUDA;
+            }
+        }
+        cudaFreeAsync(ro.ws, st);
+        cudaFreeAsync(SA, st);
+        return s;
     }
     if (s == CSK_OK) {
         const void* G = nullptr;

@@ -267,8 +267,13 @@ def test_gauss_matches_oracle():
         assert np.allclose(Z, G @ S, rtol=0, atol=1e-13 / np.sqrt(k2) * 4)
 
 
-@pytest.mark.parametrize("d,n,k1,k2", [(4096, 8, 128, 16), (20000, 16, 512, 32), (5000, 3, 18, 6)])
-def test_ms_apply_matches_oracle(d, n, k1, k2):
+@pytest.mark.parametrize("transpose", ["0", "1"])
+@pytest.mark.parametrize("d,n,k1,k2", [(4096, 8, 128, 16), (20000, 16, 512, 32), (5000, 3, 18, 6),
+                                       (30011, 129, 4096, 260), (200003, 64, 131072, 130)])
+def test_ms_apply_matches_oracle(monkeypatch, transpose, d, n, k1, k2):
+    # default: the G-stage runs on the CountSketch's row-major SA^T (Z = G (SA^T)^T per column chunk,
+    # P:L228), including 2-chunk (129 + b) and chunk-major (k1 = 131072) layouts; "1" = transpose + NN GEMM
+    monkeypatch.setenv("CSK_MS_TRANSPOSE", transpose)
     plan = csk.cs_plan(d, k1, 3)
     A = synth.gaussian_matrix(d, n, seed=1)
     b = synth.rhs(A, "easy", seed=1)
