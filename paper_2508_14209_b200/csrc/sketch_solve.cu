@@ -50,27 +50,59 @@ static csk_status gs_apply_impl(int64_t d, int64_t row0, int64_t k, uint64_t see
     cublasHandle_t h;
     csk_status s = blas_handle(st, &h);
     if (s != CSK_OK) return s;
-    // chunk: the G slice (k x mc doubles) is 1/4 of L2, so it is consumed from L2 by the GEMM
+    // chunk: the G slice (k x mc doubles) is 1/4 of L2, so it is consumed from L2 by the GEMM.
+    // Two slices alternate: chunk i+1's Gaussians are generated on a second stream (fp64 ALU:
+    // log, sqrt, sincospi) while chunk i's GEMM runs (fp64 DMMA), ordered by events.
     int64_t mc = std::max<int64_t>(256, (int64_t)device_info().l2_bytes / 4 / (8 * k));
     if (const char* e = std::getenv("CSK_GS_CHUNK")) mc = std::max<int64_t>(2, std::atoll(e));
     mc = std::min(mc, d);
     double* G = nullptr;
-    CSK_CUDA_TRY(cudaMallocAsync(&G, (size_t)k * mc * 8, st));
+    CSK_CUDA_TRY(cudaMallocAsync(&G, 2 * (size_t)k * mc * 8, st));
+    cudaStream_t gen = nullptr;
+    cudaEvent_t ev[5] = {};
+    CSK_CUDA_TRY(cudaStreamCreateWithFlags(&gen, cudaStreamNonBlocking));
+    for (auto& e : ev) CSK_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    // ev[0]: G allocated (st); ev[1 + s]: slice s generated (gen); ev[3 + s]: slice s consumed (st)
+    CSK_CUDA_TRY(cudaEventRecord(ev[0], st));
+    CSK_CUDA_TRY(cudaStreamWaitEvent(gen, ev[0], 0));
     const double one = 1.0, zero = 0.0, div = std::sqrt((double)k);
     cublasStatus_t bs = CUBLAS_STATUS_SUCCESS;
-    for (int64_t c0 = 0; c0 < d && bs == CUBLAS_STATUS_SUCCESS; c0 += mc) {
+    auto generate = [&](int64_t c0, int slot) -> csk_status {
         const int64_t m = std::min(mc, d - c0);
         const int64_t total = k * m;
         const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(total / 2, 256), 148 * 16);
-        gauss_kernel<double><<<grid, 256, 0, st>>>(G, total, div, (uint32_t)seed, (uint32_t)(seed >> 32),
-                                                   (row0 + c0) * (k / 2));
+        gauss_kernel<double><<<grid, 256, 0, gen>>>(G + (size_t)slot * k * mc, total, div, (uint32_t)seed,
+                                                    (uint32_t)(seed >> 32), (row0 + c0) * (k / 2));
         CSK_LAUNCH_CHECK();
+        CSK_CUDA_TRY(cudaEventRecord(ev[1 + slot], gen));
+        return CSK_OK;
+    };
+    csk_status gs_st = generate(0, 0);
+    int64_t it = 0;
+    for (int64_t c0 = 0; gs_st == CSK_OK && c0 < d && bs == CUBLAS_STATUS_SUCCESS; c0 += mc, ++it) {
+        const int slot = (int)(it & 1);
+        const int64_t m = std::min(mc, d - c0);
+        if (c0 + mc < d) {   // next slice on the generator stream, once its previous GEMM is done
+            if (it >= 1) CSK_CUDA_TRY(cudaStreamWaitEvent(gen, ev[3 + (slot ^ 1)], 0));
+            gs_st = generate(c0 + mc, slot ^ 1);
+        }
+        CSK_CUDA_TRY(cudaStreamWaitEvent(st, ev[1 + slot], 0));
+        const double* Gs = G + (size_t)slot * k * mc;
         const double* beta = c0 == 0 ? &zero : &one;
         if (n > 0)
-            bs = cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)k, (int)n, (int)m, &one, G, (int)k, A + c0, (int)lda, beta,
-                             Z, (int)ldz);
+            bs = cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)k, (int)n, (int)m, &one, Gs, (int)k, A + c0, (int)lda,
+                             beta, Z, (int)ldz);
         if (b && bs == CUBLAS_STATUS_SUCCESS)
-            bs = cublasDgemv(h, CUBLAS_OP_N, (int)k, (int)m, &one, G, (int)k, b + c0, 1, beta, Z + (size_t)n * ldz, 1);
+            bs = cublasDgemv(h, CUBLAS_OP_N, (int)k, (int)m, &one, Gs, (int)k, b + c0, 1, beta, Z + (size_t)n * ldz, 1);
+        CSK_CUDA_TRY(cudaEventRecord(ev[3 + slot], st));
+    }
+    // every generated slice was waited on by st before its GEMM, so freeing G on st is ordered after
+    // the generator's writes; the stream and events are released once their pending work completes
+    for (auto& e : ev) cudaEventDestroy(e);
+    cudaStreamDestroy(gen);
+    if (gs_st != CSK_OK) {
+        cudaFreeAsync(G, st);
+        return gs_st;
     }
     cudaFreeAsync(G, st);
     if (bs != CUBLAS_STATUS_SUCCESS) {
