@@ -160,3 +160,16 @@ def test_rc_phases_row_partitioned(p):
     assert np.linalg.norm(A @ (host(x) - xo)) / nb <= max(1e-8, 64 * U * 1e8 * rr)
     x1 = host(csk.rc_lstsq(csk.cs_plan(d, k1, 2), k2, Ad, bd))
     assert np.linalg.norm(A @ (host(x) - x1)) / nb <= max(1e-8, 64 * U * 1e8 * rr)
+
+
+def test_rc_lstsq_wide_uses_blas_pass():
+    # n > 128: the fused DMMA pass does not apply; the row-chunked cuBLAS pass must match the oracle
+    d, n = 30011, 160
+    k1, k2 = 2 * n * n, 2 * n
+    A, b = _case(d, n, 1e4, "easy", seed=11)
+    plan = csk.cs_plan(d, k1, 6)
+    x = host(csk.rc_lstsq(plan, k2, gpu_colmajor(A), gpu_colmajor(b)))
+    xo, _ = _oracle(A, b, k1, k2, seed=6)
+    nb = np.linalg.norm(b)
+    rr = oracle.residual_norm(A, b, xo) / nb
+    assert np.linalg.norm(A @ (x - xo)) / nb <= max(1e-8, 64 * U * 1e4 * rr)
