@@ -438,6 +438,20 @@ def bench_ours(args, cfg):
         del buf32, SA32
         torch.cuda.empty_cache()
 
+    # ---- plan costs, warm (cuBLAS and the modules already loaded): codes (a1) of a second plan, and
+    # the Gaussian G (a4) it draws on first use = its first ms_apply minus a warm ms_apply
+    ev0.record(stream)
+    plan2 = csk.cs_plan(d, k1, SKETCH_SEED + 1, row0=row0)
+    ev1.record(stream)
+    barrier()
+    plan_warm_ms = ev0.elapsed_time(ev1)
+    ev0.record(stream)
+    csk.ms_apply(plan2, k2, A, b=b, Z=Z)
+    ev1.record(stream)
+    barrier()
+    g_gen_ms = max(0.0, ev0.elapsed_time(ev1) - msa_ms)
+    plan2.close()
+
     # ---- roofline attribution of the dominant kernel (N = 1): the same launch with its A loads
     # skipped (reduce path alone) and with its reductions skipped (HBM read path alone), via the
     # library's compile-time experiment variants (CSK_EXP, DESIGN.md 6.1/6.1b).  If the full
@@ -570,8 +584,9 @@ def bench_ours(args, cfg):
                      "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
                      "frac_of_8TBs_nominal": achieved / NOMINAL_HBM_GBS, "attribution": attribution},
         "cpu_baseline": cpu,
-        "phases_ms": {"cs_apply": cs_ms, "g_stage": msa_ms - cs_ms, "solve": solve_ms, "plan_codes": plan_ms,
-                      "gauss_first_use": gauss_first_ms},
+        "phases_ms": {"cs_apply": cs_ms, "g_stage": msa_ms - cs_ms, "solve": solve_ms,
+                      "plan_codes_warm": plan_warm_ms, "g_generation_warm": g_gen_ms,
+                      "plan_codes_first_call": plan_ms, "first_ms_apply_incl_library_init": gauss_first_ms},
         "cs_apply_gbs": bytes_step / (cs_ms * 1e-3) / 1e9,
         "cs_apply_input_families": families,
         "count_srht_multisketch": msh,
