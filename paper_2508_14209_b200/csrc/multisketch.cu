@@ -146,9 +146,9 @@ static csk_status sketch_host_rows(csk_plan_t plan, int64_t n, const double* A, 
     for (int64_t r0 = 0; r0 < d && s == CSK_OK; r0 += chunk, k ^= 1) {
         const int64_t rows = std::min(chunk, d - r0);
         CSK_CUDA_TRY(cudaStreamWaitEvent(cs, consumed[k], 0));
-        for (int c = 0; c < n; ++c)
-            CSK_CUDA_TRY(cudaMemcpyAsync(stage[k] + (int64_t)c * rows, A + r0 + (int64_t)c * lda, rows * 8,
-                                         cudaMemcpyHostToDevice, cs));
+        if (n > 0)   // one strided copy per chunk (n column segments), not n separate copies
+            CSK_CUDA_TRY(cudaMemcpy2DAsync(stage[k], rows * 8, A + r0, lda * 8, rows * 8, n, cudaMemcpyHostToDevice,
+                                           cs));
         if (b) CSK_CUDA_TRY(cudaMemcpyAsync(stage[k] + n * rows, b + r0, rows * 8, cudaMemcpyHostToDevice, cs));
         CSK_CUDA_TRY(cudaEventRecord(copied[k], cs));
         CSK_CUDA_TRY(cudaStreamWaitEvent(st, copied[k], 0));
