@@ -9,6 +9,7 @@ baseline (a8) is timed beside it on the same [A b].
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
   python bench.py --config srht | rc       # the NEXT rows (SRHT, rand_cholQR), one GPU
+  python bench.py --config kappa           # Fig 8: residual vs kappa(A) for every solver
 
 Rank 0 prints ONE JSON line.  value = whole-job GB/s of [A b] sketched and solved
 (sum over ranks of d*(n+1)*8 bytes / max-over-ranks step time).  Weak scaling:
@@ -615,6 +616,8 @@ NEXT_CONFIGS = {
     "rc": dict(d=1 << 23, n=128, k1=32768, k2=256, kappa=1e10,
                name="NEXT-1 rand_cholQR LS (Alg 5) on C4's [A b]: d=2^23, n=128, kappa(A)=1e10, k1=2n^2, k2=2n"),
 }
+NEXT_CONFIGS["kappa"] = dict(d=1 << 17, n=16,
+                             name="NEXT-4 Fig 8 kappa sweep (P:L360-369): d=2^17, n=16, b = A e, kappa(A) = 1 .. 1e14")
 DGEMM_TFS_MEASURED = 35.41   # profiles/r01_measured_b200.json: cuBLAS DGEMM 8192^3 on this pool's B200
 
 
@@ -630,6 +633,56 @@ def _timed(fn, steps, warmup, stream):
     e1.record(stream)
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / steps
+
+
+def bench_kappa(args, cfg):
+    """Fig 8 as a GPU experiment: relative residual ||b - Ax|| / ||b|| of every solver vs kappa(A) on
+    a consistent b = A e (an exact solution exists).  NE degrades past kappa ~ 1e8; the
+    sketch-and-solve solvers and rand_cholQR track the QR solve."""
+    import torch
+    import paper_2508_14209_b200 as csk
+    import synth
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    d, n = cfg["d"], cfg["n"]
+    k1, k2 = 2 * n * n, 2 * n
+    plan = csk.cs_plan(d, k1, SKETCH_SEED)
+    rows = []
+    t0 = time.perf_counter()
+    for e in range(0, 15, 2):
+        kappa = 10.0 ** e
+        A = synth.ill_conditioned_torch(d, n, kappa, seed=DATA_SEED, device=dev)
+        b = synth.rhs_torch(A, "consistent", seed=DATA_SEED)
+        nb = float(torch.linalg.norm(b))
+        row = {"kappa": kappa}
+        def resid(x):
+            return float(torch.linalg.norm(b - A @ x)) / nb
+        solvers = {
+            "ne": lambda: csk.ne_lstsq(A, b),
+            "ms": lambda: csk.ms_lstsq(plan, k2, A, b)[0],
+            "msh": lambda: csk.msh_lstsq(plan, k2, A, b)[0],
+            "cs": lambda: csk.cs_lstsq(plan, A, b)[0],
+            "gs": lambda: csk.gs_lstsq(A, b, k2, SKETCH_SEED)[0],
+            "rc": lambda: csk.rc_lstsq(plan, k2, A, b),
+        }
+        for name, fn in solvers.items():
+            try:
+                row[name] = resid(fn())
+            except csk.CskError as ex:
+                row[name] = str(ex).split(":")[1].strip()
+        Q, R = torch.linalg.qr(A)
+        row["qr"] = resid(torch.linalg.solve_triangular(R, (Q.t() @ b)[:, None], upper=True)[:, 0])
+        rows.append(row)
+    line = {"metric": "relative residual ||b - Ax||/||b|| vs kappa(A), b = A e (Fig 8)", "value": None,
+            "unit": "ratio", "n_gpus": 1, "steps": 1, "warmup": 0, "ms_per_step": (time.perf_counter() - t0) * 1e3,
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["name"], "k1": k1, "k2": k2}, "sweep": rows,
+            "note": "accuracy experiment (P:L360-369), not a throughput line; NE fails past kappa ~ 1e8"}
+    print(json.dumps(line), flush=True)
+    return 0
 
 
 def bench_next(args, cfg):
@@ -765,6 +818,8 @@ def main():
             print(json.dumps({"impl": "reference", "unavailable": "NEXT rows are measured against the oracle inside "
                                                                   "the line's cpu_baseline"}))
             return 0
+        if args.config == "kappa":
+            return bench_kappa(args, NEXT_CONFIGS["kappa"])
         return bench_next(args, NEXT_CONFIGS[args.config])
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
