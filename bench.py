@@ -10,6 +10,7 @@ baseline (a8) is timed beside it on the same [A b].
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
   python bench.py --config srht | rc       # the NEXT rows (SRHT, rand_cholQR), one GPU
   python bench.py --config kappa           # Fig 8: residual vs kappa(A) for every solver
+  python bench.py --config fig35           # Figs 3-5: sketch / LS times over the paper's (d, n) grid
 
 Rank 0 prints ONE JSON line.  value = whole-job GB/s of [A b] sketched and solved
 (sum over ranks of d*(n+1)*8 bytes / max-over-ranks step time).  Weak scaling:
@@ -618,6 +619,8 @@ NEXT_CONFIGS = {
 }
 NEXT_CONFIGS["kappa"] = dict(d=1 << 17, n=16,
                              name="NEXT-4 Fig 8 kappa sweep (P:L360-369): d=2^17, n=16, b = A e, kappa(A) = 1 .. 1e14")
+NEXT_CONFIGS["fig35"] = dict(name="Figs 3-5 grid (P:L240-336): d in {2^21, 2^22, 2^23}, n in {32, 64, 128, 256}; "
+                                   "sketch and least-squares times of every operator on one B200")
 DGEMM_TFS_MEASURED = 35.41   # profiles/r01_measured_b200.json: cuBLAS DGEMM 8192^3 on this pool's B200
 
 
@@ -681,6 +684,68 @@ def bench_kappa(args, cfg):
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["name"], "k1": k1, "k2": k2}, "sweep": rows,
             "note": "accuracy experiment (P:L360-369), not a throughput line; NE fails past kappa ~ 1e8"}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def bench_fig35(args, cfg):
+    """The paper's evaluation grid on B200: per (d, n), sketch times (Fig 3: Gram A^T A, Gaussian sketch
+    k = 2n, CountSketch k1 = 2n^2, SRHT k = 2n, multisketch 2n x 2n^2) with their HBM throughput
+    (Fig 4: % of the measured copy bandwidth), and least-squares times (Fig 5: NE, Gaussian,
+    CountSketch-only, multisketch, rand_cholQR; kappa(A) = 1e2 as in P:L322)."""
+    import torch
+    import paper_2508_14209_b200 as csk
+    import synth
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    peak, _ = hbm_peak()
+    steps, warm = max(3, args.steps // 4), 2
+    grid = []
+    t0 = time.perf_counter()
+    for logd in (21, 22, 23):
+        for n in (32, 64, 128, 256):
+            d = 1 << logd
+            k1, k2 = 2 * n * n, 2 * n
+            buf = synth.colmajor_empty(torch, d, n + 1, torch.float64, dev)
+            buf[:, :n] = synth.ill_conditioned_torch(d, n, 1e2, seed=DATA_SEED, device=dev)
+            buf[:, n] = synth.rhs_torch(buf[:, :n], "easy", seed=DATA_SEED)
+            A, b = buf[:, :n], buf[:, n]
+            plan = csk.cs_plan(d, k1, SKETCH_SEED)
+            x = torch.empty(n, dtype=torch.float64, device=dev)
+            abytes = d * n * 8
+            C = torch.empty((n, n), dtype=torch.float64, device=dev)
+            t = {}
+            t["gram"] = _timed(lambda: torch.matmul(A.t(), A, out=C), steps, warm, stream)
+            t["gaussian"] = _timed(lambda: csk.gs_apply(A, k2, SKETCH_SEED), steps, warm, stream)
+            t["countsketch"] = _timed(lambda: csk.cs_apply(plan, A), steps, warm, stream)
+            t["srht"] = _timed(lambda: csk.srht_apply(A, k2, SKETCH_SEED), steps, warm, stream)
+            t["multisketch"] = _timed(lambda: csk.ms_apply(plan, k2, A), steps, warm, stream)
+            ls = {}
+            def ne():
+                try:
+                    csk.ne_lstsq(A, b, x=x)
+                except csk.CskError:
+                    pass
+            ls["ne"] = _timed(ne, steps, warm, stream)
+            ls["gaussian"] = _timed(lambda: csk.gs_lstsq(A, b, k2, SKETCH_SEED, x=x), steps, warm, stream)
+            ls["countsketch"] = _timed(lambda: csk.cs_lstsq(plan, A, b, x=x), steps, warm, stream)
+            ls["multisketch"] = _timed(lambda: csk.ms_lstsq(plan, k2, A, b, x=x), steps, warm, stream)
+            ls["rand_cholqr"] = _timed(lambda: csk.rc_lstsq(plan, k2, A, b, x=x), steps, warm, stream)
+            grid.append({"d": d, "n": n, "sketch_ms": t, "lstsq_ms": ls,
+                         "sketch_pct_of_hbm": {k: 100.0 * abytes / (v * 1e-3) / 1e9 / peak for k, v in t.items()},
+                         "speedup_multisketch_vs_ne": ls["ne"] / ls["multisketch"]})
+            log(f"[fig35] d=2^{logd} n={n}: " + ", ".join(f"{k} {v:.2f}" for k, v in ls.items()))
+            del buf, A, b, plan, C
+            torch.cuda.empty_cache()
+    line = {"metric": "sketch and least-squares times over the paper's (d, n) grid (Figs 3-5)", "value": None,
+            "unit": "ms", "n_gpus": 1, "steps": steps, "warmup": warm, "ms_per_step": (time.perf_counter() - t0) * 1e3,
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["name"], "kappa": 1e2, "rhs": "easy"}, "grid": grid,
+            "note": "Gram = torch.matmul (cuBLAS DGEMM) A^T A; pct_of_hbm = d*n*8 bytes / time / measured copy BW"}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -820,6 +885,8 @@ def main():
             return 0
         if args.config == "kappa":
             return bench_kappa(args, NEXT_CONFIGS["kappa"])
+        if args.config == "fig35":
+            return bench_fig35(args, NEXT_CONFIGS["fig35"])
         return bench_next(args, NEXT_CONFIGS[args.config])
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
