@@ -543,10 +543,14 @@ __global__ void __launch_bounds__(C::kWarps * 32, 1) cs_bulk_kernel(const uint32
 // back to clamped scalar loads.
 constexpr int kB32Rows = 32;
 
-template <int W, int EXP, bool SPLIT = false, bool PRED = false>
+template <int W, int EXP, bool SPLIT = false, bool PRED = false, bool MIX = false>
 __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __restrict__ code, int64_t rows,
                                                                Cols<double> cols, int ncols, int ldtile,
-                                                               double* __restrict__ SAt, RowLayout L, int k1) {
+                                                               double* __restrict__ SAt, RowLayout L, int k1,
+                                                               int mix_rt = 32) {
+    // MIX (rows of <= 32 columns, e.g. n = 32): a 256-B bulk reduction per row leaves the kernel
+    // bound by the TMA operation rate, not by L2 sectors, so rows mix_rt..31 of each tile go out
+    // as one coalesced warp-wide red.global.add.f64 each instead -- a second, independent issue path.
     // Split mode (L.sep >= 0): columns [0, ncols) go through the row bulk reductions and column
     // ncols (the odd last one, b at C2) is accumulated per CTA in shared memory (k1 doubles) and
     // flushed once: a 64-column row is 512 B = 16 L2 sectors, a 65-column row 17 -- the L2 fp64
@@ -637,7 +641,7 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (r0 + lane < rows && !(EXP & 1)) {
+        if (r0 + lane < rows && !(EXP & 1) && (!MIX || lane < mix_rt)) {
             const uint32_t bytes = (uint32_t)(((nc + 1) & ~1) * 8);
             double* dst = SAt + L.base(ch, code_bucket(crow));
             const uint32_t src = (uint32_t)__cvta_generic_to_shared(tile + lane * ldtile);
@@ -646,6 +650,12 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
                          : "memory");
         }
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        if constexpr (MIX) {
+            for (int rr = mix_rt; rr < kB32Rows; ++rr) {
+                const uint32_t cr = __shfl_sync(0xffffffffu, crow, rr);
+                if (r0 + rr < rows && lane < nc) red_add_f64(SAt + L.base(ch, code_bucket(cr)) + lane, tile[rr * ldtile + lane]);
+            }
+        }
     }
     if constexpr (split) {   // one bulk reduce-add of this CTA's k1 sums into the separate column
         __syncthreads();
@@ -968,7 +978,7 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
                     const int ld32 = ldtile % 4 == 0 ? ldtile + 2 : ldtile;   // == 2 mod 4
                     const int nbulk = L.sep >= 0 ? ncols - 1 : ncols;   // split: the last column goes apart
                     const int64_t units32 = ceil_div(rows, kB32Rows) * ceil_div(nbulk, cw);
-                    auto launch32 = [&](auto kern, int W) -> csk_status {
+                    auto launch32 = [&](auto kern, int W, int mrt = 32) -> csk_status {
                         const size_t smem = (size_t)W * kB32Rows * ld32 * sizeof(double) +
                                             (L.sep >= 0 ? (size_t)plan->k1 * sizeof(double) : 0);
                         if (smem > (size_t)di.smem_optin) return CSK_EUNSUPPORTED;
@@ -977,13 +987,19 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
                         if (const char* g = std::getenv("CSK_GRID")) blocks = std::max(1, std::atoi(g));   // experiment
                         prof_mark(st, true);   // right before the launch: host prep is not timed
                         kern<<<(unsigned)blocks, W * 32, smem, st>>>(code, rows, cols, nbulk, ld32, out, L,
-                                                                     (int)plan->k1);
+                                                                     (int)plan->k1, mrt);
                         CSK_LAUNCH_CHECK();
                         return CSK_OK;
                     };
                     csk_status r32;
+                    // rows per tile kept on the TMA path in MIX mode (experiment, opt-in: at n = 32 every
+                    // split measured slower than TMA alone -- 0.72 ms (32) vs 0.89 (24), 0.96 (16), 1.11 (0))
+                    const char* mxe = std::getenv("CSK_MIX_RT");
+                    const int mix_rt = mxe ? std::max(0, std::min(32, std::atoi(mxe))) : 32;
                     if (L.sep >= 0)
                         r32 = launch32(cs_bulk32_kernel<8, 0, true>, 8);
+                    else if (cw <= 32 && nbulk <= cw && expv == 0 && b32 == 8 && mix_rt < 32)
+                        r32 = launch32(cs_bulk32_kernel<8, 0, false, false, true>, 8, mix_rt);   // narrow rows
                     else if (cw < kBulkMaxCols - 3 && expv == 0 && b32 == 8)
                         r32 = launch32(cs_bulk32_kernel<8, 0, false, true>, 8);   // narrow chunks (C3)
                     else if (b32 == 6)

@@ -445,3 +445,19 @@ def test_cs_apply_split_integer_exact(monkeypatch):
     got = host(csk.cs_apply(plan, gpu_colmajor(A), b=gpu_colmajor(b)))
     exp = oracle.cs_apply(h, s, A, k1, b=b)
     assert np.array_equal(got, exp)
+
+
+@pytest.mark.parametrize("mix_rt", ["16", "0", "8", "32"])
+@pytest.mark.parametrize("d,n,k1", [(100003, 32, 2048), (40000, 17, 512), (5000, 2, 64)])
+def test_cs_apply_narrow_rows_mixed_paths(monkeypatch, mix_rt, d, n, k1):
+    # rows of <= 32 columns: mix_rt rows per 32-row tile by TMA bulk reductions, the rest by
+    # warp-wide red.global.add.f64 (32 = TMA only); every split must match the oracle
+    monkeypatch.setenv("CSK_MIX_RT", mix_rt)
+    A = synth.gaussian_matrix(d, n, seed=4)
+    plan = csk.cs_plan(d, k1, 5)
+    h, s = oracle.codes(d, k1, 5)
+    for variant in ("auto", "B"):
+        _check_apply(plan, h, s, A, None, variant)
+    Ai = synth.integer_matrix(d, n, seed=6)
+    got = host(csk.cs_apply(plan, gpu_colmajor(Ai)))
+    assert np.array_equal(got, oracle.cs_apply(h, s, Ai, k1))
