@@ -642,6 +642,118 @@ __global__ void __launch_bounds__((kWsSolve + kWsGram) * 32, 1)
     }
 }
 
+// ------------------------------------------------- wide n (128 < n <= 256): TRSM to a workspace
+// The fused kernels keep packed R0 in shared memory, which no longer fits next to the Q tiles past
+// n = 128.  Here the TRSM warps of rc_pass_v3_kernel run alone (4 warps x 16 rows = 64-row tiles,
+// two 8-row groups per warp, A in a register ring), with the packed R0 and the 8x8 diagonal inverses
+// read through the read-only cache from global memory (L2-resident: 0.3 MB at n = 256), the warp's
+// Q rows in shared memory, and each finished tile written to the Q0 workspace column by column
+// (coalesced); cuBLAS DGEMM/DGEMV then form [Q0^T Q0 | Q0^T b] chunk by chunk.
+__global__ void rc_pack_r0_kernel(const double* __restrict__ R0g, int ldr0g, int n, int NB, double* __restrict__ R0p,
+                                  double* __restrict__ Wd) {
+    // packed upper R0 (as rc_pass_*: block J holds rows 0..8J+7 with ld 8J+12) and W_J = R_JJ^-1
+    for (int J = blockIdx.x; J < NB; J += gridDim.x) {
+        for (int e = threadIdx.x; e < 8 * (8 * J + 8); e += blockDim.x) {
+            const int k = e % (8 * J + 8), j = 8 * J + e / (8 * J + 8);
+            const double v = (k < n && j < n) ? R0g[k + (int64_t)j * ldr0g] : (k == j ? 1.0 : 0.0);
+            R0p[rc_r0_off(J) + (j - 8 * J) * (8 * J + 12) + k] = (k <= j) ? v : 0.0;
+        }
+        __syncthreads();
+        if (threadIdx.x < 8) {
+            const int c = threadIdx.x;
+            const double* rd = R0p + rc_r0_off(J) + 8 * J;
+            const int ldJ = 8 * J + 12;
+            double w[8];
+            for (int r = 7; r >= 0; --r) {
+                double acc = (r == c) ? 1.0 : 0.0;
+                for (int l = r + 1; l < 8; ++l) acc -= rd[l * ldJ + r] * w[l];
+                w[r] = acc / rd[r * ldJ + r];
+            }
+            for (int r = 0; r < 8; ++r) Wd[J * 96 + c * 12 + r] = w[r];
+        }
+        __syncthreads();
+    }
+}
+
+template <int NB>
+__global__ void __launch_bounds__(kWsSolve * 32, 1)
+    rc_trsm_kernel(const double* __restrict__ A, int64_t lda, int64_t d, int n, const double* __restrict__ R0p,
+                   const double* __restrict__ Wd, double* __restrict__ Q, int64_t ldq) {
+    constexpr int NP = 8 * NB, LD = NP + 4;
+    constexpr int P = 8;
+    extern __shared__ __align__(16) double qsm[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    double* qw = qsm + (size_t)warp * 16 * LD;                 // this warp's 16 Q rows
+    const int64_t ntiles = (d + kV3Rows - 1) / kV3Rows;
+    const int64_t my = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    double pa0[P], pa1[P], pb0[P], pb1[P];
+    auto load_step = [&](int64_t i, int J, double& a0, double& a1, double& b0, double& b1) {
+        const int64_t r0 = (blockIdx.x + i * gridDim.x) * kV3Rows + 16 * warp + g;
+        const int c0 = 8 * J + 2 * t;
+        const bool ok = i < my;
+        const bool va = ok && r0 < d, vb = ok && r0 + 8 < d;
+        const double* p0 = A + (int64_t)min(c0, n - 1) * lda;
+        const double* p1 = A + (int64_t)min(c0 + 1, n - 1) * lda;
+        const int64_t ra = va ? r0 : 0, rb = vb ? r0 + 8 : 0;
+        a0 = ldcs_pred_rc(p0 + ra, va && c0 < n);
+        a1 = ldcs_pred_rc(p1 + ra, va && c0 + 1 < n);
+        b0 = ldcs_pred_rc(p0 + rb, vb && c0 < n);
+        b1 = ldcs_pred_rc(p1 + rb, vb && c0 + 1 < n);
+    };
+#pragma unroll
+    for (int J = 0; J < P; ++J) load_step(0, J, pa0[J], pa1[J], pb0[J], pb1[J]);
+    double* qrowA = qw + g * LD;
+    double* qrowB = qrowA + 8 * LD;
+    for (int64_t i = 0; i < my; ++i) {
+#pragma unroll
+        for (int J = 0; J < NB; ++J) {
+            double tA0 = pa0[J % P], tA1 = pa1[J % P], tB0 = pb0[J % P], tB1 = pb1[J % P];
+            if (J + P < NB)
+                load_step(i, J + P, pa0[J % P], pa1[J % P], pb0[J % P], pb1[J % P]);
+            else
+                load_step(i + 1, J + P - NB, pa0[J % P], pa1[J % P], pb0[J % P], pb1[J % P]);
+            double a00 = 0.0, a01 = 0.0, a10 = 0.0, a11 = 0.0, b00 = 0.0, b01 = 0.0, b10 = 0.0, b11 = 0.0;
+            const double* qa = qrowA + t;
+            const double* qb = qrowB + t;
+            const double* rb = R0p + rc_r0_off(J) + g * (8 * J + 12) + t;
+#pragma unroll
+            for (int k = 0; k < 8 * J; k += 8) {
+                const double r0v = __ldg(rb + k), r1v = __ldg(rb + k + 4);
+                dmma884(a00, a01, qa[k], r0v);
+                dmma884(b00, b01, qb[k], r0v);
+                dmma884(a10, a11, qa[k + 4], r1v);
+                dmma884(b10, b11, qb[k + 4], r1v);
+            }
+            tA0 -= a00 + a10;
+            tA1 -= a01 + a11;
+            tB0 -= b00 + b10;
+            tB1 -= b01 + b11;
+            const int src0 = (lane & ~3) | (t >> 1), src1 = (lane & ~3) | (2 + (t >> 1));
+            const double xa00 = __shfl_sync(0xffffffffu, tA0, src0), xa01 = __shfl_sync(0xffffffffu, tA1, src0);
+            const double xa10 = __shfl_sync(0xffffffffu, tA0, src1), xa11 = __shfl_sync(0xffffffffu, tA1, src1);
+            const double xb00 = __shfl_sync(0xffffffffu, tB0, src0), xb01 = __shfl_sync(0xffffffffu, tB1, src0);
+            const double xb10 = __shfl_sync(0xffffffffu, tB0, src1), xb11 = __shfl_sync(0xffffffffu, tB1, src1);
+            const double* wb = Wd + J * 96 + g * 12 + t;
+            const double w0 = __ldg(wb), w1 = __ldg(wb + 4);
+            double qa0 = 0.0, qa1 = 0.0, qb0 = 0.0, qb1 = 0.0;
+            dmma884(qa0, qa1, (t & 1) ? xa01 : xa00, w0);
+            dmma884(qb0, qb1, (t & 1) ? xb01 : xb00, w0);
+            dmma884(qa0, qa1, (t & 1) ? xa11 : xa10, w1);
+            dmma884(qb0, qb1, (t & 1) ? xb11 : xb10, w1);
+            *reinterpret_cast<double2*>(qrowA + 8 * J + 2 * t) = make_double2(qa0, qa1);
+            *reinterpret_cast<double2*>(qrowB + 8 * J + 2 * t) = make_double2(qb0, qb1);
+            __syncwarp();
+        }
+        // the warp's 16 rows -> Q0 (column-major): lanes 0-15 column c, lanes 16-31 column c+1
+        const int64_t rbase = (blockIdx.x + i * gridDim.x) * kV3Rows + 16 * warp;
+        const int rr = lane & 15;
+        for (int c = lane >> 4; c < n; c += 2)
+            if (rbase + rr < d) Q[rbase + rr + (int64_t)c * ldq] = qw[rr * LD + c];
+        __syncwarp();
+    }
+}
+
 // C[e] = sum_p part[p][e], fixed order (deterministic for a given grid)
 __global__ void rc_reduce_kernel(const double* __restrict__ part, int parts, int64_t elems, double* __restrict__ C) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < elems; e += (int64_t)gridDim.x * blockDim.x) {
@@ -711,6 +823,47 @@ static csk_status rc_gram_impl(int64_t d, int64_t n, const double* A, int64_t ld
             part, grid, (int64_t)nc * nc, Cw);
         CSK_LAUNCH_CHECK();
         CSK_CUDA_TRY(cudaFreeAsync(part, st));
+    } else if (n <= 256 && !(pe && std::atoi(pe) == 0)) {
+        // 128 < n <= 256: DMMA TRSM kernel into a row-chunked Q0 workspace + cuBLAS Gram per chunk
+        const int nb = 32, NP = 8 * nb, LD = NP + 4;
+        int64_t mc = std::min<int64_t>(d, 1 << 20);
+        cublasHandle_t h;
+        s = blas_handle(st, &h);
+        if (s != CSK_OK) {
+            if (Cw != C) cudaFreeAsync(Cw, st);
+            return s;
+        }
+        double* ws = nullptr;
+        const size_t pk = (size_t)rc_r0_off(nb), wd = (size_t)nb * 96;
+        CSK_CUDA_TRY(cudaMallocAsync(&ws, (pk + wd + (size_t)mc * n) * 8, st));
+        double* R0p = ws;
+        double* Wd = ws + pk;
+        double* Qw = Wd + wd;
+        rc_pack_r0_kernel<<<nb, 256, 0, st>>>(R0, (int)ldr0, (int)n, nb, R0p, Wd);
+        CSK_LAUNCH_CHECK();
+        const size_t smem = (size_t)kWsSolve * 16 * LD * 8;
+        CSK_CUDA_TRY(cudaFuncSetAttribute(rc_trsm_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const DeviceInfo& di = device_info();
+        const double one = 1.0, zero = 0.0;
+        cublasStatus_t bs = CUBLAS_STATUS_SUCCESS;
+        for (int64_t r0 = 0; r0 < d && bs == CUBLAS_STATUS_SUCCESS; r0 += mc) {
+            const int64_t m = std::min(mc, d - r0);
+            const int grid = (int)std::min<int64_t>(ceil_div(m, kV3Rows), di.num_sms);
+            rc_trsm_kernel<32><<<grid, kWsSolve * 32, smem, st>>>(A + r0, lda, m, (int)n, R0p, Wd, Qw, m);
+            CSK_LAUNCH_CHECK();
+            const double* beta = r0 == 0 ? &zero : &one;
+            bs = cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)n, (int)n, (int)m, &one, Qw, (int)m, Qw, (int)m, beta, Cw,
+                             nc);
+            if (bs == CUBLAS_STATUS_SUCCESS)
+                bs = cublasDgemv(h, CUBLAS_OP_T, (int)m, (int)n, &one, Qw, (int)m, b + r0, 1, beta,
+                                 Cw + (size_t)n * nc, 1);
+        }
+        cudaFreeAsync(ws, st);
+        if (bs != CUBLAS_STATUS_SUCCESS) {
+            set_error("cuBLAS rand_cholQR Gram failed (%d)", (int)bs);
+            s = CSK_ECUDA;
+        }
+        if (s == CSK_OK) CSK_CUDA_TRY(cudaMemsetAsync(Cw + (size_t)n * nc + n, 0, 8, st));
     } else {
         // row-chunked cuBLAS: chunk copy -> DTRSM in place -> DGEMM (Q0^T Q0) + DGEMV (Q0^T b); the chunk's Q0
         // (rows x n doubles) stays L2-resident between the calls

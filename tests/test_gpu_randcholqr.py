@@ -162,10 +162,16 @@ def test_rc_phases_row_partitioned(p):
     assert np.linalg.norm(A @ (host(x) - x1)) / nb <= max(1e-8, 64 * U * 1e8 * rr)
 
 
-def test_rc_lstsq_wide_uses_blas_pass():
-    # n > 128: the fused DMMA pass does not apply; the row-chunked cuBLAS pass must match the oracle
-    d, n = 30011, 160
-    k1, k2 = 2 * n * n, 2 * n
+@pytest.mark.parametrize("path", ["trsm", "blas"])
+@pytest.mark.parametrize("n,k1", [(160, 2 * 160 * 160), (256, 4096), (129, 2 * 129 * 129)])
+def test_rc_lstsq_wide(monkeypatch, path, n, k1):
+    # 128 < n <= 256: the DMMA TRSM-to-workspace kernel + cuBLAS Gram ("trsm"), or the row-chunked
+    # cuBLAS DTRSM pass ("blas"); both must match the oracle.  (n = 256 with a smaller k1 keeps the
+    # oracle's compensated G-stage to seconds; rand_cholQR needs only a subspace embedding.)
+    if path == "blas":
+        monkeypatch.setenv("CSK_RC_PATH", "0")
+    d = 30011
+    k2 = 2 * n
     A, b = _case(d, n, 1e4, "easy", seed=11)
     plan = csk.cs_plan(d, k1, 6)
     x = host(csk.rc_lstsq(plan, k2, gpu_colmajor(A), gpu_colmajor(b)))
