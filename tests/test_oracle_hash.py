@@ -121,3 +121,19 @@ def test_count_sort_matches_numpy():
 def test_count_sort_empty():
     offsets, perm = oracle.count_sort(np.zeros(0, np.int32), 5)
     assert np.array_equal(offsets, np.zeros(6)) and perm.size == 0
+
+
+def test_survey_known_answers():
+    # codes and Gaussians of seed 1 from an independent Python transcription (tests/golden)
+    path = os.path.join(os.path.dirname(__file__), "golden", "survey_codes_gauss_kat.txt")
+    rows = [ln.split() for ln in open(path) if ln.strip() and not ln.startswith("#")]
+    for r in rows:
+        if r[0] == "codes":
+            k1, i, hv, sv = int(r[1]), int(r[2]), int(r[3]), int(r[4])
+            h, s = oracle.codes(8, k1, 1)
+            assert (int(h[i]), int(s[i])) == (hv, sv), r
+    G = oracle.gauss(1, 4, 1)          # k2 = 1: no scaling, elements e = 0..3 in order
+    for r in rows:
+        if r[0] == "gauss":
+            e, v = int(r[1]), float(r[2])
+            assert abs(G[0, e] - v) <= 1e-14 * max(1.0, abs(v)), r
