@@ -590,7 +590,11 @@ csk_status qr_wy_launch(const double* Z, int64_t ldz, int m, int nc, double* Rg,
             break;
         }
     if (P == 0) return CSK_OK;
-    if (const char* e = std::getenv("CSK_QR_WY_P")) P = std::max(P, std::min(16, std::atoi(e)));
+    // wide sketches: a 16-CTA cluster (measured, scripts/solve_timing.py: 256 x 129 280 -> 235 us,
+    // 512 x 257 575 -> 502 us; 128 x 65 is fastest on one CTA, 110 vs 132 us)
+    if (m >= 256 && nc >= 64) P = 16;
+    if (const char* e = std::getenv("CSK_QR_WY_P"))
+        if (*e) P = std::max(P, std::min(16, std::atoi(e)));
     P = std::min(P, npan);
     const size_t smem = wy_smem_doubles(m, nc, P) * 8;
     WyArgs a;
