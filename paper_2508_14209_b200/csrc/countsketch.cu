@@ -41,6 +41,10 @@ struct RowLayout {
     bool chunk_major = false;
     bool tma = false;   // launch marked TMA-eligible by cs_apply_impl (variants X / B-with-TMA)
     int64_t sep = -1;   // >= 0: the last column is accumulated apart (B32 "split"), k1 doubles at SAt + sep
+    // fp32 accumulation (fp32 input): ncopies row-block copies of a float SA^T (lc, cs in floats),
+    // copy p takes rows [p * rows_per_copy, ...) so every bucket sum in a copy has a bounded depth
+    int ncopies = 0;
+    int64_t rows_per_copy = 0, copy_stride = 0;
     __host__ __device__ int64_t base(int ch, uint32_t bucket) const { return (int64_t)ch * cs + (int64_t)bucket * lc; }
 };
 
@@ -671,6 +675,120 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// ------------------------------------------------ fp32 input, fp32 accumulation (variant B)
+// fp32 bucket sums carry half the L2 reduction bytes of fp64 ones (the bound of this kernel family,
+// DESIGN.md 6.1b), but a sequential fp32 sum over a whole bucket (2048 rows at C2) could reach
+// ~1.2e-4 * sum|terms| (SURVEY 8(a')), above BASELINE's 1e-5.  So the rows are split into ncopies
+// blocks, each reduced into its own float SA^T copy with a mean bucket depth <= 64 (any order: the
+// error is <= (depth - 1) u32 sum|terms| <= ~1e-5 only past depth ~168, ~13 standard deviations
+// above the mean), and cs_combine_f32_kernel adds the copies in fp64 and rounds once.
+// Tiles: 32 rows x cw (<= 66) columns per warp; lane (p, half) loads rows 2p, 2p+1 of column
+// 2j + half as one float2 (128-B segments per half-warp); lane r bulk-reduces row r (.add.f32).
+template <int W>
+__global__ void __launch_bounds__(W * 32, 1) cs_bulk32f_kernel(const uint32_t* __restrict__ code, int64_t rows,
+                                                                Cols<float> cols, int ncols, int ldtile,
+                                                                float* __restrict__ SAt, RowLayout L) {
+    // 64-row tiles: lane l loads rows 2l, 2l+1 of every column as one float2 (256-B segments, the
+    // bytes in flight per warp of the fp64 kernel), transposes them into a row-major float tile and
+    // bulk-reduces rows l and l + 32
+    constexpr int kR = 64;
+    const int cw = L.cw;
+    extern __shared__ __align__(16) float f32_smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float* tile = f32_smem + (size_t)warp * kR * ldtile;
+    for (int e = lane; e < kR * ldtile; e += 32) tile[e] = 0.0f;
+    __syncwarp();
+    const int nchunks = (ncols + cw - 1) / cw;
+    const int64_t ngroups = (rows + kR - 1) / kR;
+    const int64_t nunits = ngroups * nchunks;
+    const int64_t gwarp = blockIdx.x * (int64_t)W + warp;
+    const int64_t nwarps = (int64_t)gridDim.x * W;
+    const bool al8 = (cols.lda & 1) == 0 && (((uintptr_t)cols.A & 7) == 0) &&
+                     (cols.b == nullptr || ((uintptr_t)cols.b & 7) == 0);
+    for (int64_t u = gwarp; u < nunits; u += nwarps) {
+        int64_t g;
+        int ch;
+        unit_coords(u, nchunks, ngroups, L.chunk_major, g, ch);
+        const int c0 = ch * cw;
+        const int nc = min(cw, ncols - c0);
+        const int64_t r0 = g * kR;
+        const bool full = r0 + kR <= rows && al8;
+        const int64_t ra = min(r0 + 2 * lane, rows - 1), rb = min(r0 + 2 * lane + 1, rows - 1);
+        const uint32_t ca = __ldg(code + ra), cb = __ldg(code + rb);
+        const uint32_t c1 = __ldg(code + min(r0 + lane, rows - 1)), c2 = __ldg(code + min(r0 + 32 + lane, rows - 1));
+        float2 v[kBulkMaxCols];
+#pragma unroll
+        for (int c = 0; c < kBulkMaxCols; ++c) {
+            const float* col = cols.col(c0 + min(c, nc - 1));
+            float2 x;
+            if (full) {
+                x = __ldcs(reinterpret_cast<const float2*>(col + r0 + 2 * lane));
+            } else {
+                x.x = __ldcs(col + ra);
+                x.y = r0 + 2 * lane + 1 < rows ? __ldcs(col + rb) : 0.0f;
+            }
+            v[c] = (c < nc) ? x : make_float2(0.0f, 0.0f);
+        }
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+        float* ta = tile + (2 * lane) * ldtile;
+        float* tb = ta + ldtile;
+        const uint32_t sa = ca & 0x80000000u, sb = cb & 0x80000000u;
+        const int nc4 = (nc + 3) & ~3;   // 16-B multiple: zero the padding columns
+#pragma unroll
+        for (int c = 0; c < kBulkMaxCols; ++c) {
+            if (c < nc) {
+                ta[c] = __uint_as_float(__float_as_uint(v[c].x) ^ sa);
+                tb[c] = __uint_as_float(__float_as_uint(v[c].y) ^ sb);
+            } else if (c < nc4) {
+                ta[c] = 0.0f;
+                tb[c] = 0.0f;
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int r = lane + 32 * h;
+            if (r0 + r < rows) {
+                const uint32_t cr = h ? c2 : c1;
+                const int64_t copy = (r0 + r) / L.rows_per_copy;
+                float* dst = SAt + copy * L.copy_stride + (int64_t)ch * L.cs + (int64_t)code_bucket(cr) * L.lc;
+                const uint32_t src = (uint32_t)__cvta_generic_to_shared(tile + r * ldtile);
+                asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst),
+                             "r"(src), "r"((uint32_t)(nc4 * 4))
+                             : "memory");
+            }
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// SA[m, c] = (float) sum_p (double) copy_p[m, c]  (fixed order over p)
+__global__ void cs_combine_f32_kernel(const float* __restrict__ SAt, RowLayout L, int64_t k1, int ncols,
+                                      float* __restrict__ SA, int64_t ldsa) {
+    __shared__ float t[32][33];
+    const int64_t m0 = blockIdx.x * 32;
+    const int c0 = blockIdx.y * 32;
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const int64_t m = m0 + j;
+        const int c = c0 + threadIdx.x;
+        double acc = 0.0;
+        if (m < k1 && c < ncols) {
+            const int64_t off = (int64_t)(c / L.cw) * L.cs + m * L.lc + (c % L.cw);
+            for (int q = 0; q < L.ncopies; ++q) acc += (double)SAt[q * L.copy_stride + off];
+        }
+        t[j][threadIdx.x] = (float)acc;
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const int c = c0 + j;
+        const int64_t m = m0 + threadIdx.x;
+        if (m < k1 && c < ncols) SA[m + (int64_t)c * ldsa] = t[threadIdx.x][j];
+    }
+}
+
 // SA^T (row-major workspace, fp64) -> SA (column-major, ldsa, T)
 template <typename T>
 __global__ void transpose_out_kernel(const double* __restrict__ SAt, RowLayout L, int64_t k1, int ncols,
@@ -964,6 +1082,22 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
                 return r;
             }
             const int cw = L.cw;   // bulk_chunk_width(ncols), set with the layout by cs_apply_impl
+            if constexpr (sizeof(T) == 4) {
+                if (L.ncopies > 0) {   // fp32 accumulation into bounded-depth copies
+                    const int ldf = ((cw + 3) & ~3) + 4;   // 16-B rows, == 4 mod 8 floats
+                    const size_t smem = (size_t)8 * 64 * ldf * sizeof(float);
+                    CSK_CUDA_TRY(cudaFuncSetAttribute(cs_bulk32f_kernel<8>,
+                                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                    const int64_t units = ceil_div(rows, 64) * ceil_div(ncols, cw);
+                    const int64_t blocks = std::min<int64_t>(ceil_div(units, 8), (int64_t)di.num_sms);
+                    prof_mark(st, true);
+                    cs_bulk32f_kernel<8><<<(unsigned)blocks, 256, smem, st>>>(
+                        code, rows, *reinterpret_cast<const Cols<float>*>(&cols), ncols, ldf,
+                        reinterpret_cast<float*>(out), L);
+                    CSK_LAUNCH_CHECK();
+                    return CSK_OK;
+                }
+            }
             const int ldtile = (cw + 1) & ~1;
             const int64_t units = ceil_div(rows, kBulkRows) * ceil_div(ncols, cw);
             const char* ex = std::getenv("CSK_EXP");
@@ -1188,6 +1322,23 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
                     L.sep = k1 * L.lc;
                     ws_doubles = (size_t)k1 * L.lc + (size_t)k1;
                 }
+                // fp32 input: fp32 accumulation in row-block copies of mean bucket depth <= 64
+                // Opt-in (CSK_F32ACC=1): measured slower than fp64 accumulation at C2 fp32 (2.47 ms with
+                // 32-row tiles, 3.95 ms with 64-row tiles, vs 2.02 ms): half the reduction bytes buy
+                // nothing (the L2 adds the same number of elements per row) and the float tile writes
+                // of 16-B aligned rows cannot avoid 8-way bank conflicts.
+                const char* f32e = std::getenv("CSK_F32ACC");
+                if (dtype == CSK_F32 && !tma && variant == CSK_VAR_BULK_ROW && !L.chunk_major &&
+                    f32e && std::atoi(f32e) == 1) {
+                    const int64_t rows = row_end - row_begin;
+                    const int64_t ncp = std::max<int64_t>(1, std::min<int64_t>(256, ceil_div(rows, 64 * k1)));
+                    L.cs = nchunks > 1 ? ((L.cw + 3) & ~3) : L.cw;
+                    L.lc = std::max<int64_t>((ncols + 3) & ~3, nchunks * (int64_t)((L.cw + 3) & ~3));
+                    L.ncopies = (int)ncp;
+                    L.rows_per_copy = ceil_div(rows, ncp);
+                    L.copy_stride = k1 * L.lc;                       // floats
+                    ws_doubles = (size_t)ceil_div(ncp * L.copy_stride, 2);
+                }
             }
         } else {
             L.cw = ncols;   // T (and L/S fallbacks): its own 32-column chunks, regular layout
@@ -1233,6 +1384,18 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
         rowout->lc = L.lc;
         rowout->cs = L.cs;
         rowout->ncols = ncols;
+        return CSK_OK;
+    }
+    if (s == CSK_OK && tgt.owned && L.ncopies > 0) {
+        dim3 grid((unsigned)ceil_div(k1, 32), (unsigned)ceil_div(ncols, 32));
+        cs_combine_f32_kernel<<<grid, dim3(32, 8), 0, st>>>(reinterpret_cast<const float*>(tgt.buf), L, k1, ncols,
+                                                            static_cast<float*>(SA), ldsa);
+        count_launch();
+        cudaFreeAsync(tgt.buf, st);
+        if (cudaGetLastError() != cudaSuccess) {
+            set_error("cs_apply fp32 combine launch failed");
+            return CSK_ECUDA;
+        }
         return CSK_OK;
     }
     if (s == CSK_OK && tgt.owned) {

@@ -461,3 +461,27 @@ def test_cs_apply_narrow_rows_mixed_paths(monkeypatch, mix_rt, d, n, k1):
     Ai = synth.integer_matrix(d, n, seed=6)
     got = host(csk.cs_apply(plan, gpu_colmajor(Ai)))
     assert np.array_equal(got, oracle.cs_apply(h, s, Ai, k1))
+
+
+@pytest.mark.parametrize("acc", ["1", "0"])
+@pytest.mark.parametrize("d,n,with_b,k1,off", [(1 << 21, 64, True, 2048, 0), (300007, 40, False, 512, 0),
+                                               (100003, 129, True, 1024, 0), (50001, 7, True, 4096, 1)])
+def test_cs_apply_fp32_accumulation(monkeypatch, acc, d, n, with_b, k1, off):
+    # fp32 input: fp32 sums in row-block copies of bounded bucket depth, combined in fp64 ("1"), or
+    # fp64 accumulation ("0"); both within 1e-5 * sum|terms| (BASELINE.json).  off = 1 misaligns A by
+    # one float (no float2 loads).
+    monkeypatch.setenv("CSK_F32ACC", acc)
+    A = synth.gaussian_matrix(d, n, seed=3, dtype=np.float32)
+    b = synth.rhs(A.astype(np.float64), "easy", seed=3).astype(np.float32) if with_b else None
+    plan = csk.cs_plan(d, k1, 4)
+    h, s = oracle.codes(d, k1, 4)
+    big = np.zeros((d + off, n), dtype=np.float32, order="F")
+    big[off:] = A
+    Ad = gpu_colmajor(big)[off:]
+    bd = None if b is None else gpu_colmajor(b)
+    SA = host(csk.cs_apply(plan, Ad, b=bd))
+    exp, T = oracle.cs_apply(h, s, A, k1, b=b, with_abs=True)
+    assert_within_T(SA, exp, T, 1e-5)
+    Ai = synth.integer_matrix(d, n, seed=6, dtype=np.float32)
+    got = host(csk.cs_apply(plan, gpu_colmajor(Ai)))
+    assert np.array_equal(got.astype(np.float64), oracle.cs_apply(h, s, Ai, k1))
