@@ -442,6 +442,8 @@ csk_status solve_impl(int64_t k2, int64_t n, const double* Z, int64_t ldz, doubl
     const size_t scratch_bytes = qr_wy_scratch_doubles(m, nc) * 8;
     const size_t scratch_off = (wbytes + 64 + (x_host ? n * 8 : 0) + 255) & ~(size_t)255;   // 16-B vector loads
     CSK_CUDA_TRY(cudaMallocAsync(&W, scratch_off + scratch_bytes, st));
+    // R's unused (lower) part is read by 16-B block loads and by the R export: keep it defined
+    CSK_CUDA_TRY(cudaMemsetAsync(W, 0, wbytes + 64, st));   // + the status struct (its padding is copied out)
     sd = reinterpret_cast<SolveStatus*>(reinterpret_cast<char*>(W) + wbytes);
     xd = x_host ? reinterpret_cast<double*>(reinterpret_cast<char*>(W) + wbytes + 64) : x;
     double* scratch = reinterpret_cast<double*>(reinterpret_cast<char*>(W) + scratch_off);

@@ -778,6 +778,7 @@ static csk_status rc_gram_impl(int64_t d, int64_t n, const double* A, int64_t ld
     // the fused kernels and the reduction write an nc x nc C with ld nc; copy out when ldc differs
     double* Cw = C;
     if (ldc != nc) CSK_CUDA_TRY(cudaMallocAsync(&Cw, (size_t)nc * nc * 8, st));
+    CSK_CUDA_TRY(cudaMemsetAsync(Cw, 0, (size_t)nc * nc * 8, st));   // the lower part stays defined (0)
     csk_status s = CSK_OK;
     if (fused) {
         const int nb = n <= 16 ? 2 : n <= 32 ? 4 : n <= 64 ? 8 : 16;

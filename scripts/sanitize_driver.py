@@ -1,0 +1,74 @@
+"""Every kernel of libcsk at C1-like sizes, for compute-sanitizer (memcheck / racecheck / synccheck /
+initcheck, tier T4).  Prints one line per call; a sanitizer error shows in its report."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2508_14209_b200 as csk  # noqa: E402
+import synth  # noqa: E402
+
+
+def cm(a):
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(a).T)).cuda().t() if np.ndim(a) == 2 else \
+        torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def env(**kv):
+    for k, v in kv.items():
+        if v is None:
+            os.environ.pop(k, None)
+        else:
+            os.environ[k] = v
+
+
+d, n = 8192, 8
+A = synth.gaussian_matrix(d, n, seed=2)
+b = synth.rhs(A, "hard", seed=2)
+Ad, bd = cm(A), cm(b)
+plan = csk.cs_plan(d, 128, 1, sort=True)
+for v in ("L", "T", "S", "G", "B", "X"):
+    csk.cs_apply(plan, Ad, b=bd, variant=v)
+    print("cs_apply", v, flush=True)
+csk.cs_apply(plan, cm(A.astype(np.float32)), b=cm(b.astype(np.float32)))
+print("cs_apply fp32", flush=True)
+wide = synth.gaussian_matrix(4096, 129, seed=3)
+csk.cs_apply(csk.cs_plan(4096, 256, 2), cm(wide), b=cm(wide[:, 0].copy()))
+print("cs_apply 2 chunks", flush=True)
+for k, vv in (("CSK_SPLIT", "1"), ("CSK_MIX_RT", "16"), ("CSK_F32ACC", "1")):
+    env(**{k: vv})
+    AA = A if k != "CSK_F32ACC" else A.astype(np.float32)
+    csk.cs_apply(plan, cm(AA if k != "CSK_MIX_RT" else AA[:, :8]), b=None if k == "CSK_MIX_RT" else cm(b.astype(AA.dtype)))
+    env(**{k: None})
+    print("cs_apply", k, flush=True)
+Z = csk.ms_apply(plan, 16, Ad, b=bd)
+for e in ({}, {"CSK_QR_WY": "0"}, {"CSK_QR_WY": "0", "CSK_QR_SINGLE": "1"}, {"CSK_QR_WY_P": "2"}):
+    env(**e)
+    csk.ms_solve(Z, n)
+    env(**{k: None for k in e})
+    print("ms_solve", e, flush=True)
+csk.ne_lstsq(Ad, bd)
+print("ne_lstsq", flush=True)
+for e in ({}, {"CSK_RC_KERNEL": "1"}, {"CSK_RC_KERNEL": "2"}, {"CSK_RC_PATH": "0"}):
+    env(**e)
+    csk.rc_lstsq(plan, 16, Ad, bd)
+    env(**{k: None for k in e})
+    print("rc_lstsq", e, flush=True)
+Aw = synth.gaussian_matrix(2048, 136, seed=4)
+csk.rc_lstsq(csk.cs_plan(2048, 4096, 3), 272, cm(Aw), cm(Aw[:, 0].copy()))
+print("rc_lstsq wide", flush=True)
+As = synth.gaussian_matrix(1 << 13, 3, seed=5)
+for e in ({}, {"CSK_SRHT_KERNEL": "2"}, {"CSK_SRHT_KERNEL": "1"}, {"CSK_SRHT_KERNEL": "1", "CSK_SRHT_TMA": "0"}):
+    env(**e)
+    csk.srht_apply(cm(As), 40, 1)
+    env(**{k: None for k in e})
+    print("srht_apply", e, flush=True)
+csk.srht_apply(cm(As[:1024]), 20, 1)
+print("srht_apply small", flush=True)
+csk.gs_lstsq(Ad, bd, 16, 1)
+csk.cs_lstsq(plan, Ad, bd)
+csk.msh_lstsq(plan, 16, Ad, bd)
+torch.cuda.synchronize()
+print("gs/cs/msh lstsq done", flush=True)
