@@ -290,10 +290,17 @@ def bench_ours(args, cfg):
     import synth
 
     ws, rank, local = dist_env()
+    # CSK_BENCH_BACKEND=gloo lets the N > 1 logic run with several ranks on one GPU (a test of the
+    # partitioning, barriers and max-over-ranks timing; NCCL refuses two ranks on one device)
+    backend = os.environ.get("CSK_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     if args.variant != "auto":
         os.environ["CSK_VARIANT"] = str(csk.csk.VARIANTS[args.variant])
     n, k1, k2 = cfg["n"], cfg["k1"], cfg["k2"]
@@ -576,7 +583,7 @@ def bench_ours(args, cfg):
         "config": {"workload": cfg["name"], "d_per_rank": d, "d_global": d_glob, "n": n, "k1": k1, "k2": k2,
                    "rhs": "b = A e + eta, eta ~ N(0, 0.01)", "variant": variant,
                    "l2": "inputs (%.1f GB per rank) > 126 MB L2; no flush needed" % (bytes_step / 1e9),
-                   "parallelism": f"row-partitioned dp{ws}" + (" + NCCL all-reduce of Z" if ws > 1 else "")},
+                   "parallelism": f"row-partitioned dp{ws}" + (f" + {backend.upper()} all-reduce of Z" if ws > 1 else "")},
         "clocks": clocks.summary(),
         "e2e": e2e,
         "gpu_launches": launches,
