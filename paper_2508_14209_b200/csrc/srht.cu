@@ -480,6 +480,117 @@ __global__ void __launch_bounds__(kHWWarps * 32) srht_warp_kernel(const double* 
     }
 }
 
+// TMA-fed warp-block variant: as srht_warp_kernel, but each warp's next 1024-row block arrives by
+// one cp.async.bulk (8 KB) into a per-warp stage while the current block is transformed, so the
+// HBM stream no longer pauses for the FWHT (the register kernel is latency-bound at 16 warps/SM
+// when k = 256).  Needs 16-B aligned columns.
+template <int R>
+__global__ void __launch_bounds__(kHWWarps * 32) srht_warp_tma_kernel(const double* __restrict__ A, int64_t lda,
+                                                                      const double* __restrict__ bvec, int n,
+                                                                      int ncols, int64_t nblk, int64_t hb0,
+                                                                      const uint32_t* __restrict__ dbits,
+                                                                      const uint32_t* __restrict__ psamp, int k,
+                                                                      double scale, double* __restrict__ Y,
+                                                                      int64_t ldy) {
+    extern __shared__ __align__(128) double wsm[];
+    __shared__ uint32_t smap[kHW / 32];
+    __shared__ __align__(8) uint64_t bar[kHWWarps];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* stage = wsm + (size_t)warp * (kHW + kHWPad);
+    double* xs = stage + kHW;
+    for (int w = threadIdx.x; w < kHW / 32; w += blockDim.x) smap[w] = 0u;
+    __syncthreads();
+    int pl[R];
+    uint32_t ph[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int j = lane + 32 * r;
+        const uint32_t pj = j < k ? psamp[j] : 0u;
+        pl[r] = (int)(pj & (kHW - 1));
+        ph[r] = pj / kHW;
+        if (j < k && warp == 0) atomicOr(&smap[pl[r] >> 5], 1u << (pl[r] & 31));
+    }
+    __syncthreads();
+    const uint32_t mymap = smap[lane];
+    const int64_t total = nblk * ncols;
+    const int64_t nw = (int64_t)gridDim.x * kHWWarps, gw = (int64_t)blockIdx.x * kHWWarps + warp;
+    const int64_t per = (total + nw - 1) / nw;
+    const int64_t u0 = gw * per, u1 = min(total, u0 + per);
+    if (u0 >= u1) return;
+    auto src_of = [&](int64_t u) {
+        const int c = (int)(u / nblk);
+        const int64_t blk = u - (int64_t)c * nblk;
+        return (c < n ? A + (int64_t)c * lda : bvec) + blk * kHW;
+    };
+    if (lane == 0) {
+        mbar_init(&bar[warp], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_expect_tx(&bar[warp], kHW * 8);
+        bulk_load_1d(stage, src_of(u0), kHW * 8, &bar[warp]);
+    }
+    __syncwarp();
+    double acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+    int cur = (int)(u0 / nblk);
+    uint32_t parity = 0;
+    for (int64_t u = u0; u < u1; ++u) {
+        const int c = (int)(u / nblk);
+        const int64_t blk = u - (int64_t)c * nblk;
+        if (c != cur) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int j = lane + 32 * r;
+                if (j < k) atomicAdd(Y + j + (int64_t)cur * ldy, acc[r] * scale);
+                acc[r] = 0.0;
+            }
+            cur = c;
+        }
+        const uint32_t* db = dbits + blk * (kHW / 32);
+        uint32_t dw[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) dw[e] = __ldg(db + e);
+        mbar_wait(&bar[warp], parity);
+        parity ^= 1u;
+        double x[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+            const uint32_t bit = (dw[e] >> lane) & 1u;
+            x[e] = __longlong_as_double(__double_as_longlong(stage[e * 32 + lane]) ^ ((long long)bit << 63));
+        }
+        __syncwarp();   // every lane has read the stage: the next block may overwrite it
+        if (lane == 0 && u + 1 < u1) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&bar[warp], kHW * 8);
+            bulk_load_1d(stage, src_of(u + 1), kHW * 8, &bar[warp]);
+        }
+        fwht32(x);   // bits 5..9
+#pragma unroll
+        for (int e = 0; e < 32; ++e) xs[hpadw(e * 32 + lane)] = x[e];
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < 32; ++e) x[e] = xs[hpadw(lane * 32 + e)];
+        fwht32(x);   // bits 0..4
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+            if ((mymap >> e) & 1u) xs[hpadw(lane * 32 + e)] = x[e];
+        __syncwarp();
+        const uint32_t hi = (uint32_t)(hb0 + blk);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const double v = xs[hpadw(pl[r])];
+            acc[r] += (__popc(ph[r] & hi) & 1) ? -v : v;
+        }
+        __syncwarp();
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int j = lane + 32 * r;
+        if (j < k) atomicAdd(Y + j + (int64_t)cur * ldy, acc[r] * scale);
+    }
+}
+
 // d < 4096: one CTA per column, the whole vector in shared memory, radix-2 stages (Alg 3's
 // butterflies, one barrier per stage).
 __global__ void __launch_bounds__(256) srht_small_kernel(const double* __restrict__ A, int64_t lda,
@@ -555,7 +666,22 @@ csk_status srht_impl(int64_t d, int64_t dglob, int64_t row0, int64_t k, uint64_t
         const char* e = std::getenv("CSK_SRHT_TMA");
         const char* v = std::getenv("CSK_SRHT_KERNEL");   // experiment: 1 = 3-phase, 2 = radix-64 blocks
         const int kv = v ? std::atoi(v) : 0;
-        if (kv == 0 && k <= 512) {
+        const char* wte = std::getenv("CSK_SRHT_WTMA");   // experiment: 0 = register warp kernel for every k
+        const int wt = wte ? std::atoi(wte) : 1;
+        if (kv == 0 && al && ((k > 128 && k <= 256 && wt >= 1) || (k <= 128 && wt == 2))) {
+            // the TMA-fed warp kernel: k = 2n = 256 1.87 -> 1.61 ms at d = 2^23 x 129 (the register
+            // kernel is latency-bound there); k <= 128 only on request (CSK_SRHT_WTMA=2)
+            auto kern = k <= 128 ? srht_warp_tma_kernel<4> : srht_warp_tma_kernel<8>;
+            const size_t smem = (size_t)kHWWarps * (kHW + kHWPad) * 8;
+            CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            CSK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kHWWarps * 32, smem));
+            const int64_t nblk1 = d / kHW, total1 = nblk1 * ncols;
+            const int64_t grid = std::min<int64_t>(ceil_div(total1, kHWWarps), (int64_t)di.num_sms * std::max(per_sm, 1));
+            prof_mark(st, true);
+            kern<<<(unsigned)grid, kHWWarps * 32, smem, st>>>(A, lda, b, (int)n, (int)ncols, nblk1, row0 / kHW, dbits,
+                                                              psamp, (int)k, scale, Y, ldy);
+            CSK_LAUNCH_CHECK();
+        } else if (kv == 0 && k <= 512) {
             auto kern = k <= 128 ? srht_warp_kernel<4> : k <= 256 ? srht_warp_kernel<8> : srht_warp_kernel<16>;
             // experiment: shared-memory carveout %.  The driver default measured best (1.49 ms at
             // d=2^24 x 65, k=128): a larger carveout shrinks L1, which stages the in-flight loads.
