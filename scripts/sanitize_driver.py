@@ -65,6 +65,8 @@ for e in ({}, {"CSK_SRHT_KERNEL": "2"}, {"CSK_SRHT_KERNEL": "1"}, {"CSK_SRHT_KER
     csk.srht_apply(cm(As), 40, 1)
     env(**{k: None for k in e})
     print("srht_apply", e, flush=True)
+csk.srht_apply(cm(As), 200, 1)                     # TMA-fed warp kernel (128 < k <= 256)
+print("srht_apply k=200", flush=True)
 csk.srht_apply(cm(As[:1024]), 20, 1)
 print("srht_apply small", flush=True)
 csk.gs_lstsq(Ad, bd, 16, 1)
