@@ -57,3 +57,21 @@ def test_binding_has_no_cpu_fallback():
     text = open(os.path.join(PKG, "csk.py")).read()
     assert "no CPU fallback" in text
     assert "numpy.linalg" not in text and "np.linalg" not in text
+
+
+def test_binding_arity_matches_header():
+    # every function the binding declares argtypes for takes exactly as many parameters as csk.h says
+    hdr = open(os.path.join(ROOT, "include", "csk.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    decls = {}
+    for m in re.finditer(r"\b(?:csk_status|void|const char\*|uint64_t)\s+(\w+)\s*\(([^;{]*?)\)\s*;", hdr):
+        params = [p for p in m.group(2).split(",") if p.strip() and p.strip() != "void"]
+        decls[m.group(1)] = len(params)
+    L = csk.lib()
+    checked = 0
+    for name, n in decls.items():
+        f = getattr(L, name, None)
+        if f is not None and getattr(f, "argtypes", None) is not None:
+            assert len(f.argtypes) == n, (name, len(f.argtypes), n)
+            checked += 1
+    assert checked >= 20, checked
