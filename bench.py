@@ -327,7 +327,7 @@ def bench_ours(args, cfg):
     # ---- plan (a1 codes; a4 G is drawn on first use and cached)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    plan = csk.cs_plan(d, k1, SKETCH_SEED, row0=row0, sort=(args.variant == "G"))
+    plan = csk.cs_plan(d, k1, SKETCH_SEED, row0=row0, sort=(args.variant == "G"), hash=args.hash_plan)
     ev1.record(stream)
     torch.cuda.synchronize()
     plan_ms = ev0.elapsed_time(ev1)
@@ -582,6 +582,7 @@ def bench_ours(args, cfg):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "step_ms_stats": step_stats,
         "config": {"workload": cfg["name"], "d_per_rank": d, "d_global": d_glob, "n": n, "k1": k1, "k2": k2,
                    "rhs": "b = A e + eta, eta ~ N(0, 0.01)", "variant": variant,
+                   "codes": "hashed on the fly" if args.hash_plan else "stored (4 B/row)",
                    "l2": "inputs (%.1f GB per rank) > 126 MB L2; no flush needed" % (bytes_step / 1e9),
                    "parallelism": f"row-partitioned dp{ws}" + (f" + {backend.upper()} all-reduce of Z" if ws > 1 else "")},
         "clocks": clocks.summary(),
@@ -875,6 +876,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--variant", default="auto", choices=["auto", "L", "T", "S", "G", "B", "X"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--hash-plan", action="store_true",
+                    help="CSK_PLAN_HASH: no stored codes, the CountSketch kernel hashes rows on the fly")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ne", action="store_true", help="skip the normal-equations baseline")
     ap.add_argument("--cs-only", action="store_true", help="experiment mode: a step is cs_apply alone")

@@ -64,6 +64,10 @@ typedef enum {
 
 /* cs_plan flags */
 #define CSK_PLAN_SORT 0x2u    /* also build the stable counting sort (needed by CSK_VAR_SORTED) */
+#define CSK_PLAN_HASH 0x4u    /* store no codes: the fp64 row-tile CountSketch recomputes h(i), s(i)
+                                 from (seed, global row) on the fly -- the hash-based generation of
+                                 P:L389 -- and every other consumer materialises the codes on first
+                                 use (ignored together with CSK_PLAN_SORT, which needs them) */
 
 typedef struct csk_plan_s* csk_plan_t;
 
@@ -77,7 +81,7 @@ typedef struct csk_plan_s* csk_plan_t;
  *   d      rows of the (local) block, 1 <= d <= 2^31 - 1
  *   k1     embedding dimension, 1 <= k1 <= 2^31 - 1
  *   seed   sketch seed (Philox key);  row0 >= 0 global index of local row 0
- *   flags  0 or CSK_PLAN_SORT
+ *   flags  0, CSK_PLAN_SORT and/or CSK_PLAN_HASH
  *   out    receives the plan handle (NULL on failure) */
 csk_status cs_plan(int64_t d, int64_t k1, uint64_t seed, int64_t row0, uint32_t flags,
                    void* stream, csk_plan_t* out);

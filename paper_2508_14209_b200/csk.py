@@ -22,6 +22,7 @@ VAR_AUTO, VAR_ATOMIC_COL, VAR_ATOMIC_ROW, VAR_SMEM, VAR_SORTED, VAR_BULK_ROW, VA
 VARIANTS = {"auto": VAR_AUTO, "L": VAR_ATOMIC_COL, "T": VAR_ATOMIC_ROW, "S": VAR_SMEM, "G": VAR_SORTED,
             "B": VAR_BULK_ROW, "X": VAR_TMA_ROW}
 PLAN_SORT = 0x2
+PLAN_HASH = 0x4
 
 _lock = threading.Lock()
 _lib = None
@@ -195,10 +196,12 @@ class Plan:
         return code, offsets, perm
 
 
-def cs_plan(d: int, k1: int, seed: int, row0: int = 0, sort: bool = False, stream=None) -> Plan:
+def cs_plan(d: int, k1: int, seed: int, row0: int = 0, sort: bool = False, stream=None, hash: bool = False) -> Plan:
+    """hash=True: CSK_PLAN_HASH (no stored codes; the fp64 row-tile kernel hashes rows on the fly)."""
     _torch()
     h = ctypes.c_void_p()
-    _check(lib().cs_plan(d, k1, seed, row0, PLAN_SORT if sort else 0, _stream(stream), ctypes.byref(h)), "cs_plan")
+    flags = (PLAN_SORT if sort else 0) | (PLAN_HASH if hash else 0)
+    _check(lib().cs_plan(d, k1, seed, row0, flags, _stream(stream), ctypes.byref(h)), "cs_plan")
     return Plan(h.value, d, k1, row0, seed, sort)
 
 

@@ -45,6 +45,9 @@ struct RowLayout {
     // copy p takes rows [p * rows_per_copy, ...) so every bucket sum in a copy has a bounded depth
     int ncopies = 0;
     int64_t rows_per_copy = 0, copy_stride = 0;
+    // CSK_PLAN_HASH: global row of local row 0 and the Philox key (codes recomputed in the kernel)
+    int64_t g0 = 0;
+    uint32_t hkey0 = 0, hkey1 = 0;
     __host__ __device__ int64_t base(int ch, uint32_t bucket) const { return (int64_t)ch * cs + (int64_t)bucket * lc; }
 };
 
@@ -547,7 +550,7 @@ __global__ void __launch_bounds__(C::kWarps * 32, 1) cs_bulk_kernel(const uint32
 // back to clamped scalar loads.
 constexpr int kB32Rows = 32;
 
-template <int W, int EXP, bool SPLIT = false, bool PRED = false, bool MIX = false>
+template <int W, int EXP, bool SPLIT = false, bool PRED = false, bool MIX = false, bool HASH = false>
 __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __restrict__ code, int64_t rows,
                                                                Cols<double> cols, int ncols, int ldtile,
                                                                double* __restrict__ SAt, RowLayout L, int k1,
@@ -587,8 +590,23 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
         const int64_t r0 = g * kB32Rows;
         const bool full = r0 + kB32Rows <= rows;
         const int64_t ra = min(r0 + 2 * p, rows - 1), rb = min(r0 + 2 * p + 1, rows - 1);
-        const uint32_t ca = __ldg(code + ra), cb = __ldg(code + rb);
-        const uint32_t crow = __ldg(code + min(r0 + lane, rows - 1));
+        uint32_t ca, cb, crow;
+        if constexpr (HASH) {
+            // CSK_PLAN_HASH (hash-based generation on the fly): lane r hashes row r0 + r
+            // (one Philox4x32-10 block, the word of its row) and the pair rows come by shuffle --
+            // no code array is read; the same function codes_kernel stores (R3)
+            const uint64_t gr = (uint64_t)(L.g0 + min(r0 + lane, rows - 1));
+            const uint4 x = hash_block(gr, L.hkey0, L.hkey1);
+            const uint32_t jw = (uint32_t)gr & 3u;
+            const uint32_t w = jw == 0 ? x.x : jw == 1 ? x.y : jw == 2 ? x.z : x.w;
+            crow = code_from_word(w, (uint32_t)k1);
+            ca = __shfl_sync(0xffffffffu, crow, 2 * p);
+            cb = __shfl_sync(0xffffffffu, crow, 2 * p + 1);
+        } else {
+            ca = __ldg(code + ra);
+            cb = __ldg(code + rb);
+            crow = __ldg(code + min(r0 + lane, rows - 1));
+        }
         if constexpr (split) {   // row r0 + lane of the split column into this CTA's shared buckets
             const double bv = ldcs_pred(cols.col(ncols) + min(r0 + lane, rows - 1), r0 + lane < rows);
             if (r0 + lane < rows) atomicAdd(sb + code_bucket(crow), apply_sign(bv, crow));
@@ -1033,9 +1051,17 @@ template <typename T>
 static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> cols, int64_t row_begin,
                               int64_t row_end, double* out, int64_t ldo, const RowLayout& L, cudaStream_t st) {
     const DeviceInfo& di = device_info();
-    const uint32_t* code = reinterpret_cast<const uint32_t*>(plan->code) + row_begin;
     const int64_t rows = row_end - row_begin;
     if (rows <= 0) return CSK_OK;
+    // CSK_PLAN_HASH: only the default fp64 32-row kernels hash rows on the fly; every other
+    // kernel reads the code array, materialised on first use
+    const bool may_hash = plan->code == nullptr && variant == CSK_VAR_BULK_ROW && !L.tma && sizeof(T) == 8 &&
+                          L.sep < 0;
+    if (plan->code == nullptr && !may_hash) {
+        const csk_status es = ensure_codes(plan, st);
+        if (es != CSK_OK) return es;
+    }
+    const uint32_t* code = plan->code ? reinterpret_cast<const uint32_t*>(plan->code) + row_begin : nullptr;
     switch (variant) {
         case CSK_VAR_ATOMIC_COL: {
             const int64_t blocks = std::min<int64_t>(ceil_div(rows, 256), (int64_t)di.num_sms * 8);
@@ -1149,11 +1175,30 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
                     // split measured slower than TMA alone -- 0.72 ms (32) vs 0.89 (24), 0.96 (16), 1.11 (0))
                     const char* mxe = std::getenv("CSK_MIX_RT");
                     const int mix_rt = mxe ? std::max(0, std::min(32, std::atoi(mxe))) : 32;
+                    const bool narrow = cw < kBulkMaxCols - 3;
+                    if (code == nullptr) {   // CSK_PLAN_HASH plan
+                        const char* he = std::getenv("CSK_L2HINT");
+                        const bool hint = !(he && std::atoi(he) == 0);
+                        RowLayout LH = L;
+                        LH.g0 = plan->row0 + row_begin;
+                        LH.hkey0 = (uint32_t)plan->seed;
+                        LH.hkey1 = (uint32_t)(plan->seed >> 32);
+                        const size_t smem = (size_t)8 * kB32Rows * ld32 * sizeof(double);
+                        auto kern = narrow ? cs_bulk32_kernel<8, 0, false, true, false, true>
+                                           : cs_bulk32_kernel<8, 0, false, false, false, true>;
+                        CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                        const int64_t blocks = std::min<int64_t>(ceil_div(units32, 8), (int64_t)di.num_sms);
+                        prof_mark(st, true);
+                        kern<<<(unsigned)blocks, 256, smem, st>>>(nullptr, rows, cols, nbulk, ld32, out, LH,
+                                                                  (int)plan->k1, narrow && hint ? -1 : 32);
+                        CSK_LAUNCH_CHECK();
+                        return CSK_OK;
+                    }
                     if (L.sep >= 0)
                         r32 = launch32(cs_bulk32_kernel<8, 0, true>, 8);
                     else if (cw <= 32 && nbulk <= cw && expv == 0 && b32 == 8 && mix_rt < 32)
                         r32 = launch32(cs_bulk32_kernel<8, 0, false, false, true>, 8, mix_rt);   // narrow rows
-                    else if (cw < kBulkMaxCols - 3 && expv == 0 && b32 == 8) {
+                    else if (narrow && expv == 0 && b32 == 8) {
                         // evict_last hint on the reductions (C3: 2.11 -> 2.07 ms, DRAM writes 806 -> 712 MB);
                         // CSK_L2HINT=0 turns it off
                         const char* he = std::getenv("CSK_L2HINT");
@@ -1172,6 +1217,11 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
                                           : launch32(cs_bulk32_kernel<8, 0>, 8);
                     if (r32 != CSK_EUNSUPPORTED) return r32;
                 }
+            }
+            if (code == nullptr) {   // hash plan on a path without an on-the-fly kernel
+                const csk_status es = ensure_codes(plan, st);
+                if (es != CSK_OK) return es;
+                code = reinterpret_cast<const uint32_t*>(plan->code) + row_begin;
             }
             auto launch = [&](auto cfg) -> csk_status {
                 using C = decltype(cfg);
@@ -1290,6 +1340,10 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
     tma = tma && !std::getenv("CSK_NO_TMA") && (n == 0 || b == nullptr ||
                                                (const char*)b == (const char*)A + (size_t)n * lda * esz);
     tma = tma && ((uintptr_t)base & 15) == 0 && (ncols == 1 || ((lda * (int64_t)esz) & 15) == 0);
+    if (tma && plan->code == nullptr) {   // hash plan: the TMA kernels read codes
+        const csk_status es = ensure_codes(plan, st);
+        if (es != CSK_OK) return es;
+    }
     tma = tma && (((uintptr_t)(plan->code + row_begin)) & 15) == 0 && tensor_map_encoder() != nullptr;
     if (variant == CSK_VAR_TMA_ROW && !tma) variant = CSK_VAR_ATOMIC_ROW;
 

@@ -68,7 +68,8 @@ struct csk_plan_s {
     uint64_t seed = 0;
     int device = -1;
     bool from_arrays = false;
-    int32_t* code = nullptr;      // d codes: bucket | sign << 31
+    int32_t* code = nullptr;      // d codes: bucket | sign << 31 (NULL for a CSK_PLAN_HASH plan until needed)
+    bool hash = false;            // CSK_PLAN_HASH: kernels may hash rows on the fly
     int64_t* offsets = nullptr;   // k1 + 1 (CSK_PLAN_SORT)
     int32_t* perm = nullptr;      // d      (CSK_PLAN_SORT)
     std::mutex mu;                // guards the Gaussian caches
@@ -101,6 +102,16 @@ __host__ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
     return c;
 }
 
+// code of GLOBAL row g (R3): word g & 3 of Philox(ctr = (lo32(g>>2), hi32(g>>2), 0, 0), key = seed),
+// bucket = mulhi(w, k1), sign bit = w & 1 -- the same function codes_kernel stores
+__device__ __forceinline__ uint4 hash_block(uint64_t g, uint32_t key0, uint32_t key1) {
+    const uint64_t q = g >> 2;
+    return philox4x32_10(make_uint4((uint32_t)q, (uint32_t)(q >> 32), 0u, 0u), make_uint2(key0, key1));
+}
+__device__ __forceinline__ uint32_t code_from_word(uint32_t w, uint32_t k1) {
+    return __umulhi(w, k1) | ((w & 1u) << 31);
+}
+
 // code word: bucket in bits 0..30, sign (1 = negative) in bit 31
 __host__ __device__ __forceinline__ uint32_t code_bucket(uint32_t code) { return code & 0x7fffffffu; }
 __host__ __device__ __forceinline__ uint64_t code_sign_mask64(uint32_t code) {
@@ -127,6 +138,9 @@ struct Cols {
     int n;
     __device__ __forceinline__ const T* col(int c) const { return c < n ? A + (int64_t)c * lda : b; }
 };
+
+// plan.cu: materialise the codes of a CSK_PLAN_HASH plan (no-op when present)
+csk_status ensure_codes(csk_plan_t plan, cudaStream_t st);
 
 // mbarrier + 1-D bulk copy (TMA) helpers, shared by the CountSketch and SRHT kernels
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {

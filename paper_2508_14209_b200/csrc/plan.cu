@@ -262,14 +262,17 @@ static csk_status alloc_plan(int64_t d, int64_t k1, uint32_t flags, csk_plan_t* 
     *out = nullptr;
     CSK_REQUIRE(d >= 1 && d <= 2147483647LL, CSK_EINVAL, "d=%lld must be in [1, 2^31-1]", (long long)d);
     CSK_REQUIRE(k1 >= 1 && k1 <= 2147483647LL, CSK_EINVAL, "k1=%lld must be in [1, 2^31-1]", (long long)k1);
-    CSK_REQUIRE((flags & ~CSK_PLAN_SORT) == 0, CSK_EINVAL, "unknown plan flags 0x%x", flags);
+    CSK_REQUIRE((flags & ~(CSK_PLAN_SORT | CSK_PLAN_HASH)) == 0, CSK_EINVAL, "unknown plan flags 0x%x", flags);
     csk_plan_t plan = new (std::nothrow) csk_plan_s();
     CSK_REQUIRE(plan != nullptr, CSK_ENOMEM, "plan allocation failed");
     plan->d = d;
     plan->k1 = k1;
     cudaGetDevice(&plan->device);
     // codes are padded by 32 zero entries: 64/128-B bulk copies of a tile's codes never read past the end
-    if (cudaMalloc(&plan->code, (d + 32) * 4) != cudaSuccess || cudaMemset(plan->code + d, 0, 32 * 4) != cudaSuccess ||
+    const bool hash = (flags & CSK_PLAN_HASH) && !(flags & CSK_PLAN_SORT);
+    plan->hash = hash;
+    if ((!hash && (cudaMalloc(&plan->code, (d + 32) * 4) != cudaSuccess ||
+                   cudaMemset(plan->code + d, 0, 32 * 4) != cudaSuccess)) ||
         ((flags & CSK_PLAN_SORT) &&
          (cudaMalloc(&plan->offsets, (k1 + 1) * 8) != cudaSuccess || cudaMalloc(&plan->perm, d * 4) != cudaSuccess))) {
         cudaGetLastError();
@@ -278,6 +281,21 @@ static csk_status alloc_plan(int64_t d, int64_t k1, uint32_t flags, csk_plan_t* 
         return CSK_ENOMEM;
     }
     *plan_out = plan;
+    return CSK_OK;
+}
+
+csk_status ensure_codes(csk_plan_t plan, cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(plan->mu);
+    if (plan->code != nullptr) return CSK_OK;
+    int32_t* code = nullptr;
+    CSK_CUDA_TRY(cudaMalloc(&code, (plan->d + 32) * 4));
+    CSK_CUDA_TRY(cudaMemsetAsync(code + plan->d, 0, 32 * 4, st));
+    const int64_t blocks4 = ceil_div(ceil_div(plan->d + 3, 4) + 1, 256);
+    const unsigned grid = (unsigned)std::min<int64_t>(blocks4, 65535 * 4);
+    codes_kernel<<<grid, 256, 0, st>>>(code, plan->d, (uint32_t)plan->k1, (uint32_t)plan->seed,
+                                       (uint32_t)(plan->seed >> 32), plan->row0);
+    CSK_LAUNCH_CHECK();
+    plan->code = code;
     return CSK_OK;
 }
 
@@ -296,14 +314,16 @@ csk_status cs_plan(int64_t d, int64_t k1, uint64_t seed, int64_t row0, uint32_t 
     plan->seed = seed;
     plan->row0 = row0;
     cudaStream_t st = (cudaStream_t)stream;
-    const int64_t blocks4 = ceil_div(ceil_div(d + 3, 4) + 1, 256);
-    const unsigned grid = (unsigned)std::min<int64_t>(blocks4, 65535 * 4);
-    codes_kernel<<<grid, 256, 0, st>>>(plan->code, d, (uint32_t)k1, (uint32_t)seed, (uint32_t)(seed >> 32), row0);
-    count_launch();
-    if (cudaGetLastError() != cudaSuccess) {
-        set_error("codes_kernel launch failed");
-        cs_plan_destroy(plan);
-        return CSK_ECUDA;
+    if (!plan->hash) {
+        const int64_t blocks4 = ceil_div(ceil_div(d + 3, 4) + 1, 256);
+        const unsigned grid = (unsigned)std::min<int64_t>(blocks4, 65535 * 4);
+        codes_kernel<<<grid, 256, 0, st>>>(plan->code, d, (uint32_t)k1, (uint32_t)seed, (uint32_t)(seed >> 32), row0);
+        count_launch();
+        if (cudaGetLastError() != cudaSuccess) {
+            set_error("codes_kernel launch failed");
+            cs_plan_destroy(plan);
+            return CSK_ECUDA;
+        }
     }
     if (flags & CSK_PLAN_SORT) {
         s = build_sort(plan, st);
@@ -351,8 +371,13 @@ csk_status cs_plan_from_arrays(int64_t d, int64_t k1, const int32_t* h, const in
     return CSK_OK;
 }
 
+
 csk_status cs_plan_export(csk_plan_t plan, int32_t* code, int64_t* offsets, int32_t* perm, void* stream) {
     CSK_REQUIRE(plan != nullptr, CSK_EINVAL, "plan is NULL");
+    if (code) {
+        const csk_status es = csk::ensure_codes(plan, (cudaStream_t)stream);
+        if (es != CSK_OK) return es;
+    }
     CSK_REQUIRE((offsets == nullptr && perm == nullptr) || plan->perm != nullptr, CSK_EUNSUPPORTED,
                 "plan was built without CSK_PLAN_SORT");
     cudaStream_t st = (cudaStream_t)stream;

@@ -485,3 +485,50 @@ def test_cs_apply_fp32_accumulation(monkeypatch, acc, d, n, with_b, k1, off):
     Ai = synth.integer_matrix(d, n, seed=6, dtype=np.float32)
     got = host(csk.cs_apply(plan, gpu_colmajor(Ai)))
     assert np.array_equal(got.astype(np.float64), oracle.cs_apply(h, s, Ai, k1))
+
+
+# ------------------------------------------------ CSK_PLAN_HASH (codes hashed on the fly)
+@pytest.mark.parametrize("d,n,with_b,k1,row0", [(100003, 64, True, 8192, 0), (4099, 100, False, 777, 5),
+                                                (77777, 128, True, 4096, (1 << 33) + 3), (5000, 300, True, 65536, 1),
+                                                (31, 3, False, 7, 2), (1 << 20, 20, True, 1 << 17, 0)])
+def test_hash_plan_matches_oracle(d, n, with_b, k1, row0):
+    # the on-the-fly kernel (wide rows, narrow chunk-major slices, ragged tails, unaligned row0)
+    plan = csk.cs_plan(d, k1, 7, row0=row0, hash=True)
+    h, s = oracle.codes(d, k1, 7, row0)
+    A = synth.gaussian_matrix(d, n, seed=4)
+    b = synth.rhs(A, "hard", seed=4) if with_b else None
+    _check_apply(plan, h, s, A, b, "B")
+    Ai = synth.integer_matrix(d, n, seed=8)
+    got = host(csk.cs_apply(plan, gpu_colmajor(Ai)))
+    assert np.array_equal(got, oracle.cs_apply(h, s, Ai, k1))
+
+
+def test_hash_plan_materialises_codes_for_other_consumers():
+    d, n, k1 = 20011, 9, 1000
+    A = synth.integer_matrix(d, n, seed=2)
+    h, s = oracle.codes(d, k1, 3, 11)
+    exp = oracle.cs_apply(h, s, A, k1)
+    for variant in ["L", "T", "S", "X", "auto"]:   # each a fresh hash plan: the first use builds the codes
+        plan = csk.cs_plan(d, k1, 3, row0=11, hash=True)
+        assert np.array_equal(host(csk.cs_apply(plan, gpu_colmajor(A), variant=variant)), exp)
+    plan = csk.cs_plan(d, k1, 3, row0=11, hash=True)
+    code, _, _ = plan.export()
+    hh, ss = unpack(code)
+    assert np.array_equal(hh, h) and np.array_equal(ss, s)
+    # fp32 input and odd lda (no 16-B loads) also go through the stored codes
+    plan = csk.cs_plan(d, k1, 3, row0=11, hash=True)
+    got = host(csk.cs_apply(plan, gpu_colmajor(A.astype(np.float32))))
+    assert np.array_equal(got.astype(np.float64), exp)
+
+
+def test_hash_plan_ms_lstsq_matches_stored_codes():
+    d, n, k2 = 1 << 16, 16, 32
+    k1 = 2 * n * n
+    A = synth.ill_conditioned(d, n, 1e6, seed=3)
+    b = synth.rhs(A, "hard", seed=3)
+    x0, r0 = csk.ms_lstsq(csk.cs_plan(d, k1, 5), k2, gpu_colmajor(A), gpu_colmajor(b))
+    x1, r1 = csk.ms_lstsq(csk.cs_plan(d, k1, 5, hash=True), k2, gpu_colmajor(A), gpu_colmajor(b))
+    # same codes; the reduction order is not deterministic, so within the LS tolerance (R16)
+    nb = np.linalg.norm(b)
+    assert np.linalg.norm(A @ (host(x0) - host(x1))) / nb <= 1e-8
+    assert abs(r0 - r1) <= 1e-8 * nb
