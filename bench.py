@@ -340,14 +340,24 @@ def bench_ours(args, cfg):
 
     SA_ws = synth.colmajor_empty(torch, k1, ncols, torch.float64, dev)
 
-    def step():
+    # a7's numerical status and sketched residual stay on the device (ms_solve_async): one slot per
+    # step, all checked after the timed region, so no step drains the GPU with a host sync
+    st_buf = torch.zeros(max(args.steps, args.warmup, 1), dtype=torch.int32, device=dev)
+    rs_buf = torch.zeros(max(args.steps, args.warmup, 1), dtype=torch.float64, device=dev)
+
+    def step(i=0):
         if args.cs_only:                                 # kernel experiments: the CountSketch alone
             csk.cs_apply(plan, A, b=b, SA=SA_ws)
-            return 0.0
+            return
         csk.ms_apply(plan, k2, A, b=b, Z=Z)
         if ws > 1:
             dist.all_reduce(Z.t())                       # a6: NCCL over NVLink (contiguous view of Z)
-        return csk.ms_solve(Z, n, x=x)[1]               # a7 (synchronises: numerical status)
+        csk.ms_solve_async(Z, n, x=x, status=st_buf[i:i + 1], sk_resid=rs_buf[i:i + 1])   # a7
+
+    def check_status(what, count):
+        bad = int((st_buf[:count] != 0).sum().item())
+        if bad:
+            raise RuntimeError(f"{what}: {bad} step(s) returned a singular sketched R")
 
     def barrier():
         if ws > 1:
@@ -361,9 +371,11 @@ def bench_ours(args, cfg):
         dist.all_reduce(t_, op=dist.ReduceOp.MAX)
         return float(t_.item())
 
-    for _ in range(args.warmup):
-        step()
+    for i in range(args.warmup):
+        step(i)
     barrier()
+    check_status("warm-up", args.warmup)
+    st_buf.fill_(-1)
     clocks = ClockSampler(local)
     csk.launch_count(reset=True)
     # the dominant kernel (cs_apply main kernel) is timed inside the timed region: the library
@@ -378,11 +390,13 @@ def bench_ours(args, cfg):
         ev0.record(stream)
         for i in range(args.steps):
             step_ev[i][0].record(stream)
-            step()
+            step(i)
             step_ev[i][1].record(stream)
         ev1.record(stream)
         barrier()
         torch.cuda.nvtx.range_pop()
+    if not args.cs_only:
+        check_status("timed steps", args.steps)   # every slot written (-1 = not run) and OK
     launches = csk.launch_count() // max(1, args.steps) * args.steps
     step_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     value = ws * bytes_step / (step_ms * 1e-3) / 1e9

@@ -23,7 +23,7 @@
  *      variant not applicable to this plan/shape ......... CSK_EUNSUPPORTED
  *  - cs_plan*, cs_apply and ms_apply are asynchronous on the stream.
  *    ms_solve, ms_lstsq and ne_lstsq synchronise the stream before returning
- *    (they report a numerical status).
+ *    (they report a numerical status); ms_solve_async leaves it on the device.
  */
 #ifndef CSK_H
 #define CSK_H
@@ -141,6 +141,18 @@ csk_status ms_apply(csk_plan_t plan, int64_t k2, csk_dtype dtype, int64_t n, con
  * Synchronises the stream. */
 csk_status ms_solve(int64_t k2, int64_t n, const double* Z, int64_t ldz, double* x,
                     double* sk_resid, void* stream);
+
+/* ms_solve_async: ms_solve without the host synchronisation, for pipelined
+ * callers (one solve per batch, status checked later).  Same arithmetic and
+ * launches as ms_solve.
+ *   x         device pointer, n doubles
+ *   sk_resid  DEVICE pointer or NULL: receives |R[n,n]|
+ *   status    DEVICE pointer to one int32: receives CSK_OK or CSK_ESINGULAR
+ *             (the numerical status ms_solve would return), stream-ordered
+ * Returns CSK_OK once the work is enqueued (argument and launch errors are
+ * returned immediately); asynchronous on the stream. */
+csk_status ms_solve_async(int64_t k2, int64_t n, const double* Z, int64_t ldz, double* x,
+                          double* sk_resid, int32_t* status, void* stream);
 
 /* ms_lstsq: multisketched sketch-and-solve least squares min ||G S (A x - b)||
  * (Alg 1 with S := G S1; "multisketch" bars of Fig 5):

@@ -67,6 +67,7 @@ def lib():
                 "cs_apply": [P, I32, I64, P, I64, P, P, I64, I32, P],
                 "ms_apply": [P, I64, I32, I64, P, I64, P, P, I64, P],
                 "ms_solve": [I64, I64, P, I64, P, P, P],
+                "ms_solve_async": [I64, I64, P, I64, P, P, P, P],
                 "ms_lstsq": [P, I64, I64, P, I64, P, P, P, P],
                 "ne_lstsq": [I64, I64, P, I64, P, P, P],
                 "rc_lstsq": [P, I64, I64, P, I64, P, P, P, I64, P],
@@ -264,6 +265,22 @@ def ms_solve(Z, n: int, x=None, stream=None):
     _check(lib().ms_solve(Z.shape[0], n, pZ, ldz, ctypes.c_void_p(x.data_ptr()), ctypes.byref(r),
                           _stream(stream, Z.device)), "ms_solve")
     return x, r.value
+
+
+def ms_solve_async(Z, n: int, x=None, status=None, sk_resid=None, stream=None):
+    """ms_solve without the host sync: (x, status, sk_resid) as device tensors (int32, fp64)."""
+    torch = _torch()
+    if x is None:
+        x = torch.empty(n, dtype=torch.float64, device=Z.device)
+    if status is None:
+        status = torch.empty(1, dtype=torch.int32, device=Z.device)
+    if sk_resid is None:
+        sk_resid = torch.empty(1, dtype=torch.float64, device=Z.device)
+    pZ, ldz = _colmajor(Z, "Z")
+    _check(lib().ms_solve_async(Z.shape[0], n, pZ, ldz, ctypes.c_void_p(x.data_ptr()),
+                                ctypes.c_void_p(sk_resid.data_ptr()), ctypes.c_void_p(status.data_ptr()),
+                                _stream(stream, Z.device)), "ms_solve_async")
+    return x, status, sk_resid
 
 
 def ms_lstsq(plan: Plan, k2: int, A, b, x=None, stream=None):

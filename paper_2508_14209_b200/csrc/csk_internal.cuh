@@ -201,7 +201,8 @@ size_t qr_wy_scratch_doubles(int m, int nc);
 csk_status ms_apply_impl(csk_plan_t plan, int64_t k2, csk_dtype dtype, int64_t n, const void* A, int64_t lda,
                          const void* b, void* Z, int64_t ldz, cudaStream_t st);
 csk_status solve_impl(int64_t k2, int64_t n, const double* Z, int64_t ldz, double* x, double* sk_resid,
-                      cudaStream_t st, bool x_host, double* R_out);
+                      cudaStream_t st, bool x_host, double* R_out,
+                      int32_t* status_dev = nullptr, double* resid_dev = nullptr);
 csk_status blas_handle(cudaStream_t st, cublasHandle_t* out);
 // multisketch.cu: N(0,1) pairs of Philox stream 1 divided by div, starting at pair t_off
 template <typename T>

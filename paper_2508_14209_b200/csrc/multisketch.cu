@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(kQrcThreads, 1) qr_cluster_kernel(const double
 }
 
 csk_status solve_impl(int64_t k2, int64_t n, const double* Z, int64_t ldz, double* x, double* sk_resid,
-                      cudaStream_t st, bool x_host, double* R_out) {
+                      cudaStream_t st, bool x_host, double* R_out, int32_t* status_dev, double* resid_dev) {
     CSK_REQUIRE(Z != nullptr && x != nullptr, CSK_EINVAL, "Z and x must be non-NULL");
     CSK_REQUIRE(n >= 1 && n <= 65535, CSK_EINVAL, "n=%lld must be in [1, 65535]", (long long)n);
     CSK_REQUIRE(k2 >= n + 1, CSK_ESHAPE, "k2=%lld must be >= n+1=%lld", (long long)k2, (long long)(n + 1));
@@ -509,6 +509,13 @@ csk_status solve_impl(int64_t k2, int64_t n, const double* Z, int64_t ldz, doubl
     }
     }
 launched:
+    if (status_dev) {   // asynchronous form (ms_solve_async): the status stays on the device, no sync
+        CSK_CUDA_TRY(cudaMemcpyAsync(status_dev, &sd->status, sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+        if (resid_dev)
+            CSK_CUDA_TRY(cudaMemcpyAsync(resid_dev, &sd->sk_resid, sizeof(double), cudaMemcpyDeviceToDevice, st));
+        CSK_CUDA_TRY(cudaFreeAsync(W, st));
+        return CSK_OK;
+    }
     SolveStatus hs;
     CSK_CUDA_TRY(cudaMemcpyAsync(&hs, sd, sizeof(hs), cudaMemcpyDeviceToHost, st));
     if (x_host) CSK_CUDA_TRY(cudaMemcpyAsync(x, xd, n * 8, cudaMemcpyDeviceToHost, st));
@@ -620,6 +627,14 @@ csk_status ms_apply(csk_plan_t plan, int64_t k2, csk_dtype dtype, int64_t n, con
 csk_status ms_solve(int64_t k2, int64_t n, const double* Z, int64_t ldz, double* x, double* sk_resid, void* stream) {
     CSK_REQUIRE(x == nullptr || is_device_pointer(x), CSK_EINVAL, "x must be a device pointer");
     return solve_impl(k2, n, Z, ldz, x, sk_resid, (cudaStream_t)stream, false, nullptr);
+}
+
+csk_status ms_solve_async(int64_t k2, int64_t n, const double* Z, int64_t ldz, double* x, double* sk_resid,
+                          int32_t* status, void* stream) {
+    CSK_REQUIRE(x == nullptr || is_device_pointer(x), CSK_EINVAL, "x must be a device pointer");
+    CSK_REQUIRE(status != nullptr && is_device_pointer(status), CSK_EINVAL, "status must be a device pointer");
+    CSK_REQUIRE(sk_resid == nullptr || is_device_pointer(sk_resid), CSK_EINVAL, "sk_resid must be a device pointer");
+    return solve_impl(k2, n, Z, ldz, x, nullptr, (cudaStream_t)stream, false, nullptr, status, sk_resid);
 }
 
 csk_status ms_lstsq(csk_plan_t plan, int64_t k2, int64_t n, const double* A, int64_t lda, const double* b, double* x,

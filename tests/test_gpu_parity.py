@@ -337,6 +337,27 @@ def test_ms_solve_singular(solver_env):
     assert e.value.status == csk.csk.ESINGULAR
 
 
+def test_ms_solve_async_matches_oracle_and_reports_status(solver_env):
+    # the asynchronous form: same launches, the status and |R_nn| left on the device
+    rng = np.random.default_rng(8)
+    for m, n in [(128, 64), (256, 128), (40, 3), (512, 256)]:
+        Z = rng.standard_normal((m, n + 1))
+        x, st, r = csk.ms_solve_async(gpu_colmajor(Z), n)
+        torch.cuda.synchronize()
+        xo, ro = oracle.sketch_solve(Z, n)
+        assert int(st.item()) == csk.csk.OK
+        assert np.linalg.norm(Z[:, :n] @ (host(x) - xo)) <= 1e-12 * np.linalg.norm(Z[:, n]), (m, n)
+        assert abs(float(r.item()) - ro) <= 1e-12 * np.linalg.norm(Z[:, n]), (m, n)
+    Z = np.zeros((10, 4))
+    Z[:, 0] = 1.0
+    Z[:, 3] = 1.0
+    _, st, _ = csk.ms_solve_async(gpu_colmajor(Z), 3)
+    assert int(st.item()) == csk.csk.ESINGULAR
+    with pytest.raises(csk.CskError) as e:   # the status must live on the device
+        csk.ms_solve_async(gpu_colmajor(Z), 3, status=torch.zeros(1, dtype=torch.int32))
+    assert e.value.status == csk.csk.EINVAL
+
+
 @pytest.mark.parametrize("kappa", [1e2, 1e10])
 @pytest.mark.parametrize("mode", ["easy", "hard", "consistent"])
 def test_ms_lstsq_matches_oracle(kappa, mode):
