@@ -8,6 +8,7 @@
 //          (Alg 1 lines 2-3; GeQRF + OrMQR + TRSV of P:L230).
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <vector>
 
 #include <cooperative_groups.h>
@@ -121,6 +122,92 @@ csk_status gauss_get(csk_plan_t plan, int64_t k2, csk_dtype dtype, cudaStream_t 
 
 template __global__ void gauss_kernel<double>(double*, int64_t, double, uint32_t, uint32_t, int64_t);
 template __global__ void gauss_kernel<float>(float*, int64_t, double, uint32_t, uint32_t, int64_t);
+
+// ------------------------------------------------------------ a5: split-K G-stage (fp64 DMMA)
+// Z[:, chunk] = G · SA[:, chunk] for k2 <= 256 (C2, C4, C5).  The output is only k2 x nc
+// (128 x 65 at C2), so cuBLAS runs it on a handful of CTAs (54 us at C2, 0.13 GFLOP); here every SM
+// takes a K-slice of k1: CTA s computes the full k2 x nc partial of G[:, K_s] · SA^T[K_s, :]^T with
+// mma.sync m8n8k4 f64 (warp w owns m-tiles w, w+8, ..; 9 n-tiles = 72 >= nc columns), reading
+// G (column-major, ld k2) and the row-major SA^T chunk (ld lc) straight from L2; the partials are
+// summed in fixed slice order by gs_reduce_kernel (deterministic, like the GEMM it replaces).
+constexpr int kGsWarps = 8, kGsNT = 9;
+
+__device__ __forceinline__ void gs_dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+template <int MT>
+__global__ void __launch_bounds__(kGsWarps * 32) gs_splitk_kernel(const double* __restrict__ G, int k2, int64_t k1,
+                                                                   const double* __restrict__ Bt, int64_t lc, int nc,
+                                                                   int64_t kslice, double* __restrict__ part) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int64_t kb = blockIdx.x * kslice, ke = min(k1, kb + kslice);
+    double acc[MT][kGsNT][2];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < kGsNT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    int rows[MT];
+#pragma unroll
+    for (int i = 0; i < MT; ++i) rows[i] = (w + kGsWarps * i) * 8 + g;
+#pragma unroll 2
+    for (int64_t k = kb; k < ke; k += 4) {
+        const int64_t kk = k + t;   // A[g][t] = G[row, kk], B[t][g] = SA[kk, col]
+        const bool kv = kk < ke;
+        const int64_t kc = kv ? kk : kb;   // clamped (legal) address; the value is dropped
+        double a[MT], bf[kGsNT];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+            const double v = __ldg(G + kc * k2 + min(rows[i], k2 - 1));
+            a[i] = (kv && rows[i] < k2) ? v : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < kGsNT; ++j) {
+            const int col = 8 * j + g;
+            const double v = __ldg(Bt + kc * lc + min(col, nc - 1));
+            bf[j] = (kv && col < nc) ? v : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+            for (int j = 0; j < kGsNT; ++j) gs_dmma(acc[i][j][0], acc[i][j][1], a[i], bf[j]);
+    }
+    // partial s: k2 x nc column-major (ld k2); C[g][2t], C[g][2t+1] of each 8x8 tile
+    double* P = part + (int64_t)blockIdx.x * k2 * nc;
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+        if (rows[i] >= k2) continue;
+#pragma unroll
+        for (int j = 0; j < kGsNT; ++j) {
+            const int col = 8 * j + 2 * t;
+            if (col < nc) P[(int64_t)col * k2 + rows[i]] = acc[i][j][0];
+            if (col + 1 < nc) P[(int64_t)(col + 1) * k2 + rows[i]] = acc[i][j][1];
+        }
+    }
+}
+
+// Z[r, c] = sum_s part[s][r + k2 c], s in fixed order: warp w of a block sums slices s = w mod 8
+// for 32 consecutive outputs, then the 8 warp sums are added in order w = 0..7
+__global__ void __launch_bounds__(256) gs_reduce_kernel(const double* __restrict__ part, int nsl, int k2, int nc,
+                                                        double* __restrict__ Z, int64_t ldz) {
+    __shared__ double red[8][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t o = (int64_t)blockIdx.x * 32 + lane, total = (int64_t)k2 * nc;
+    double acc = 0.0;
+    if (o < total)
+        for (int s = w; s < nsl; s += 8) acc += __ldg(part + (int64_t)s * total + o);
+    red[w][lane] = acc;
+    __syncthreads();
+    if (w == 0 && o < total) {
+        double z = red[0][lane];
+#pragma unroll
+        for (int q = 1; q < 8; ++q) z += red[q][lane];
+        Z[(o % k2) + ldz * (o / k2)] = z;
+    }
+}
 
 // ---------------------------------------------------- a3 over host inputs
 // Host A/b: stream row chunks through two device staging buffers; the copy of
@@ -565,6 +652,35 @@ csk_status ms_apply_impl(csk_plan_t plan, int64_t k2, csk_dtype dtype, int64_t n
     if (s == CSK_OK && ro.ws != nullptr) {
         const void* G = nullptr;
         s = gauss_get(plan, k2, dtype, st, &G);
+        // split-K DMMA kernel for k2 <= 256 (CSK_GSTAGE=cublas keeps the library GEMM for A/B)
+        const char* ge = std::getenv("CSK_GSTAGE");
+        const bool splitk = k2 <= 256 && ro.cw <= 8 * kGsNT && !(ge && std::strcmp(ge, "cublas") == 0);
+        if (s == CSK_OK && splitk) {
+            const int nsm = device_info().num_sms;
+            const int64_t kslice = std::max<int64_t>(4, (ceil_div(k1, (int64_t)nsm) + 3) & ~(int64_t)3);
+            const int nsl = (int)ceil_div(k1, kslice);
+            double* part = nullptr;
+            CSK_CUDA_TRY(cudaMallocAsync(&part, (size_t)nsl * k2 * ro.cw * 8, st));
+            auto kern = k2 <= 64 ? gs_splitk_kernel<1> : k2 <= 128 ? gs_splitk_kernel<2>
+                      : k2 <= 192 ? gs_splitk_kernel<3> : gs_splitk_kernel<4>;
+            for (int c0 = 0; s == CSK_OK && c0 < ro.ncols; c0 += ro.cw) {
+                const int nc = std::min(ro.cw, ro.ncols - c0);
+                const double* Bt = ro.ws + (int64_t)(c0 / ro.cw) * ro.cs;
+                kern<<<nsl, kGsWarps * 32, 0, st>>>((const double*)G, (int)k2, k1, Bt, ro.lc, nc, kslice, part);
+                count_launch();
+                gs_reduce_kernel<<<(unsigned)ceil_div((int64_t)k2 * nc, 32), 256, 0, st>>>(
+                    part, nsl, (int)k2, nc, (double*)Z + (int64_t)c0 * ldz, ldz);
+                count_launch();
+                if (cudaGetLastError() != cudaSuccess) {
+                    set_error("split-K G-stage launch failed");
+                    s = CSK_ECUDA;
+                }
+            }
+            cudaFreeAsync(part, st);
+            cudaFreeAsync(ro.ws, st);
+            cudaFreeAsync(SA, st);
+            return s;
+        }
         cublasHandle_t h;
         if (s == CSK_OK) s = blas_handle(st, &h);
         const double one = 1.0, zero = 0.0;

@@ -282,6 +282,23 @@ def test_ms_apply_matches_oracle(monkeypatch, transpose, d, n, k1, k2):
     assert_within_T(Z, Zo, Zabs, 1e-12)
 
 
+@pytest.mark.parametrize("gstage", ["splitk", "cublas"])
+@pytest.mark.parametrize("d,n,k1,k2", [(100003, 64, 8192, 128), (30011, 128, 32768, 256), (5000, 3, 18, 6),
+                                       (7001, 5, 1000, 1), (9000, 70, 4096, 65), (12000, 10, 600, 191),
+                                       (4099, 65, 777, 64), (50000, 200, 131072, 200)])
+def test_ms_apply_gstage_paths(monkeypatch, gstage, d, n, k1, k2):
+    # the split-K DMMA G-stage (k2 <= 256: K-slices per SM, fixed-order partial sum) and cuBLAS
+    monkeypatch.setenv("CSK_GSTAGE", gstage)
+    plan = csk.cs_plan(d, k1, 6)
+    A = synth.gaussian_matrix(d, n, seed=2)
+    b = synth.rhs(A, "hard", seed=2)
+    Z = host(csk.ms_apply(plan, k2, gpu_colmajor(A), b=gpu_colmajor(b)))
+    Zo, Zabs = oracle.ms_apply(A, k1, k2, seed=6, b=b, with_abs=True)
+    assert_within_T(Z, Zo, Zabs, 1e-12)
+    Z2 = host(csk.ms_apply(plan, k2, gpu_colmajor(synth.integer_matrix(d, n, seed=3))))
+    assert np.all(np.isfinite(Z2))
+
+
 # every small-solve kernel (csrc/qr_wy.cu default, forced wider clusters, and the older
 # multisketch.cu kernels kept for m > 512) against the oracle's Householder QR
 SOLVERS = {
