@@ -124,8 +124,8 @@ template __global__ void gauss_kernel<double>(double*, int64_t, double, uint32_t
 template __global__ void gauss_kernel<float>(float*, int64_t, double, uint32_t, uint32_t, int64_t);
 
 // ------------------------------------------------------------ a5: split-K G-stage (fp64 DMMA)
-// Z[:, chunk] = G · SA[:, chunk] for k2 <= 256 (C2, C4, C5).  The output is only k2 x nc
-// (128 x 65 at C2), so cuBLAS runs it on a handful of CTAs (54 us at C2, 0.13 GFLOP); here every SM
+// Z[:, chunk] = G · SA[:, chunk] for k2 <= 256 (C2, C4, C5), opt-in (CSK_GSTAGE=splitk; slower than
+// cuBLAS's own split-K GEMM).  The output is only k2 x nc (128 x 65 at C2); every SM
 // takes a K-slice of k1: CTA s computes the full k2 x nc partial of G[:, K_s] · SA^T[K_s, :]^T with
 // mma.sync m8n8k4 f64 (warp w owns m-tiles w, w+8, ..; 9 n-tiles = 72 >= nc columns), reading
 // G (column-major, ld k2) and the row-major SA^T chunk (ld lc) straight from L2; the partials are
@@ -652,9 +652,10 @@ csk_status ms_apply_impl(csk_plan_t plan, int64_t k2, csk_dtype dtype, int64_t n
     if (s == CSK_OK && ro.ws != nullptr) {
         const void* G = nullptr;
         s = gauss_get(plan, k2, dtype, st, &G);
-        // split-K DMMA kernel for k2 <= 256 (CSK_GSTAGE=cublas keeps the library GEMM for A/B)
+        // split-K DMMA kernel for k2 <= 256, opt-in (CSK_GSTAGE=splitk): cuBLAS picks split-K itself
+        // here and measured faster (ncu, C2: 11.6 + 5.9 us vs 14.7 + 7.7; C4: 115 vs 140 us), DESIGN 6.3
         const char* ge = std::getenv("CSK_GSTAGE");
-        const bool splitk = k2 <= 256 && ro.cw <= 8 * kGsNT && !(ge && std::strcmp(ge, "cublas") == 0);
+        const bool splitk = k2 <= 256 && ro.cw <= 8 * kGsNT && ge && std::strcmp(ge, "splitk") == 0;
         if (s == CSK_OK && splitk) {
             const int nsm = device_info().num_sms;
             const int64_t kslice = std::max<int64_t>(4, (ceil_div(k1, (int64_t)nsm) + 3) & ~(int64_t)3);
