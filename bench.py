@@ -345,14 +345,40 @@ def bench_ours(args, cfg):
     st_buf = torch.zeros(max(args.steps, args.warmup, 1), dtype=torch.int32, device=dev)
     rs_buf = torch.zeros(max(args.steps, args.warmup, 1), dtype=torch.float64, device=dev)
 
+    # Batches are pipelined over two streams (unless --no-pipeline): the small solve of step i (a few
+    # CTAs for ~0.1-0.6 ms) runs on its own stream while step i+1's sketch starts; Z and x are
+    # double-buffered and slot reuse waits for the solve that last read it.  Every step still runs
+    # the whole path on its own batch; the timed region ends after both streams drain.
+    pipe = not args.no_pipeline and not args.cs_only
+    s_solve = torch.cuda.Stream(device=dev) if pipe else stream
+    Zs = [Z, synth.colmajor_empty(torch, k2, ncols, torch.float64, dev)]
+    xs = [x, torch.empty(n, dtype=torch.float64, device=dev)]
+    slot_free = [None, None]
+
     def step(i=0):
         if args.cs_only:                                 # kernel experiments: the CountSketch alone
             csk.cs_apply(plan, A, b=b, SA=SA_ws)
             return
-        csk.ms_apply(plan, k2, A, b=b, Z=Z)
+        sl = i & 1 if pipe else 0
+        if slot_free[sl] is not None:
+            stream.wait_event(slot_free[sl])
+        csk.ms_apply(plan, k2, A, b=b, Z=Zs[sl])
         if ws > 1:
-            dist.all_reduce(Z.t())                       # a6: NCCL over NVLink (contiguous view of Z)
-        csk.ms_solve_async(Z, n, x=x, status=st_buf[i:i + 1], sk_resid=rs_buf[i:i + 1])   # a7
+            dist.all_reduce(Zs[sl].t())                  # a6: NCCL over NVLink (contiguous view of Z)
+        if pipe:
+            e = torch.cuda.Event()
+            e.record(stream)
+            s_solve.wait_event(e)
+        csk.ms_solve_async(Zs[sl], n, x=xs[sl], status=st_buf[i:i + 1], sk_resid=rs_buf[i:i + 1],
+                           stream=s_solve)               # a7
+        if pipe:
+            e = torch.cuda.Event()
+            e.record(s_solve)
+            slot_free[sl] = e
+
+    def join():
+        if pipe:
+            stream.wait_stream(s_solve)
 
     def check_status(what, count):
         bad = int((st_buf[:count] != 0).sum().item())
@@ -392,6 +418,7 @@ def bench_ours(args, cfg):
             step_ev[i][0].record(stream)
             step(i)
             step_ev[i][1].record(stream)
+        join()
         ev1.record(stream)
         barrier()
         torch.cuda.nvtx.range_pop()
@@ -550,6 +577,8 @@ def bench_ours(args, cfg):
     acc = {}
     if not args.cs_only:
         step()
+        join()
+        torch.cuda.synchronize()
         acc["rel_residual_ms"] = float(torch.linalg.norm(b - A @ x) / torch.linalg.norm(b))
     if ws == 1 and d * ncols * 8 <= 16e9 and not args.no_acc and not args.cs_only:
         R = torch.linalg.qr(buf, mode="r")[1]
@@ -597,6 +626,8 @@ def bench_ours(args, cfg):
         "config": {"workload": cfg["name"], "d_per_rank": d, "d_global": d_glob, "n": n, "k1": k1, "k2": k2,
                    "rhs": "b = A e + eta, eta ~ N(0, 0.01)", "variant": variant,
                    "codes": "hashed on the fly" if args.hash_plan else "stored (4 B/row)",
+                   "pipeline": ("solve of step i on a second stream, overlapping step i+1's sketch (Z, x "
+                                "double-buffered)") if pipe else "serial (one stream)",
                    "l2": "inputs (%.1f GB per rank) > 126 MB L2; no flush needed" % (bytes_step / 1e9),
                    "parallelism": f"row-partitioned dp{ws}" + (f" + {backend.upper()} all-reduce of Z" if ws > 1 else "")},
         "clocks": clocks.summary(),
@@ -890,6 +921,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--variant", default="auto", choices=["auto", "L", "T", "S", "G", "B", "X"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-pipeline", action="store_true",
+                    help="run each step's solve on the sketch stream (no overlap with the next step)")
     ap.add_argument("--hash-plan", action="store_true",
                     help="CSK_PLAN_HASH: no stored codes, the CountSketch kernel hashes rows on the fly")
     ap.add_argument("--no-cpu", action="store_true")
