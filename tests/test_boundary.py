@@ -75,3 +75,14 @@ def test_binding_arity_matches_header():
             assert len(f.argtypes) == n, (name, len(f.argtypes), n)
             checked += 1
     assert checked >= 20, checked
+
+
+def test_binding_constants_match_header():
+    # status codes, variants and plan flags the binding passes across the ABI equal csk.h's
+    hdr = open(os.path.join(ROOT, "include", "csk.h")).read()
+    flags = {m.group(1): int(m.group(2), 16) for m in re.finditer(r"#define CSK_PLAN_(\w+)\s+0x([0-9a-fA-F]+)u", hdr)}
+    assert flags.get("SORT") == csk.PLAN_SORT and flags.get("HASH") == csk.PLAN_HASH, flags
+    body = hdr[hdr.index("typedef enum {"):hdr.index("} csk_status;")]
+    status = {m.group(1): int(m.group(2)) for m in re.finditer(r"CSK_(\w+)\s*=\s*(\d+)", body)}
+    for name in ("OK", "EINVAL", "ESHAPE", "EDTYPE", "ENOMEM", "ECUDA", "ENOTPD", "ESINGULAR", "EUNSUPPORTED"):
+        assert status[name] == getattr(csk, name), name
