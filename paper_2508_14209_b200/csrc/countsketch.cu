@@ -48,6 +48,7 @@ struct RowLayout {
     // CSK_PLAN_HASH: global row of local row 0 and the Philox key (codes recomputed in the kernel)
     int64_t g0 = 0;
     uint32_t hkey0 = 0, hkey1 = 0;
+    unsigned long long* work = nullptr;   // B32 dynamic work counter (zeroed with the workspace), or static
     __host__ __device__ int64_t base(int ch, uint32_t bucket) const { return (int64_t)ch * cs + (int64_t)bucket * lc; }
 };
 
@@ -581,7 +582,21 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
     const int64_t gwarp = blockIdx.x * (int64_t)W + warp;
     const int64_t nwarps = (int64_t)gridDim.x * W;
     constexpr int kJ = kBulkMaxCols / 2;
-    for (int64_t u = gwarp; u < nunits; u += nwarps) {
+    // Work distribution: with L.work (a zeroed counter after the workspace) warps take batches of
+    // kGrab consecutive units from one atomic counter, so CTAs that start late (SMs still held by an
+    // overlapping kernel, e.g. the previous batch's solve) just take fewer units; else static
+    // round-robin.  Units are taken in increasing order either way (chunk-major slices stay hot).
+    constexpr int kGrab = 8;
+    const bool dyn = L.work != nullptr;
+    int64_t u = gwarp, uend = gwarp + 1;
+    if (dyn) {
+        unsigned long long ub = 0;
+        if (lane == 0) ub = atomicAdd(L.work, (unsigned long long)kGrab);
+        ub = __shfl_sync(0xffffffffu, ub, 0);
+        u = (int64_t)ub;
+        uend = min(u + kGrab, nunits);
+    }
+    for (; u < nunits;) {
         int64_t g;
         int ch;
         unit_coords(u, nchunks, ngroups, L.chunk_major, g, ch);
@@ -695,6 +710,18 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
             for (int rr = mix_rt; rr < kB32Rows; ++rr) {
                 const uint32_t cr = __shfl_sync(0xffffffffu, crow, rr);
                 if (r0 + rr < rows && lane < nc) red_add_f64(SAt + L.base(ch, code_bucket(cr)) + lane, tile[rr * ldtile + lane]);
+            }
+        }
+        if (++u >= uend) {
+            if (dyn) {
+                unsigned long long ub = 0;
+                if (lane == 0) ub = atomicAdd(L.work, (unsigned long long)kGrab);
+                ub = __shfl_sync(0xffffffffu, ub, 0);
+                u = (int64_t)ub;
+                uend = min(u + kGrab, nunits);
+            } else {
+                u += nwarps - 1;
+                uend = u + 1;
             }
         }
     }
@@ -1435,8 +1462,12 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
         tgt.ld = ldsa;
     }
     if (tgt.owned) {
-        CSK_CUDA_TRY(cudaMallocAsync(&tgt.buf, ws_doubles * sizeof(double), st));
-        CSK_CUDA_TRY(cudaMemsetAsync(tgt.buf, 0, ws_doubles * sizeof(double), st));
+        // + 2 doubles: the B32 kernel's work counter, zeroed by the same memset (CSK_DYN=0: static)
+        CSK_CUDA_TRY(cudaMallocAsync(&tgt.buf, (ws_doubles + 2) * sizeof(double), st));
+        CSK_CUDA_TRY(cudaMemsetAsync(tgt.buf, 0, (ws_doubles + 2) * sizeof(double), st));
+        const char* dy = std::getenv("CSK_DYN");
+        if (!(dy && std::atoi(dy) == 0))
+            L.work = reinterpret_cast<unsigned long long*>(tgt.buf + ws_doubles);
     } else if (variant != CSK_VAR_SORTED && !accumulate) {
         // zero SA (ldsa may exceed k1: clear the k1 x ncols window only)
         if (ldsa == k1) {
