@@ -1463,7 +1463,7 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
     }
     if (tgt.owned) {
         // + 2 doubles: the B32 kernel's work counter, zeroed by the same memset (CSK_DYN=0: static)
-        CSK_CUDA_TRY(cudaMallocAsync(&tgt.buf, (ws_doubles + 2) * sizeof(double), st));
+        CSK_CUDA_TRY(csk_malloc_async(&tgt.buf, (ws_doubles + 2) * sizeof(double), st));
         CSK_CUDA_TRY(cudaMemsetAsync(tgt.buf, 0, (ws_doubles + 2) * sizeof(double), st));
         const char* dy = std::getenv("CSK_DYN");
         if (!(dy && std::atoi(dy) == 0))

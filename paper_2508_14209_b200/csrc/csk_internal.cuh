@@ -57,8 +57,16 @@ struct DeviceInfo {
     int num_sms = 0;
     int smem_optin = 0;      // max dynamic smem per block (bytes)
     int l2_bytes = 0;
+    cudaMemPool_t pool = nullptr;   // the library's stream-ordered pool (plan.cu)
 };
 const DeviceInfo& device_info();   // of the current device
+
+// stream-ordered allocation from the library pool of the current device (freed with cudaFreeAsync)
+cudaError_t csk_malloc_async(void** p, size_t bytes, cudaStream_t st);
+template <typename T>
+inline cudaError_t csk_malloc_async(T** p, size_t bytes, cudaStream_t st) {
+    return csk_malloc_async(reinterpret_cast<void**>(p), bytes, st);
+}
 
 // -------------------------------------------------------------------- plan
 }  // namespace csk

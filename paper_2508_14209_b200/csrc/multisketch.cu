@@ -223,7 +223,7 @@ static csk_status sketch_host_rows(csk_plan_t plan, int64_t n, const double* A, 
     cudaStream_t cs = nullptr;
     CSK_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     for (int i = 0; i < 2; ++i) {
-        CSK_CUDA_TRY(cudaMallocAsync(&stage[i], (size_t)chunk * ncols * 8, st));
+        CSK_CUDA_TRY(csk_malloc_async(&stage[i], (size_t)chunk * ncols * 8, st));
         CSK_CUDA_TRY(cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming));
         CSK_CUDA_TRY(cudaEventCreateWithFlags(&consumed[i], cudaEventDisableTiming));
         CSK_CUDA_TRY(cudaEventRecord(consumed[i], st));
@@ -528,7 +528,7 @@ csk_status solve_impl(int64_t k2, int64_t n, const double* Z, int64_t ldz, doubl
     const size_t wbytes = (size_t)(m + 1) * nc * 8;   // >= the R of the WY path, (nc rounded to even) x nc
     const size_t scratch_bytes = qr_wy_scratch_doubles(m, nc) * 8;
     const size_t scratch_off = (wbytes + 64 + (x_host ? n * 8 : 0) + 255) & ~(size_t)255;   // 16-B vector loads
-    CSK_CUDA_TRY(cudaMallocAsync(&W, scratch_off + scratch_bytes, st));
+    CSK_CUDA_TRY(csk_malloc_async(&W, scratch_off + scratch_bytes, st));
     // R's unused (lower) part is read by 16-B block loads and by the R export: keep it defined
     CSK_CUDA_TRY(cudaMemsetAsync(W, 0, wbytes + 64, st));   // + the status struct (its padding is copied out)
     sd = reinterpret_cast<SolveStatus*>(reinterpret_cast<char*>(W) + wbytes);
@@ -641,11 +641,11 @@ csk_status ms_apply_impl(csk_plan_t plan, int64_t k2, csk_dtype dtype, int64_t n
     const bool rowmajor = dtype == CSK_F64 && !host_in && !(te && std::atoi(te) == 1);
     if (host_in) {
         CSK_REQUIRE(n == 0 || lda >= plan->d, CSK_ESHAPE, "lda < d");
-        CSK_CUDA_TRY(cudaMallocAsync(&SA, (size_t)k1 * ncols * esz, st));
+        CSK_CUDA_TRY(csk_malloc_async(&SA, (size_t)k1 * ncols * esz, st));
         CSK_CUDA_TRY(cudaMemsetAsync(SA, 0, (size_t)k1 * ncols * 8, st));
         s = sketch_host_rows(plan, n, (const double*)A, lda, (const double*)b, (double*)SA, k1, st);
     } else {
-        CSK_CUDA_TRY(cudaMallocAsync(&SA, (size_t)k1 * ncols * esz, st));
+        CSK_CUDA_TRY(csk_malloc_async(&SA, (size_t)k1 * ncols * esz, st));
         s = cs_apply_impl(plan, dtype, n, A, lda, b, SA, k1, CSK_VAR_AUTO, st, 0, plan->d, false,
                           rowmajor ? &ro : nullptr);
     }
@@ -661,7 +661,7 @@ csk_status ms_apply_impl(csk_plan_t plan, int64_t k2, csk_dtype dtype, int64_t n
             const int64_t kslice = std::max<int64_t>(4, (ceil_div(k1, (int64_t)nsm) + 3) & ~(int64_t)3);
             const int nsl = (int)ceil_div(k1, kslice);
             double* part = nullptr;
-            CSK_CUDA_TRY(cudaMallocAsync(&part, (size_t)nsl * k2 * ro.cw * 8, st));
+            CSK_CUDA_TRY(csk_malloc_async(&part, (size_t)nsl * k2 * ro.cw * 8, st));
             auto kern = k2 <= 64 ? gs_splitk_kernel<1> : k2 <= 128 ? gs_splitk_kernel<2>
                       : k2 <= 192 ? gs_splitk_kernel<3> : gs_splitk_kernel<4>;
             for (int c0 = 0; s == CSK_OK && c0 < ro.ncols; c0 += ro.cw) {
@@ -762,7 +762,7 @@ csk_status ms_lstsq(csk_plan_t plan, int64_t k2, int64_t n, const double* A, int
     CSK_REQUIRE(k2 >= n + 1, CSK_ESHAPE, "k2=%lld must be >= n+1", (long long)k2);
     cudaStream_t st = (cudaStream_t)stream;
     double* Z = nullptr;
-    CSK_CUDA_TRY(cudaMallocAsync(&Z, (size_t)k2 * (n + 1) * 8, st));
+    CSK_CUDA_TRY(csk_malloc_async(&Z, (size_t)k2 * (n + 1) * 8, st));
     csk_status s = ms_apply_impl(plan, k2, CSK_F64, n, A, lda, b, Z, k2, st);
     if (s == CSK_OK) s = solve_impl(k2, n, Z, k2, x, sk_resid, st, !is_device_pointer(x), nullptr);
     cudaFreeAsync(Z, st);

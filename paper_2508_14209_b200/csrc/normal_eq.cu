@@ -91,7 +91,7 @@ static csk_status gram_split_k(cublasHandle_t h, int64_t d, int n, const double*
     const int64_t tail = d - P * rb;
     const int64_t elems = (int64_t)nc * nc;
     double* W = nullptr;
-    CSK_CUDA_TRY(cudaMallocAsync(&W, (size_t)(P + 1) * elems * 8, st));
+    CSK_CUDA_TRY(csk_malloc_async(&W, (size_t)(P + 1) * elems * 8, st));
     CSK_CUDA_TRY(cudaMemsetAsync(W, 0, (size_t)(P + 1) * elems * 8, st));
     const double one = 1.0, zero = 0.0;
     const bool fused = b == A + (int64_t)n * lda;
@@ -141,7 +141,7 @@ extern "C" csk_status ne_lstsq(int64_t d, int64_t n, const double* A, int64_t ld
     if (s != CSK_OK) return s;
     double* C = nullptr;
     const size_t cbytes = (size_t)nc * nc * 8;
-    CSK_CUDA_TRY(cudaMallocAsync(&C, 2 * cbytes + 64, st));
+    CSK_CUDA_TRY(csk_malloc_async(&C, 2 * cbytes + 64, st));
     double* Sg = C + (size_t)nc * nc;
     int* sd = reinterpret_cast<int*>(Sg + (size_t)nc * nc);
     const double one = 1.0, zero = 0.0;

@@ -5,6 +5,7 @@
 // a2 sort : stable LSD radix sort of rows by bucket -> offsets[k1+1], perm[d]
 //   (BASELINE.json north_star form 1: "one-time integer counting-sort of h").
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -39,15 +40,39 @@ const DeviceInfo& device_info() {
     cudaDeviceGetAttribute(&info.num_sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&info.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaDeviceGetAttribute(&info.l2_bytes, cudaDevAttrL2CacheSize, dev);
-    // keep freed workspaces mapped in the stream-ordered pool: per-call cudaMallocAsync /
-    // cudaFreeAsync of SA, Z and QR workspaces must not unmap and remap pages at every sync
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    // The library's own stream-ordered pool (workspaces of SA, Z, QR, ... are cudaMallocAsync'd per
+    // call): freed blocks stay mapped (release threshold max), and a block freed on one stream is
+    // reused on another only through an event dependency the caller made, never through hidden
+    // internal dependencies or opportunistic reuse -- with those (the default pool's defaults) a
+    // two-stream pipeline (bench --pipeline) saw single steps of 9-23 ms in 5 of 10 C3/C4 runs, none
+    // in 10 runs without.  CSK_POOL_NODEP=0 restores the default behaviour.
+    {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        if (cudaMemPoolCreate(&info.pool, &props) != cudaSuccess) {
+            info.pool = nullptr;
+            cudaDeviceGetDefaultMemPool(&info.pool, dev);
+        }
+        if (info.pool) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(info.pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            const char* e = std::getenv("CSK_POOL_NODEP");
+            if (!(e && std::atoi(e) == 0)) {
+                int zero = 0;
+                cudaMemPoolSetAttribute(info.pool, cudaMemPoolReuseAllowInternalDependencies, &zero);
+                cudaMemPoolSetAttribute(info.pool, cudaMemPoolReuseAllowOpportunistic, &zero);
+            }
+        }
     }
     cudaGetLastError();
     return cache.emplace(dev, info).first->second;
+}
+
+cudaError_t csk_malloc_async(void** p, size_t bytes, cudaStream_t st) {
+    const DeviceInfo& di = device_info();
+    return di.pool ? cudaMallocFromPoolAsync(p, bytes, di.pool, st) : cudaMallocAsync(p, bytes, st);
 }
 
 bool is_device_pointer(const void* p) {
@@ -217,11 +242,11 @@ static csk_status build_sort(csk_plan_t plan, cudaStream_t st) {
     uint32_t *k_a = nullptr, *k_b = nullptr, *hist = nullptr;
     int32_t* v_b = nullptr;
     int64_t* tile_off = nullptr;
-    CSK_CUDA_TRY(cudaMallocAsync(&k_a, d * 4, st));
-    CSK_CUDA_TRY(cudaMallocAsync(&k_b, d * 4, st));
-    CSK_CUDA_TRY(cudaMallocAsync(&v_b, d * 4, st));
-    CSK_CUDA_TRY(cudaMallocAsync(&hist, 256 * ntiles * 4, st));
-    CSK_CUDA_TRY(cudaMallocAsync(&tile_off, (256 * ntiles + 1) * 8, st));
+    CSK_CUDA_TRY(csk_malloc_async(&k_a, d * 4, st));
+    CSK_CUDA_TRY(csk_malloc_async(&k_b, d * 4, st));
+    CSK_CUDA_TRY(csk_malloc_async(&v_b, d * 4, st));
+    CSK_CUDA_TRY(csk_malloc_async(&hist, 256 * ntiles * 4, st));
+    CSK_CUDA_TRY(csk_malloc_async(&tile_off, (256 * ntiles + 1) * 8, st));
     CSK_CUDA_TRY(cudaMemcpyAsync(k_a, plan->code, d * 4, cudaMemcpyDeviceToDevice, st));
     uint32_t* kin = k_a;
     uint32_t* kout = k_b;

@@ -779,7 +779,7 @@ static csk_status rc_gram_impl(int64_t d, int64_t n, const double* A, int64_t ld
     const bool fused = n <= 128 && !(pe && std::atoi(pe) == 0);
     // the fused kernels and the reduction write an nc x nc C with ld nc; copy out when ldc differs
     double* Cw = C;
-    if (ldc != nc) CSK_CUDA_TRY(cudaMallocAsync(&Cw, (size_t)nc * nc * 8, st));
+    if (ldc != nc) CSK_CUDA_TRY(csk_malloc_async(&Cw, (size_t)nc * nc * 8, st));
     CSK_CUDA_TRY(cudaMemsetAsync(Cw, 0, (size_t)nc * nc * 8, st));   // the lower part stays defined (0)
     csk_status s = CSK_OK;
     if (fused) {
@@ -792,7 +792,7 @@ static csk_status rc_gram_impl(int64_t d, int64_t n, const double* A, int64_t ld
         const int64_t tiles = ceil_div(d, kRcRows);
         const int grid = (int)std::min<int64_t>(tiles, di.num_sms);
         double* part = nullptr;
-        CSK_CUDA_TRY(cudaMallocAsync(&part, (size_t)grid * nc * nc * 8, st));
+        CSK_CUDA_TRY(csk_malloc_async(&part, (size_t)grid * nc * nc * 8, st));
         CSK_CUDA_TRY(cudaMemsetAsync(part, 0, (size_t)grid * nc * nc * 8, st));
         const char* ke = std::getenv("CSK_RC_KERNEL");   // 1 = unpipelined, 2 = 32-row pipeline (alternatives)
         const int kv = ke ? std::atoi(ke) : 0;
@@ -838,7 +838,7 @@ static csk_status rc_gram_impl(int64_t d, int64_t n, const double* A, int64_t ld
         }
         double* ws = nullptr;
         const size_t pk = (size_t)rc_r0_off(nb), wd = (size_t)nb * 96;
-        CSK_CUDA_TRY(cudaMallocAsync(&ws, (pk + wd + (size_t)mc * n) * 8, st));
+        CSK_CUDA_TRY(csk_malloc_async(&ws, (pk + wd + (size_t)mc * n) * 8, st));
         double* R0p = ws;
         double* Wd = ws + pk;
         double* Qw = Wd + wd;
@@ -876,7 +876,7 @@ static csk_status rc_gram_impl(int64_t d, int64_t n, const double* A, int64_t ld
         cublasHandle_t h;
         s = blas_handle(st, &h);
         double* Wk = nullptr;
-        if (s == CSK_OK) CSK_CUDA_TRY(cudaMallocAsync(&Wk, (size_t)mc * n * 8, st));
+        if (s == CSK_OK) CSK_CUDA_TRY(csk_malloc_async(&Wk, (size_t)mc * n * 8, st));
         const double one = 1.0, zero = 0.0;
         cublasStatus_t bs = CUBLAS_STATUS_SUCCESS;
         for (int64_t r0 = 0; s == CSK_OK && r0 < d && bs == CUBLAS_STATUS_SUCCESS; r0 += mc) {
@@ -919,7 +919,7 @@ static csk_status rc_finish_impl(int64_t n, const double* C, int64_t ldc, const 
     const int nc = (int)n + 1;
     auto pad = [](size_t cnt) { return (cnt + 31) & ~(size_t)31; };
     double* ws = nullptr;
-    CSK_CUDA_TRY(cudaMallocAsync(&ws, (2 * pad((size_t)nc * nc) + pad(nc) + 32) * 8, st));
+    CSK_CUDA_TRY(csk_malloc_async(&ws, (2 * pad((size_t)nc * nc) + pad(nc) + 32) * 8, st));
     double* Cc = ws;
     double* S = Cc + pad((size_t)nc * nc);
     double* u = S + pad((size_t)nc * nc);
@@ -949,7 +949,7 @@ static csk_status rc_r0_impl(int64_t k2, int64_t n, const double* Z, int64_t ldz
     CSK_REQUIRE(ldr0 >= n, CSK_ESHAPE, "ldr0 < n");
     const int nc = (int)n + 1;
     double* ws = nullptr;
-    CSK_CUDA_TRY(cudaMallocAsync(&ws, ((size_t)nc * nc + nc) * 8, st));
+    CSK_CUDA_TRY(csk_malloc_async(&ws, ((size_t)nc * nc + nc) * 8, st));
     csk_status s = solve_impl(k2, n, Z, ldz, ws + (size_t)nc * nc, nullptr, st, false, ws);
     if (s == CSK_OK)
         CSK_CUDA_TRY(cudaMemcpy2DAsync(R0, ldr0 * 8, ws, nc * 8, n * 8, n, cudaMemcpyDeviceToDevice, st));
@@ -973,7 +973,7 @@ static csk_status rc_impl(csk_plan_t plan, int64_t k2, int64_t n, const double* 
     const int nc = (int)n + 1;
     auto pad = [](size_t cnt) { return (cnt + 31) & ~(size_t)31; };
     double* ws = nullptr;
-    CSK_CUDA_TRY(cudaMallocAsync(&ws, (pad((size_t)k2 * nc) + 2 * pad((size_t)nc * nc)) * 8, st));
+    CSK_CUDA_TRY(csk_malloc_async(&ws, (pad((size_t)k2 * nc) + 2 * pad((size_t)nc * nc)) * 8, st));
     double* Z = ws;
     double* R0 = Z + pad((size_t)k2 * nc);      // n x n, ld nc
     double* C = R0 + pad((size_t)nc * nc);      // nc x nc

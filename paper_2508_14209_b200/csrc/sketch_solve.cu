@@ -57,7 +57,7 @@ static csk_status gs_apply_impl(int64_t d, int64_t row0, int64_t k, uint64_t see
     if (const char* e = std::getenv("CSK_GS_CHUNK")) mc = std::max<int64_t>(2, std::atoll(e));
     mc = std::min(mc, d);
     double* G = nullptr;
-    CSK_CUDA_TRY(cudaMallocAsync(&G, 2 * (size_t)k * mc * 8, st));
+    CSK_CUDA_TRY(csk_malloc_async(&G, 2 * (size_t)k * mc * 8, st));
     cudaStream_t gen = nullptr;
     cudaEvent_t ev[5] = {};
     CSK_CUDA_TRY(cudaStreamCreateWithFlags(&gen, cudaStreamNonBlocking));
@@ -120,7 +120,7 @@ static csk_status msh_apply_impl(csk_plan_t plan, int64_t k2, int64_t n, const d
     CSK_REQUIRE((k1 & (k1 - 1)) == 0, CSK_ESHAPE, "Count+SRHT needs k1=%lld a power of two", (long long)k1);
     CSK_REQUIRE(ncols >= 1 && Z != nullptr, CSK_EINVAL, "bad arguments");
     double* SA = nullptr;
-    CSK_CUDA_TRY(cudaMallocAsync(&SA, (size_t)k1 * ncols * 8, st));
+    CSK_CUDA_TRY(csk_malloc_async(&SA, (size_t)k1 * ncols * 8, st));
     csk_status s = cs_apply_impl(plan, CSK_F64, n, A, lda, b, SA, k1, CSK_VAR_AUTO, st, 0, plan->d, false);
     if (s == CSK_OK) s = srht_impl(k1, k1, 0, k2, plan->seed, ncols, SA, k1, nullptr, Z, ldz, st);
     cudaFreeAsync(SA, st);
@@ -149,7 +149,7 @@ static csk_status cs_lstsq_impl(csk_plan_t plan, int64_t n, const double* A, int
     auto pad = [](size_t c) { return (c + 31) & ~(size_t)31; };
     const size_t total = pad((size_t)k1 * nc) + pad(nc) + pad(nc) + pad((size_t)lwork) + 32;
     double* ws = nullptr;
-    CSK_CUDA_TRY(cudaMallocAsync(&ws, total * 8, st));
+    CSK_CUDA_TRY(csk_malloc_async(&ws, total * 8, st));
     double* SA = ws;
     double* tau = SA + pad((size_t)k1 * nc);
     double* dg = tau + pad(nc);
@@ -193,7 +193,7 @@ static csk_status sketch_then_solve(int64_t k, int64_t n, double* x, double* sk_
     CSK_REQUIRE(x != nullptr && n >= 1, CSK_EINVAL, "x NULL or n < 1");
     CSK_REQUIRE(k >= n + 1, CSK_ESHAPE, "k=%lld must be >= n+1", (long long)k);
     double* Z = nullptr;
-    CSK_CUDA_TRY(cudaMallocAsync(&Z, (size_t)k * (n + 1) * 8, st));
+    CSK_CUDA_TRY(csk_malloc_async(&Z, (size_t)k * (n + 1) * 8, st));
     csk_status s = apply(Z);
     if (s == CSK_OK) s = solve_impl(k, n, Z, k, x, sk_resid, st, !is_device_pointer(x), nullptr);
     cudaFreeAsync(Z, st);

@@ -639,7 +639,7 @@ csk_status srht_impl(int64_t d, int64_t dglob, int64_t row0, int64_t k, uint64_t
                 "srht_apply takes device pointers");
     const int64_t nwords = (d + 31) / 32;
     uint32_t* ws = nullptr;
-    CSK_CUDA_TRY(cudaMallocAsync(&ws, (size_t)(nwords + k) * 4, st));
+    CSK_CUDA_TRY(csk_malloc_async(&ws, (size_t)(nwords + k) * 4, st));
     uint32_t* dbits = ws;
     uint32_t* psamp = ws + nwords;
     const uint32_t key0 = (uint32_t)seed, key1 = (uint32_t)(seed >> 32);
