@@ -345,11 +345,11 @@ def bench_ours(args, cfg):
     st_buf = torch.zeros(max(args.steps, args.warmup, 1), dtype=torch.int32, device=dev)
     rs_buf = torch.zeros(max(args.steps, args.warmup, 1), dtype=torch.float64, device=dev)
 
-    # With --pipeline, batches are pipelined over two streams: the small solve of step i (a few
+    # Batches are pipelined over two streams (unless --no-pipeline): the small solve of step i (a few
     # CTAs for ~0.1-0.6 ms) runs on its own stream while step i+1's sketch starts; Z and x are
     # double-buffered and slot reuse waits for the solve that last read it.  Every step still runs
     # the whole path on its own batch; the timed region ends after both streams drain.
-    pipe = args.pipeline and not args.cs_only
+    pipe = not args.no_pipeline and not args.cs_only
     prio = int(os.environ.get("CSK_SOLVE_PRIO", "0"))   # experiment: solve-stream priority
     host_bound = os.environ.get("CSK_HOST_BOUND", "1") != "0"   # experiment: unbounded host run-ahead
     s_solve = torch.cuda.Stream(device=dev, priority=prio) if pipe else stream
@@ -925,10 +925,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--variant", default="auto", choices=["auto", "L", "T", "S", "G", "B", "X"])
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--pipeline", action="store_true",
-                    help="opt-in: run step i's solve on a second stream, overlapping step i+1's sketch "
-                         "(faster median, but rare multi-ms step outliers at C3/C4; DESIGN.md 7)")
-    ap.add_argument("--no-pipeline", action="store_true", help="(default) one stream per step")
+    ap.add_argument("--pipeline", action="store_true", help="(default) step i's solve on a second stream, "
+                                                                "overlapping step i+1's sketch (DESIGN.md 7)")
+    ap.add_argument("--no-pipeline", action="store_true", help="one stream per step (serial)")
     ap.add_argument("--hash-plan", action="store_true",
                     help="CSK_PLAN_HASH: no stored codes, the CountSketch kernel hashes rows on the fly")
     ap.add_argument("--no-cpu", action="store_true")
