@@ -74,3 +74,25 @@ csk.cs_lstsq(plan, Ad, bd)
 csk.msh_lstsq(plan, 16, Ad, bd)
 torch.cuda.synchronize()
 print("gs/cs/msh lstsq done", flush=True)
+# hash plans (codes on the fly, wide and narrow-chunk kernels), the split-K G-stage, the async solve,
+# and the two-stream pipeline pattern of bench.py
+hp = csk.cs_plan(d, 128, 5, row0=3, hash=True)
+csk.cs_apply(hp, Ad, b=bd)
+csk.cs_apply(csk.cs_plan(4096, 1 << 17, 2, hash=True), cm(wide), b=cm(wide[:, 0].copy()))
+print("hash plans done", flush=True)
+env(CSK_GSTAGE="splitk")
+Zk = csk.ms_apply(plan, 16, Ad, b=bd)
+env(CSK_GSTAGE=None)
+print("split-K G-stage done", flush=True)
+s2 = torch.cuda.Stream()
+Zs = [csk.ms_apply(plan, 16, Ad, b=bd) for _ in range(2)]
+for i in range(4):
+    csk.ms_apply(plan, 16, Ad, b=bd, Z=Zs[i & 1])
+    ev = torch.cuda.Event()
+    ev.record()
+    s2.wait_event(ev)
+    x, st, r = csk.ms_solve_async(Zs[i & 1], n, stream=s2)
+    torch.cuda.current_stream().wait_stream(s2)
+torch.cuda.synchronize()
+assert int(st.item()) == 0
+print("async solve pipeline done", flush=True)
