@@ -550,6 +550,9 @@ __global__ void __launch_bounds__(C::kWarps * 32, 1) cs_bulk_kernel(const uint32
 // bulk-reduces row r.  fp64, 16-B aligned columns (lda even); the ragged last tile falls
 // back to clamped scalar loads.
 constexpr int kB32Rows = 32;
+// row r of a warp's tile: 8-row group g = r >> 3 is shifted by 2g doubles (rows never overlap, 16-B aligned)
+__device__ __forceinline__ int b32_row(int r, int ld) { return r * ld + 2 * (r >> 3); }
+constexpr int kB32Pad = 6;   // doubles per warp tile beyond 32 rows (the shift of the last group)
 
 template <int W, int EXP, bool SPLIT = false, bool PRED = false, bool MIX = false, bool HASH = false>
 __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __restrict__ code, int64_t rows,
@@ -566,11 +569,17 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
     const int cw = L.cw;
     extern __shared__ __align__(16) double b32_smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int p = lane & 15, half = lane >> 4;
-    double* tile = b32_smem + (size_t)warp * kB32Rows * ldtile;
+    // lane = 2p + half: each 16-lane phase of an 8-B STS covers 8 row pairs x both column parities,
+    // so with the row shift below its 16 lanes hit 16 distinct double-banks (one wavefront per phase);
+    // the loads cover the same 256-B column segments as any other lane order
+    const int p = lane >> 1, half = lane & 1;
+    // 8-row groups are shifted by 2 doubles each (b32_row): with ld == 2 mod 4 the row pairs of one
+    // STS otherwise land on 4 of 8 even double-banks (ncu: 75% of the shared wavefronts were
+    // conflicts)
+    double* tile = b32_smem + (size_t)warp * (kB32Rows * ldtile + kB32Pad);
     constexpr bool split = SPLIT;   // compile-time: the default kernel carries none of the split code
-    double* sb = b32_smem + (size_t)W * kB32Rows * ldtile;   // split: k1 bucket sums of column ncols
-    for (int e = lane; e < kB32Rows * ldtile; e += 32) tile[e] = 0.0;
+    double* sb = b32_smem + (size_t)W * (kB32Rows * ldtile + kB32Pad);   // split: k1 bucket sums of column ncols
+    for (int e = lane; e < kB32Rows * ldtile + kB32Pad; e += 32) tile[e] = 0.0;
     if constexpr (split) {
         for (int e = threadIdx.x; e < k1; e += blockDim.x) sb[e] = 0.0;
         __syncthreads();
@@ -661,8 +670,8 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
         // the TMA engine must have finished reading this tile (bulk ops of the previous unit)
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncwarp();
-        double* ta = tile + (2 * p) * ldtile;
-        double* tb = ta + ldtile;
+        double* ta = tile + b32_row(2 * p, ldtile);
+        double* tb = tile + b32_row(2 * p + 1, ldtile);
         const long long sa = (long long)code_sign_mask64(ca), sb = (long long)code_sign_mask64(cb);
 #pragma unroll
         for (int j = 0; j < kJ; ++j) {
@@ -681,7 +690,7 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
         if (r0 + lane < rows && !(EXP & 1) && (!MIX || lane < mix_rt)) {
             const uint32_t bytes = (uint32_t)(((nc + 1) & ~1) * 8);
             double* dst = SAt + L.base(ch, code_bucket(crow));
-            const uint32_t src = (uint32_t)__cvta_generic_to_shared(tile + lane * ldtile);
+            const uint32_t src = (uint32_t)__cvta_generic_to_shared(tile + b32_row(lane, ldtile));
             if constexpr (PRED) {
                 // narrow chunks (C3): the chunk's SA^T slice (54 MB) competes with the streamed A for
                 // L2; mark the reductions evict_last so the slice is not written back mid-pass
@@ -709,7 +718,7 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
         if constexpr (MIX) {
             for (int rr = mix_rt; rr < kB32Rows; ++rr) {
                 const uint32_t cr = __shfl_sync(0xffffffffu, crow, rr);
-                if (r0 + rr < rows && lane < nc) red_add_f64(SAt + L.base(ch, code_bucket(cr)) + lane, tile[rr * ldtile + lane]);
+                if (r0 + rr < rows && lane < nc) red_add_f64(SAt + L.base(ch, code_bucket(cr)) + lane, tile[b32_row(rr, ldtile) + lane]);
             }
         }
         if (++u >= uend) {
@@ -1185,7 +1194,7 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
                     const int nbulk = L.sep >= 0 ? ncols - 1 : ncols;   // split: the last column goes apart
                     const int64_t units32 = ceil_div(rows, kB32Rows) * ceil_div(nbulk, cw);
                     auto launch32 = [&](auto kern, int W, int mrt = 32) -> csk_status {
-                        const size_t smem = (size_t)W * kB32Rows * ld32 * sizeof(double) +
+                        const size_t smem = (size_t)W * (kB32Rows * ld32 + kB32Pad) * sizeof(double) +
                                             (L.sep >= 0 ? (size_t)plan->k1 * sizeof(double) : 0);
                         if (smem > (size_t)di.smem_optin) return CSK_EUNSUPPORTED;
                         CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1210,7 +1219,7 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
                         LH.g0 = plan->row0 + row_begin;
                         LH.hkey0 = (uint32_t)plan->seed;
                         LH.hkey1 = (uint32_t)(plan->seed >> 32);
-                        const size_t smem = (size_t)8 * kB32Rows * ld32 * sizeof(double);
+                        const size_t smem = (size_t)8 * (kB32Rows * ld32 + kB32Pad) * sizeof(double);
                         auto kern = narrow ? cs_bulk32_kernel<8, 0, false, true, false, true>
                                            : cs_bulk32_kernel<8, 0, false, false, false, true>;
                         CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
