@@ -49,6 +49,7 @@ struct RowLayout {
     int64_t g0 = 0;
     uint32_t hkey0 = 0, hkey1 = 0;
     unsigned long long* work = nullptr;   // B32 dynamic work counter (zeroed with the workspace), or static
+    int grab = 8;                         // units per counter grab (CSK_GRAB, experiment)
     __host__ __device__ int64_t base(int ch, uint32_t bucket) const { return (int64_t)ch * cs + (int64_t)bucket * lc; }
 };
 
@@ -595,7 +596,7 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
     // kGrab consecutive units from one atomic counter, so CTAs that start late (SMs still held by an
     // overlapping kernel, e.g. the previous batch's solve) just take fewer units; else static
     // round-robin.  Units are taken in increasing order either way (chunk-major slices stay hot).
-    constexpr int kGrab = 8;
+    const int kGrab = L.grab;
     const bool dyn = L.work != nullptr;
     int64_t u = gwarp, uend = gwarp + 1;
     if (dyn) {
@@ -1477,6 +1478,7 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
         const char* dy = std::getenv("CSK_DYN");
         if (!(dy && std::atoi(dy) == 0))
             L.work = reinterpret_cast<unsigned long long*>(tgt.buf + ws_doubles);
+        if (const char* g = std::getenv("CSK_GRAB")) L.grab = std::max(1, std::atoi(g));
     } else if (variant != CSK_VAR_SORTED && !accumulate) {
         // zero SA (ldsa may exceed k1: clear the k1 x ncols window only)
         if (ldsa == k1) {
