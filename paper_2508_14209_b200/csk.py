@@ -53,9 +53,7 @@ def lib():
     with _lock:
         if _lib is None:
             path = _build.LIB
-            if os.environ.get("CSK_LIB_OVERRIDE"):   # experiments: A/B against another build of the library
-                path = os.environ["CSK_LIB_OVERRIDE"]
-            elif _build.needs_build():
+            if _build.needs_build():
                 path = _build.build()
             L = ctypes.CDLL(path)
             P, I64, U64, U32, I32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int
@@ -82,8 +80,6 @@ def lib():
                 "msh_lstsq": [P, I64, I64, P, I64, P, P, P, P],
             }
             for name, argt in sigs.items():
-                if os.environ.get("CSK_LIB_OVERRIDE") and not hasattr(L, name):
-                    continue   # an older build under A/B: only its own entry points are bound
                 f = getattr(L, name)
                 f.argtypes = argt
                 f.restype = ctypes.c_int
@@ -129,7 +125,7 @@ def _colmajor(t, name):
     if t is None:
         return None, 0
     if t.dim() == 1:
-        if t.stride(0) != 1:
+        if t.stride(0) != 1 and t.shape[0] > 1:
             raise ValueError(f"{name} must be contiguous")
         return ctypes.c_void_p(t.data_ptr()), t.shape[0]
     if t.dim() != 2 or (t.stride(0) != 1 and t.shape[0] > 1):
@@ -145,6 +141,59 @@ def _dtype_code(t):
     if t.dtype == torch.float32:
         return F32
     raise TypeError(f"unsupported dtype {t.dtype}")
+
+
+# ---------------------------------------------------------------- validation
+# Every pointer handed to the library is checked here first (shape, dtype, device): the C side
+# validates sizes and leading dimensions, but it cannot see how many elements a buffer holds.
+def _need(t, name, dtype=None, rows=None, min_cols=None, cols=None, device=None, allow_host=False):
+    import torch
+    if t is None:
+        raise ValueError(f"{name} is required")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if t.dtype not in (torch.float64, torch.float32):
+        raise TypeError(f"{name}: unsupported dtype {t.dtype}")
+    if not t.is_cuda and not allow_host:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if device is not None and t.is_cuda and t.device != device:
+        raise ValueError(f"{name} is on {t.device}, expected {device}")
+    r = t.shape[0]
+    c = 1 if t.dim() == 1 else t.shape[1]
+    if rows is not None and r != rows:
+        raise ValueError(f"{name} has {r} rows, expected {rows}")
+    if cols is not None and c != cols:
+        raise ValueError(f"{name} has {c} columns, expected {cols}")
+    if min_cols is not None and c < min_cols:
+        raise ValueError(f"{name} has {c} columns, needs >= {min_cols}")
+    return t
+
+
+def _vec(t, name, n, dtype=None, device=None, allow_host=False):
+    if t is None:
+        raise ValueError(f"{name} is required")
+    if t.dim() != 1:
+        raise ValueError(f"{name} must be a vector")
+    return _need(t, name, dtype=dtype, rows=n, device=device, allow_host=allow_host)
+
+
+def _inputs(A, b, d, allow_host=False):
+    """Validate [A b] against d rows: same dtype, same device; returns (ref tensor, n, ncols)."""
+    if A is None and b is None:
+        raise ValueError("A and b cannot both be None")
+    ref = A if A is not None else b
+    if A is not None:
+        if A.dim() != 2:
+            raise ValueError("A must be a (d, n) matrix")
+        _need(A, "A", rows=d, allow_host=allow_host)
+    if b is not None:
+        _vec(b, "b", d, dtype=ref.dtype, allow_host=allow_host)
+        if A is not None and b.is_cuda != A.is_cuda:
+            raise ValueError("A and b must both be on the GPU or both on the host")
+        if A is not None and A.is_cuda and b.device != A.device:
+            raise ValueError("A and b must be on the same device")
+    n = 0 if A is None else A.shape[1]
+    return ref, n, n + (1 if b is not None else 0)
 
 
 def launch_count(reset: bool = False) -> int:
@@ -218,18 +267,13 @@ def cs_plan_from_arrays(h, s, k1: int, sort: bool = False, stream=None) -> Plan:
     return Plan(out.value, h.shape[0], k1, 0, None, sort)
 
 
-def _ncols(A, b):
-    n = 0 if A is None else (A.shape[1] if A.dim() == 2 else 1)
-    return n, n + (1 if b is not None else 0)
-
-
 def cs_apply(plan: Plan, A, b=None, SA=None, variant="auto", stream=None):
     """SA = S [A b] (k1 x ncols column-major, allocated if not given)."""
     torch = _torch()
-    ref = A if A is not None else b
-    n, ncols = _ncols(A, b)
+    ref, n, ncols = _inputs(A, b, plan.d)
     if SA is None:
         SA = torch.empty((ncols, plan.k1), dtype=ref.dtype, device=ref.device).t()
+    _need(SA, "SA", dtype=ref.dtype, rows=plan.k1, min_cols=ncols, device=ref.device)
     pA, lda = _colmajor(A, "A") if A is not None else (None, plan.d)
     pb, _ = _colmajor(b, "b")
     pS, ldsa = _colmajor(SA, "SA")
@@ -242,11 +286,11 @@ def cs_apply(plan: Plan, A, b=None, SA=None, variant="auto", stream=None):
 def ms_apply(plan: Plan, k2: int, A, b=None, Z=None, stream=None):
     """Z = G S [A b] (k2 x ncols column-major).  A, b may be CPU tensors (streamed)."""
     torch = _torch()
-    ref = A if A is not None else b
-    n, ncols = _ncols(A, b)
+    ref, n, ncols = _inputs(A, b, plan.d, allow_host=True)
     dev = ref.device if ref.is_cuda else torch.device("cuda", torch.cuda.current_device())
     if Z is None:
         Z = torch.empty((ncols, k2), dtype=ref.dtype, device=dev).t()
+    _need(Z, "Z", dtype=ref.dtype, rows=k2, min_cols=ncols, device=dev)
     pA, lda = _colmajor(A, "A") if A is not None else (None, plan.d)
     pb, _ = _colmajor(b, "b")
     pZ, ldz = _colmajor(Z, "Z")
@@ -258,8 +302,10 @@ def ms_apply(plan: Plan, k2: int, A, b=None, Z=None, stream=None):
 def ms_solve(Z, n: int, x=None, stream=None):
     """(x, sketched residual) from the augmented sketch Z = [GSA | GSb] (k2 x (n+1))."""
     torch = _torch()
+    _need(Z, "Z", dtype=torch.float64, min_cols=n + 1)
     if x is None:
         x = torch.empty(n, dtype=torch.float64, device=Z.device)
+    _vec(x, "x", n, dtype=torch.float64, device=Z.device)
     pZ, ldz = _colmajor(Z, "Z")
     r = ctypes.c_double()
     _check(lib().ms_solve(Z.shape[0], n, pZ, ldz, ctypes.c_void_p(x.data_ptr()), ctypes.byref(r),
@@ -270,12 +316,18 @@ def ms_solve(Z, n: int, x=None, stream=None):
 def ms_solve_async(Z, n: int, x=None, status=None, sk_resid=None, stream=None):
     """ms_solve without the host sync: (x, status, sk_resid) as device tensors (int32, fp64)."""
     torch = _torch()
+    _need(Z, "Z", dtype=torch.float64, min_cols=n + 1)
     if x is None:
         x = torch.empty(n, dtype=torch.float64, device=Z.device)
+    _vec(x, "x", n, dtype=torch.float64, device=Z.device)
     if status is None:
         status = torch.empty(1, dtype=torch.int32, device=Z.device)
     if sk_resid is None:
         sk_resid = torch.empty(1, dtype=torch.float64, device=Z.device)
+    if status.dtype != torch.int32 or status.numel() < 1:
+        raise TypeError("status must be an int32 tensor with >= 1 element")
+    if sk_resid.dtype != torch.float64 or sk_resid.numel() < 1:
+        raise TypeError("sk_resid must be a float64 tensor with >= 1 element")
     pZ, ldz = _colmajor(Z, "Z")
     _check(lib().ms_solve_async(Z.shape[0], n, pZ, ldz, ctypes.c_void_p(x.data_ptr()),
                                 ctypes.c_void_p(sk_resid.data_ptr()), ctypes.c_void_p(status.data_ptr()),
@@ -286,10 +338,13 @@ def ms_solve_async(Z, n: int, x=None, status=None, sk_resid=None, stream=None):
 def ms_lstsq(plan: Plan, k2: int, A, b, x=None, stream=None):
     """Multisketched sketch-and-solve: (x, sketched residual).  A, b, x may be CPU tensors."""
     torch = _torch()
+    _need(A, "A", dtype=torch.float64, rows=plan.d, allow_host=True)
+    _inputs(A, b, plan.d, allow_host=True)
     n = A.shape[1]
     dev = A.device if A.is_cuda else torch.device("cuda", torch.cuda.current_device())
     if x is None:
         x = torch.empty(n, dtype=torch.float64, device=dev if A.is_cuda else "cpu")
+    _vec(x, "x", n, dtype=torch.float64, allow_host=True)
     pA, lda = _colmajor(A, "A")
     pb, _ = _colmajor(b, "b")
     r = ctypes.c_double()
@@ -301,9 +356,12 @@ def ms_lstsq(plan: Plan, k2: int, A, b, x=None, stream=None):
 def ne_lstsq(A, b, x=None, stream=None):
     """Normal-equations least squares (cuBLAS Gram + Cholesky); raises CskError(ENOTPD) on breakdown."""
     torch = _torch()
+    _need(A, "A", dtype=torch.float64)
     d, n = A.shape
+    _inputs(A, b, d)
     if x is None:
         x = torch.empty(n, dtype=torch.float64, device=A.device)
+    _vec(x, "x", n, dtype=torch.float64, device=A.device)
     pA, lda = _colmajor(A, "A")
     pb, _ = _colmajor(b, "b")
     _check(lib().ne_lstsq(d, n, pA, lda, pb, ctypes.c_void_p(x.data_ptr()), _stream(stream, A.device)), "ne_lstsq")
@@ -313,9 +371,12 @@ def ne_lstsq(A, b, x=None, stream=None):
 def rc_lstsq(plan: Plan, k2: int, A, b, x=None, want_R: bool = False, stream=None):
     """rand_cholQR least squares (Alg 5): the true LS solution x (and R = R1 R0 if want_R)."""
     torch = _torch()
+    _need(A, "A", dtype=torch.float64, rows=plan.d)
     d, n = A.shape
+    _inputs(A, b, d)
     if x is None:
         x = torch.empty(n, dtype=torch.float64, device=A.device)
+    _vec(x, "x", n, dtype=torch.float64, device=A.device)
     R = torch.empty((n, n), dtype=torch.float64, device=A.device).t() if want_R else None
     pA, lda = _colmajor(A, "A")
     pb, _ = _colmajor(b, "b")
@@ -329,11 +390,12 @@ def srht_apply(A, k: int, seed: int, b=None, Y=None, dglob: int | None = None, r
     """SRHT Y = k^-1/2 P H D [A b] (k x ncols) of the rows [row0, row0 + d) of a dglob-row matrix."""
     torch = _torch()
     d = A.shape[0] if A is not None else b.shape[0]
-    n = A.shape[1] if A is not None else 0
-    ncols = n + (b is not None)
-    dev = A.device if A is not None else b.device
+    ref, n, ncols = _inputs(A, b, d)
+    _need(ref, "A" if A is not None else "b", dtype=torch.float64)
+    dev = ref.device
     if Y is None:
         Y = torch.empty((ncols, k), dtype=torch.float64, device=dev).t()
+    _need(Y, "Y", dtype=torch.float64, rows=k, min_cols=ncols, device=dev)
     pA, lda = _colmajor(A, "A") if A is not None else (None, max(d, 1))
     pb, _ = _colmajor(b, "b")
     pY, ldy = _colmajor(Y, "Y")
@@ -346,10 +408,12 @@ def gs_apply(A, k: int, seed: int, b=None, Z=None, row0: int = 0, stream=None):
     """Gaussian sketch Z = G [A b] (k x ncols), G k x d ~ N(0, 1/k) generated by row chunks."""
     torch = _torch()
     d = A.shape[0] if A is not None else b.shape[0]
-    n = A.shape[1] if A is not None else 0
-    dev = A.device if A is not None else b.device
+    ref, n, ncols = _inputs(A, b, d)
+    _need(ref, "A" if A is not None else "b", dtype=torch.float64)
+    dev = ref.device
     if Z is None:
-        Z = torch.empty((n + (b is not None), k), dtype=torch.float64, device=dev).t()
+        Z = torch.empty((ncols, k), dtype=torch.float64, device=dev).t()
+    _need(Z, "Z", dtype=torch.float64, rows=k, min_cols=ncols, device=dev)
     pA, lda = _colmajor(A, "A") if A is not None else (None, max(d, 1))
     pb, _ = _colmajor(b, "b")
     pZ, ldz = _colmajor(Z, "Z")
@@ -359,11 +423,23 @@ def gs_apply(A, k: int, seed: int, b=None, Z=None, row0: int = 0, stream=None):
 
 def _solve_out(n, dev, x):
     torch = _torch()
-    return torch.empty(n, dtype=torch.float64, device=dev) if x is None else x
+    x = torch.empty(n, dtype=torch.float64, device=dev) if x is None else x
+    return _vec(x, "x", n, dtype=torch.float64, device=dev)
+
+
+def _ls_inputs(A, b, d=None):
+    import torch
+    _need(A, "A", dtype=torch.float64, rows=d)
+    if A.dim() != 2:
+        raise ValueError("A must be a (d, n) matrix")
+    _inputs(A, b, A.shape[0])
+    if b is None:
+        raise ValueError("b is required")
 
 
 def gs_lstsq(A, b, k: int, seed: int, x=None, stream=None):
     """Gaussian sketch-and-solve: (x, sketched residual)."""
+    _ls_inputs(A, b)
     d, n = A.shape
     x = _solve_out(n, A.device, x)
     pA, lda = _colmajor(A, "A")
@@ -376,6 +452,7 @@ def gs_lstsq(A, b, k: int, seed: int, x=None, stream=None):
 
 def cs_lstsq(plan: Plan, A, b, x=None, stream=None):
     """CountSketch-only sketch-and-solve (GEQRF of the k1 x (n+1) sketch): (x, sketched residual)."""
+    _ls_inputs(A, b, plan.d)
     n = A.shape[1]
     x = _solve_out(n, A.device, x)
     pA, lda = _colmajor(A, "A")
@@ -389,9 +466,11 @@ def cs_lstsq(plan: Plan, A, b, x=None, stream=None):
 def msh_apply(plan: Plan, k2: int, A, b=None, Z=None, stream=None):
     """Count+SRHT multisketch Z = SRHT_k2 (S1 [A b])."""
     torch = _torch()
-    n = A.shape[1]
+    _need(A, "A", dtype=torch.float64, rows=plan.d)
+    _, n, ncols = _inputs(A, b, plan.d)
     if Z is None:
-        Z = torch.empty((n + (b is not None), k2), dtype=torch.float64, device=A.device).t()
+        Z = torch.empty((ncols, k2), dtype=torch.float64, device=A.device).t()
+    _need(Z, "Z", dtype=torch.float64, rows=k2, min_cols=ncols, device=A.device)
     pA, lda = _colmajor(A, "A")
     pb, _ = _colmajor(b, "b")
     pZ, ldz = _colmajor(Z, "Z")
@@ -401,6 +480,7 @@ def msh_apply(plan: Plan, k2: int, A, b=None, Z=None, stream=None):
 
 def msh_lstsq(plan: Plan, k2: int, A, b, x=None, stream=None):
     """Count+SRHT multisketch sketch-and-solve: (x, sketched residual)."""
+    _ls_inputs(A, b, plan.d)
     n = A.shape[1]
     x = _solve_out(n, A.device, x)
     pA, lda = _colmajor(A, "A")
@@ -414,6 +494,7 @@ def msh_lstsq(plan: Plan, k2: int, A, b, x=None, stream=None):
 def rc_r0(Z, n: int, stream=None):
     """R0 (n x n, upper) of the Householder QR of the (all-reduced) sketch Z = [GSA | GSb]."""
     torch = _torch()
+    _need(Z, "Z", dtype=torch.float64, min_cols=n + 1)
     R0 = torch.zeros((n, n), dtype=torch.float64, device=Z.device).t()
     pZ, ldz = _colmajor(Z, "Z")
     _check(lib().rc_r0(Z.shape[0], n, pZ, ldz, ctypes.c_void_p(R0.data_ptr()), n, _stream(stream, Z.device)), "rc_r0")
@@ -423,7 +504,9 @@ def rc_r0(Z, n: int, stream=None):
 def rc_gram(A, b, R0, stream=None):
     """[Q0^T Q0 | Q0^T b] ((n+1) x (n+1); upper triangle + column n) over this block's rows, Q0 = A R0^-1."""
     torch = _torch()
+    _ls_inputs(A, b)
     d, n = A.shape
+    _need(R0, "R0", dtype=torch.float64, rows=n, cols=n, device=A.device)
     C = torch.zeros((n + 1, n + 1), dtype=torch.float64, device=A.device).t()
     pA, lda = _colmajor(A, "A")
     pb, _ = _colmajor(b, "b")
@@ -437,6 +520,8 @@ def rc_finish(C, R0, want_R: bool = False, stream=None):
     """x (and R = R1 R0) from the (all-reduced) C and R0."""
     torch = _torch()
     n = R0.shape[0]
+    _need(R0, "R0", dtype=torch.float64, rows=n, cols=n)
+    _need(C, "C", dtype=torch.float64, rows=n + 1, min_cols=n + 1, device=R0.device)
     x = torch.empty(n, dtype=torch.float64, device=C.device)
     R = torch.empty((n, n), dtype=torch.float64, device=C.device).t() if want_R else None
     pC, ldc = _colmajor(C, "C")

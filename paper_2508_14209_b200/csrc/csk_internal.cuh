@@ -135,6 +135,17 @@ __device__ __forceinline__ float apply_sign(float v, uint32_t code) {
 }
 
 // ------------------------------------------------------------ launch helpers
+// runs f on scope exit (every return path releases streams, events and workspaces)
+template <typename F>
+struct ScopeExit {
+    F f;
+    ~ScopeExit() { f(); }
+};
+template <typename F>
+ScopeExit<F> on_exit(F f) {
+    return ScopeExit<F>{f};
+}
+
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // validated column-pointer table for [A b]: column c < n is A + c*lda, column n is b

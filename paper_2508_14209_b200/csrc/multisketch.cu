@@ -20,18 +20,25 @@ namespace csk {
 
 // --------------------------------------------------------------- cuBLAS
 csk_status blas_handle(cudaStream_t st, cublasHandle_t* out) {
-    static thread_local std::map<int, cublasHandle_t> handles;
+    // one handle per (thread, device, stream): cuBLAS keeps its split-K workspace in the handle,
+    // so GEMMs in flight on two streams of one thread must not share one
+    static thread_local std::map<std::pair<int, cudaStream_t>, cublasHandle_t> handles;
     int dev = 0;
     CSK_CUDA_TRY(cudaGetDevice(&dev));
-    auto it = handles.find(dev);
+    const auto key = std::make_pair(dev, st);
+    auto it = handles.find(key);
     if (it == handles.end()) {
         cublasHandle_t h = nullptr;
         CSK_REQUIRE(cublasCreate(&h) == CUBLAS_STATUS_SUCCESS, CSK_ECUDA, "cublasCreate failed");
         // fp64 stays fp64; no TF32 for fp32 (tolerance 1e-5 needs full fp32 products)
         cublasSetMathMode(h, CUBLAS_PEDANTIC_MATH);
-        it = handles.emplace(dev, h).first;
+        if (cublasSetStream(h, st) != CUBLAS_STATUS_SUCCESS) {
+            cublasDestroy(h);
+            set_error("cublasSetStream failed");
+            return CSK_ECUDA;
+        }
+        it = handles.emplace(key, h).first;
     }
-    CSK_REQUIRE(cublasSetStream(it->second, st) == CUBLAS_STATUS_SUCCESS, CSK_ECUDA, "cublasSetStream failed");
     *out = it->second;
     return CSK_OK;
 }
@@ -219,8 +226,17 @@ static csk_status sketch_host_rows(csk_plan_t plan, int64_t n, const double* A, 
     const int64_t d = plan->d;
     const int64_t chunk = std::min<int64_t>(d, std::max<int64_t>(1 << 16, (int64_t)(256ll << 20) / (8 * ncols)));
     double* stage[2] = {nullptr, nullptr};
-    cudaEvent_t copied[2], consumed[2];
+    cudaEvent_t copied[2] = {}, consumed[2] = {};
     cudaStream_t cs = nullptr;
+    auto cleanup = on_exit([&] {
+        if (cs) cudaStreamSynchronize(cs);
+        for (int i = 0; i < 2; ++i) {
+            if (stage[i]) cudaFreeAsync(stage[i], st);
+            if (copied[i]) cudaEventDestroy(copied[i]);
+            if (consumed[i]) cudaEventDestroy(consumed[i]);
+        }
+        if (cs) cudaStreamDestroy(cs);
+    });
     CSK_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     for (int i = 0; i < 2; ++i) {
         CSK_CUDA_TRY(csk_malloc_async(&stage[i], (size_t)chunk * ncols * 8, st));
@@ -243,14 +259,6 @@ static csk_status sketch_host_rows(csk_plan_t plan, int64_t n, const double* A, 
                           CSK_VAR_AUTO, st, r0, r0 + rows, /*accumulate=*/true);
         CSK_CUDA_TRY(cudaEventRecord(consumed[k], st));
     }
-    CSK_CUDA_TRY(cudaStreamSynchronize(cs));
-    for (int i = 0; i < 2; ++i) {
-        cudaFreeAsync(stage[i], st);
-        cudaEventDestroy(copied[i]);
-        cudaEventDestroy(consumed[i]);
-    }
-    cudaStreamDestroy(cs);
-    (void)ncols;
     return s;
 }
 

@@ -310,16 +310,28 @@ static csk_status alloc_plan(int64_t d, int64_t k1, uint32_t flags, csk_plan_t* 
 }
 
 csk_status ensure_codes(csk_plan_t plan, cudaStream_t st) {
+    // A CSK_PLAN_HASH plan materialises its codes on first use by a kernel that reads them.  The
+    // codes are published (plan->code) only after the stream has finished writing them, so a
+    // consumer on another stream or thread never sees a half-written array.
     std::lock_guard<std::mutex> lk(plan->mu);
     if (plan->code != nullptr) return CSK_OK;
     int32_t* code = nullptr;
     CSK_CUDA_TRY(cudaMalloc(&code, (plan->d + 32) * 4));
-    CSK_CUDA_TRY(cudaMemsetAsync(code + plan->d, 0, 32 * 4, st));
     const int64_t blocks4 = ceil_div(ceil_div(plan->d + 3, 4) + 1, 256);
     const unsigned grid = (unsigned)std::min<int64_t>(blocks4, 65535 * 4);
-    codes_kernel<<<grid, 256, 0, st>>>(code, plan->d, (uint32_t)plan->k1, (uint32_t)plan->seed,
-                                       (uint32_t)(plan->seed >> 32), plan->row0);
-    CSK_LAUNCH_CHECK();
+    cudaError_t e = cudaMemsetAsync(code + plan->d, 0, 32 * 4, st);
+    if (e == cudaSuccess) {
+        codes_kernel<<<grid, 256, 0, st>>>(code, plan->d, (uint32_t)plan->k1, (uint32_t)plan->seed,
+                                           (uint32_t)(plan->seed >> 32), plan->row0);
+        count_launch();
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+        cudaFree(code);
+        set_error("materialising the codes of a hash plan failed: %s", cudaGetErrorString(e));
+        return CSK_ECUDA;
+    }
     plan->code = code;
     return CSK_OK;
 }

@@ -57,9 +57,17 @@ static csk_status gs_apply_impl(int64_t d, int64_t row0, int64_t k, uint64_t see
     if (const char* e = std::getenv("CSK_GS_CHUNK")) mc = std::max<int64_t>(2, std::atoll(e));
     mc = std::min(mc, d);
     double* G = nullptr;
-    CSK_CUDA_TRY(csk_malloc_async(&G, 2 * (size_t)k * mc * 8, st));
     cudaStream_t gen = nullptr;
     cudaEvent_t ev[5] = {};
+    // every generated slice is waited on by st before its GEMM, so freeing G on st is ordered after
+    // the generator's writes; the stream and events are released once their pending work completes
+    auto cleanup = on_exit([&] {
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+        if (gen) cudaStreamDestroy(gen);
+        if (G) cudaFreeAsync(G, st);
+    });
+    CSK_CUDA_TRY(csk_malloc_async(&G, 2 * (size_t)k * mc * 8, st));
     CSK_CUDA_TRY(cudaStreamCreateWithFlags(&gen, cudaStreamNonBlocking));
     for (auto& e : ev) CSK_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     // ev[0]: G allocated (st); ev[1 + s]: slice s generated (gen); ev[3 + s]: slice s consumed (st)
@@ -96,15 +104,7 @@ static csk_status gs_apply_impl(int64_t d, int64_t row0, int64_t k, uint64_t see
             bs = cublasDgemv(h, CUBLAS_OP_N, (int)k, (int)m, &one, Gs, (int)k, b + c0, 1, beta, Z + (size_t)n * ldz, 1);
         CSK_CUDA_TRY(cudaEventRecord(ev[3 + slot], st));
     }
-    // every generated slice was waited on by st before its GEMM, so freeing G on st is ordered after
-    // the generator's writes; the stream and events are released once their pending work completes
-    for (auto& e : ev) cudaEventDestroy(e);
-    cudaStreamDestroy(gen);
-    if (gs_st != CSK_OK) {
-        cudaFreeAsync(G, st);
-        return gs_st;
-    }
-    cudaFreeAsync(G, st);
+    if (gs_st != CSK_OK) return gs_st;
     if (bs != CUBLAS_STATUS_SUCCESS) {
         set_error("cuBLAS Gaussian sketch failed (%d)", (int)bs);
         return CSK_ECUDA;

@@ -96,29 +96,3 @@ def rc_lstsq_distributed(A_local, b_local, row0: int, k1: int, k2: int, seed: in
     R0 = r0_(Z, n)                                                                  # line 2 (redundant per rank)
     C = _all_reduce_colmajor(gram_(A_local, b_local, R0), group)                    # lines 3-4
     return finish_(C, R0)                                                           # lines 5-8
-
-
-def _cuda_srht(A_local, b_local, k, seed, dglob, row0):
-    from . import csk
-    return csk.srht_apply(A_local, k, seed, b=b_local, dglob=dglob, row0=row0)
-
-
-def _cuda_gauss(A_local, b_local, k, seed, row0):
-    from . import csk
-    return csk.gs_apply(A_local, k, seed, b=b_local, row0=row0)
-
-
-def srht_distributed(A_local, b_local, k: int, seed: int, dglob: int, row0: int, group=None, local_srht=None):
-    """SRHT Y = k^-1/2 P H D [A b] of a row-partitioned [A b] (P:L383-386 notes the SRHT's global FWHT
-    is the hard part of distributing it): with H_d = H_{d/L} (x) H_L each rank's rows form whole
-    L-blocks, its partial Y is a sum over its blocks, and one SUM all-reduce of the k x (n+1) Y
-    completes the transform (row0 and the rank's row count must be multiples of 4096)."""
-    srht_ = local_srht or _cuda_srht
-    return _all_reduce_colmajor(srht_(A_local, b_local, k, seed, dglob, row0), group)
-
-
-def gs_distributed(A_local, b_local, k: int, seed: int, row0: int, group=None, local_gauss=None):
-    """Gaussian sketch G [A b] of a row-partitioned [A b]: G = [G^(1) ... G^(p)],
-    each rank generating its own columns of G from the global row index, then one SUM all-reduce."""
-    gauss_ = local_gauss or _cuda_gauss
-    return _all_reduce_colmajor(gauss_(A_local, b_local, k, seed, row0), group)

@@ -107,3 +107,47 @@ def rhs_torch(A, mode: str = "easy", seed: int = 2):
         g = _torch_gen(torch, seed, STREAM_NOISE, A.device)
         b += mu + math.sqrt(var) * torch.randn(b.shape, dtype=b.dtype, device=A.device, generator=g)
     return b
+
+
+# ------------------------------------------------- row-partitioned device inputs (multi-GPU bench)
+def row_block_size(d_global: int) -> int:
+    """Rows per generator block of a d_global-row matrix: a function of the global shape only, so
+    every row partition (any world size dividing d_global / block) sees the same global matrix."""
+    return max(1, min(1 << 22, d_global // 8))
+
+
+def gaussian_rows_torch(d_global: int, row0: int, rows: int, ncols: int, seed: int = 2, device="cuda",
+                        out=None):
+    """Rows [row0, row0 + rows) of the d_global x ncols Gaussian matrix whose row block q (of
+    row_block_size rows) is drawn from generator (seed, q): identical bytes for any partition."""
+    import torch
+    blk = row_block_size(d_global)
+    if out is None:
+        out = colmajor_empty(torch, rows, ncols, torch.float64, device)
+    q0, q1 = row0 // blk, (row0 + rows - 1) // blk
+    for q in range(q0, q1 + 1):
+        g = _torch_gen(torch, seed * 7919 + q, STREAM_GAUSS_A, device)
+        nb = min(blk, d_global - q * blk)
+        block = torch.randn((ncols, nb), dtype=torch.float64, device=device, generator=g).t()
+        a, e = max(row0, q * blk), min(row0 + rows, q * blk + nb)
+        out[a - row0:e - row0] = block[a - q * blk:e - q * blk]
+        del block
+    return out
+
+
+def noise_rows_torch(d_global: int, row0: int, rows: int, mode: str = "easy", seed: int = 2, device="cuda"):
+    """eta of b = A e + eta for rows [row0, row0 + rows), drawn per global row block like the matrix."""
+    import torch
+    mu, var = NOISE[mode]
+    eta = torch.zeros(rows, dtype=torch.float64, device=device)
+    if var == 0.0:
+        return eta
+    blk = row_block_size(d_global)
+    q0, q1 = row0 // blk, (row0 + rows - 1) // blk
+    for q in range(q0, q1 + 1):
+        g = _torch_gen(torch, seed * 7919 + q, STREAM_NOISE, device)
+        nb = min(blk, d_global - q * blk)
+        block = mu + math.sqrt(var) * torch.randn(nb, dtype=torch.float64, device=device, generator=g)
+        a, e = max(row0, q * blk), min(row0 + rows, q * blk + nb)
+        eta[a - row0:e - row0] = block[a - q * blk:e - q * blk]
+    return eta

@@ -16,8 +16,7 @@ import oracle
 import synth
 import scipy.linalg
 
-from paper_2508_14209_b200.dist import (gs_distributed, ms_lstsq_distributed, rc_lstsq_distributed, row_block,
-                                        srht_distributed)
+from paper_2508_14209_b200.dist import ms_lstsq_distributed, rc_lstsq_distributed, row_block
 
 D, N, K1, K2, SEED = 9001, 6, 72, 14, 3
 
@@ -152,62 +151,3 @@ def test_rc_distributed_matches_single_process(world):
         assert np.linalg.norm(A @ (x - xo)) <= 64 * 2.2e-16 * (nb + 1e6 * r)
         assert np.linalg.norm(A @ (x - xs)) <= 64 * 2.2e-16 * (nb + 1e6 * r)
     assert all(np.array_equal(res[0][1], x) for _, x in res)
-
-
-# ------------------------------------------------------- SRHT and Gaussian sketch over ranks
-# The injected local operator is the oracle on the rank's rows embedded in the global matrix with
-# every other row zeroed (zero rows contribute nothing to a linear sketch), so the reference is
-# exactly the single-process oracle on the whole matrix.
-DS = 1 << 14          # SRHT: power of two, rank blocks multiples of 4096
-
-
-def _srht_local(A_local, b_local, k, seed, dglob, row0):
-    Af = np.zeros((dglob, A_local.shape[1]))
-    bf = np.zeros(dglob)
-    Af[row0:row0 + A_local.shape[0]] = A_local.numpy()
-    bf[row0:row0 + A_local.shape[0]] = b_local.numpy()
-    return torch.from_numpy(np.ascontiguousarray(oracle.srht_apply(Af, k, seed, b=bf).T)).t()
-
-
-def _gauss_local(A_local, b_local, k, seed, row0):
-    G = oracle.gauss(k, row0 + A_local.shape[0], seed)[:, row0:]
-    Ab = np.column_stack([A_local.numpy(), b_local.numpy()])
-    return torch.from_numpy(np.ascontiguousarray(oracle.gemm_comp(G, Ab).T)).t()
-
-
-def _sketch_worker(rank, world, port, q):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    A = synth.gaussian_matrix(DS, 5, seed=8)
-    b = synth.rhs(A, "hard", seed=8)
-    blk = DS // world
-    r0 = rank * blk
-    A_local = torch.from_numpy(np.ascontiguousarray(A[r0:r0 + blk].T)).t()
-    b_local = torch.from_numpy(b[r0:r0 + blk].copy())
-    Y = srht_distributed(A_local, b_local, 40, 3, DS, r0, local_srht=_srht_local)
-    Z = gs_distributed(A_local, b_local, 12, 3, r0, local_gauss=_gauss_local)
-    q.put((rank, Y.numpy(), Z.numpy()))
-    dist.destroy_process_group()
-
-
-def test_srht_and_gauss_distributed():
-    world = 2
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_sketch_worker, args=(r, world, port, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    res = [q.get(timeout=120) for _ in range(world)]
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
-    A = synth.gaussian_matrix(DS, 5, seed=8)
-    b = synth.rhs(A, "hard", seed=8)
-    Ab = np.column_stack([A, b])
-    Yo = oracle.srht_apply(A, 40, 3, b=b)
-    Zo, Zabs = oracle.gemm_comp(oracle.gauss(12, DS, 3), Ab, np.abs(Ab))
-    T = np.abs(Ab).sum(axis=0)[None, :] / np.sqrt(40)
-    for _, Y, Z in res:
-        assert np.all(np.abs(Y - Yo) <= 1e-12 * T)
-        assert np.all(np.abs(Z - Zo) <= 1e-12 * Zabs)

@@ -14,7 +14,7 @@ import pytest
 
 import oracle
 import synth
-from tests._util import assert_within_T, gpu_colmajor, host, unpack
+from tests._util import assert_within_T, check_fitted, check_le, gpu_colmajor, host, ls_tol, unpack
 
 pytestmark = pytest.mark.gpu
 
@@ -264,7 +264,9 @@ def test_gauss_matches_oracle():
         S = np.zeros((k1, k1))
         S[h, np.arange(k1)] = s
         G = oracle.gauss(k2, k1, 77)
-        assert np.allclose(Z, G @ S, rtol=0, atol=1e-13 / np.sqrt(k2) * 4)
+        # G S with S a signed permutation is exact, so Z - G S is the Box-Muller difference itself:
+        # |dN| <= 1e-13, |dG| = |dN| / sqrt(k2)
+        check_le(np.abs(Z - G @ S).max(), 1e-13 / np.sqrt(k2), "max |G_gpu - G_oracle|")
 
 
 @pytest.mark.parametrize("transpose", ["0", "1"])
@@ -324,8 +326,8 @@ def test_ms_solve_matches_oracle(solver_env):
         x, r = csk.ms_solve(gpu_colmajor(Z), n)
         xo, ro = oracle.sketch_solve(Z, n)
         err = np.linalg.norm(Z[:, :n] @ (host(x) - xo))
-        assert err <= 1e-12 * np.linalg.norm(Z[:, n]), (m, n, err)
-        assert abs(r - ro) <= 1e-12 * np.linalg.norm(Z[:, n]), (m, n)
+        check_le(err / np.linalg.norm(Z[:, n]), 1e-12, f"ms_solve {m}x{n} ||Z_A dx||/||z||")
+        check_le(abs(r - ro) / np.linalg.norm(Z[:, n]), 1e-12, f"ms_solve {m}x{n} |d sk_resid|/||z||")
 
 
 @pytest.mark.parametrize("kappa", [1e6, 1e12])
@@ -341,8 +343,8 @@ def test_ms_solve_ill_conditioned(solver_env, kappa):
     nz = np.linalg.norm(z)
     rr = ro / nz
     tol = max(1e-12, 64 * 2.2e-16 * kappa * rr)
-    assert np.linalg.norm(Z1 @ (host(x) - xo)) / nz <= tol
-    assert abs(r - ro) <= tol * nz
+    check_fitted(Z1, host(x) - xo, nz, tol)
+    check_le(abs(r - ro) / nz, tol, "|d sk_resid| / ||z||")
 
 
 def test_ms_solve_singular(solver_env):
@@ -388,11 +390,13 @@ def test_ms_lstsq_matches_oracle(kappa, mode):
     nb = np.linalg.norm(b)
     # R16: fitted values agree to 1e-8 relative; for kappa = 1e10 with a noisy b the
     # problem itself amplifies O(u) input rounding by kappa * ||r|| / ||b|| (Wedin), so
-    # the bound is max(1e-8, 64 u kappa ||r|| / ||b||)
+    # the bound is max(1e-8, 64 u kappa ||r|| / ||b||) (R16b)
     rr = oracle.residual_norm(A, b, xo) / nb
-    tol = max(1e-8, 64 * 2.2e-16 * kappa * rr)
-    assert np.linalg.norm(A @ (host(x) - xo)) / nb <= tol
-    assert abs(r - ro) <= tol * nb         # |d ||r||| <= ||A dx||, same first-order bound
+    tol = ls_tol(kappa, rr)                 # = 1e-8 for the consistent b and for kappa = 1e2
+    if mode == "consistent" or kappa <= 1e2:
+        assert tol == 1e-8
+    check_fitted(A, host(x) - xo, nb, tol)
+    check_le(abs(r - ro) / nb, tol, "|d sk_resid| / ||b||")   # |d ||r||| <= ||A dx||, same first-order bound
 
 
 def test_ms_lstsq_host_inputs_streamed():
@@ -408,11 +412,11 @@ def test_ms_lstsq_host_inputs_streamed():
     assert not xh.is_cuda
     xo, ro = oracle.ms_lstsq(A, b, k1, k2, seed=2)
     nb = np.linalg.norm(b)
-    assert np.linalg.norm(A @ (xh.numpy() - xo)) / nb <= 1e-8
-    assert np.linalg.norm(A @ (host(xd) - xo)) / nb <= 1e-8
+    check_fitted(A, xh.numpy() - xo, nb, 1e-8)
+    check_fitted(A, host(xd) - xo, nb, 1e-8)
     # pageable host memory works too
     xp, _ = csk.ms_lstsq(plan, k2, torch.from_numpy(np.ascontiguousarray(A.T)).t(), torch.from_numpy(b))
-    assert np.linalg.norm(A @ (xp.numpy() - xo)) / nb <= 1e-8
+    check_fitted(A, xp.numpy() - xo, nb, 1e-8)
 
 
 # -------------------------------------------------------- normal equations
@@ -427,7 +431,7 @@ def test_ne_lstsq_matches_oracle():
     Ab = gpu_colmajor(np.column_stack([A, b]))
     x2 = host(csk.ne_lstsq(Ab[:, :n], Ab[:, n]))
     for x in (x1, x2):
-        assert np.linalg.norm(A @ (x - xo)) / nb <= 1e-8
+        check_fitted(A, x - xo, nb, 1e-8)
 
 
 def test_ne_lstsq_breaks_down_at_kappa_1e10():
@@ -568,5 +572,5 @@ def test_hash_plan_ms_lstsq_matches_stored_codes():
     x1, r1 = csk.ms_lstsq(csk.cs_plan(d, k1, 5, hash=True), k2, gpu_colmajor(A), gpu_colmajor(b))
     # same codes; the reduction order is not deterministic, so within the LS tolerance (R16)
     nb = np.linalg.norm(b)
-    assert np.linalg.norm(A @ (host(x0) - host(x1))) / nb <= 1e-8
+    check_fitted(A, host(x0) - host(x1), nb, 1e-8)
     assert abs(r0 - r1) <= 1e-8 * nb

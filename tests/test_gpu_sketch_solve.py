@@ -8,7 +8,7 @@ import pytest
 
 import oracle
 import synth
-from tests._util import gpu_colmajor, host, unpack
+from tests._util import check_fitted, check_le, gpu_colmajor, host, ls_tol, unpack
 
 pytestmark = pytest.mark.gpu
 
@@ -62,7 +62,7 @@ def test_gs_lstsq_matches_oracle(kappa):
     Zo = oracle.gemm_comp(oracle.gauss(k, d, seed=3), np.column_stack([A, b]))
     xo, ro = oracle.sketch_solve(Zo, n)
     nb, tol = _ls_tol(A, b, xo, kappa)
-    assert np.linalg.norm(A @ (host(x) - xo)) / nb <= tol
+    check_fitted(A, host(x) - xo, nb, tol)
     assert abs(r - ro) <= tol * nb
 
 
@@ -78,7 +78,7 @@ def test_cs_lstsq_matches_oracle(kappa, mode):
     h, s, = oracle.codes(d, k1, 2)
     xo, ro = oracle.sketch_solve(oracle.cs_apply(h, s, A, k1, b=b), n)
     nb, tol = _ls_tol(A, b, xo, kappa)
-    assert np.linalg.norm(A @ (host(x) - xo)) / nb <= tol
+    check_fitted(A, host(x) - xo, nb, tol)
     assert abs(r - ro) <= tol * nb + 1e-300
 
 
@@ -109,7 +109,7 @@ def test_msh_lstsq_matches_oracle():
     Zo = oracle.srht_apply(oracle.cs_apply(h, s, A, k1, b=b), k2, seed=1)
     xo, ro = oracle.sketch_solve(Zo, n)
     nb, tol = _ls_tol(A, b, xo, 1e6)
-    assert np.linalg.norm(A @ (host(x) - xo)) / nb <= tol
+    check_fitted(A, host(x) - xo, nb, tol)
 
 
 def test_msh_needs_power_of_two_k1():
