@@ -1351,7 +1351,8 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
     CSK_REQUIRE(ncols64 >= 1 && ncols64 <= 65536, CSK_EINVAL, "n + (b != NULL) = %lld must be in [1, 65536]",
                 (long long)ncols64);
     CSK_REQUIRE(n == 0 || A != nullptr, CSK_EINVAL, "A is NULL");
-    CSK_REQUIRE(SA != nullptr, CSK_EINVAL, "SA is NULL");
+    CSK_REQUIRE(SA != nullptr || rowout != nullptr, CSK_EINVAL, "SA is NULL");
+    if (rowout != nullptr) *rowout = RowOut{};
     CSK_REQUIRE(row_begin >= 0 && row_begin < row_end && row_end <= plan->d, CSK_EINVAL, "bad row range");
     CSK_REQUIRE(n == 0 || lda >= row_end - row_begin, CSK_ESHAPE, "lda=%lld < rows=%lld", (long long)lda,
                 (long long)(row_end - row_begin));
@@ -1428,7 +1429,7 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
                                   (b == nullptr || ((uintptr_t)b & 15) == 0);
                 const char* b32e = std::getenv("CSK_B32");
                 const char* spe = std::getenv("CSK_SPLIT");
-                if (!tma && variant == CSK_VAR_BULK_ROW && al32 && !(b32e && std::atoi(b32e) == 0) &&
+                if (!tma && variant == CSK_VAR_BULK_ROW && al32 && !(b32e && std::atoi(b32e) == 0) && !rowout &&
                     spe && std::atoi(spe) == 1 && nchunks == 1 && (ncols & 1) && ncols >= 5 &&
                     (k1 & 1) == 0 && k1 <= 10240 && n > 0 && (b != nullptr || n >= 5)) {
                     L.cw = ncols - 1;
@@ -1443,7 +1444,7 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
                 // nothing (the L2 adds the same number of elements per row) and the float tile writes
                 // of 16-B aligned rows cannot avoid 8-way bank conflicts.
                 const char* f32e = std::getenv("CSK_F32ACC");
-                if (dtype == CSK_F32 && !tma && variant == CSK_VAR_BULK_ROW && !L.chunk_major &&
+                if (dtype == CSK_F32 && !tma && variant == CSK_VAR_BULK_ROW && !L.chunk_major && !rowout &&
                     f32e && std::atoi(f32e) == 1) {
                     const int64_t rows = row_end - row_begin;
                     const int64_t ncp = std::max<int64_t>(1, std::min<int64_t>(256, ceil_div(rows, 64 * k1)));
@@ -1464,6 +1465,10 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
         tgt.ld = L.lc;
         tgt.owned = true;
     } else if (dtype == CSK_F32) {
+        tgt.ld = k1;
+        tgt.owned = true;
+        ws_doubles = (size_t)k1 * ncols;
+    } else if (SA == nullptr) {   // rowout with a column-major variant: private fp64 target, converted below
         tgt.ld = k1;
         tgt.owned = true;
         ws_doubles = (size_t)k1 * ncols;
@@ -1496,15 +1501,23 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
         s = run_variant<float>(variant, plan, ncols, cols, row_begin, row_end, tgt.buf, tgt.ld, L, st);
     }
     prof_mark(st, false);
-    if (rowout != nullptr) rowout->ws = nullptr;
-    if (s == CSK_OK && tgt.owned && rowout != nullptr && variant_rowmajor(variant) && dtype == CSK_F64 && L.sep < 0) {
-        // the caller (ms_apply) consumes the row-major SA^T directly (Z^T = Y^T G^T, no transpose)
-        rowout->ws = tgt.buf;
-        rowout->cw = L.cw;
-        rowout->lc = L.lc;
-        rowout->cs = L.cs;
-        rowout->ncols = ncols;
-        return CSK_OK;
+    if (rowout != nullptr) {
+        if (s == CSK_OK && variant_rowmajor(variant) && L.sep < 0 && L.ncopies == 0) {
+            // the caller (ms_apply) consumes the row-major SA^T directly (Z^T = Y^T G^T, no transpose)
+            rowout->ws = tgt.buf;
+            rowout->cw = L.cw;
+            rowout->lc = L.lc;
+            rowout->cs = L.cs;
+            rowout->ncols = ncols;
+            return CSK_OK;
+        }
+        if (s == CSK_OK) {
+            // column-major fp64 result (variants L, S, G) -> row-major workspace
+            CSK_REQUIRE(!variant_rowmajor(variant), CSK_EUNSUPPORTED, "row-major hand-over not available here");
+            s = rows_from_colmajor(tgt.buf, tgt.ld, k1, ncols, rowout, st);
+        }
+        if (tgt.owned) cudaFreeAsync(tgt.buf, st);
+        return s;
     }
     if (s == CSK_OK && tgt.owned && L.ncopies > 0) {
         dim3 grid((unsigned)ceil_div(k1, 32), (unsigned)ceil_div(ncols, 32));

@@ -81,8 +81,7 @@ struct csk_plan_s {
     int64_t* offsets = nullptr;   // k1 + 1 (CSK_PLAN_SORT)
     int32_t* perm = nullptr;      // d      (CSK_PLAN_SORT)
     std::mutex mu;                // guards the Gaussian caches
-    std::map<int64_t, double*> gauss64;
-    std::map<int64_t, float*> gauss32;
+    std::map<int64_t, double*> gauss64;   // G per k2 (ld round_up(k2, 8), tail padded)
 };
 
 namespace csk {
@@ -198,10 +197,22 @@ struct RowOut {
     int cw = 0, ncols = 0;
     int64_t lc = 0, cs = 0;
 };
+// multisketch.cu: column-major fp64 SA (ld) -> a new regular row-major workspace described by *ro
+csk_status rows_from_colmajor(const double* SA, int64_t ld, int64_t k1, int ncols, RowOut* ro, cudaStream_t st);
+// With rowout != NULL the result is ALWAYS handed over as an fp64 row-major workspace (SA may be NULL);
+// the caller cudaFreeAsync's rowout->ws.
 csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void* A, int64_t lda,
                          const void* b, void* SA, int64_t ldsa, int variant, cudaStream_t st,
                          int64_t row_begin, int64_t row_end, bool accumulate, RowOut* rowout = nullptr);
-csk_status gauss_get(csk_plan_t plan, int64_t k2, csk_dtype dtype, cudaStream_t st, const void** G);
+// the plan's cached G (k2 x k1, fp64, column-major with ld *ldg = round_up(k2, 8), rows past k2 zero,
+// followed by kGstageTailPad zero doubles so 128-row tiles may read past the last column)
+constexpr int kGstageTailPad = 256;
+csk_status gauss_get(csk_plan_t plan, int64_t k2, cudaStream_t st, const double** G, int64_t* ldg);
+// gstage.cu: Z (k2 x ro.ncols, column-major ldz, fp64 or fp32) = G Y with Y^T the row-major workspace
+// described by ro (chunks of <= kGstageMaxCw columns), hand-written fp64 DMMA (a5)
+constexpr int kGstageMaxCw = 72;
+csk_status gstage_launch(const double* G, int64_t ldg, int64_t k2, int64_t k1, const RowOut& ro, void* Z,
+                         int64_t ldz, bool z_f32, cudaStream_t st);
 struct cublasContext;
 csk_status blas_handle(cudaStream_t st, struct cublasContext** h);
 

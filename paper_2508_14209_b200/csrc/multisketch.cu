@@ -2,8 +2,8 @@
 //
 // a4 G:    k2 x k1 Gaussian, G_ij ~ N(0, 1/k2) ("2n x 2n^2 Gaussian"),
 //          Philox stream 1 + Box-Muller (R4), cached in the plan per k2.
-// a5 Z:    Z = G (S [A b])  -- the multisketch S2(S1 x), a plain DGEMM
-//          (fp64 DMMA tensor cores via cuBLAS; Table 1 P:L99 "n^4" term).
+// a5 Z:    Z = G (S [A b])  -- the multisketch S2(S1 x), the hand-written fp64 DMMA
+//          G-stage of gstage.cu on the CountSketch's row-major workspace (Table 1 P:L99 "n^4" term).
 // a7 solve: Householder QR of Z = [GSA | GSb] in one CTA, back substitution
 //          (Alg 1 lines 2-3; GeQRF + OrMQR + TRSV of P:L230).
 #include <algorithm>
@@ -64,157 +64,62 @@ __global__ void gauss_kernel(T* __restrict__ G, int64_t total, double inv_sqrt_s
     }
 }
 
-csk_status gauss_get(csk_plan_t plan, int64_t k2, csk_dtype dtype, cudaStream_t st, const void** out) {
-    std::lock_guard<std::mutex> lk(plan->mu);
-    if (dtype == CSK_F64) {
-        auto it = plan->gauss64.find(k2);
-        if (it != plan->gauss64.end()) {
-            *out = it->second;
-            return CSK_OK;
-        }
-    } else {
-        auto it = plan->gauss32.find(k2);
-        if (it != plan->gauss32.end()) {
-            *out = it->second;
-            return CSK_OK;
-        }
-    }
-    const int64_t total = k2 * plan->k1;
-    const size_t esz = dtype == CSK_F64 ? 8 : 4;
-    void* G = nullptr;
-    if (cudaMalloc(&G, (size_t)total * esz) != cudaSuccess) {
-        cudaGetLastError();
-        set_error("allocation of G (%lld x %lld) failed", (long long)k2, (long long)plan->k1);
-        return CSK_ENOMEM;
-    }
-    const double div = std::sqrt((double)k2);
-    const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(std::max<int64_t>(total / 2, 1), 256), 148 * 32);
-    if (dtype == CSK_F64)
-        gauss_kernel<double><<<grid, 256, 0, st>>>((double*)G, total, div, (uint32_t)plan->seed,
-                                                    (uint32_t)(plan->seed >> 32), 0);
-    else
-        gauss_kernel<float><<<grid, 256, 0, st>>>((float*)G, total, div, (uint32_t)plan->seed,
-                                                   (uint32_t)(plan->seed >> 32), 0);
-    count_launch();
-    if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) {
-        cudaFree(G);
-        set_error("gauss_kernel failed");
-        return CSK_ECUDA;
-    }
-    if (total & 1) {
-        // odd total: the last element has no Box-Muller partner; draw its pair and keep the cosine
-        // half (the kernel above covers pairs only) -- recompute on the host, same formula
-        const int64_t t = total >> 1;
-        uint4 x = philox4x32_10(make_uint4((uint32_t)t, (uint32_t)(t >> 32), 1u, 0u),
-                                make_uint2((uint32_t)plan->seed, (uint32_t)(plan->seed >> 32)));
+// G stored with a padded leading dimension for the G-stage's 16-B tile loads: element e = r + c k2 of
+// the Philox stream (R4) lives at G[r + c ldg]; rows k2..ldg-1 and the tail stay zero
+__global__ void gauss_ld_kernel(double* __restrict__ G, int64_t k2, int64_t ldg, int64_t total, double div,
+                                uint32_t key_lo, uint32_t key_hi) {
+    const int64_t npairs = (total + 1) >> 1;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < npairs; t += (int64_t)gridDim.x * blockDim.x) {
+        const uint4 x = philox4x32_10(make_uint4((uint32_t)t, (uint32_t)(t >> 32), 1u, 0u), make_uint2(key_lo, key_hi));
         const uint64_t w1 = ((uint64_t)x.y << 32) | x.x;
         const uint64_t w2 = ((uint64_t)x.w << 32) | x.z;
         const double u1 = (double)((w1 >> 11) + 1) * 0x1.0p-53;
         const double u2 = (double)(w2 >> 11) * 0x1.0p-53;
-        const double v = (std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586476925286766559 * u2)) / div;
-        if (dtype == CSK_F64) {
-            CSK_CUDA_TRY(cudaMemcpy((double*)G + total - 1, &v, 8, cudaMemcpyHostToDevice));
-        } else {
-            const float f = (float)v;
-            CSK_CUDA_TRY(cudaMemcpy((float*)G + total - 1, &f, 4, cudaMemcpyHostToDevice));
-        }
+        const double rho = sqrt(-2.0 * log(u1));
+        double sn, cs;
+        sincospi(2.0 * u2, &sn, &cs);
+        const int64_t e0 = 2 * t, e1 = 2 * t + 1;
+        G[(e0 % k2) + (e0 / k2) * ldg] = (rho * cs) / div;
+        if (e1 < total) G[(e1 % k2) + (e1 / k2) * ldg] = (rho * sn) / div;
     }
-    if (dtype == CSK_F64)
-        plan->gauss64[k2] = (double*)G;
-    else
-        plan->gauss32[k2] = (float*)G;
+}
+
+csk_status gauss_get(csk_plan_t plan, int64_t k2, cudaStream_t st, const double** out, int64_t* ldg_out) {
+    std::lock_guard<std::mutex> lk(plan->mu);
+    const int64_t ldg = (k2 + 7) & ~(int64_t)7;
+    *ldg_out = ldg;
+    auto it = plan->gauss64.find(k2);
+    if (it != plan->gauss64.end()) {
+        *out = it->second;
+        return CSK_OK;
+    }
+    const int64_t total = k2 * plan->k1;
+    const size_t bytes = ((size_t)ldg * plan->k1 + kGstageTailPad) * sizeof(double);
+    double* G = nullptr;
+    if (cudaMalloc(&G, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        set_error("allocation of G (%lld x %lld) failed", (long long)k2, (long long)plan->k1);
+        return CSK_ENOMEM;
+    }
+    auto fail = [&](const char* what) {
+        cudaFree(G);
+        set_error("%s", what);
+        return CSK_ECUDA;
+    };
+    if (cudaMemsetAsync(G, 0, bytes, st) != cudaSuccess) return fail("G memset failed");
+    const double div = std::sqrt((double)k2);
+    const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(std::max<int64_t>((total + 1) / 2, 1), 256), 148 * 32);
+    gauss_ld_kernel<<<grid, 256, 0, st>>>(G, k2, ldg, total, div, (uint32_t)plan->seed, (uint32_t)(plan->seed >> 32));
+    count_launch();
+    // synchronised before the pointer is published: a consumer on another stream may read it next
+    if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) return fail("gauss kernel failed");
+    plan->gauss64[k2] = G;
     *out = G;
     return CSK_OK;
 }
 
 template __global__ void gauss_kernel<double>(double*, int64_t, double, uint32_t, uint32_t, int64_t);
 template __global__ void gauss_kernel<float>(float*, int64_t, double, uint32_t, uint32_t, int64_t);
-
-// ------------------------------------------------------------ a5: split-K G-stage (fp64 DMMA)
-// Z[:, chunk] = G · SA[:, chunk] for k2 <= 256 (C2, C4, C5), opt-in (CSK_GSTAGE=splitk; slower than
-// cuBLAS's own split-K GEMM).  The output is only k2 x nc (128 x 65 at C2); every SM
-// takes a K-slice of k1: CTA s computes the full k2 x nc partial of G[:, K_s] · SA^T[K_s, :]^T with
-// mma.sync m8n8k4 f64 (warp w owns m-tiles w, w+8, ..; 9 n-tiles = 72 >= nc columns), reading
-// G (column-major, ld k2) and the row-major SA^T chunk (ld lc) straight from L2; the partials are
-// summed in fixed slice order by gs_reduce_kernel (deterministic, like the GEMM it replaces).
-constexpr int kGsWarps = 8, kGsNT = 9;
-
-__device__ __forceinline__ void gs_dmma(double& c0, double& c1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                 : "+d"(c0), "+d"(c1)
-                 : "d"(a), "d"(b));
-}
-
-template <int MT>
-__global__ void __launch_bounds__(kGsWarps * 32) gs_splitk_kernel(const double* __restrict__ G, int k2, int64_t k1,
-                                                                   const double* __restrict__ Bt, int64_t lc, int nc,
-                                                                   int64_t kslice, double* __restrict__ part) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int g = lane >> 2, t = lane & 3;
-    const int64_t kb = blockIdx.x * kslice, ke = min(k1, kb + kslice);
-    double acc[MT][kGsNT][2];
-#pragma unroll
-    for (int i = 0; i < MT; ++i)
-#pragma unroll
-        for (int j = 0; j < kGsNT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    int rows[MT];
-#pragma unroll
-    for (int i = 0; i < MT; ++i) rows[i] = (w + kGsWarps * i) * 8 + g;
-#pragma unroll 2
-    for (int64_t k = kb; k < ke; k += 4) {
-        const int64_t kk = k + t;   // A[g][t] = G[row, kk], B[t][g] = SA[kk, col]
-        const bool kv = kk < ke;
-        const int64_t kc = kv ? kk : kb;   // clamped (legal) address; the value is dropped
-        double a[MT], bf[kGsNT];
-#pragma unroll
-        for (int i = 0; i < MT; ++i) {
-            const double v = __ldg(G + kc * k2 + min(rows[i], k2 - 1));
-            a[i] = (kv && rows[i] < k2) ? v : 0.0;
-        }
-#pragma unroll
-        for (int j = 0; j < kGsNT; ++j) {
-            const int col = 8 * j + g;
-            const double v = __ldg(Bt + kc * lc + min(col, nc - 1));
-            bf[j] = (kv && col < nc) ? v : 0.0;
-        }
-#pragma unroll
-        for (int i = 0; i < MT; ++i)
-#pragma unroll
-            for (int j = 0; j < kGsNT; ++j) gs_dmma(acc[i][j][0], acc[i][j][1], a[i], bf[j]);
-    }
-    // partial s: k2 x nc column-major (ld k2); C[g][2t], C[g][2t+1] of each 8x8 tile
-    double* P = part + (int64_t)blockIdx.x * k2 * nc;
-#pragma unroll
-    for (int i = 0; i < MT; ++i) {
-        if (rows[i] >= k2) continue;
-#pragma unroll
-        for (int j = 0; j < kGsNT; ++j) {
-            const int col = 8 * j + 2 * t;
-            if (col < nc) P[(int64_t)col * k2 + rows[i]] = acc[i][j][0];
-            if (col + 1 < nc) P[(int64_t)(col + 1) * k2 + rows[i]] = acc[i][j][1];
-        }
-    }
-}
-
-// Z[r, c] = sum_s part[s][r + k2 c], s in fixed order: warp w of a block sums slices s = w mod 8
-// for 32 consecutive outputs, then the 8 warp sums are added in order w = 0..7
-__global__ void __launch_bounds__(256) gs_reduce_kernel(const double* __restrict__ part, int nsl, int k2, int nc,
-                                                        double* __restrict__ Z, int64_t ldz) {
-    __shared__ double red[8][32];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t o = (int64_t)blockIdx.x * 32 + lane, total = (int64_t)k2 * nc;
-    double acc = 0.0;
-    if (o < total)
-        for (int s = w; s < nsl; s += 8) acc += __ldg(part + (int64_t)s * total + o);
-    red[w][lane] = acc;
-    __syncthreads();
-    if (w == 0 && o < total) {
-        double z = red[0][lane];
-#pragma unroll
-        for (int q = 1; q < 8; ++q) z += red[q][lane];
-        Z[(o % k2) + ldz * (o / k2)] = z;
-    }
-}
 
 // ---------------------------------------------------- a3 over host inputs
 // Host A/b: stream row chunks through two device staging buffers; the copy of
@@ -624,8 +529,47 @@ launched:
     return CSK_OK;
 }
 
+// SA (k1 x ncols column-major fp64, ld) -> the regular row-major workspace (lc = round_up(ncols, 2))
+__global__ void colmajor_to_rows_kernel(const double* __restrict__ SA, int64_t ld, int64_t k1, int ncols,
+                                        double* __restrict__ Yt, int64_t lc) {
+    __shared__ double t[32][33];
+    const int64_t m0 = blockIdx.x * 32;
+    const int c0 = blockIdx.y * 32;
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const int c = c0 + j;
+        const int64_t m = m0 + threadIdx.x;
+        t[j][threadIdx.x] = (m < k1 && c < ncols) ? SA[m + (int64_t)c * ld] : 0.0;
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const int64_t m = m0 + j;
+        const int c = c0 + threadIdx.x;
+        if (m < k1 && c < (int)lc) Yt[m * lc + c] = t[threadIdx.x][j];
+    }
+}
+
+csk_status rows_from_colmajor(const double* SA, int64_t ld, int64_t k1, int ncols, RowOut* ro, cudaStream_t st) {
+    const int64_t lc = (ncols + 1) & ~1;
+    double* Yt = nullptr;
+    CSK_CUDA_TRY(csk_malloc_async(&Yt, (size_t)k1 * lc * sizeof(double), st));
+    dim3 grid((unsigned)ceil_div(k1, 32), (unsigned)ceil_div(lc, 32));
+    colmajor_to_rows_kernel<<<grid, dim3(32, 8), 0, st>>>(SA, ld, k1, ncols, Yt, lc);
+    count_launch();
+    if (cudaGetLastError() != cudaSuccess) {
+        cudaFreeAsync(Yt, st);
+        set_error("row-major conversion launch failed");
+        return CSK_ECUDA;
+    }
+    ro->ws = Yt;
+    ro->ncols = ncols;
+    ro->lc = lc;
+    ro->cw = ncols;
+    ro->cs = ncols;
+    return CSK_OK;
+}
+
 csk_status ms_apply_impl(csk_plan_t plan, int64_t k2, csk_dtype dtype, int64_t n, const void* A, int64_t lda,
-                                const void* b, void* Z, int64_t ldz, cudaStream_t st) {
+                         const void* b, void* Z, int64_t ldz, cudaStream_t st) {
     CSK_REQUIRE(plan != nullptr, CSK_EINVAL, "plan is NULL");
     CSK_REQUIRE(Z != nullptr, CSK_EINVAL, "Z is NULL");
     CSK_REQUIRE(k2 >= 1 && k2 <= 1 << 20, CSK_EINVAL, "k2=%lld out of range", (long long)k2);
@@ -637,104 +581,38 @@ csk_status ms_apply_impl(csk_plan_t plan, int64_t k2, csk_dtype dtype, int64_t n
     const bool host_in = (n > 0 && !is_device_pointer(A)) || (b && !is_device_pointer(b));
     CSK_REQUIRE(!host_in || dtype == CSK_F64, CSK_EDTYPE, "host-resident inputs are supported for fp64 only");
     const int64_t k1 = plan->k1;
-    const size_t esz = dtype == CSK_F64 ? 8 : 4;
-    void* SA = nullptr;
     csk_status s;
     RowOut ro;
-    // fp64 device inputs: take the CountSketch's row-major SA^T and run the G-stage as
-    // Z^T-style transposed products on it -- P:L228's "interpreted Y stored in row-major as the
-    // transpose ... computed Z^T = Y^T G^T" -- so the k1 x ncols transpose is never done
-    // (CSK_MS_TRANSPOSE=1 restores the transpose + NN GEMM for measurement).
-    const char* te = std::getenv("CSK_MS_TRANSPOSE");
-    const bool rowmajor = dtype == CSK_F64 && !host_in && !(te && std::atoi(te) == 1);
+    // a3: the CountSketch hands over its fp64 row-major SA^T workspace ("interpreted Y stored in
+    // row-major as the transpose ... computed Z^T = Y^T G^T"), so no k1 x ncols transpose is made on the
+    // default path
     if (host_in) {
         CSK_REQUIRE(n == 0 || lda >= plan->d, CSK_ESHAPE, "lda < d");
-        CSK_CUDA_TRY(csk_malloc_async(&SA, (size_t)k1 * ncols * esz, st));
-        CSK_CUDA_TRY(cudaMemsetAsync(SA, 0, (size_t)k1 * ncols * 8, st));
-        s = sketch_host_rows(plan, n, (const double*)A, lda, (const double*)b, (double*)SA, k1, st);
-    } else {
-        CSK_CUDA_TRY(csk_malloc_async(&SA, (size_t)k1 * ncols * esz, st));
-        s = cs_apply_impl(plan, dtype, n, A, lda, b, SA, k1, CSK_VAR_AUTO, st, 0, plan->d, false,
-                          rowmajor ? &ro : nullptr);
-    }
-    if (s == CSK_OK && ro.ws != nullptr) {
-        const void* G = nullptr;
-        s = gauss_get(plan, k2, dtype, st, &G);
-        // split-K DMMA kernel for k2 <= 256, opt-in (CSK_GSTAGE=splitk): cuBLAS picks split-K itself
-        // here and measured faster (ncu, C2: 11.6 + 5.9 us vs 14.7 + 7.7; C4: 115 vs 140 us), DESIGN 6.3
-        const char* ge = std::getenv("CSK_GSTAGE");
-        const bool splitk = k2 <= 256 && ro.cw <= 8 * kGsNT && ge && std::strcmp(ge, "splitk") == 0;
-        if (s == CSK_OK && splitk) {
-            const int nsm = device_info().num_sms;
-            const int64_t kslice = std::max<int64_t>(4, (ceil_div(k1, (int64_t)nsm) + 3) & ~(int64_t)3);
-            const int nsl = (int)ceil_div(k1, kslice);
-            double* part = nullptr;
-            CSK_CUDA_TRY(csk_malloc_async(&part, (size_t)nsl * k2 * ro.cw * 8, st));
-            auto kern = k2 <= 64 ? gs_splitk_kernel<1> : k2 <= 128 ? gs_splitk_kernel<2>
-                      : k2 <= 192 ? gs_splitk_kernel<3> : gs_splitk_kernel<4>;
-            for (int c0 = 0; s == CSK_OK && c0 < ro.ncols; c0 += ro.cw) {
-                const int nc = std::min(ro.cw, ro.ncols - c0);
-                const double* Bt = ro.ws + (int64_t)(c0 / ro.cw) * ro.cs;
-                kern<<<nsl, kGsWarps * 32, 0, st>>>((const double*)G, (int)k2, k1, Bt, ro.lc, nc, kslice, part);
-                count_launch();
-                gs_reduce_kernel<<<(unsigned)ceil_div((int64_t)k2 * nc, 32), 256, 0, st>>>(
-                    part, nsl, (int)k2, nc, (double*)Z + (int64_t)c0 * ldz, ldz);
-                count_launch();
-                if (cudaGetLastError() != cudaSuccess) {
-                    set_error("split-K G-stage launch failed");
-                    s = CSK_ECUDA;
-                }
-            }
-            cudaFreeAsync(part, st);
-            cudaFreeAsync(ro.ws, st);
-            cudaFreeAsync(SA, st);
-            return s;
-        }
-        cublasHandle_t h;
-        if (s == CSK_OK) s = blas_handle(st, &h);
-        const double one = 1.0, zero = 0.0;
-        for (int c0 = 0; s == CSK_OK && c0 < ro.ncols; c0 += ro.cw) {
-            // chunk columns c0 .. c0+nc of SA are rows of SA^T: as a column-major (nc x k1) matrix
-            // with ld lc starting at chunk * cs, it is SA[:, chunk]^T
-            const int nc = std::min(ro.cw, ro.ncols - c0);
-            const double* Bt = ro.ws + (int64_t)(c0 / ro.cw) * ro.cs;
-            const cublasStatus_t bs = cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, (int)k2, nc, (int)k1, &one,
-                                                  (const double*)G, (int)k2, Bt, (int)ro.lc, &zero,
-                                                  (double*)Z + (int64_t)c0 * ldz, (int)ldz);
-            if (bs != CUBLAS_STATUS_SUCCESS) {
-                set_error("cuBLAS G-stage GEMM failed (%d)", (int)bs);
-                s = CSK_ECUDA;
-            }
-        }
-        cudaFreeAsync(ro.ws, st);
+        double* SA = nullptr;
+        CSK_CUDA_TRY(csk_malloc_async(&SA, (size_t)k1 * ncols * 8, st));
+        s = cudaMemsetAsync(SA, 0, (size_t)k1 * ncols * 8, st) == cudaSuccess ? CSK_OK : CSK_ECUDA;
+        if (s == CSK_OK) s = sketch_host_rows(plan, n, (const double*)A, lda, (const double*)b, SA, k1, st);
+        if (s == CSK_OK) s = rows_from_colmajor(SA, k1, k1, (int)ncols, &ro, st);
         cudaFreeAsync(SA, st);
+    } else {
+        s = cs_apply_impl(plan, dtype, n, A, lda, b, nullptr, k1, CSK_VAR_AUTO, st, 0, plan->d, false, &ro);
+    }
+    if (s != CSK_OK) {
+        if (ro.ws) cudaFreeAsync(ro.ws, st);
         return s;
     }
-    if (s == CSK_OK) {
-        const void* G = nullptr;
-        s = gauss_get(plan, k2, dtype, st, &G);
-        if (s == CSK_OK) {
-            cublasHandle_t h;
-            s = blas_handle(st, &h);
-            if (s == CSK_OK) {
-                cublasStatus_t bs;
-                if (dtype == CSK_F64) {
-                    const double one = 1.0, zero = 0.0;
-                    bs = cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)k2, (int)ncols, (int)k1, &one, (const double*)G,
-                                     (int)k2, (const double*)SA, (int)k1, &zero, (double*)Z, (int)ldz);
-                } else {
-                    const float one = 1.0f, zero = 0.0f;
-                    bs = cublasSgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)k2, (int)ncols, (int)k1, &one, (const float*)G,
-                                     (int)k2, (const float*)SA, (int)k1, &zero, (float*)Z, (int)ldz);
-                }
-                if (bs != CUBLAS_STATUS_SUCCESS) {
-                    set_error("cuBLAS G-stage GEMM failed (%d)", (int)bs);
-                    s = CSK_ECUDA;
-                }
-            }
-        }
+    // a regular (one-row) layout wider than the G-stage's chunk is the same memory cut into 64-column chunks
+    if (ro.cw > kGstageMaxCw) {
+        ro.cw = 64;
+        ro.cs = 64;
     }
-    cudaFreeAsync(SA, st);
+    // a4 + a5: G from the plan (drawn once per k2), Z = G Y on the fp64 tensor pipe (fp32 input: the
+    // sketch was accumulated in fp64, R12, and Z is rounded to fp32 once)
+    const double* G = nullptr;
+    int64_t ldg = 0;
+    s = gauss_get(plan, k2, st, &G, &ldg);
+    if (s == CSK_OK) s = gstage_launch(G, ldg, k2, k1, ro, Z, ldz, dtype == CSK_F32, st);
+    cudaFreeAsync(ro.ws, st);
     return s;
 }
 

@@ -439,7 +439,6 @@ void cs_plan_destroy(csk_plan_t plan) {
     cudaFree(plan->offsets);
     cudaFree(plan->perm);
     for (auto& kv : plan->gauss64) cudaFree(kv.second);
-    for (auto& kv : plan->gauss32) cudaFree(kv.second);
     delete plan;
 }
 

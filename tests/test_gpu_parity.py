@@ -269,13 +269,13 @@ def test_gauss_matches_oracle():
         check_le(np.abs(Z - G @ S).max(), 1e-13 / np.sqrt(k2), "max |G_gpu - G_oracle|")
 
 
-@pytest.mark.parametrize("transpose", ["0", "1"])
 @pytest.mark.parametrize("d,n,k1,k2", [(4096, 8, 128, 16), (20000, 16, 512, 32), (5000, 3, 18, 6),
-                                       (30011, 129, 4096, 260), (200003, 64, 131072, 130)])
-def test_ms_apply_matches_oracle(monkeypatch, transpose, d, n, k1, k2):
-    # default: the G-stage runs on the CountSketch's row-major SA^T (Z = G (SA^T)^T per column chunk,
-    # P:L228), including 2-chunk (129 + b) and chunk-major (k1 = 131072) layouts; "1" = transpose + NN GEMM
-    monkeypatch.setenv("CSK_MS_TRANSPOSE", transpose)
+                                       (30011, 129, 4096, 260), (200003, 64, 131072, 130), (7001, 5, 1000, 1),
+                                       (9000, 70, 4096, 65), (12000, 10, 600, 191), (4099, 65, 777, 64),
+                                       (100003, 64, 8192, 128), (30011, 128, 32768, 256)])
+def test_ms_apply_matches_oracle(d, n, k1, k2):
+    # the hand-written DMMA G-stage (gstage.cu) on the CountSketch's row-major SA^T: one chunk (C2-like),
+    # two chunks (129 + b), chunk-major (k1 = 131072), k2 not a multiple of 8, k1 not a multiple of 32
     plan = csk.cs_plan(d, k1, 3)
     A = synth.gaussian_matrix(d, n, seed=1)
     b = synth.rhs(A, "easy", seed=1)
@@ -284,21 +284,63 @@ def test_ms_apply_matches_oracle(monkeypatch, transpose, d, n, k1, k2):
     assert_within_T(Z, Zo, Zabs, 1e-12)
 
 
-@pytest.mark.parametrize("gstage", ["splitk", "cublas"])
-@pytest.mark.parametrize("d,n,k1,k2", [(100003, 64, 8192, 128), (30011, 128, 32768, 256), (5000, 3, 18, 6),
-                                       (7001, 5, 1000, 1), (9000, 70, 4096, 65), (12000, 10, 600, 191),
-                                       (4099, 65, 777, 64), (50000, 200, 131072, 200)])
-def test_ms_apply_gstage_paths(monkeypatch, gstage, d, n, k1, k2):
-    # the split-K DMMA G-stage (k2 <= 256: K-slices per SM, fixed-order partial sum) and cuBLAS
-    monkeypatch.setenv("CSK_GSTAGE", gstage)
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("d,n,k1,k2", [(9000, 70, 4096, 65), (50000, 100, 2048, 200), (3001, 4, 64, 8)])
+def test_ms_apply_every_countsketch_variant(monkeypatch, variant, d, n, k1, k2):
+    # every CountSketch variant feeds the same G-stage: row-major workspaces directly (T, B, X; T's
+    # one-row layout wider than 72 columns is re-cut into 64-column chunks), column-major ones (L, S, G)
+    # through the row-major conversion
+    monkeypatch.setenv("CSK_VARIANT", str(csk.csk.VARIANTS[variant]))
+    plan = csk.cs_plan(d, k1, 4, sort=(variant == "G"))
+    A = synth.gaussian_matrix(d, n, seed=5)
+    b = synth.rhs(A, "hard", seed=5)
+    Z = host(csk.ms_apply(plan, k2, gpu_colmajor(A), b=gpu_colmajor(b)))
+    Zo, Zabs = oracle.ms_apply(A, k1, k2, seed=4, b=b, with_abs=True)
+    assert_within_T(Z, Zo, Zabs, 1e-12)
+
+
+def test_ms_apply_gstage_large_k2_and_k1():
+    # k2 = 512, k1 = 131072 (C3's G-stage shape): 4 M-tiles, stream-K over 5 chunk-major chunks
+    d, n, k1, k2 = 300007, 256, 131072, 512
     plan = csk.cs_plan(d, k1, 6)
     A = synth.gaussian_matrix(d, n, seed=2)
     b = synth.rhs(A, "hard", seed=2)
     Z = host(csk.ms_apply(plan, k2, gpu_colmajor(A), b=gpu_colmajor(b)))
     Zo, Zabs = oracle.ms_apply(A, k1, k2, seed=6, b=b, with_abs=True)
     assert_within_T(Z, Zo, Zabs, 1e-12)
-    Z2 = host(csk.ms_apply(plan, k2, gpu_colmajor(synth.integer_matrix(d, n, seed=3))))
-    assert np.all(np.isfinite(Z2))
+
+
+@pytest.mark.parametrize("ctas", ["1", "3", "7", "1000"])
+def test_ms_apply_gstage_any_split_deterministic(monkeypatch, ctas):
+    # the stream-K split (1 CTA = no split, ragged splits, more CTAs than k-blocks): same tolerance,
+    # and each split is bitwise reproducible (fixed-order partial sums)
+    monkeypatch.setenv("CSK_GS_CTAS", ctas)
+    d, n, k1, k2 = 60000, 70, 4000, 140
+    plan = csk.cs_plan(d, k1, 2)
+    Ai = synth.integer_matrix(d, n, seed=3)
+    A = synth.gaussian_matrix(d, n, seed=3)
+    Ad = gpu_colmajor(A)
+    Z1 = host(csk.ms_apply(plan, k2, Ad))
+    Z2 = host(csk.ms_apply(plan, k2, Ad))
+    Zo, Zabs = oracle.ms_apply(A, k1, k2, seed=2, with_abs=True)
+    assert_within_T(Z1, Zo, Zabs, 1e-12)
+    # the CountSketch's atomics reorder SA's sums, so bitwise reproducibility is checked on integer A
+    Zi1 = host(csk.ms_apply(plan, k2, gpu_colmajor(Ai)))
+    Zi2 = host(csk.ms_apply(plan, k2, gpu_colmajor(Ai)))
+    assert np.array_equal(Zi1, Zi2)
+    del Z2
+
+
+def test_ms_apply_fp32_input():
+    # fp32 [A b]: the sketch accumulates in fp64 (R12), the G-stage runs in fp64, Z is rounded once
+    d, n, k1, k2 = 40000, 33, 2048, 66
+    plan = csk.cs_plan(d, k1, 8)
+    A = synth.gaussian_matrix(d, n, seed=4, dtype=np.float32)
+    b = synth.gaussian_matrix(d, 1, seed=5, dtype=np.float32)[:, 0]
+    Z = host(csk.ms_apply(plan, k2, gpu_colmajor(A), b=gpu_colmajor(b)))
+    assert Z.dtype == np.float32
+    Zo, Zabs = oracle.ms_apply(A, k1, k2, seed=8, b=b, with_abs=True)
+    assert_within_T(Z, Zo, Zabs, 1e-5)
 
 
 # every small-solve kernel (csrc/qr_wy.cu default, forced wider clusters, and the older
