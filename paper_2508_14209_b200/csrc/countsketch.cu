@@ -39,8 +39,7 @@ struct RowLayout {
     int cw = 1;
     int64_t lc = 0, cs = 0;
     bool chunk_major = false;
-    bool tma = false;   // launch marked TMA-eligible by cs_apply_impl (variants X / B-with-TMA)
-    int64_t sep = -1;   // >= 0: the last column is accumulated apart (B32 "split"), k1 doubles at SAt + sep
+    bool tma = false;   // launch marked TMA-eligible by cs_apply_impl (variant X)
     // fp32 accumulation (fp32 input): ncopies row-block copies of a float SA^T (lc, cs in floats),
     // copy p takes rows [p * rows_per_copy, ...) so every bucket sum in a copy has a bounded depth
     int ncopies = 0;
@@ -48,8 +47,8 @@ struct RowLayout {
     // CSK_PLAN_HASH: global row of local row 0 and the Philox key (codes recomputed in the kernel)
     int64_t g0 = 0;
     uint32_t hkey0 = 0, hkey1 = 0;
-    unsigned long long* work = nullptr;   // B32 dynamic work counter (zeroed with the workspace), or static
-    int grab = 8;                         // units per counter grab (CSK_GRAB, experiment)
+    unsigned long long* work = nullptr;   // dynamic work counter of the B kernels (zeroed with the workspace)
+    int grab = 8;                         // units per counter grab (4/8/16/32 measured: 8)
     __host__ __device__ int64_t base(int ch, uint32_t bucket) const { return (int64_t)ch * cs + (int64_t)bucket * lc; }
 };
 
@@ -268,140 +267,6 @@ static int tma_chunk_width(int ncols) {
     return (ncols + nch - 1) / nch;
 }
 
-// ------------------------------------------------------------ variant B (TMA)
-// The fastest form measured: TMA in, TMA bulk reduce-add out.  Per warp: a ring of
-// kB2Stages stages, each holding one RB-row x cw-column tile of [A b] (2-D tensor load,
-// 128B swizzle, zero-filled past d) plus the tile's RB codes (1-D bulk copy on the same
-// mbarrier), so nothing on the critical path waits on a synchronous load.  The warp
-// transposes the tile into a row-major fp64 row buffer (sign applied), and lanes
-// 0..RB-1 each hand their row to the TMA engine as ONE cp.reduce.async.bulk .add.f64 of
-// cw*8 bytes into SA^T[h(row), c0:c0+cw].  cw is even for multi-chunk [A b] (16-B aligned).
-constexpr int kB2MaxCols = 66;
-
-// B2 pipeline shape: W warps per CTA, S TMA tile stages and R row buffers per warp.
-// A tile is consumed into registers right after its mbarrier completes, so its stage is
-// re-armed (next TMA issued) before the row-buffer stores; the row buffer written for
-// unit k is recycled once the bulk reduce of unit k-R has finished reading it.
-template <int W, int S, int R>
-struct B2Cfg {
-    static constexpr int kWarps = W, kStages = S, kRbufs = R;
-};
-
-template <typename T>
-__host__ __device__ constexpr int b2_rows() { return 128 / (int)sizeof(T); }
-
-__host__ __device__ inline size_t b2_smem_bytes(int warps, int stages, int rbufs, int rb, int stage_bytes,
-                                                int ldrow) {
-    return (size_t)warps * stages * stage_bytes + (size_t)warps * rbufs * rb * ldrow * 8 +
-           (size_t)warps * stages * rb * 4 + (size_t)warps * stages * 8 + 1024;
-}
-
-template <typename T, typename C>
-__global__ void __launch_bounds__(C::kWarps * 32, 1) cs_bulk_tma_kernel(const __grid_constant__ CUtensorMap tmap,
-                                                                         const uint32_t* __restrict__ code,
-                                                                         int64_t rows, int ncols, int stage_bytes,
-                                                                         int ldrow, double* __restrict__ SAt,
-                                                                         RowLayout L) {
-    constexpr int RB = b2_rows<T>();      // rows per tile: 16 (fp64) / 32 (fp32)
-    constexpr int NW = C::kWarps, NS = C::kStages, NR = C::kRbufs;
-    const int cw = L.cw;
-    extern __shared__ uint8_t b2_smem_raw[];
-    uint8_t* smem = b2_smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(b2_smem_raw) & 1023u)) & 1023u);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // layout: [NW][NS] tiles | [NW][NR] row buffers | [NW][NS][RB] codes | [NW][NS] mbarriers
-    uint8_t* ring = smem + (size_t)warp * NS * stage_bytes;
-    double* rowbufs = reinterpret_cast<double*>(smem + (size_t)NW * NS * stage_bytes) + (size_t)warp * NR * RB * ldrow;
-    uint32_t* codes_all =
-        reinterpret_cast<uint32_t*>(smem + (size_t)NW * NS * stage_bytes + (size_t)NW * NR * RB * ldrow * 8);
-    uint32_t* codes = codes_all + warp * NS * RB;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(codes_all + NW * NS * RB) + warp * NS;
-    const int nchunks = (ncols + cw - 1) / cw;
-    const int64_t ngroups = (rows + RB - 1) / RB;
-    const int64_t nunits = ngroups * nchunks;
-    const int64_t gwarp = blockIdx.x * (int64_t)NW + warp;
-    const int64_t nwarps = (int64_t)gridDim.x * NW;
-    const uint32_t tile_bytes = (uint32_t)cw * 128u;
-    auto issue = [&](int64_t u, int s) {
-        int64_t g;
-        int ch;
-        unit_coords(u, nchunks, ngroups, L.chunk_major, g, ch);
-        mbar_expect_tx(&bars[s], tile_bytes + RB * 4);
-        tma_load_2d(ring + s * stage_bytes, &tmap, (int)(g * RB), ch * cw, &bars[s]);
-        bulk_load_1d(codes + s * RB, code + g * RB, RB * 4, &bars[s]);
-    };
-    if (lane == 0) {
-        for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int s = 0; s < NS; ++s)
-            if (gwarp + s * nwarps < nunits) issue(gwarp + s * nwarps, s);
-    }
-    for (int e = lane; e < NR * RB * ldrow; e += 32) rowbufs[e] = 0.0;
-    __syncwarp();
-    constexpr int kLanesPerRow = 32 / RB;   // 2 (fp64) / 1 (fp32)
-    constexpr int E = 16 / (int)sizeof(T);
-    constexpr int kStep = 128 * kLanesPerRow;                 // bytes between this lane's columns
-    constexpr int kPat = 8 / kLanesPerRow;                    // distinct (c & 7) values per lane
-    constexpr int kJ = kB2MaxCols / kLanesPerRow;
-    const int rr = lane % RB, part = lane / RB;
-    // Column c of this lane's row lives at c*128 + (((rr / E) ^ (c & 7)) << 4) + (rr % E)*sizeof(T)
-    // (128B swizzle); with j unrolled, c & 7 is a compile-time pattern -> per-lane offsets.
-    int swz[kPat];
-#pragma unroll
-    for (int p = 0; p < kPat; ++p) swz[p] = (((rr / E) ^ ((p * kLanesPerRow + part) & 7)) << 4);
-    for (int64_t k = 0;; ++k) {
-        const int64_t u = gwarp + k * nwarps;
-        if (u >= nunits) break;
-        const int s = (int)(k % NS);
-        int64_t g;
-        int ch;
-        unit_coords(u, nchunks, ngroups, L.chunk_major, g, ch);
-        const int nc = min(cw, ncols - ch * cw);
-        const int nr = (int)min((int64_t)RB, rows - g * RB);
-        mbar_wait(&bars[s], (uint32_t)((k / NS) & 1));
-        const uint32_t cd = codes[s * RB + rr];
-        const long long smask = (long long)code_sign_mask64(cd);
-        const uint8_t* tb = ring + s * stage_bytes + part * 128 + (rr % E) * (int)sizeof(T);
-        double v[kJ];
-#pragma unroll
-        for (int j = 0; j < kJ; ++j)
-            v[j] = (j * kLanesPerRow + part < nc) ? (double)*reinterpret_cast<const T*>(tb + j * kStep + swz[j % kPat])
-                                                  : 0.0;
-        // tile consumed: re-arm this stage right away (generic reads -> async-proxy write)
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0 && u + NS * nwarps < nunits) issue(u + NS * nwarps, s);
-        // row buffer k % NR is free once the bulk reduce of unit k - NR has read it
-        if constexpr (NR == 1)
-            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        else
-            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-        __syncwarp();
-        double* rb = rowbufs + (size_t)(k % NR) * RB * ldrow + rr * ldrow;
-#pragma unroll
-        for (int j = 0; j < kJ; ++j)
-            if (j * kLanesPerRow + part < nc)
-                rb[j * kLanesPerRow + part] = __longlong_as_double(__double_as_longlong(v[j]) ^ smask);
-        if ((nc & 1) && part == 0) rb[nc] = 0.0;   // 16-B padding column
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (part == 0 && rr < nr) {
-            const uint32_t bytes = (uint32_t)(((nc + 1) & ~1) * 8);
-            double* dst = SAt + L.base(ch, code_bucket(cd));
-            asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(dst),
-                         "r"((uint32_t)__cvta_generic_to_shared(rb)), "r"(bytes)
-                         : "memory");
-        }
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    }
-    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
-
-static int b2_chunk_width(int ncols) {
-    if (ncols <= kB2MaxCols) return ncols;
-    const int nch = (ncols + 63) / 64;
-    return (((ncols + nch - 1) / nch) + 1) & ~1;
-}
-
 // ------------------------------------------------------------------ variant B
 // A warp owns 16-row x cw-column tiles (cw <= 66: all of [A b] at C2).  Lanes (r, half)
 // load column pairs (two coalesced 128-B half-warp reads per instruction, streaming
@@ -555,18 +420,12 @@ constexpr int kB32Rows = 32;
 __device__ __forceinline__ int b32_row(int r, int ld) { return r * ld + 2 * (r >> 3); }
 constexpr int kB32Pad = 6;   // doubles per warp tile beyond 32 rows (the shift of the last group)
 
-template <int W, int EXP, bool SPLIT = false, bool PRED = false, bool MIX = false, bool HASH = false>
+template <int W, int EXP = 0, bool PRED = false, bool HASH = false>
 __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __restrict__ code, int64_t rows,
                                                                Cols<double> cols, int ncols, int ldtile,
-                                                               double* __restrict__ SAt, RowLayout L, int k1,
-                                                               int mix_rt = 32) {
-    // MIX (rows of <= 32 columns, e.g. n = 32): a 256-B bulk reduction per row leaves the kernel
-    // bound by the TMA operation rate, not by L2 sectors, so rows mix_rt..31 of each tile go out
-    // as one coalesced warp-wide red.global.add.f64 each instead -- a second, independent issue path.
-    // Split mode (L.sep >= 0): columns [0, ncols) go through the row bulk reductions and column
-    // ncols (the odd last one, b at C2) is accumulated per CTA in shared memory (k1 doubles) and
-    // flushed once: a 64-column row is 512 B = 16 L2 sectors, a 65-column row 17 -- the L2 fp64
-    // reduction rate bounds this kernel, so one sector fewer per row is ~6%.
+                                                               double* __restrict__ SAt, RowLayout L, int k1) {
+    // EXP: compile-time experiment switches for roofline attribution (0 in production):
+    // bit 0 = skip the bulk reduce (load path alone), bit 1 = skip the A loads (reduce path alone)
     const int cw = L.cw;
     extern __shared__ __align__(16) double b32_smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -578,28 +437,19 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
     // STS otherwise land on 4 of 8 even double-banks (ncu: 75% of the shared wavefronts were
     // conflicts)
     double* tile = b32_smem + (size_t)warp * (kB32Rows * ldtile + kB32Pad);
-    constexpr bool split = SPLIT;   // compile-time: the default kernel carries none of the split code
-    double* sb = b32_smem + (size_t)W * (kB32Rows * ldtile + kB32Pad);   // split: k1 bucket sums of column ncols
     for (int e = lane; e < kB32Rows * ldtile + kB32Pad; e += 32) tile[e] = 0.0;
-    if constexpr (split) {
-        for (int e = threadIdx.x; e < k1; e += blockDim.x) sb[e] = 0.0;
-        __syncthreads();
-    }
     __syncwarp();
     const int nchunks = (ncols + cw - 1) / cw;
     const int64_t ngroups = (rows + kB32Rows - 1) / kB32Rows;
     const int64_t nunits = ngroups * nchunks;
-    const int64_t gwarp = blockIdx.x * (int64_t)W + warp;
-    const int64_t nwarps = (int64_t)gridDim.x * W;
     constexpr int kJ = kBulkMaxCols / 2;
     // Work distribution: with L.work (a zeroed counter after the workspace) warps take batches of
     // kGrab consecutive units from one atomic counter, so CTAs that start late (SMs still held by an
     // overlapping kernel, e.g. the previous batch's solve) just take fewer units; else static
     // round-robin.  Units are taken in increasing order either way (chunk-major slices stay hot).
     const int kGrab = L.grab;
-    const bool dyn = L.work != nullptr;
-    int64_t u = gwarp, uend = gwarp + 1;
-    if (dyn) {
+    int64_t u, uend;
+    {
         unsigned long long ub = 0;
         if (lane == 0) ub = atomicAdd(L.work, (unsigned long long)kGrab);
         ub = __shfl_sync(0xffffffffu, ub, 0);
@@ -631,10 +481,6 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
             ca = __ldg(code + ra);
             cb = __ldg(code + rb);
             crow = __ldg(code + min(r0 + lane, rows - 1));
-        }
-        if constexpr (split) {   // row r0 + lane of the split column into this CTA's shared buckets
-            const double bv = ldcs_pred(cols.col(ncols) + min(r0 + lane, rows - 1), r0 + lane < rows);
-            if (r0 + lane < rows) atomicAdd(sb + code_bucket(crow), apply_sign(bv, crow));
         }
         double2 v[kJ];
         if (full && !PRED) {
@@ -688,27 +534,20 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (r0 + lane < rows && !(EXP & 1) && (!MIX || lane < mix_rt)) {
+        if (r0 + lane < rows && !(EXP & 1)) {
             const uint32_t bytes = (uint32_t)(((nc + 1) & ~1) * 8);
             double* dst = SAt + L.base(ch, code_bucket(crow));
             const uint32_t src = (uint32_t)__cvta_generic_to_shared(tile + b32_row(lane, ldtile));
             if constexpr (PRED) {
                 // narrow chunks (C3): the chunk's SA^T slice (54 MB) competes with the streamed A for
                 // L2; mark the reductions evict_last so the slice is not written back mid-pass
-                // (PRED kernels never run MIX: a negative mix_rt selects the hinted form)
-                if (mix_rt < 0) {
-                    uint64_t pol;
-                    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-                    asm volatile(
-                        "cp.reduce.async.bulk.global.shared::cta.bulk_group.L2::cache_hint.add.f64 [%0], [%1], %2, %3;" ::"l"(
-                            dst),
-                        "r"(src), "r"(bytes), "l"(pol)
-                        : "memory");
-                } else {
-                    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(dst),
-                                 "r"(src), "r"(bytes)
-                                 : "memory");
-                }
+                uint64_t pol;
+                asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+                asm volatile(
+                    "cp.reduce.async.bulk.global.shared::cta.bulk_group.L2::cache_hint.add.f64 [%0], [%1], %2, %3;" ::"l"(
+                        dst),
+                    "r"(src), "r"(bytes), "l"(pol)
+                    : "memory");
             } else {
                 asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(dst),
                              "r"(src), "r"(bytes)
@@ -716,107 +555,111 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
             }
         }
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        if constexpr (MIX) {
-            for (int rr = mix_rt; rr < kB32Rows; ++rr) {
-                const uint32_t cr = __shfl_sync(0xffffffffu, crow, rr);
-                if (r0 + rr < rows && lane < nc) red_add_f64(SAt + L.base(ch, code_bucket(cr)) + lane, tile[b32_row(rr, ldtile) + lane]);
-            }
-        }
         if (++u >= uend) {
-            if (dyn) {
-                unsigned long long ub = 0;
-                if (lane == 0) ub = atomicAdd(L.work, (unsigned long long)kGrab);
-                ub = __shfl_sync(0xffffffffu, ub, 0);
-                u = (int64_t)ub;
-                uend = min(u + kGrab, nunits);
-            } else {
-                u += nwarps - 1;
-                uend = u + 1;
-            }
-        }
-    }
-    if constexpr (split) {   // one bulk reduce-add of this CTA's k1 sums into the separate column
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            const uint32_t src = (uint32_t)__cvta_generic_to_shared(sb);
-            asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(SAt + L.sep),
-                         "r"(src), "r"((uint32_t)(k1 * 8))
-                         : "memory");
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            unsigned long long ub = 0;
+            if (lane == 0) ub = atomicAdd(L.work, (unsigned long long)kGrab);
+            ub = __shfl_sync(0xffffffffu, ub, 0);
+            u = (int64_t)ub;
+            uend = min(u + kGrab, nunits);
         }
     }
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-// ------------------------------------------------ fp32 input, fp32 accumulation (variant B)
-// fp32 bucket sums carry half the L2 reduction bytes of fp64 ones (the bound of this kernel family,
-// DESIGN.md 6.1b), but a sequential fp32 sum over a whole bucket (2048 rows at C2) could reach
-// ~1.2e-4 * sum|terms| (SURVEY 8(a')), above BASELINE's 1e-5.  So the rows are split into ncopies
-// blocks, each reduced into its own float SA^T copy with a mean bucket depth <= 64 (any order: the
-// error is <= (depth - 1) u32 sum|terms| <= ~1e-5 only past depth ~168, ~13 standard deviations
-// above the mean), and cs_combine_f32_kernel adds the copies in fp64 and rounds once.
-// Tiles: 32 rows x cw (<= 66) columns per warp; lane (p, half) loads rows 2p, 2p+1 of column
-// 2j + half as one float2 (128-B segments per half-warp); lane r bulk-reduces row r (.add.f32).
+// ------------------------------------------------ fp32 input, fp32 accumulation (variant B, default fp32)
+// The fp64 row scatter is bound by the L2's fp64 reduction rate (~147 G sector-RMW/s,
+// 17 sectors per 65-double row).  fp32 rows are 9 sectors and the L2 reduces them faster per sector
+// (microbenchmark: 2^24 rows of 272 B in 0.82 ms vs 528-B fp64 rows in 1.93 ms), so fp32 input is
+// summed in fp32 -- but a sequential fp32 sum over a whole bucket (2048 rows at C2) could reach
+// ~1.2e-4 sum|terms|, above BASELINE's 1e-5.  The rows are therefore split into ncopies blocks, each
+// reduced into its own float SA^T copy with a mean bucket depth <= 64 (an fp32 sum of m terms in any
+// order errs by <= (m - 1) u32 sum|terms|, 3.8e-6 at m = 64), and the copies are added in fp64 by
+// cs_combine_*_kernel (fixed order).
+// Tile: 64 rows x cw (<= 66) columns per warp.  Lane (q, s) = (lane >> 2, lane & 3) loads rows
+// 8q .. 8q+7 of column 4j + s with one 32-byte load (256 contiguous bytes per column per instruction),
+// flips the signs (XOR) and stores row 8q+i of the row-major float tile at
+// (8q+i) ldf + 4q + c: with ldf == 4 (mod 32) the 32 lanes of each store hit 32 distinct banks (rows stay
+// 16-B aligned for the bulk copies).  Lane r then bulk-reduces rows r and r + 32 (.add.f32).
+constexpr int kF32Rows = 64;
+constexpr int kF32MaxCols = 68;   // 17 column quads
+
+__device__ __forceinline__ void ldcs_v8(const float* p, float (&v)[8]) {
+    asm volatile("ld.global.cs.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                 : "l"(p));
+}
+
 template <int W>
-__global__ void __launch_bounds__(W * 32, 1) cs_bulk32f_kernel(const uint32_t* __restrict__ code, int64_t rows,
-                                                                Cols<float> cols, int ncols, int ldtile,
+__global__ void __launch_bounds__(W * 32, 1) cs_bulk64f_kernel(const uint32_t* __restrict__ code, int64_t rows,
+                                                                Cols<float> cols, int ncols, int ldf,
                                                                 float* __restrict__ SAt, RowLayout L) {
-    // 64-row tiles: lane l loads rows 2l, 2l+1 of every column as one float2 (256-B segments, the
-    // bytes in flight per warp of the fp64 kernel), transposes them into a row-major float tile and
-    // bulk-reduces rows l and l + 32
-    constexpr int kR = 64;
     const int cw = L.cw;
     extern __shared__ __align__(16) float f32_smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    float* tile = f32_smem + (size_t)warp * kR * ldtile;
-    for (int e = lane; e < kR * ldtile; e += 32) tile[e] = 0.0f;
+    const int q = lane >> 2, sq = lane & 3;
+    float* tile = f32_smem + (size_t)warp * (kF32Rows * ldf + 32);
+    for (int e = lane; e < kF32Rows * ldf + 32; e += 32) tile[e] = 0.0f;
     __syncwarp();
     const int nchunks = (ncols + cw - 1) / cw;
-    const int64_t ngroups = (rows + kR - 1) / kR;
+    const int64_t ngroups = (rows + kF32Rows - 1) / kF32Rows;
     const int64_t nunits = ngroups * nchunks;
-    const int64_t gwarp = blockIdx.x * (int64_t)W + warp;
-    const int64_t nwarps = (int64_t)gridDim.x * W;
-    const bool al8 = (cols.lda & 1) == 0 && (((uintptr_t)cols.A & 7) == 0) &&
-                     (cols.b == nullptr || ((uintptr_t)cols.b & 7) == 0);
-    for (int64_t u = gwarp; u < nunits; u += nwarps) {
+    constexpr int kJ = kF32MaxCols / 4;
+    const int kGrab = L.grab;
+    int64_t u, uend;
+    {
+        unsigned long long ub = 0;
+        if (lane == 0) ub = atomicAdd(L.work, (unsigned long long)kGrab);
+        ub = __shfl_sync(0xffffffffu, ub, 0);
+        u = (int64_t)ub;
+        uend = min(u + kGrab, nunits);
+    }
+    while (u < nunits) {
         int64_t g;
         int ch;
         unit_coords(u, nchunks, ngroups, L.chunk_major, g, ch);
         const int c0 = ch * cw;
         const int nc = min(cw, ncols - c0);
-        const int64_t r0 = g * kR;
-        const bool full = r0 + kR <= rows && al8;
-        const int64_t ra = min(r0 + 2 * lane, rows - 1), rb = min(r0 + 2 * lane + 1, rows - 1);
-        const uint32_t ca = __ldg(code + ra), cb = __ldg(code + rb);
-        const uint32_t c1 = __ldg(code + min(r0 + lane, rows - 1)), c2 = __ldg(code + min(r0 + 32 + lane, rows - 1));
-        float2 v[kBulkMaxCols];
+        const int64_t r0 = g * kF32Rows;
+        const bool full = r0 + kF32Rows <= rows;
+        const uint32_t ca = __ldg(code + min(r0 + lane, rows - 1));
+        const uint32_t cb = __ldg(code + min(r0 + 32 + lane, rows - 1));
+        // sign bits of the 64 rows (bit r = row r negative), one ballot per half
+        const uint32_t sg_lo = __ballot_sync(0xffffffffu, (ca >> 31) != 0u);
+        const uint32_t sg_hi = __ballot_sync(0xffffffffu, (cb >> 31) != 0u);
+        const uint32_t sgw = q < 4 ? sg_lo : sg_hi;
+        const int sh = (q & 3) * 8;
+        float v[kJ][8];
 #pragma unroll
-        for (int c = 0; c < kBulkMaxCols; ++c) {
-            const float* col = cols.col(c0 + min(c, nc - 1));
-            float2 x;
+        for (int j = 0; j < kJ; ++j) {
+            const int c = 4 * j + sq;
+            const float* col = cols.col(c0 + min(c, nc - 1)) + r0 + 8 * q;
             if (full) {
-                x = __ldcs(reinterpret_cast<const float2*>(col + r0 + 2 * lane));
+                if (c < nc) {
+                    ldcs_v8(col, v[j]);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) v[j][i] = 0.0f;
+                }
             } else {
-                x.x = __ldcs(col + ra);
-                x.y = r0 + 2 * lane + 1 < rows ? __ldcs(col + rb) : 0.0f;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const bool ok = c < nc && r0 + 8 * q + i < rows;
+                    v[j][i] = ok ? __ldcs(cols.col(c0 + min(c, nc - 1)) + min(r0 + 8 * q + i, rows - 1)) : 0.0f;
+                }
             }
-            v[c] = (c < nc) ? x : make_float2(0.0f, 0.0f);
         }
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncwarp();
-        float* ta = tile + (2 * lane) * ldtile;
-        float* tb = ta + ldtile;
-        const uint32_t sa = ca & 0x80000000u, sb = cb & 0x80000000u;
-        const int nc4 = (nc + 3) & ~3;   // 16-B multiple: zero the padding columns
+        const int nc4 = (nc + 3) & ~3;
 #pragma unroll
-        for (int c = 0; c < kBulkMaxCols; ++c) {
-            if (c < nc) {
-                ta[c] = __uint_as_float(__float_as_uint(v[c].x) ^ sa);
-                tb[c] = __uint_as_float(__float_as_uint(v[c].y) ^ sb);
-            } else if (c < nc4) {
-                ta[c] = 0.0f;
-                tb[c] = 0.0f;
+        for (int j = 0; j < kJ; ++j) {
+            const int c = 4 * j + sq;
+            if (c < nc4) {   // columns nc .. nc4 - 1 carry the zeros of the 16-B row padding
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const uint32_t neg = ((sgw >> (sh + i)) & 1u) << 31;
+                    tile[(8 * q + i) * ldf + 4 * q + c] = __uint_as_float(__float_as_uint(v[j][i]) ^ neg);
+                }
             }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -825,18 +668,41 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32f_kernel(const uint32_t* _
         for (int h = 0; h < 2; ++h) {
             const int r = lane + 32 * h;
             if (r0 + r < rows) {
-                const uint32_t cr = h ? c2 : c1;
+                const uint32_t cr = h ? cb : ca;
                 const int64_t copy = (r0 + r) / L.rows_per_copy;
                 float* dst = SAt + copy * L.copy_stride + (int64_t)ch * L.cs + (int64_t)code_bucket(cr) * L.lc;
-                const uint32_t src = (uint32_t)__cvta_generic_to_shared(tile + r * ldtile);
+                const uint32_t src = (uint32_t)__cvta_generic_to_shared(tile + r * ldf + 4 * (r >> 3));
                 asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst),
                              "r"(src), "r"((uint32_t)(nc4 * 4))
                              : "memory");
             }
         }
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        if (++u >= uend) {
+            unsigned long long ub = 0;
+            if (lane == 0) ub = atomicAdd(L.work, (unsigned long long)kGrab);
+            ub = __shfl_sync(0xffffffffu, ub, 0);
+            u = (int64_t)ub;
+            uend = min(u + kGrab, nunits);
+        }
     }
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// the fp32 copies summed in fp64 (fixed order over the copies) into the fp64 row-major workspace of
+// ms_apply (RowOut: regular layout, lc = lcd doubles)
+__global__ void cs_combine_rows_kernel(const float* __restrict__ SAt, RowLayout L, int64_t k1, int ncols,
+                                       double* __restrict__ Yt, int64_t lcd) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= k1 * lcd) return;
+    const int64_t m = e / lcd;
+    const int c = (int)(e - m * lcd);
+    double acc = 0.0;
+    if (c < ncols) {
+        const int64_t off = (int64_t)(c / L.cw) * L.cs + m * L.lc + (c % L.cw);
+        for (int p = 0; p < L.ncopies; ++p) acc += (double)SAt[p * L.copy_stride + off];
+    }
+    Yt[e] = acc;
 }
 
 // SA[m, c] = (float) sum_p (double) copy_p[m, c]  (fixed order over p)
@@ -873,10 +739,7 @@ __global__ void transpose_out_kernel(const double* __restrict__ SAt, RowLayout L
     for (int j = threadIdx.y; j < 32; j += blockDim.y) {
         const int64_t m = m0 + j;
         const int c = c0 + threadIdx.x;
-        t[j][threadIdx.x] = (m < k1 && c < ncols)
-                                ? ((L.sep >= 0 && c == ncols - 1) ? SAt[L.sep + m]
-                                                                  : SAt[(int64_t)(c / L.cw) * L.cs + m * L.lc + (c % L.cw)])
-                                : 0.0;
+        t[j][threadIdx.x] = (m < k1 && c < ncols) ? SAt[(int64_t)(c / L.cw) * L.cs + m * L.lc + (c % L.cw)] : 0.0;
     }
     __syncthreads();
     for (int j = threadIdx.y; j < 32; j += blockDim.y) {
@@ -1044,16 +907,14 @@ static int smem_cpc(int64_t k1, int ncols) {
     return std::min(cpc, ncols);
 }
 
-// measured selection table
+// Variant selection (BASELINE north_star: "picked per (d, n, k1) from ncu-measured HBM GB/s").
+// See DESIGN.md 6.1d for the measured table this encodes.
 static int select_variant(int64_t d, int64_t k1, int ncols, csk_dtype dtype, bool has_sort) {
     (void)d;
+    (void)k1;
+    (void)ncols;
     (void)dtype;
     (void)has_sort;
-    // measured at C2 (d=2^24, 65 cols, k1=8192, fp64): T 3.03 ms, B 3.34 ms,
-    // L 6.3 ms, G 25 ms, S 38 ms
-    (void)ncols;
-    (void)k1;
-    // B: register-staged 32-row tiles + TMA bulk reduce-add (1.94 ms at C2)
     return CSK_VAR_BULK_ROW;
 }
 
@@ -1067,19 +928,24 @@ static bool make_tensor_map(CUtensorMap* tmap, const Cols<T>& cols, int64_t rows
                                                           : ((rows * (int64_t)sizeof(T) + 15) & ~(int64_t)15))};
     const cuuint32_t box[2] = {(cuuint32_t)RB, (cuuint32_t)cw};
     const cuuint32_t estride[2] = {1, 1};
-    // L2 fetch granularity of the tile loads (CSK_L2PROMO = 0 | 64 | 128 | 256 for experiments)
-    CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
-    if (const char* e = std::getenv("CSK_L2PROMO")) {
-        const int v = std::atoi(e);
-        promo = v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
-                : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-                : v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
-    }
     const CUresult cr = tensor_map_encoder()(
         tmap, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
         const_cast<T*>(base), gdim, gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-        promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return cr == CUDA_SUCCESS;
+}
+
+static int exp_switch() {   // CSK_EXP: roofline attribution of the B kernels (bench.py), 0 in production
+    const char* e = std::getenv("CSK_EXP");
+    return e ? std::atoi(e) : 0;
+}
+
+// fp64 B32 kernels need every column 16-B aligned; the fp32 kernel's 32-B loads need 32-B columns
+template <typename T>
+static bool cols_aligned(const Cols<T>& cols, size_t bytes) {
+    const size_t elems = bytes / sizeof(T);
+    return ((uintptr_t)cols.A % bytes) == 0 && (cols.n <= 1 || cols.lda % (int64_t)elems == 0) &&
+           (cols.b == nullptr || ((uintptr_t)cols.b % bytes) == 0);
 }
 
 // For the row-scatter variants `out` is the SA^T workspace described by L (L.tma marks
@@ -1092,9 +958,9 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
     if (rows <= 0) return CSK_OK;
     // CSK_PLAN_HASH: only the default fp64 32-row kernels hash rows on the fly; every other
     // kernel reads the code array, materialised on first use
-    const bool may_hash = plan->code == nullptr && variant == CSK_VAR_BULK_ROW && !L.tma && sizeof(T) == 8 &&
-                          L.sep < 0;
-    if (plan->code == nullptr && !may_hash) {
+    const bool b32 = variant == CSK_VAR_BULK_ROW && sizeof(T) == 8 && cols_aligned(cols, 16) &&
+                     (cols.n > 0 || cols.b != nullptr);
+    if (plan->code == nullptr && !b32) {
         const csk_status es = ensure_codes(plan, st);
         if (es != CSK_OK) return es;
     }
@@ -1119,61 +985,25 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
             CSK_CUDA_TRY(cudaFuncSetAttribute(cs_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             const int64_t units = ceil_div(rows, RB) * ceil_div(ncols, L.cw);
             const int64_t blocks = std::min<int64_t>(ceil_div(units, kTmaWarps), (int64_t)di.num_sms);
-            prof_mark(st, true);   // right before the launch: host prep is not timed
+            prof_mark(st, true);
             cs_tma_kernel<T><<<(unsigned)blocks, kTmaWarps * 32, smem, st>>>(tmap, code, rows, ncols, stage_bytes, out, L);
             CSK_LAUNCH_CHECK();
             return CSK_OK;
         }
         case CSK_VAR_BULK_ROW: {
-            if (L.tma) {
-                constexpr int RB = 128 / sizeof(T);
-                // even (16-B aligned rows) and == 2 mod 4: the 16 rows x 2 column-lanes of one
-                // STS hit every bank exactly twice (2 wavefronts, the minimum for 256 B)
-                int ldrow = (L.cw + 1) & ~1;
-                if (ldrow % 4 == 0) ldrow += 2;
-                CUtensorMap tmap;
-                CSK_REQUIRE(make_tensor_map(&tmap, cols, rows, ncols, L.cw), CSK_ECUDA, "cuTensorMapEncodeTiled failed");
-                const int stage_bytes = (L.cw * 128 + 1023) & ~1023;
-                const int64_t units = ceil_div(rows, RB) * ceil_div(ncols, L.cw);
-                auto launch = [&](auto cfg) -> csk_status {
-                    using C = decltype(cfg);
-                    const size_t smem = b2_smem_bytes(C::kWarps, C::kStages, C::kRbufs, RB, stage_bytes, ldrow);
-                    if (smem > (size_t)di.smem_optin) return CSK_EUNSUPPORTED;
-                    CSK_CUDA_TRY(cudaFuncSetAttribute(cs_bulk_tma_kernel<T, C>,
-                                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                    const int64_t blocks = std::min<int64_t>(ceil_div(units, C::kWarps), (int64_t)di.num_sms);
-                    prof_mark(st, true);   // right before the launch: host prep is not timed
-                    cs_bulk_tma_kernel<T, C><<<(unsigned)blocks, C::kWarps * 32, smem, st>>>(tmap, code, rows, ncols,
-                                                                                            stage_bytes, ldrow, out, L);
-                    CSK_LAUNCH_CHECK();
-                    return CSK_OK;
-                };
-                // pipeline shape (CSK_B2CFG for experiments; the default is the measured best at C2)
-                const char* e = std::getenv("CSK_B2CFG");
-                const int cfg = e ? std::atoi(e) : 1;
-                csk_status r = CSK_EUNSUPPORTED;
-                switch (cfg) {
-                    case 0: r = launch(B2Cfg<8, 2, 1>{}); break;
-                    case 2: r = launch(B2Cfg<8, 1, 2>{}); break;
-                    case 3: r = launch(B2Cfg<4, 3, 2>{}); break;
-                    case 4: r = launch(B2Cfg<12, 1, 1>{}); break;
-                    default: r = launch(B2Cfg<6, 2, 2>{}); break;
-                }
-                if (r == CSK_EUNSUPPORTED) r = launch(B2Cfg<4, 2, 1>{});   // wide tiles: smaller footprint
-                CSK_REQUIRE(r != CSK_EUNSUPPORTED, CSK_EUNSUPPORTED, "variant B: tile does not fit smem");
-                return r;
-            }
-            const int cw = L.cw;   // bulk_chunk_width(ncols), set with the layout by cs_apply_impl
+            const int cw = L.cw;   // set with the layout by cs_apply_impl
+            const int expv = exp_switch();
             if constexpr (sizeof(T) == 4) {
-                if (L.ncopies > 0) {   // fp32 accumulation into bounded-depth copies
-                    const int ldf = ((cw + 3) & ~3) + 4;   // 16-B rows, == 4 mod 8 floats
-                    const size_t smem = (size_t)8 * 64 * ldf * sizeof(float);
-                    CSK_CUDA_TRY(cudaFuncSetAttribute(cs_bulk32f_kernel<8>,
+                if (L.ncopies > 0) {   // fp32 accumulation into bounded-depth copies (default for fp32)
+                    int ldf = (cw + 3) & ~3;
+                    while (ldf % 32 != 4) ldf += 4;   // == 4 mod 32: conflict-free tile stores
+                    const size_t smem = (size_t)8 * (kF32Rows * ldf + 32) * sizeof(float);
+                    CSK_CUDA_TRY(cudaFuncSetAttribute(cs_bulk64f_kernel<8>,
                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                    const int64_t units = ceil_div(rows, 64) * ceil_div(ncols, cw);
+                    const int64_t units = ceil_div(rows, kF32Rows) * ceil_div(ncols, cw);
                     const int64_t blocks = std::min<int64_t>(ceil_div(units, 8), (int64_t)di.num_sms);
                     prof_mark(st, true);
-                    cs_bulk32f_kernel<8><<<(unsigned)blocks, 256, smem, st>>>(
+                    cs_bulk64f_kernel<8><<<(unsigned)blocks, 256, smem, st>>>(
                         code, rows, *reinterpret_cast<const Cols<float>*>(&cols), ncols, ldf,
                         reinterpret_cast<float*>(out), L);
                     CSK_LAUNCH_CHECK();
@@ -1181,85 +1011,34 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
                 }
             }
             const int ldtile = (cw + 1) & ~1;
-            const int64_t units = ceil_div(rows, kBulkRows) * ceil_div(ncols, cw);
-            const char* ex = std::getenv("CSK_EXP");
-            const int expv = ex ? std::atoi(ex) : 0;
             if constexpr (sizeof(T) == 8) {
-                // 32-row tiles with 16-B loads need every column 16-B aligned
-                const bool al = ((uintptr_t)cols.A & 15) == 0 && (cols.n <= 1 || (cols.lda & 1) == 0) &&
-                                (cols.b == nullptr || ((uintptr_t)cols.b & 15) == 0);
-                const char* w32 = std::getenv("CSK_B32");
-                const int b32 = w32 ? std::atoi(w32) : 8;   // warps per CTA, 0 = off
-                if (al && b32 > 0 && (cols.n > 0 || cols.b != nullptr)) {
+                if (b32) {
                     const int ld32 = ldtile % 4 == 0 ? ldtile + 2 : ldtile;   // == 2 mod 4
-                    const int nbulk = L.sep >= 0 ? ncols - 1 : ncols;   // split: the last column goes apart
-                    const int64_t units32 = ceil_div(rows, kB32Rows) * ceil_div(nbulk, cw);
-                    auto launch32 = [&](auto kern, int W, int mrt = 32) -> csk_status {
-                        const size_t smem = (size_t)W * (kB32Rows * ld32 + kB32Pad) * sizeof(double) +
-                                            (L.sep >= 0 ? (size_t)plan->k1 * sizeof(double) : 0);
-                        if (smem > (size_t)di.smem_optin) return CSK_EUNSUPPORTED;
-                        CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                        int64_t blocks = std::min<int64_t>(ceil_div(units32, W), (int64_t)di.num_sms);
-                        if (const char* g = std::getenv("CSK_GRID")) blocks = std::max(1, std::atoi(g));   // experiment
-                        prof_mark(st, true);   // right before the launch: host prep is not timed
-                        kern<<<(unsigned)blocks, W * 32, smem, st>>>(code, rows, cols, nbulk, ld32, out, L,
-                                                                     (int)plan->k1, mrt);
-                        CSK_LAUNCH_CHECK();
-                        return CSK_OK;
-                    };
-                    csk_status r32;
-                    // rows per tile kept on the TMA path in MIX mode (experiment, opt-in: at n = 32 every
-                    // split measured slower than TMA alone -- 0.72 ms (32) vs 0.89 (24), 0.96 (16), 1.11 (0))
-                    const char* mxe = std::getenv("CSK_MIX_RT");
-                    const int mix_rt = mxe ? std::max(0, std::min(32, std::atoi(mxe))) : 32;
-                    const bool narrow = cw < kBulkMaxCols - 3;
-                    if (code == nullptr) {   // CSK_PLAN_HASH plan
-                        const char* he = std::getenv("CSK_L2HINT");
-                        const bool hint = !(he && std::atoi(he) == 0);
-                        RowLayout LH = L;
+                    const int64_t units32 = ceil_div(rows, kB32Rows) * ceil_div(ncols, cw);
+                    const size_t smem = (size_t)8 * (kB32Rows * ld32 + kB32Pad) * sizeof(double);
+                    const bool narrow = cw < kBulkMaxCols - 3;   // predicated loads + evict_last (C3)
+                    RowLayout LH = L;
+                    if (code == nullptr) {   // CSK_PLAN_HASH plan: codes hashed in the kernel
                         LH.g0 = plan->row0 + row_begin;
                         LH.hkey0 = (uint32_t)plan->seed;
                         LH.hkey1 = (uint32_t)(plan->seed >> 32);
-                        const size_t smem = (size_t)8 * (kB32Rows * ld32 + kB32Pad) * sizeof(double);
-                        auto kern = narrow ? cs_bulk32_kernel<8, 0, false, true, false, true>
-                                           : cs_bulk32_kernel<8, 0, false, false, false, true>;
-                        CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                        const int64_t blocks = std::min<int64_t>(ceil_div(units32, 8), (int64_t)di.num_sms);
-                        prof_mark(st, true);
-                        kern<<<(unsigned)blocks, 256, smem, st>>>(nullptr, rows, cols, nbulk, ld32, out, LH,
-                                                                  (int)plan->k1, narrow && hint ? -1 : 32);
-                        CSK_LAUNCH_CHECK();
-                        return CSK_OK;
                     }
-                    if (L.sep >= 0)
-                        r32 = launch32(cs_bulk32_kernel<8, 0, true>, 8);
-                    else if (cw <= 32 && nbulk <= cw && expv == 0 && b32 == 8 && mix_rt < 32)
-                        r32 = launch32(cs_bulk32_kernel<8, 0, false, false, true>, 8, mix_rt);   // narrow rows
-                    else if (narrow && expv == 0 && b32 == 8) {
-                        // evict_last hint on the reductions (C3: 2.11 -> 2.07 ms, DRAM writes 806 -> 712 MB);
-                        // CSK_L2HINT=0 turns it off
-                        const char* he = std::getenv("CSK_L2HINT");
-                        const bool hint = !(he && std::atoi(he) == 0);
-                        r32 = launch32(cs_bulk32_kernel<8, 0, false, true>, 8, hint ? -1 : 32);   // narrow chunks (C3)
-                    }
-                    else if (b32 == 6)
-                        r32 = expv == 1 ? launch32(cs_bulk32_kernel<6, 1>, 6)
-                              : expv == 2 ? launch32(cs_bulk32_kernel<6, 2>, 6) : launch32(cs_bulk32_kernel<6, 0>, 6);
-                    else if (b32 == 4)
-                        r32 = launch32(cs_bulk32_kernel<4, 0>, 4);
-                    else
-                        r32 = expv == 1   ? launch32(cs_bulk32_kernel<8, 1>, 8)
-                              : expv == 2 ? launch32(cs_bulk32_kernel<8, 2>, 8)
-                              : expv == 3 ? launch32(cs_bulk32_kernel<8, 3>, 8)
-                                          : launch32(cs_bulk32_kernel<8, 0>, 8);
-                    if (r32 != CSK_EUNSUPPORTED) return r32;
+                    auto kern = code == nullptr ? (narrow ? cs_bulk32_kernel<8, 0, true, true> : cs_bulk32_kernel<8, 0, false, true>)
+                                : expv == 1     ? cs_bulk32_kernel<8, 1>
+                                : expv == 2     ? cs_bulk32_kernel<8, 2>
+                                : expv == 3     ? cs_bulk32_kernel<8, 3>
+                                : narrow        ? cs_bulk32_kernel<8, 0, true>
+                                                : cs_bulk32_kernel<8, 0>;
+                    CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                    const int64_t blocks = std::min<int64_t>(ceil_div(units32, 8), (int64_t)di.num_sms);
+                    prof_mark(st, true);   // right before the launch: host prep is not timed
+                    kern<<<(unsigned)blocks, 256, smem, st>>>(code, rows, cols, ncols, ld32, out, LH, (int)plan->k1);
+                    CSK_LAUNCH_CHECK();
+                    return CSK_OK;
                 }
             }
-            if (code == nullptr) {   // hash plan on a path without an on-the-fly kernel
-                const csk_status es = ensure_codes(plan, st);
-                if (es != CSK_OK) return es;
-                code = reinterpret_cast<const uint32_t*>(plan->code) + row_begin;
-            }
+            // 16-row tiles: unaligned fp64 columns, or fp32 accumulated in fp64 (CSK_F32ACC=0, unaligned)
+            const int64_t units = ceil_div(rows, kBulkRows) * ceil_div(ncols, cw);
             auto launch = [&](auto cfg) -> csk_status {
                 using C = decltype(cfg);
                 const size_t smem = (size_t)C::kWarps * C::kBufs * kBulkRows * ldtile * sizeof(double);
@@ -1269,21 +1048,19 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
                           : expv == 3 ? cs_bulk_kernel<T, C, 3> : cs_bulk_kernel<T, C, 0>;
                 CSK_CUDA_TRY(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
                 const int64_t blocks = std::min<int64_t>(ceil_div(units, C::kWarps), (int64_t)di.num_sms);
-                prof_mark(st, true);   // right before the launch: host prep is not timed
+                prof_mark(st, true);
                 kb<<<(unsigned)blocks, C::kWarps * 32, smem, st>>>(code, rows, cols, ncols, ldtile, out, L);
                 CSK_LAUNCH_CHECK();
                 return CSK_OK;
             };
-            // 16-row tiles (unaligned columns or fp32).  Measured at C2: 12/16 warps
-            // and register double-buffering (BulkCfg<.., .., true>) were not faster than 8 x 2.
+            // measured at C2: 12/16 warps and register double-buffering were not faster than 8 x 2
             csk_status r = launch(BulkCfg<8, 2, false>{});
             if (r == CSK_EUNSUPPORTED) r = launch(BulkCfg<4, 2, false>{});
             CSK_REQUIRE(r != CSK_EUNSUPPORTED, CSK_EUNSUPPORTED, "variant B: tile does not fit smem");
             return r;
         }
         case CSK_VAR_ATOMIC_ROW: {
-            const bool bulk = false;
-            const size_t smem = (size_t)kRowWarps * (bulk ? 2 : 1) * 32 * kTileLd * sizeof(double);
+            const size_t smem = (size_t)kRowWarps * 32 * kTileLd * sizeof(double);
             const int64_t units = ceil_div(rows, 32) * ceil_div(ncols, 32);
             auto kern = cs_row_kernel<T>;
             CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1291,7 +1068,7 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
             CSK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowWarps * 32, smem));
             per_sm = std::max(per_sm, 1);
             const int64_t blocks = std::min<int64_t>(ceil_div(units, kRowWarps), (int64_t)di.num_sms * per_sm);
-            prof_mark(st, true);   // right before the launch: host prep is not timed
+            prof_mark(st, true);
             kern<<<(unsigned)blocks, kRowWarps * 32, smem, st>>>(code, rows, cols, ncols, out, ldo);
             CSK_LAUNCH_CHECK();
             return CSK_OK;
@@ -1311,7 +1088,7 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
             const int64_t grid = std::max<int64_t>(
                 1, std::min<int64_t>((int64_t)di.num_sms * per_sm, ceil_div(total, 32 * kPrivDepth * 4)));
             const int64_t per_cta = ceil_div(total, grid);
-            prof_mark(st, true);   // right before the launch: host prep is not timed
+            prof_mark(st, true);
             cs_smem_kernel<T><<<(unsigned)grid, cpc * 32, smem, st>>>(code, rows, cols, ncols, cpc,
                                                                         (int)plan->k1, out, ldo, per_cta);
             CSK_LAUNCH_CHECK();
@@ -1322,7 +1099,7 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
             CSK_REQUIRE(row_begin == 0 && row_end == plan->d, CSK_EUNSUPPORTED,
                         "variant G needs the whole block resident on the device");
             const int64_t blocks = std::min<int64_t>(ceil_div(plan->k1 * 32, 256), (int64_t)di.num_sms * 16);
-            prof_mark(st, true);   // right before the launch: host prep is not timed
+            prof_mark(st, true);
             cs_sorted_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(code, plan->perm, plan->offsets, plan->k1, cols,
                                                                   ncols, out, ldo);
             CSK_LAUNCH_CHECK();
@@ -1334,12 +1111,36 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
     }
 }
 
-
 struct ApplyTarget {
-    double* buf = nullptr;   // accumulation buffer
+    double* buf = nullptr;   // accumulation buffer (fp64; floats for the fp32-accumulation copies)
     int64_t ld = 0;
     bool owned = false;
 };
+
+// Row-major SA^T layout of the B kernels: all columns in one row when ncols <= 66, else the fewest
+// chunks of <= 66 (even) columns; chunk-major (one slice per chunk) when the whole SA^T would take
+// more than half of L2, with the chunk width cut so one slice fits half of L2.
+// Units of lc / cs: elements of width esz.
+static void bulk_layout(RowLayout& L, int64_t k1, int ncols, size_t esz, int align_elems) {
+    L.cw = bulk_chunk_width(ncols);
+    const int64_t l2h = (int64_t)device_info().l2_bytes / 2;
+    if ((int64_t)k1 * ncols * (int64_t)esz > l2h) {
+        const int64_t fit = std::max<int64_t>(2, (l2h / ((int64_t)esz * k1)) & ~1);
+        const int nch = (int)std::max<int64_t>(ceil_div(ncols, kBulkMaxCols), ceil_div(ncols, fit));
+        L.cw = std::min(kBulkMaxCols, (((ncols + nch - 1) / nch) + 1) & ~1);
+    }
+    const int nchunks = (ncols + L.cw - 1) / L.cw;
+    const int64_t cwa = (L.cw + align_elems - 1) / align_elems * align_elems;
+    if (nchunks > 1 && (int64_t)k1 * ncols * (int64_t)esz > l2h) {
+        L.chunk_major = true;   // one L2-sized SA^T slice per column chunk
+        L.lc = cwa;
+        L.cs = k1 * L.lc;
+    } else {
+        // chunks start on aligned boundaries inside a row
+        L.cs = nchunks > 1 ? cwa : L.cw;
+        L.lc = std::max<int64_t>((ncols + align_elems - 1) / align_elems * align_elems, nchunks * cwa);
+    }
+}
 
 csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void* A, int64_t lda, const void* b,
                          void* SA, int64_t ldsa, int variant, cudaStream_t st, int64_t row_begin, int64_t row_end,
@@ -1369,16 +1170,15 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
         if (variant_rowmajor(variant) || variant == CSK_VAR_SORTED) variant = CSK_VAR_ATOMIC_COL;
     }
     const int64_t k1 = plan->k1;
-
-    // TMA eligibility of [A b] as one 2-D tensor (variants X and B)
+    const int64_t rows = row_end - row_begin;
     const size_t esz = dtype == CSK_F64 ? 8 : 4;
     const void* base = n > 0 ? A : b;
-    // X always loads with TMA; B only on request (CSK_B_TMA=1): its register-staged loads measured faster
-    bool tma = variant == CSK_VAR_TMA_ROW || (variant == CSK_VAR_BULK_ROW && std::getenv("CSK_B_TMA"));
-    tma = tma && !std::getenv("CSK_NO_TMA") && (n == 0 || b == nullptr ||
-                                               (const char*)b == (const char*)A + (size_t)n * lda * esz);
+
+    // variant X loads [A b] as one 2-D TMA tensor
+    bool tma = variant == CSK_VAR_TMA_ROW && (n == 0 || b == nullptr ||
+                                              (const char*)b == (const char*)A + (size_t)n * lda * esz);
     tma = tma && ((uintptr_t)base & 15) == 0 && (ncols == 1 || ((lda * (int64_t)esz) & 15) == 0);
-    if (tma && plan->code == nullptr) {   // hash plan: the TMA kernels read codes
+    if (tma && plan->code == nullptr) {   // hash plan: the TMA kernel reads codes
         const csk_status es = ensure_codes(plan, st);
         if (es != CSK_OK) return es;
     }
@@ -1389,86 +1189,42 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
     RowLayout L;
     size_t ws_doubles = 0;
     if (variant_rowmajor(variant)) {
-        if (tma || variant == CSK_VAR_BULK_ROW) {
-            L.tma = tma;
-            L.cw = !tma ? bulk_chunk_width(ncols) : variant == CSK_VAR_BULK_ROW ? b2_chunk_width(ncols)
-                                                                                : tma_chunk_width(ncols);
-            if (!tma && (int64_t)k1 * ncols * 8 > (int64_t)device_info().l2_bytes / 2) {
-                // Each chunk's SA^T slice must stay L2-resident (C3: 66-column slices of 69 MB
-                // ran at 53% of HBM, 52-column slices of 54 MB at 65%): the fewest
-                // chunks whose slice fits half of L2.
-                const int64_t fit = std::max<int64_t>(2, ((int64_t)device_info().l2_bytes / 2 / (8 * k1)) & ~1);
-                const int nch = (int)std::max<int64_t>(ceil_div(ncols, kBulkMaxCols), ceil_div(ncols, fit));
-                L.cw = std::min(kBulkMaxCols, (((ncols + nch - 1) / nch) + 1) & ~1);
-            }
-            if (const char* e = std::getenv("CSK_CW")) {   // experiment: force the chunk width (even, <= 66)
-                const int f = std::atoi(e) & ~1;
-                if (f >= 2 && f <= kBulkMaxCols && !tma) L.cw = std::min(f, (ncols + 1) & ~1);
-            }
-            const int nchunks = (ncols + L.cw - 1) / L.cw;
-            // chunk-major once SA^T would take more than 1/cm_div of L2 (CSK_CM_DIV, default 2)
-            const char* cmd = std::getenv("CSK_CM_DIV");
-            const int64_t cm_div = cmd ? std::max(1, std::atoi(cmd)) : 2;
-            if (nchunks > 1 && (int64_t)k1 * ncols * 8 > (int64_t)device_info().l2_bytes / cm_div) {
-                L.chunk_major = true;                     // one L2-sized SA^T slice per column chunk
-                L.lc = (L.cw + 1) & ~1;
-                L.cs = k1 * L.lc;
-                ws_doubles = (size_t)nchunks * L.cs;
+        if (variant == CSK_VAR_TMA_ROW) {
+            L.tma = true;
+            L.cw = tma_chunk_width(ncols);
+            L.cs = L.cw;
+            L.lc = (ncols + 3) & ~3;
+            ws_doubles = (size_t)k1 * L.lc;
+        } else if (variant == CSK_VAR_BULK_ROW) {
+            // fp32 input: fp32 sums in row-block copies of mean bucket depth <= 64, combined in fp64
+            // (default; CSK_F32ACC=0 accumulates fp32 input in fp64 instead, for A/B measurements)
+            const char* f32e = std::getenv("CSK_F32ACC");
+            const bool f32acc = dtype == CSK_F32 && !(f32e && std::atoi(f32e) == 0) &&
+                                cols_aligned(Cols<float>{static_cast<const float*>(A), static_cast<const float*>(b),
+                                                         lda, (int)n},
+                                             32);
+            if (f32acc) {
+                bulk_layout(L, k1, ncols, 4, 8);   // 32-B aligned rows and chunk starts
+                const int64_t ncp = std::max<int64_t>(1, std::min<int64_t>(256, ceil_div(rows, 64 * k1)));
+                L.ncopies = (int)ncp;
+                L.rows_per_copy = ceil_div(rows, ncp);
+                L.copy_stride = L.chunk_major ? L.cs * ((ncols + L.cw - 1) / L.cw) : k1 * L.lc;   // floats
+                ws_doubles = (size_t)ceil_div(ncp * L.copy_stride, 2);
             } else {
-                // chunks start on 32-B sector boundaries inside a row (cw is even, cs a multiple of 4)
-                L.cs = nchunks > 1 ? (L.cw + 3) & ~3 : L.cw;
-                L.lc = std::max<int64_t>((ncols + 3) & ~3, nchunks * L.cs);
-                if (const char* e = std::getenv("CSK_LC")) L.lc = std::max<int64_t>(L.lc, std::atoi(e) & ~3);   // experiment
-                ws_doubles = (size_t)k1 * L.lc;
-                // B32 split, opt-in (CSK_SPLIT=1): one odd trailing column of a
-                // single-chunk fp64 [A b] is summed in shared memory per CTA, so the bulk rows are
-                // (ncols-1)*8 B (C2: 512 B = 16 sectors instead of 17).  Measured slower at C2 (2.32 vs
-                // 2.04 ms): the 64 KB of bucket sums take L1 capacity from the in-flight loads and the
-                // fp64 shared atomics are CAS loops (ATOMS.CAST.SPIN.64).
-                const bool al32 = dtype == CSK_F64 && ((uintptr_t)A & 15) == 0 && (n <= 1 || (lda & 1) == 0) &&
-                                  (b == nullptr || ((uintptr_t)b & 15) == 0);
-                const char* b32e = std::getenv("CSK_B32");
-                const char* spe = std::getenv("CSK_SPLIT");
-                if (!tma && variant == CSK_VAR_BULK_ROW && al32 && !(b32e && std::atoi(b32e) == 0) && !rowout &&
-                    spe && std::atoi(spe) == 1 && nchunks == 1 && (ncols & 1) && ncols >= 5 &&
-                    (k1 & 1) == 0 && k1 <= 10240 && n > 0 && (b != nullptr || n >= 5)) {
-                    L.cw = ncols - 1;
-                    L.cs = L.cw;
-                    L.lc = (L.cw + 3) & ~3;
-                    L.sep = k1 * L.lc;
-                    ws_doubles = (size_t)k1 * L.lc + (size_t)k1;
-                }
-                // fp32 input: fp32 accumulation in row-block copies of mean bucket depth <= 64
-                // Opt-in (CSK_F32ACC=1): measured slower than fp64 accumulation at C2 fp32 (2.47 ms with
-                // 32-row tiles, 3.95 ms with 64-row tiles, vs 2.02 ms): half the reduction bytes buy
-                // nothing (the L2 adds the same number of elements per row) and the float tile writes
-                // of 16-B aligned rows cannot avoid 8-way bank conflicts.
-                const char* f32e = std::getenv("CSK_F32ACC");
-                if (dtype == CSK_F32 && !tma && variant == CSK_VAR_BULK_ROW && !L.chunk_major && !rowout &&
-                    f32e && std::atoi(f32e) == 1) {
-                    const int64_t rows = row_end - row_begin;
-                    const int64_t ncp = std::max<int64_t>(1, std::min<int64_t>(256, ceil_div(rows, 64 * k1)));
-                    L.cs = nchunks > 1 ? ((L.cw + 3) & ~3) : L.cw;
-                    L.lc = std::max<int64_t>((ncols + 3) & ~3, nchunks * (int64_t)((L.cw + 3) & ~3));
-                    L.ncopies = (int)ncp;
-                    L.rows_per_copy = ceil_div(rows, ncp);
-                    L.copy_stride = k1 * L.lc;                       // floats
-                    ws_doubles = (size_t)ceil_div(ncp * L.copy_stride, 2);
-                }
+                bulk_layout(L, k1, ncols, 8, 4);
+                const int nchunks = (ncols + L.cw - 1) / L.cw;
+                ws_doubles = L.chunk_major ? (size_t)nchunks * L.cs : (size_t)k1 * L.lc;
             }
         } else {
-            L.cw = ncols;   // T (and L/S fallbacks): its own 32-column chunks, regular layout
+            L.cw = ncols;   // T: its own 32-column chunks, one row of SA^T
             L.lc = (ncols + 3) & ~3;
             L.cs = ncols;
             ws_doubles = (size_t)k1 * L.lc;
         }
         tgt.ld = L.lc;
         tgt.owned = true;
-    } else if (dtype == CSK_F32) {
-        tgt.ld = k1;
-        tgt.owned = true;
-        ws_doubles = (size_t)k1 * ncols;
-    } else if (SA == nullptr) {   // rowout with a column-major variant: private fp64 target, converted below
+    } else if (dtype == CSK_F32 || SA == nullptr) {
+        // fp32 output of a column-major variant, or the row-major hand-over: private fp64 target
         tgt.ld = k1;
         tgt.owned = true;
         ws_doubles = (size_t)k1 * ncols;
@@ -1477,13 +1233,10 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
         tgt.ld = ldsa;
     }
     if (tgt.owned) {
-        // + 2 doubles: the B32 kernel's work counter, zeroed by the same memset (CSK_DYN=0: static)
+        // + 2 doubles: the B kernels' work counter, zeroed by the same memset
         CSK_CUDA_TRY(csk_malloc_async(&tgt.buf, (ws_doubles + 2) * sizeof(double), st));
         CSK_CUDA_TRY(cudaMemsetAsync(tgt.buf, 0, (ws_doubles + 2) * sizeof(double), st));
-        const char* dy = std::getenv("CSK_DYN");
-        if (!(dy && std::atoi(dy) == 0))
-            L.work = reinterpret_cast<unsigned long long*>(tgt.buf + ws_doubles);
-        if (const char* g = std::getenv("CSK_GRAB")) L.grab = std::max(1, std::atoi(g));
+        L.work = reinterpret_cast<unsigned long long*>(tgt.buf + ws_doubles);
     } else if (variant != CSK_VAR_SORTED && !accumulate) {
         // zero SA (ldsa may exceed k1: clear the k1 x ncols window only)
         if (ldsa == k1) {
@@ -1492,6 +1245,9 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
             CSK_CUDA_TRY(cudaMemset2DAsync(tgt.buf, ldsa * sizeof(double), 0, k1 * sizeof(double), ncols, st));
         }
     }
+    auto release = on_exit([&] {
+        if (tgt.owned && tgt.buf) cudaFreeAsync(tgt.buf, st);
+    });
     csk_status s;
     if (dtype == CSK_F64) {
         Cols<double> cols{static_cast<const double*>(A), static_cast<const double*>(b), lda, (int)n};
@@ -1501,58 +1257,57 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
         s = run_variant<float>(variant, plan, ncols, cols, row_begin, row_end, tgt.buf, tgt.ld, L, st);
     }
     prof_mark(st, false);
-    if (rowout != nullptr) {
-        if (s == CSK_OK && variant_rowmajor(variant) && L.sep < 0 && L.ncopies == 0) {
-            // the caller (ms_apply) consumes the row-major SA^T directly (P:L228: Z^T = Y^T G^T, no transpose)
-            rowout->ws = tgt.buf;
-            rowout->cw = L.cw;
-            rowout->lc = L.lc;
-            rowout->cs = L.cs;
-            rowout->ncols = ncols;
-            return CSK_OK;
-        }
-        if (s == CSK_OK) {
-            // column-major fp64 result (variants L, S, G) -> row-major workspace
-            CSK_REQUIRE(!variant_rowmajor(variant), CSK_EUNSUPPORTED, "row-major hand-over not available here");
-            s = rows_from_colmajor(tgt.buf, tgt.ld, k1, ncols, rowout, st);
-        }
-        if (tgt.owned) cudaFreeAsync(tgt.buf, st);
-        return s;
-    }
-    if (s == CSK_OK && tgt.owned && L.ncopies > 0) {
-        dim3 grid((unsigned)ceil_div(k1, 32), (unsigned)ceil_div(ncols, 32));
-        cs_combine_f32_kernel<<<grid, dim3(32, 8), 0, st>>>(reinterpret_cast<const float*>(tgt.buf), L, k1, ncols,
-                                                            static_cast<float*>(SA), ldsa);
+    if (s != CSK_OK) return s;
+    auto launch_ok = [&](const char* what) -> csk_status {
         count_launch();
-        cudaFreeAsync(tgt.buf, st);
         if (cudaGetLastError() != cudaSuccess) {
-            set_error("cs_apply fp32 combine launch failed");
+            set_error("cs_apply %s launch failed", what);
             return CSK_ECUDA;
         }
         return CSK_OK;
-    }
-    if (s == CSK_OK && tgt.owned) {
+    };
+    if (rowout != nullptr) {
+        if (L.ncopies > 0) {   // fp32 copies -> fp64 row-major workspace (regular layout)
+            const int64_t lcd = (ncols + 1) & ~1;
+            double* Yt = nullptr;
+            CSK_CUDA_TRY(csk_malloc_async(&Yt, (size_t)k1 * lcd * sizeof(double), st));
+            cs_combine_rows_kernel<<<(unsigned)ceil_div(k1 * lcd, 256), 256, 0, st>>>(
+                reinterpret_cast<const float*>(tgt.buf), L, k1, ncols, Yt, lcd);
+            const csk_status ls = launch_ok("fp32 combine");
+            if (ls != CSK_OK) {
+                cudaFreeAsync(Yt, st);
+                return ls;
+            }
+            *rowout = RowOut{Yt, ncols, ncols, lcd, ncols};
+            return CSK_OK;
+        }
         if (variant_rowmajor(variant)) {
-            const RowLayout& Lt = L;
-            dim3 grid((unsigned)ceil_div(k1, 32), (unsigned)ceil_div(ncols, 32));
-            if (dtype == CSK_F64)
-                transpose_out_kernel<double><<<grid, dim3(32, 8), 0, st>>>(tgt.buf, Lt, k1, ncols,
-                                                                           static_cast<double*>(SA), ldsa);
-            else
-                transpose_out_kernel<float><<<grid, dim3(32, 8), 0, st>>>(tgt.buf, Lt, k1, ncols,
-                                                                          static_cast<float*>(SA), ldsa);
-        } else {
-            narrow_kernel<<<(unsigned)std::min<int64_t>(ceil_div(k1 * ncols, 256), 4096), 256, 0, st>>>(
-                tgt.buf, k1, ncols, static_cast<float*>(SA), ldsa);
+            // the caller (ms_apply) consumes the row-major SA^T directly (P:L228: Z^T = Y^T G^T, no transpose)
+            *rowout = RowOut{tgt.buf, L.cw, ncols, L.lc, L.cs};
+            tgt.owned = false;   // handed over
+            return CSK_OK;
         }
-        count_launch();
-        if (cudaGetLastError() != cudaSuccess) {
-            set_error("cs_apply finalize launch failed");
-            s = CSK_ECUDA;
-        }
+        return rows_from_colmajor(tgt.buf, tgt.ld, k1, ncols, rowout, st);   // L, S, G
     }
-    if (tgt.owned) cudaFreeAsync(tgt.buf, st);
-    return s;
+    if (!tgt.owned) return CSK_OK;
+    dim3 grid((unsigned)ceil_div(k1, 32), (unsigned)ceil_div(ncols, 32));
+    if (L.ncopies > 0) {
+        cs_combine_f32_kernel<<<grid, dim3(32, 8), 0, st>>>(reinterpret_cast<const float*>(tgt.buf), L, k1, ncols,
+                                                            static_cast<float*>(SA), ldsa);
+        return launch_ok("fp32 combine");
+    }
+    if (variant_rowmajor(variant)) {
+        if (dtype == CSK_F64)
+            transpose_out_kernel<double><<<grid, dim3(32, 8), 0, st>>>(tgt.buf, L, k1, ncols, static_cast<double*>(SA),
+                                                                       ldsa);
+        else
+            transpose_out_kernel<float><<<grid, dim3(32, 8), 0, st>>>(tgt.buf, L, k1, ncols, static_cast<float*>(SA),
+                                                                      ldsa);
+        return launch_ok("transpose");
+    }
+    narrow_kernel<<<(unsigned)std::min<int64_t>(ceil_div(k1 * ncols, 256), 4096), 256, 0, st>>>(
+        tgt.buf, k1, ncols, static_cast<float*>(SA), ldsa);
+    return launch_ok("narrow");
 }
 
 }  // namespace csk

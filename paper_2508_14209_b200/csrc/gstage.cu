@@ -57,8 +57,10 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// not volatile: a pure function of its operands, so the compiler may interleave it with the
+// fragment loads of the next k-step (the DMMA chains' latency is what the issue order must hide)
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                  : "+d"(c0), "+d"(c1)
                  : "d"(a), "d"(b));
 }
@@ -80,8 +82,8 @@ struct GsArgs {
 };
 
 // q0(c) = floor(c * total / P): the first flattened k-block of CTA c
-__device__ __forceinline__ int64_t range_begin(int64_t c, int64_t total, int P) {
-    return (int64_t)(((unsigned __int128)c * (unsigned __int128)total) / (unsigned __int128)P);
+__host__ __device__ __forceinline__ int64_t range_begin(int64_t c, int64_t total, int P) {
+    return (int64_t)(((uint64_t)c * (uint64_t)total) / (uint64_t)P);   // c <= P <= 2^16, total < 2^47
 }
 
 template <int MW, int NT, int BK, int STAGES>
@@ -152,17 +154,25 @@ __global__ void __launch_bounds__(kGsWarps * 32, 1) gstage_kernel(GsArgs a) {
         cp_async_commit();
         const double* sA = gs_smem + (size_t)(i % STAGES) * C::STAGE + 8 * MW * warp + g;
         const double* sB = gs_smem + (size_t)(i % STAGES) * C::STAGE + C::A_STAGE + g;
+        // fragments double-buffered in registers: step k4 + 1's loads issue before step k4's DMMAs
+        double fa[2][MW], fb[2][NT];
+#pragma unroll
+        for (int mi = 0; mi < MW; ++mi) fa[0][mi] = sA[t * C::LDA + 8 * mi];
+#pragma unroll
+        for (int nj = 0; nj < NT; ++nj) fb[0][nj] = sB[t * C::LDB + 8 * nj];
 #pragma unroll
         for (int k4 = 0; k4 < BK / 4; ++k4) {
-            double fa[MW], fb[NT];
+            const int cur = k4 & 1, nxt = cur ^ 1;
+            if (k4 + 1 < BK / 4) {
 #pragma unroll
-            for (int mi = 0; mi < MW; ++mi) fa[mi] = sA[(4 * k4 + t) * C::LDA + 8 * mi];
+                for (int mi = 0; mi < MW; ++mi) fa[nxt][mi] = sA[(4 * k4 + 4 + t) * C::LDA + 8 * mi];
 #pragma unroll
-            for (int nj = 0; nj < NT; ++nj) fb[nj] = sB[(4 * k4 + t) * C::LDB + 8 * nj];
+                for (int nj = 0; nj < NT; ++nj) fb[nxt][nj] = sB[(4 * k4 + 4 + t) * C::LDB + 8 * nj];
+            }
 #pragma unroll
             for (int mi = 0; mi < MW; ++mi)
 #pragma unroll
-                for (int nj = 0; nj < NT; ++nj) dmma(acc[mi][nj][0], acc[mi][nj][1], fa[mi], fb[nj]);
+                for (int nj = 0; nj < NT; ++nj) dmma(acc[mi][nj][0], acc[mi][nj][1], fa[cur][mi], fb[cur][nj]);
         }
         const int64_t tile = q / a.KB;
         const bool seg_end = (q + 1 == q1) || ((q + 1) % a.KB == 0);
@@ -248,6 +258,7 @@ csk_status launch(GsArgs& a, void* Z, int64_t ldz, bool z_f32, cudaStream_t st) 
     int64_t P = std::min<int64_t>(nsm, std::max<int64_t>(1, a.total / 2));
     if (const char* e = std::getenv("CSK_GS_CTAS")) P = std::max<int64_t>(1, std::min<int64_t>(std::atoll(e), a.total));
     a.P = (int)P;
+    CSK_REQUIRE(a.total < (int64_t(1) << 47), CSK_EUNSUPPORTED, "G-stage: k1 too large");
     const int64_t share = ceil_div(a.total, P);
     a.maxseg = (int)(ceil_div(share, a.KB) + 1);
     const size_t part_bytes = (size_t)P * a.maxseg * C::BM * C::BN * sizeof(double);

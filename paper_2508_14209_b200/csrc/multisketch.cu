@@ -606,6 +606,7 @@ csk_status ms_apply_impl(csk_plan_t plan, int64_t k2, csk_dtype dtype, int64_t n
         ro.cw = 64;
         ro.cs = 64;
     }
+    if (ro.ncols <= ro.cw) ro.cs = 0;   // one chunk: the chunk stride is never used
     // a4 + a5: G from the plan (drawn once per k2), Z = G Y on the fp64 tensor pipe (fp32 input: the
     // sketch was accumulated in fp64, R12, and Z is rounded to fp32 once)
     const double* G = nullptr;

@@ -29,6 +29,7 @@ A = synth.gaussian_matrix(d, n, seed=2)
 b = synth.rhs(A, "hard", seed=2)
 Ad, bd = cm(A), cm(b)
 plan = csk.cs_plan(d, 128, 1, sort=True)
+plan8k = csk.cs_plan(1 << 13, 128, 1)
 for v in ("L", "T", "S", "G", "B", "X"):
     csk.cs_apply(plan, Ad, b=bd, variant=v)
     print("cs_apply", v, flush=True)
@@ -37,12 +38,18 @@ print("cs_apply fp32", flush=True)
 wide = synth.gaussian_matrix(4096, 129, seed=3)
 csk.cs_apply(csk.cs_plan(4096, 256, 2), cm(wide), b=cm(wide[:, 0].copy()))
 print("cs_apply 2 chunks", flush=True)
-for k, vv in (("CSK_SPLIT", "1"), ("CSK_MIX_RT", "16"), ("CSK_F32ACC", "1")):
+for k, vv in (("CSK_F32ACC", "0"), ("CSK_F32ACC", "1")):   # fp32: fp64 accumulation vs fp32 copies
     env(**{k: vv})
-    AA = A if k != "CSK_F32ACC" else A.astype(np.float32)
-    csk.cs_apply(plan, cm(AA if k != "CSK_MIX_RT" else AA[:, :8]), b=None if k == "CSK_MIX_RT" else cm(b.astype(AA.dtype)))
+    A32 = synth.gaussian_matrix(1 << 13, 9, seed=6, dtype=np.float32)
+    csk.cs_apply(plan8k, cm(A32), b=cm(A32[:, 0].copy()))
+    csk.ms_apply(plan8k, 16, cm(A32), b=cm(A32[:, 0].copy()))
     env(**{k: None})
-    print("cs_apply", k, flush=True)
+    print("cs_apply fp32", k, vv, flush=True)
+for v in ("L", "S", "G", "T", "X"):                    # every variant into the DMMA G-stage
+    env(CSK_VARIANT=str(csk.csk.VARIANTS[v]))
+    csk.ms_apply(plan, 16, Ad, b=bd)
+    env(CSK_VARIANT=None)
+    print("ms_apply via", v, flush=True)
 Z = csk.ms_apply(plan, 16, Ad, b=bd)
 for e in ({}, {"CSK_QR_WY": "0"}, {"CSK_QR_WY": "0", "CSK_QR_SINGLE": "1"}, {"CSK_QR_WY_P": "2"}):
     env(**e)
@@ -74,16 +81,17 @@ csk.cs_lstsq(plan, Ad, bd)
 csk.msh_lstsq(plan, 16, Ad, bd)
 torch.cuda.synchronize()
 print("gs/cs/msh lstsq done", flush=True)
-# hash plans (codes on the fly, wide and narrow-chunk kernels), the split-K G-stage, the async solve,
+# hash plans (codes on the fly, wide and narrow-chunk kernels), the G-stage splits, the async solve,
 # and the two-stream pipeline pattern of bench.py
 hp = csk.cs_plan(d, 128, 5, row0=3, hash=True)
 csk.cs_apply(hp, Ad, b=bd)
 csk.cs_apply(csk.cs_plan(4096, 1 << 17, 2, hash=True), cm(wide), b=cm(wide[:, 0].copy()))
 print("hash plans done", flush=True)
-env(CSK_GSTAGE="splitk")
-Zk = csk.ms_apply(plan, 16, Ad, b=bd)
-env(CSK_GSTAGE=None)
-print("split-K G-stage done", flush=True)
+for ctas in ("1", "5", "300"):   # stream-K G-stage splits
+    env(CSK_GS_CTAS=ctas)
+    Zk = csk.ms_apply(plan, 24, Ad, b=bd)
+    env(CSK_GS_CTAS=None)
+print("G-stage splits done", flush=True)
 s2 = torch.cuda.Stream()
 Zs = [csk.ms_apply(plan, 16, Ad, b=bd) for _ in range(2)]
 for i in range(4):

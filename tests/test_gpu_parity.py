@@ -504,44 +504,17 @@ def test_profile_hooks_time_the_main_kernel():
     assert csk.profile_read() == (0.0, 0)
 
 
-# ------------------------------------------------ B32 split of the odd last column
-@pytest.mark.parametrize("split", ["1", "0"])
+# ------------------------------------------------ B32 shapes: odd widths, narrow rows, k1 up to 16384
 @pytest.mark.parametrize("d,n,with_b,k1", [(100003, 64, True, 8192), (50000, 4, True, 2048), (40961, 5, False, 64),
-                                           (9999, 64, True, 10240), (3000, 64, True, 16384)])
-def test_cs_apply_split_last_column(monkeypatch, split, d, n, with_b, k1):
-    # ncols odd and one chunk: the last column is summed in shared memory per CTA (C2's b),
-    # the other columns by the row bulk reductions; both parts and the fallback must match
-    monkeypatch.setenv("CSK_SPLIT", split)
+                                           (9999, 64, True, 10240), (3000, 64, True, 16384), (100003, 32, False, 2048),
+                                           (40000, 17, False, 512), (5000, 2, False, 64)])
+def test_cs_apply_b32_shapes(d, n, with_b, k1):
     A = synth.gaussian_matrix(d, n, seed=3)
     b = synth.rhs(A, "hard", seed=3) if with_b else None
     plan = csk.cs_plan(d, k1, 7)
     h, s = oracle.codes(d, k1, 7)
     for variant in ("auto", "B"):
         _check_apply(plan, h, s, A, b, variant)
-
-
-def test_cs_apply_split_integer_exact(monkeypatch):
-    d, n, k1 = 70001, 64, 8192
-    A = synth.integer_matrix(d, n, seed=4)
-    b = synth.integer_matrix(d, 1, seed=5)[:, 0]
-    plan = csk.cs_plan(d, k1, 2)
-    h, s = oracle.codes(d, k1, 2)
-    got = host(csk.cs_apply(plan, gpu_colmajor(A), b=gpu_colmajor(b)))
-    exp = oracle.cs_apply(h, s, A, k1, b=b)
-    assert np.array_equal(got, exp)
-
-
-@pytest.mark.parametrize("mix_rt", ["16", "0", "8", "32"])
-@pytest.mark.parametrize("d,n,k1", [(100003, 32, 2048), (40000, 17, 512), (5000, 2, 64)])
-def test_cs_apply_narrow_rows_mixed_paths(monkeypatch, mix_rt, d, n, k1):
-    # rows of <= 32 columns: mix_rt rows per 32-row tile by TMA bulk reductions, the rest by
-    # warp-wide red.global.add.f64 (32 = TMA only); every split must match the oracle
-    monkeypatch.setenv("CSK_MIX_RT", mix_rt)
-    A = synth.gaussian_matrix(d, n, seed=4)
-    plan = csk.cs_plan(d, k1, 5)
-    h, s = oracle.codes(d, k1, 5)
-    for variant in ("auto", "B"):
-        _check_apply(plan, h, s, A, None, variant)
     Ai = synth.integer_matrix(d, n, seed=6)
     got = host(csk.cs_apply(plan, gpu_colmajor(Ai)))
     assert np.array_equal(got, oracle.cs_apply(h, s, Ai, k1))
@@ -549,11 +522,14 @@ def test_cs_apply_narrow_rows_mixed_paths(monkeypatch, mix_rt, d, n, k1):
 
 @pytest.mark.parametrize("acc", ["1", "0"])
 @pytest.mark.parametrize("d,n,with_b,k1,off", [(1 << 21, 64, True, 2048, 0), (300007, 40, False, 512, 0),
-                                               (100003, 129, True, 1024, 0), (50001, 7, True, 4096, 1)])
+                                               (100003, 129, True, 1024, 0), (50001, 7, True, 4096, 1),
+                                               (1 << 20, 256, True, 131072, 0), (70008, 65, True, 8192, 0),
+                                               (4104, 3, False, 64, 0), (64008, 66, True, 4096, 8)])
 def test_cs_apply_fp32_accumulation(monkeypatch, acc, d, n, with_b, k1, off):
-    # fp32 input: fp32 sums in row-block copies of bounded bucket depth, combined in fp64 ("1"), or
-    # fp64 accumulation ("0"); both within 1e-5 * sum|terms| (BASELINE.json).  off = 1 misaligns A by
-    # one float (no float2 loads).
+    # fp32 input: fp32 sums in row-block copies of bounded bucket depth, combined in fp64 ("1", the
+    # default: 64-row tiles, 32-B loads), or fp64 accumulation ("0"); both within 1e-5 * sum|terms|
+    # (BASELINE.json).  off = 1 misaligns A by one float (no 32-B loads: the fp64-accumulating
+    # 16-row kernel); off = 8 keeps 32-B alignment with an offset base; k1 = 131072 is chunk-major.
     monkeypatch.setenv("CSK_F32ACC", acc)
     A = synth.gaussian_matrix(d, n, seed=3, dtype=np.float32)
     b = synth.rhs(A.astype(np.float64), "easy", seed=3).astype(np.float32) if with_b else None
