@@ -583,10 +583,15 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
 constexpr int kF32Rows = 64;
 constexpr int kF32MaxCols = 68;   // 17 column quads
 
-__device__ __forceinline__ void ldcs_v8(const float* p, float (&v)[8]) {
-    asm volatile("ld.global.cs.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
-                 : "l"(p));
+// predicated 32-B streaming load (branch-free: a lane with pred == false fetches nothing and gets 0;
+// the address must still be legal)
+__device__ __forceinline__ void ldcs_v8_pred(const float* p, bool pred, float (&v)[8]) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = 0.0f;
+    asm("{ .reg .pred q; setp.ne.b32 q, %9, 0;\n\t"
+        "@q ld.global.cs.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8]; }"
+        : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]), "+f"(v[6]), "+f"(v[7])
+        : "l"(p), "r"((int)pred));
 }
 
 template <int W>
@@ -623,24 +628,17 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk64f_kernel(const uint32_t* _
         const bool full = r0 + kF32Rows <= rows;
         const uint32_t ca = __ldg(code + min(r0 + lane, rows - 1));
         const uint32_t cb = __ldg(code + min(r0 + 32 + lane, rows - 1));
-        // sign bits of the 64 rows (bit r = row r negative), one ballot per half
-        const uint32_t sg_lo = __ballot_sync(0xffffffffu, (ca >> 31) != 0u);
-        const uint32_t sg_hi = __ballot_sync(0xffffffffu, (cb >> 31) != 0u);
-        const uint32_t sgw = q < 4 ? sg_lo : sg_hi;
-        const int sh = (q & 3) * 8;
         float v[kJ][8];
+        if (full) {   // one predicated 32-B load per column quad, no branches
 #pragma unroll
-        for (int j = 0; j < kJ; ++j) {
-            const int c = 4 * j + sq;
-            const float* col = cols.col(c0 + min(c, nc - 1)) + r0 + 8 * q;
-            if (full) {
-                if (c < nc) {
-                    ldcs_v8(col, v[j]);
-                } else {
+            for (int j = 0; j < kJ; ++j) {
+                const int c = 4 * j + sq;
+                ldcs_v8_pred(cols.col(c0 + min(c, nc - 1)) + r0 + 8 * q, c < nc, v[j]);
+            }
+        } else {      // the ragged last tile: clamped scalar loads
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) v[j][i] = 0.0f;
-                }
-            } else {
+            for (int j = 0; j < kJ; ++j) {
+                const int c = 4 * j + sq;
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                     const bool ok = c < nc && r0 + 8 * q + i < rows;
@@ -648,6 +646,12 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk64f_kernel(const uint32_t* _
                 }
             }
         }
+        // sign bits of the 64 rows (bit r = row r negative), one ballot per half -- after the tile's
+        // loads are issued, so the code loads' latency overlaps the column loads' instead of preceding it
+        const uint32_t sg_lo = __ballot_sync(0xffffffffu, (ca >> 31) != 0u);
+        const uint32_t sg_hi = __ballot_sync(0xffffffffu, (cb >> 31) != 0u);
+        const uint32_t sgw = q < 4 ? sg_lo : sg_hi;
+        const int sh = (q & 3) * 8;
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncwarp();
         const int nc4 = (nc + 3) & ~3;
@@ -935,6 +939,11 @@ static bool make_tensor_map(CUtensorMap* tmap, const Cols<T>& cols, int64_t rows
     return cr == CUDA_SUCCESS;
 }
 
+LaunchCaps& launch_caps() {
+    static thread_local LaunchCaps caps;
+    return caps;
+}
+
 static int exp_switch() {   // CSK_EXP: roofline attribution of the B kernels (bench.py), 0 in production
     const char* e = std::getenv("CSK_EXP");
     return e ? std::atoi(e) : 0;
@@ -1030,7 +1039,8 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
                                 : narrow        ? cs_bulk32_kernel<8, 0, true>
                                                 : cs_bulk32_kernel<8, 0>;
                     CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                    const int64_t blocks = std::min<int64_t>(ceil_div(units32, 8), (int64_t)di.num_sms);
+                    int64_t blocks = std::min<int64_t>(ceil_div(units32, 8), (int64_t)di.num_sms);
+                    if (launch_caps().cs_ctas > 0) blocks = std::min<int64_t>(blocks, launch_caps().cs_ctas);
                     prof_mark(st, true);   // right before the launch: host prep is not timed
                     kern<<<(unsigned)blocks, 256, smem, st>>>(code, rows, cols, ncols, ld32, out, LH, (int)plan->k1);
                     CSK_LAUNCH_CHECK();

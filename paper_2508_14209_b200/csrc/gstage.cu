@@ -6,19 +6,24 @@
 // CountSketch's row-major workspace (RowOut layout: element (m, c) at (c / cw) cs + m lc + (c % cw)).
 //
 // Design:
-//  * the output is tiny (k2 x (n+1)) and K = k1 is long, so the k-blocks of every output tile are
-//    flattened into one range that is split evenly over the CTAs (stream-K): CTA c takes
-//    [c total / P, (c+1) total / P) and writes one partial tile per tile it touches; a second kernel
-//    adds the partials of each tile in increasing k order (fixed order: deterministic, and the
-//    accumulation depth of one chain is bounded, see below);
-//  * CTA tile BM = 64 MW rows x BN = 8 NT columns (a column chunk of Y^T, <= 72); 8 warps, warp w owns
-//    rows [8 MW w, 8 MW (w+1)) x all BN columns: MW x NT independent DMMA m8n8k4 accumulators;
-//  * operands staged by cp.async (16 B, zero-filled past k1) into a STAGES-deep ring; shared rows are
-//    padded to ld == 4 (mod 16) doubles so the A fragment (row g, k t) and B fragment (k t, col g)
-//    loads of a half-warp hit 16 distinct double-banks (conflict-free);
-//  * error bound: a DMMA chain accumulates at most kFlushK = 4096 products, then is
-//    added into a second register accumulator; with <= ceil(k1 / 4096) + #partials further fp64 adds
-//    the error stays <= (4096 + ~50) u |G| T, inside 1e-12 |G| T.
+//  * the output is tiny (k2 x (n+1)) and K = k1 is long.  Every output tile's K range is cut into
+//    slabs of kSlabK = 4096 (the accumulation-depth bound below); the (tile, slab) k-blocks are
+//    flattened into one range split evenly over the CTAs (stream-K): CTA c takes
+//    [c total / P, (c+1) total / P), keeps one running partial tile per tile it touches (its slabs
+//    added in order), and the reduce kernel adds the CTAs' partials of each tile in CTA order
+//    (= increasing k; deterministic);
+//  * CTA tile BM = 128 rows x BN = 8 NT columns (a column chunk of Y^T, <= 72); 8 warps, warp w owns
+//    rows [16 w, 16 w + 16) x all BN columns: 2 x NT independent DMMA m8n8k4 accumulators; two CTAs
+//    per SM (16 warps: the DMMA issue latency of one warp is hidden by the others -- with one
+//    8-warp CTA the pipe was 62% busy, ncu r02);
+//  * operands staged by the TMA engine (1-D bulk copies, one per G column / Y^T row, issued by one
+//    producer warp; mbarrier completion) into a 4-deep ring; shared rows are padded to ld == 4
+//    (mod 16) doubles so the A fragment (row g, k t) and B fragment (k t, col g) loads of a half-warp
+//    hit 16 distinct double-banks (conflict-free).  Per-thread cp.async cost as many instructions as
+//    the DMMA loop itself (ncu r02);
+//  * error bound: one DMMA chain accumulates at most kSlabK = 4096 products; the
+//    ceil(k1 / 4096) slab sums and the CTA partials are then added in fp64, so the error stays
+//    <= (4096 + k1 / 4096 + #CTAs per tile) u |G| T, inside 1e-12 |G| T for k1 <= 2^27.
 #include <algorithm>
 #include <cstdlib>
 
@@ -29,40 +34,29 @@ namespace csk {
 namespace {
 
 constexpr int kGsWarps = 8;
-constexpr int kFlushK = 4096;
+constexpr int kSlabK = 4096;
+constexpr int kBK = 16;
+constexpr int kStages = 4;
+constexpr int kMW = 2;   // m8 tiles per warp
 
 __host__ __device__ constexpr int pad16_4(int x) { return ((x + 11) / 16) * 16 + 4; }   // >= x, == 4 mod 16
 
-template <int MW, int NT, int BK, int STAGES>
+template <int NT>
 struct Cfg {
-    static constexpr int BM = 8 * kGsWarps * MW;
+    static constexpr int BM = 8 * kGsWarps * kMW;   // 128
     static constexpr int BN = 8 * NT;
     static constexpr int LDA = pad16_4(BM);
     static constexpr int LDB = pad16_4(BN);
-    static constexpr int A_STAGE = BK * LDA;   // doubles
-    static constexpr int B_STAGE = BK * LDB;
+    static constexpr int A_STAGE = kBK * LDA;   // doubles
+    static constexpr int B_STAGE = kBK * LDB;
     static constexpr int STAGE = A_STAGE + B_STAGE;
-    static constexpr size_t SMEM = (size_t)STAGES * STAGE * sizeof(double);
-    static constexpr int FLUSH_BLOCKS = kFlushK / BK;
+    static constexpr size_t SMEM = (size_t)kStages * STAGE * sizeof(double);
 };
 
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
-    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
-    const int n = valid ? 16 : 0;   // src-size 0: 16 zero bytes (K tail)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-// not volatile: a pure function of its operands, so the compiler may interleave it with the
-// fragment loads of the next k-step (the DMMA chains' latency is what the issue order must hide)
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
     asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                 : "+d"(c0), "+d"(c1)
-                 : "d"(a), "d"(b));
+        : "+d"(c0), "+d"(c1)
+        : "d"(a), "d"(b));
 }
 
 struct GsArgs {
@@ -75,7 +69,9 @@ struct GsArgs {
     int cw, ncols;
     int MT, NCH;        // M tiles, column chunks
     int64_t KB;         // k-blocks per tile
-    int64_t total;      // MT * NCH * KB
+    int64_t VKB;        // k-blocks per slab
+    int64_t NS;         // slabs per tile
+    int64_t total;      // MT * NCH * NS * VKB (flattened, last slab of a tile padded)
     int P;              // CTAs
     int maxseg;         // partial slots per CTA
     double* part;       // P * maxseg partial tiles (BM x BN, column-major)
@@ -85,182 +81,228 @@ struct GsArgs {
 __host__ __device__ __forceinline__ int64_t range_begin(int64_t c, int64_t total, int P) {
     return (int64_t)(((uint64_t)c * (uint64_t)total) / (uint64_t)P);   // c <= P <= 2^16, total < 2^47
 }
+// the CTA whose range holds flattened k-block q
+__device__ __forceinline__ int cta_of(int64_t q, int64_t total, int P) {
+    int c = (int)(((uint64_t)q * (uint64_t)P) / (uint64_t)total);
+    while (c + 1 < P && range_begin(c + 1, total, P) <= q) ++c;
+    while (c > 0 && range_begin(c, total, P) > q) --c;
+    return c;
+}
 
-template <int MW, int NT, int BK, int STAGES>
-__global__ void __launch_bounds__(kGsWarps * 32, 1) gstage_kernel(GsArgs a) {
-    using C = Cfg<MW, NT, BK, STAGES>;
+// position of a flattened k-block: (tile, slab, k-block within the slab), advanced without divisions
+struct Cursor {
+    int64_t kb;      // k-block within the tile (slab * VKB + kin)
+    int64_t kin;     // k-block within the slab
+    int64_t slab, tile;
+    int mt, ch;
+    __device__ void init(int64_t q, const GsArgs& a) {
+        const int64_t vt = q / a.VKB;
+        kin = q - vt * a.VKB;
+        tile = vt / a.NS;
+        slab = vt - tile * a.NS;
+        kb = slab * a.VKB + kin;
+        mt = (int)(tile % a.MT);
+        ch = (int)(tile / a.MT);
+    }
+    __device__ void next(const GsArgs& a) {
+        ++kb;
+        if (++kin == a.VKB) {
+            kin = 0;
+            if (++slab == a.NS) {
+                slab = 0;
+                ++tile;
+                if (++mt == a.MT) {
+                    mt = 0;
+                    ++ch;
+                }
+            }
+            kb = slab * a.VKB;
+        }
+    }
+};
+
+__device__ __forceinline__ void mbar_expect_only(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((uint32_t)__cvta_generic_to_shared(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(dst)),
+        "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
+        : "memory");
+}
+
+template <int NT>
+__global__ void __launch_bounds__(kGsWarps * 32, 2) gstage_kernel(GsArgs a) {
+    using C = Cfg<NT>;
     extern __shared__ __align__(16) double gs_smem[];
+    __shared__ __align__(8) uint64_t full_bar[kStages];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
     const int64_t q0 = range_begin(blockIdx.x, a.total, a.P);
     const int64_t q1 = range_begin(blockIdx.x + 1, a.total, a.P);
     if (q0 >= q1) return;
-    const int64_t tile0 = q0 / a.KB;
+    const int64_t nq = q1 - q0;
+    if (tid < kStages) mbar_init(&full_bar[tid], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
 
-    // ---- loader: flattened k-block q -> stage slot
-    auto load = [&](int64_t q, int slot) {
-        const int64_t tile = q / a.KB, kb = q - tile * a.KB;
-        const int mt = (int)(tile % a.MT), ch = (int)(tile / a.MT);
-        const int64_t k0 = kb * BK;
-        double* sA = gs_smem + (size_t)slot * C::STAGE;
-        double* sB = sA + C::A_STAGE;
-        // G tile: BK columns of BM contiguous doubles (rows m0 .. m0 + BM; ldg >= k2 and the
-        // allocation has BM doubles of tail padding, so reads past row k2 stay in bounds)
-        const double* Gt = a.G + (int64_t)mt * C::BM;
-        constexpr int A_CHUNKS = BK * C::BM / 2;
-#pragma unroll
-        for (int i = 0; i < (A_CHUNKS + kGsWarps * 32 - 1) / (kGsWarps * 32); ++i) {
-            const int id = tid + i * kGsWarps * 32;
-            if (A_CHUNKS % (kGsWarps * 32) == 0 || id < A_CHUNKS) {
-                const int kk = id / (C::BM / 2), m2 = id - kk * (C::BM / 2);
-                const int64_t k = k0 + kk;
-                const bool v = k < a.k1;
-                cp_async16(sA + kk * C::LDA + 2 * m2, Gt + (v ? k : 0) * a.ldg + 2 * m2, v);
+    // ---- producer: warp 0 moves one k-block into a stage with 1-D bulk copies (TMA engine), one row
+    // per lane: lanes 0..15 the G rows (BM doubles, 1 KB each), lanes 16..31 the Y^T rows (the chunk's
+    // columns rounded up to 16 B); rows past k1 are zeroed in shared memory instead.  Lane 0 posts the
+    // byte count first and arrives after the warp's copies and zero stores are issued.
+    Cursor lc;
+    lc.init(q0, a);
+    auto load = [&](int slot) {
+        if (lc.kb < a.KB) {   // padding k-blocks of a short last slab load nothing (nor wait)
+            const int64_t k0 = lc.kb * kBK;
+            const int nrows = (int)(a.k1 - k0 < kBK ? a.k1 - k0 : kBK);
+            const int pieces = (min(a.cw, a.ncols - lc.ch * a.cw) + 1) >> 1;
+            const uint32_t bbytes = (uint32_t)pieces * 16;
+            uint64_t* bar = &full_bar[slot];
+            if (lane == 0) mbar_expect_only(bar, (uint32_t)nrows * (C::BM * 8 + bbytes));
+            __syncwarp();
+            double* sA = gs_smem + (size_t)slot * C::STAGE;
+            double* sB = sA + C::A_STAGE;
+            const int kk = lane & 15;
+            if (lane < 16) {
+                if (kk < nrows)
+                    bulk_g2s(sA + kk * C::LDA, a.G + (int64_t)lc.mt * C::BM + (k0 + kk) * a.ldg, C::BM * 8, bar);
+                else
+                    for (int e = 0; e < C::BM; ++e) sA[kk * C::LDA + e] = 0.0;
+            } else {
+                if (kk < nrows)
+                    bulk_g2s(sB + kk * C::LDB, a.Yt + (int64_t)lc.ch * a.cs + (k0 + kk) * a.lc, bbytes, bar);
+                else
+                    for (int e = 0; e < 2 * pieces; ++e) sB[kk * C::LDB + e] = 0.0;
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar);
         }
-        // Y^T tile: BK rows of the chunk's (<= BN) columns, 16-B pieces up to the even width
-        const int c0 = ch * a.cw;
-        const int ncw = min(a.cw, a.ncols - c0);
-        const int pieces = (ncw + 1) >> 1;
-        const double* Yc = a.Yt + (int64_t)ch * a.cs;
-        for (int id = tid; id < BK * (C::BN / 2); id += kGsWarps * 32) {
-            const int kk = id / (C::BN / 2), p = id - kk * (C::BN / 2);
-            if (p < pieces) {
-                const int64_t k = k0 + kk;
-                const bool v = k < a.k1;
-                cp_async16(sB + kk * C::LDB + 2 * p, Yc + (v ? k : 0) * a.lc + 2 * p, v);
-            }
-        }
+        lc.next(a);
     };
 
-    double acc[MW][NT][2], hi[MW][NT][2];
+    double acc[kMW][NT][2];
 #pragma unroll
-    for (int i = 0; i < MW; ++i)
+    for (int i = 0; i < kMW; ++i)
 #pragma unroll
-        for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = hi[i][j][0] = hi[i][j][1] = 0.0;
+        for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    const int64_t nq = q1 - q0;
-#pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) {
-        if (s < nq) load(q0 + s, s);
-        cp_async_commit();
-    }
-    int64_t seg_begin = q0;
+    if (warp == 0)
+        for (int s = 0; s < kStages - 1 && s < nq; ++s) load(s);
+    Cursor cc;
+    cc.init(q0, a);
+    const int64_t tile0 = cc.tile;
+    bool first_flush = true;   // the running sum of this tile's slot is not written yet
+    uint32_t phase = 0;        // bit s: parity of stage s's next completion (padding blocks skip a stage)
     for (int64_t i = 0; i < nq; ++i) {
-        const int64_t q = q0 + i;
-        cp_async_wait<STAGES - 2>();
-        __syncthreads();
-        if (i + STAGES - 1 < nq) load(q + STAGES - 1, (int)((i + STAGES - 1) % STAGES));
-        cp_async_commit();
-        const double* sA = gs_smem + (size_t)(i % STAGES) * C::STAGE + 8 * MW * warp + g;
-        const double* sB = gs_smem + (size_t)(i % STAGES) * C::STAGE + C::A_STAGE + g;
-        // fragments double-buffered in registers: step k4 + 1's loads issue before step k4's DMMAs
-        double fa[2][MW], fb[2][NT];
+        __syncthreads();   // every warp is done with the stage the producer refills next
+        if (warp == 0 && i + kStages - 1 < nq) load((int)((i + kStages - 1) % kStages));
+        if (cc.kb < a.KB) {
+            const int slot = (int)(i % kStages);
+            mbar_wait(&full_bar[slot], (phase >> slot) & 1u);
+            phase ^= 1u << slot;
+            const double* sA = gs_smem + (size_t)(i % kStages) * C::STAGE + 8 * kMW * warp + g;
+            const double* sB = gs_smem + (size_t)(i % kStages) * C::STAGE + C::A_STAGE + g;
 #pragma unroll
-        for (int mi = 0; mi < MW; ++mi) fa[0][mi] = sA[t * C::LDA + 8 * mi];
+            for (int k4 = 0; k4 < kBK / 4; ++k4) {
+                double fa[kMW], fb[NT];
 #pragma unroll
-        for (int nj = 0; nj < NT; ++nj) fb[0][nj] = sB[t * C::LDB + 8 * nj];
+                for (int mi = 0; mi < kMW; ++mi) fa[mi] = sA[(4 * k4 + t) * C::LDA + 8 * mi];
 #pragma unroll
-        for (int k4 = 0; k4 < BK / 4; ++k4) {
-            const int cur = k4 & 1, nxt = cur ^ 1;
-            if (k4 + 1 < BK / 4) {
+                for (int nj = 0; nj < NT; ++nj) fb[nj] = sB[(4 * k4 + t) * C::LDB + 8 * nj];
 #pragma unroll
-                for (int mi = 0; mi < MW; ++mi) fa[nxt][mi] = sA[(4 * k4 + 4 + t) * C::LDA + 8 * mi];
+                for (int nj = 0; nj < NT; ++nj)
 #pragma unroll
-                for (int nj = 0; nj < NT; ++nj) fb[nxt][nj] = sB[(4 * k4 + 4 + t) * C::LDB + 8 * nj];
+                    for (int mi = 0; mi < kMW; ++mi) dmma(acc[mi][nj][0], acc[mi][nj][1], fa[mi], fb[nj]);
             }
-#pragma unroll
-            for (int mi = 0; mi < MW; ++mi)
-#pragma unroll
-                for (int nj = 0; nj < NT; ++nj) dmma(acc[mi][nj][0], acc[mi][nj][1], fa[cur][mi], fb[cur][nj]);
         }
-        const int64_t tile = q / a.KB;
-        const bool seg_end = (q + 1 == q1) || ((q + 1) % a.KB == 0);
-        if (seg_end || (q - seg_begin + 1) % C::FLUSH_BLOCKS == 0) {
+        const bool cta_end = i + 1 == nq;
+        const bool slab_end = cc.kin + 1 == a.VKB;
+        const bool tile_end = slab_end && cc.slab + 1 == a.NS;
+        if (cta_end || slab_end) {
+            // fold this slab's DMMA chains (<= 4096 products) into the tile's running sum, which lives in
+            // the CTA's own partial slot (L2-resident; each thread touches only its own elements)
+            double* P = a.part + ((int64_t)blockIdx.x * a.maxseg + (cc.tile - tile0)) * (C::BM * C::BN);
 #pragma unroll
-            for (int mi = 0; mi < MW; ++mi)
+            for (int mi = 0; mi < kMW; ++mi)
 #pragma unroll
                 for (int nj = 0; nj < NT; ++nj) {
-                    hi[mi][nj][0] += acc[mi][nj][0];
-                    hi[mi][nj][1] += acc[mi][nj][1];
+                    const int m = 8 * kMW * warp + 8 * mi + g, n = 8 * nj + 2 * t;
+                    double* p0 = P + (int64_t)n * C::BM + m;
+                    double* p1 = p0 + C::BM;
+                    if (first_flush) {
+                        *p0 = acc[mi][nj][0];
+                        *p1 = acc[mi][nj][1];
+                    } else {
+                        *p0 += acc[mi][nj][0];
+                        *p1 += acc[mi][nj][1];
+                    }
                     acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
                 }
+            first_flush = tile_end;
         }
-        if (seg_end) {
-            // partial tile (BM x BN column-major) of this segment -> slot (CTA, tile - tile0)
-            double* P = a.part + ((int64_t)blockIdx.x * a.maxseg + (tile - tile0)) * (C::BM * C::BN);
-#pragma unroll
-            for (int mi = 0; mi < MW; ++mi)
-#pragma unroll
-                for (int nj = 0; nj < NT; ++nj) {
-                    const int m = 8 * MW * warp + 8 * mi + g, n = 8 * nj + 2 * t;
-                    P[(int64_t)n * C::BM + m] = hi[mi][nj][0];
-                    P[(int64_t)(n + 1) * C::BM + m] = hi[mi][nj][1];
-                    hi[mi][nj][0] = hi[mi][nj][1] = 0.0;
-                }
-            seg_begin = q + 1;
-        }
+        cc.next(a);
     }
-    cp_async_wait<0>();
 }
 
-// Z[m, c] (valid rows < k2, columns < ncols) = sum over the CTAs that touched the tile, in CTA order
-// (= increasing k), of their partials.  One thread per output element.
+// Z = sum of the partials of each tile, fixed order.  A block owns 32 consecutive elements (lane) of
+// one tile; warp w adds the partials of the contributing CTAs c_lo + w, c_lo + w + 8, ... (CTA order =
+// increasing k), and the 8 warp sums are added in warp order.
 template <typename TZ>
-__global__ void gstage_reduce_kernel(GsArgs a, int BM, int BN, TZ* __restrict__ Z, int64_t ldz) {
-    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(256) gstage_reduce_kernel(GsArgs a, int BM, int BN, TZ* __restrict__ Z,
+                                                            int64_t ldz) {
+    __shared__ double red[8][33];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t per_tile = (int64_t)BM * BN;
-    const int64_t tile = e / per_tile;
-    if (tile >= (int64_t)a.MT * a.NCH) return;
-    const int r = (int)(e - tile * per_tile);
-    const int m_loc = r % BM, n_loc = r / BM;
-    const int mt = (int)(tile % a.MT), ch = (int)(tile / a.MT);
-    const int m = mt * BM + m_loc, c = ch * a.cw + n_loc;
-    if (m >= a.k2 || n_loc >= a.cw || c >= a.ncols) return;
-    // contributors: CTAs whose range [q0, q1) meets [tile KB, (tile+1) KB)
-    const int64_t lo = tile * a.KB, hi = lo + a.KB;
-    int c_lo = 0, c_hi = a.P - 1;
-    {   // largest c with q0(c) <= lo
-        int L = 0, R = a.P - 1;
-        while (L < R) {
-            const int mid = (L + R + 1) >> 1;
-            if (range_begin(mid, a.total, a.P) <= lo) L = mid; else R = mid - 1;
-        }
-        c_lo = L;
-        L = c_lo, R = a.P - 1;   // largest c with q0(c) < hi
-        while (L < R) {
-            const int mid = (L + R + 1) >> 1;
-            if (range_begin(mid, a.total, a.P) < hi) L = mid; else R = mid - 1;
-        }
-        c_hi = L;
-    }
+    const int64_t blocks_per_tile = per_tile / 32;
+    const int64_t tile = blockIdx.x / blocks_per_tile;
+    const int r = (int)((blockIdx.x - tile * blocks_per_tile) * 32 + lane);
+    const int64_t tq = a.NS * a.VKB;   // flattened k-blocks per tile
+    const int c_lo = cta_of(tile * tq, a.total, a.P), c_hi = cta_of((tile + 1) * tq - 1, a.total, a.P);
     double z = 0.0;
-    for (int cc = c_lo; cc <= c_hi; ++cc) {
-        const int64_t q0 = range_begin(cc, a.total, a.P), q1 = range_begin(cc + 1, a.total, a.P);
-        if (q1 <= q0) continue;   // empty range (P > total)
-        const int64_t slot = (int64_t)cc * a.maxseg + (tile - q0 / a.KB);
+    for (int cc = c_lo + warp; cc <= c_hi; cc += 8) {
+        const int64_t slot = (int64_t)cc * a.maxseg + (tile - range_begin(cc, a.total, a.P) / tq);
         z += a.part[slot * per_tile + r];
     }
-    Z[m + (int64_t)c * ldz] = (TZ)z;
+    red[warp][lane] = z;
+    __syncthreads();
+    if (warp == 0) {
+        double zz = red[0][lane];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) zz += red[w][lane];
+        const int m_loc = r % BM, n_loc = r / BM;
+        const int mt = (int)(tile % a.MT), ch = (int)(tile / a.MT);
+        const int m = mt * BM + m_loc, c = ch * a.cw + n_loc;
+        if (m < a.k2 && n_loc < a.cw && c < a.ncols) Z[m + (int64_t)c * ldz] = (TZ)zz;
+    }
 }
 
-template <int MW, int NT, int BK, int STAGES>
+template <int NT>
 csk_status launch(GsArgs& a, void* Z, int64_t ldz, bool z_f32, cudaStream_t st) {
-    using C = Cfg<MW, NT, BK, STAGES>;
-    auto kern = gstage_kernel<MW, NT, BK, STAGES>;
+    using C = Cfg<NT>;
+    auto kern = gstage_kernel<NT>;
     CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     a.MT = (a.k2 + C::BM - 1) / C::BM;
     a.NCH = (a.ncols + a.cw - 1) / a.cw;
-    a.KB = ceil_div(a.k1, BK);
-    a.total = (int64_t)a.MT * a.NCH * a.KB;
+    a.KB = ceil_div(a.k1, kBK);
+    a.VKB = std::min<int64_t>(kSlabK / kBK, a.KB);
+    a.NS = ceil_div(a.KB, a.VKB);
+    a.total = (int64_t)a.MT * a.NCH * a.NS * a.VKB;
+    CSK_REQUIRE(a.total < (int64_t(1) << 47), CSK_EUNSUPPORTED, "G-stage: k1 too large");
     const int nsm = device_info().num_sms;
-    // at least ~2 k-blocks per CTA (the ring needs work to overlap), at most one CTA per SM
-    int64_t P = std::min<int64_t>(nsm, std::max<int64_t>(1, a.total / 2));
+    // two CTAs per SM, each with >= 4 k-blocks (the ring needs work to overlap)
+    int64_t P = std::min<int64_t>(2 * nsm, std::max<int64_t>(1, a.total / 4));
+    if (launch_caps().gs_ctas > 0) P = std::min<int64_t>(P, launch_caps().gs_ctas);
     if (const char* e = std::getenv("CSK_GS_CTAS")) P = std::max<int64_t>(1, std::min<int64_t>(std::atoll(e), a.total));
     a.P = (int)P;
-    CSK_REQUIRE(a.total < (int64_t(1) << 47), CSK_EUNSUPPORTED, "G-stage: k1 too large");
-    const int64_t share = ceil_div(a.total, P);
-    a.maxseg = (int)(ceil_div(share, a.KB) + 1);
+    a.maxseg = (int)(ceil_div(ceil_div(a.total, P), a.NS * a.VKB) + 1);   // tiles one CTA can touch
     const size_t part_bytes = (size_t)P * a.maxseg * C::BM * C::BN * sizeof(double);
     double* part = nullptr;
     CSK_CUDA_TRY(csk_malloc_async(&part, part_bytes, st));
@@ -268,8 +310,7 @@ csk_status launch(GsArgs& a, void* Z, int64_t ldz, bool z_f32, cudaStream_t st) 
     kern<<<(unsigned)P, kGsWarps * 32, C::SMEM, st>>>(a);
     count_launch();
     cudaError_t e1 = cudaGetLastError();
-    const int64_t outs = (int64_t)a.MT * a.NCH * C::BM * C::BN;
-    const unsigned rgrid = (unsigned)ceil_div(outs, 256);
+    const unsigned rgrid = (unsigned)((int64_t)a.MT * a.NCH * (C::BM * C::BN / 32));
     if (e1 == cudaSuccess) {
         if (z_f32)
             gstage_reduce_kernel<float><<<rgrid, 256, 0, st>>>(a, C::BM, C::BN, (float*)Z, ldz);
@@ -286,21 +327,10 @@ csk_status launch(GsArgs& a, void* Z, int64_t ldz, bool z_f32, cudaStream_t st) 
     return CSK_OK;
 }
 
-template <int MW>
-csk_status dispatch_nt(GsArgs& a, int nt, void* Z, int64_t ldz, bool z_f32, cudaStream_t st) {
-    constexpr int BK = 32;
-    constexpr int ST = 4;
-    if (nt <= 1) return launch<MW, 1, BK, ST>(a, Z, ldz, z_f32, st);
-    if (nt <= 2) return launch<MW, 2, BK, ST>(a, Z, ldz, z_f32, st);
-    if (nt <= 4) return launch<MW, 4, BK, ST>(a, Z, ldz, z_f32, st);
-    if (nt <= 7) return launch<MW, 7, BK, ST>(a, Z, ldz, z_f32, st);
-    return launch<MW, 9, BK, ST>(a, Z, ldz, z_f32, st);
-}
-
 }  // namespace
 
-// Z (k2 x ncols, column-major, ldz; fp64 or fp32) = G (k2 x k1, ldg, >= 256 doubles of tail padding)
-// times the row-major workspace described by ro (ro.cw <= 72 columns per chunk).
+// Z (k2 x ncols, column-major, ldz; fp64 or fp32) = G (k2 x k1, ldg, kGstageTailPad doubles of tail
+// padding) times the row-major workspace described by ro (ro.cw <= 72 columns per chunk).
 csk_status gstage_launch(const double* G, int64_t ldg, int64_t k2, int64_t k1, const RowOut& ro, void* Z,
                          int64_t ldz, bool z_f32, cudaStream_t st) {
     CSK_REQUIRE(ro.ws != nullptr && ro.cw >= 1 && ro.cw <= kGstageMaxCw, CSK_EINVAL,
@@ -319,9 +349,11 @@ csk_status gstage_launch(const double* G, int64_t ldg, int64_t k2, int64_t k1, c
     a.cw = ro.cw;
     a.ncols = ro.ncols;
     const int nt = (ro.cw + 7) / 8;
-    // BM = 128 rows per CTA tile (MW = 2): the two register accumulator sets (DMMA chain + flush target)
-    // of a 128 x 72 tile take 144 of a thread's registers; 256-row tiles would spill
-    return dispatch_nt<2>(a, nt, Z, ldz, z_f32, st);
+    if (nt <= 1) return launch<1>(a, Z, ldz, z_f32, st);
+    if (nt <= 2) return launch<2>(a, Z, ldz, z_f32, st);
+    if (nt <= 4) return launch<4>(a, Z, ldz, z_f32, st);
+    if (nt <= 7) return launch<7>(a, Z, ldz, z_f32, st);
+    return launch<9>(a, Z, ldz, z_f32, st);
 }
 
 }  // namespace csk
