@@ -47,6 +47,11 @@ struct RowLayout {
     // CSK_PLAN_HASH: global row of local row 0 and the Philox key (codes recomputed in the kernel)
     int64_t g0 = 0;
     uint32_t hkey0 = 0, hkey1 = 0;
+    // fp64 B32 with few buckets (k1 (n+1) small, e.g. n = 32 at k1 = 2n^2): CTA c reduces into copy
+    // c % nspread of SA^T (stride spread_stride doubles), so the bulk reduce-adds of all SMs are not
+    // funnelled into the few L2 lines of a small SA^T; the copies are summed afterwards in fixed order
+    int nspread = 1;
+    int64_t spread_stride = 0;
     unsigned long long* work = nullptr;   // dynamic work counter of the B kernels (zeroed with the workspace)
     int grab = 8;                         // units per counter grab (4/8/16/32 measured: 8)
     __host__ __device__ int64_t base(int ch, uint32_t bucket) const { return (int64_t)ch * cs + (int64_t)bucket * lc; }
@@ -416,6 +421,7 @@ __global__ void __launch_bounds__(C::kWarps * 32, 1) cs_bulk_kernel(const uint32
 // bulk-reduces row r.  fp64, 16-B aligned columns (lda even); the ragged last tile falls
 // back to clamped scalar loads.
 constexpr int kB32Rows = 32;
+constexpr int64_t kSpreadBytes = 256ll << 10;   // spread-copy footprint target (measured)
 // row r of a warp's tile: 8-row group g = r >> 3 is shifted by 2g doubles (rows never overlap, 16-B aligned)
 __device__ __forceinline__ int b32_row(int r, int ld) { return r * ld + 2 * (r >> 3); }
 constexpr int kB32Pad = 6;   // doubles per warp tile beyond 32 rows (the shift of the last group)
@@ -456,16 +462,22 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
         u = (int64_t)ub;
         uend = min(u + kGrab, nunits);
     }
-    for (; u < nunits;) {
+    // Look-ahead order: tile i is stored into the warp's shared tile, then tile i+1's loads are
+    // issued, and only then are tile i's 32 bulk reduce-adds issued -- the per-row issue loop (one
+    // uniform-datapath UBLKRED per lane, ~20-30 cycles each, ncu r02) runs while the next tile's
+    // loads are in flight instead of in front of them.  Registers hold one tile either way.
+    int ch = 0, nc = 0;
+    int64_t r0 = 0;
+    uint32_t ca = 0, cb = 0, crow = 0;
+    double2 v[kJ];
+    auto fetch = [&]() {   // coordinates, codes and loads of unit u
         int64_t g;
-        int ch;
         unit_coords(u, nchunks, ngroups, L.chunk_major, g, ch);
         const int c0 = ch * cw;
-        const int nc = min(cw, ncols - c0);
-        const int64_t r0 = g * kB32Rows;
+        nc = min(cw, ncols - c0);
+        r0 = g * kB32Rows;
         const bool full = r0 + kB32Rows <= rows;
         const int64_t ra = min(r0 + 2 * p, rows - 1), rb = min(r0 + 2 * p + 1, rows - 1);
-        uint32_t ca, cb, crow;
         if constexpr (HASH) {
             // CSK_PLAN_HASH (hash-based generation on the fly): lane r hashes row r0 + r
             // (one Philox4x32-10 block, the word of its row) and the pair rows come by shuffle --
@@ -482,7 +494,6 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
             cb = __ldg(code + rb);
             crow = __ldg(code + min(r0 + lane, rows - 1));
         }
-        double2 v[kJ];
         if (full && !PRED) {
             // (nearly) full-width chunk (C2, C4): lanes past the chunk's last column re-read that
             // column (an L1 hit, no DRAM bytes) and drop the value.  Plain loads schedule better
@@ -514,7 +525,19 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
                 v[j] = (c < nc) ? make_double2(xa, r0 + 2 * p + 1 < rows ? xb : 0.0) : make_double2(0.0, 0.0);
             }
         }
-        // the TMA engine must have finished reading this tile (bulk ops of the previous unit)
+    };
+    auto advance = [&]() {
+        if (++u >= uend) {
+            unsigned long long ub = 0;
+            if (lane == 0) ub = atomicAdd(L.work, (unsigned long long)kGrab);
+            ub = __shfl_sync(0xffffffffu, ub, 0);
+            u = (int64_t)ub;
+            uend = min(u + kGrab, nunits);
+        }
+    };
+    if (u < nunits) fetch();
+    while (u < nunits) {
+        // the TMA engine must have finished reading the tile (bulk ops of the previous unit)
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncwarp();
         double* ta = tile + b32_row(2 * p, ldtile);
@@ -534,34 +557,34 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (r0 + lane < rows && !(EXP & 1)) {
-            const uint32_t bytes = (uint32_t)(((nc + 1) & ~1) * 8);
-            double* dst = SAt + L.base(ch, code_bucket(crow));
-            const uint32_t src = (uint32_t)__cvta_generic_to_shared(tile + b32_row(lane, ldtile));
-            if constexpr (PRED) {
-                // narrow chunks (C3): the chunk's SA^T slice (54 MB) competes with the streamed A for
-                // L2; mark the reductions evict_last so the slice is not written back mid-pass
-                uint64_t pol;
-                asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-                asm volatile(
-                    "cp.reduce.async.bulk.global.shared::cta.bulk_group.L2::cache_hint.add.f64 [%0], [%1], %2, %3;" ::"l"(
-                        dst),
-                    "r"(src), "r"(bytes), "l"(pol)
-                    : "memory");
-            } else {
-                asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(dst),
-                             "r"(src), "r"(bytes)
-                             : "memory");
+        // this tile's bulk reduce-adds: lane r reduces row r (its bucket's SA^T row, spread copy of the CTA)
+        const bool bvalid = r0 + lane < rows && !(EXP & 1);
+        const uint32_t bytes = (uint32_t)(((nc + 1) & ~1) * 8);
+        double* dst = SAt + L.base(ch, code_bucket(crow)) + (int64_t)(blockIdx.x % L.nspread) * L.spread_stride;
+        const uint32_t src = (uint32_t)__cvta_generic_to_shared(tile + b32_row(lane, ldtile));
+        auto issue = [&]() {
+            if (bvalid) {
+                if constexpr (PRED) {
+                    // narrow chunks (C3): the chunk's SA^T slice (54 MB) competes with the streamed A for
+                    // L2; mark the reductions evict_last so the slice is not written back mid-pass
+                    uint64_t pol;
+                    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+                    asm volatile(
+                        "cp.reduce.async.bulk.global.shared::cta.bulk_group.L2::cache_hint.add.f64 [%0], [%1], %2, %3;" ::"l"(
+                            dst),
+                        "r"(src), "r"(bytes), "l"(pol)
+                        : "memory");
+                } else {
+                    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(dst),
+                                 "r"(src), "r"(bytes)
+                                 : "memory");
+                }
             }
-        }
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        if (++u >= uend) {
-            unsigned long long ub = 0;
-            if (lane == 0) ub = atomicAdd(L.work, (unsigned long long)kGrab);
-            ub = __shfl_sync(0xffffffffu, ub, 0);
-            u = (int64_t)ub;
-            uend = min(u + kGrab, nunits);
-        }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        };
+        advance();
+        if (u < nunits) fetch();   // next tile's loads in flight ...
+        issue();                   // ... while this tile's reduce-adds are issued
     }
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
@@ -618,17 +641,21 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk64f_kernel(const uint32_t* _
         u = (int64_t)ub;
         uend = min(u + kGrab, nunits);
     }
-    while (u < nunits) {
+    // look-ahead issue order as in cs_bulk32_kernel: store tile i, issue tile i+1's loads, then tile i's
+    // 64 bulk reduce-adds (ncu r02: the per-row issue loop otherwise ran with no loads in flight)
+    int ch = 0, nc = 0;
+    int64_t r0 = 0;
+    uint32_t ca = 0, cb = 0;
+    float v[kJ][8];
+    auto fetch = [&]() {
         int64_t g;
-        int ch;
         unit_coords(u, nchunks, ngroups, L.chunk_major, g, ch);
         const int c0 = ch * cw;
-        const int nc = min(cw, ncols - c0);
-        const int64_t r0 = g * kF32Rows;
+        nc = min(cw, ncols - c0);
+        r0 = g * kF32Rows;
         const bool full = r0 + kF32Rows <= rows;
-        const uint32_t ca = __ldg(code + min(r0 + lane, rows - 1));
-        const uint32_t cb = __ldg(code + min(r0 + 32 + lane, rows - 1));
-        float v[kJ][8];
+        ca = __ldg(code + min(r0 + lane, rows - 1));
+        cb = __ldg(code + min(r0 + 32 + lane, rows - 1));
         if (full) {   // one predicated 32-B load per column quad, no branches
 #pragma unroll
             for (int j = 0; j < kJ; ++j) {
@@ -646,8 +673,10 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk64f_kernel(const uint32_t* _
                 }
             }
         }
-        // sign bits of the 64 rows (bit r = row r negative), one ballot per half -- after the tile's
-        // loads are issued, so the code loads' latency overlaps the column loads' instead of preceding it
+    };
+    if (u < nunits) fetch();
+    while (u < nunits) {
+        // sign bits of the 64 rows (bit r = row r negative), one ballot per half
         const uint32_t sg_lo = __ballot_sync(0xffffffffu, (ca >> 31) != 0u);
         const uint32_t sg_hi = __ballot_sync(0xffffffffu, (cb >> 31) != 0u);
         const uint32_t sgw = q < 4 ? sg_lo : sg_hi;
@@ -668,20 +697,17 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk64f_kernel(const uint32_t* _
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
+        // this tile's reduce-adds: lane r reduces rows r and r + 32 into their row-block copies
+        const uint32_t bytes = (uint32_t)(nc4 * 4);
+        float* dst[2];
+        bool ok[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int r = lane + 32 * h;
-            if (r0 + r < rows) {
-                const uint32_t cr = h ? cb : ca;
-                const int64_t copy = (r0 + r) / L.rows_per_copy;
-                float* dst = SAt + copy * L.copy_stride + (int64_t)ch * L.cs + (int64_t)code_bucket(cr) * L.lc;
-                const uint32_t src = (uint32_t)__cvta_generic_to_shared(tile + r * ldf + 4 * (r >> 3));
-                asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst),
-                             "r"(src), "r"((uint32_t)(nc4 * 4))
-                             : "memory");
-            }
+            ok[h] = r0 + r < rows;
+            const int64_t copy = (r0 + r) / L.rows_per_copy;
+            dst[h] = SAt + copy * L.copy_stride + (int64_t)ch * L.cs + (int64_t)code_bucket(h ? cb : ca) * L.lc;
         }
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         if (++u >= uend) {
             unsigned long long ub = 0;
             if (lane == 0) ub = atomicAdd(L.work, (unsigned long long)kGrab);
@@ -689,6 +715,16 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk64f_kernel(const uint32_t* _
             u = (int64_t)ub;
             uend = min(u + kGrab, nunits);
         }
+        if (u < nunits) fetch();   // next tile's loads in flight while this tile is reduced
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t src = (uint32_t)__cvta_generic_to_shared(tile + (lane + 32 * h) * ldf + 4 * ((lane + 32 * h) >> 3));
+            if (ok[h])
+                asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst[h]),
+                             "r"(src), "r"(bytes)
+                             : "memory");
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
@@ -707,6 +743,15 @@ __global__ void cs_combine_rows_kernel(const float* __restrict__ SAt, RowLayout 
         for (int p = 0; p < L.ncopies; ++p) acc += (double)SAt[p * L.copy_stride + off];
     }
     Yt[e] = acc;
+}
+
+// spread copies (fp64 B32): copy 0 <- sum_p copy_p, elementwise, fixed order p = 0, 1, ...
+__global__ void cs_spread_combine_kernel(double* __restrict__ SAt, int64_t n, int nspread, int64_t stride) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        double acc = SAt[e];
+        for (int p = 1; p < nspread; ++p) acc += SAt[p * stride + e];
+        SAt[e] = acc;
+    }
 }
 
 // SA[m, c] = (float) sum_p (double) copy_p[m, c]  (fixed order over p)
@@ -939,11 +984,6 @@ static bool make_tensor_map(CUtensorMap* tmap, const Cols<T>& cols, int64_t rows
     return cr == CUDA_SUCCESS;
 }
 
-LaunchCaps& launch_caps() {
-    static thread_local LaunchCaps caps;
-    return caps;
-}
-
 static int exp_switch() {   // CSK_EXP: roofline attribution of the B kernels (bench.py), 0 in production
     const char* e = std::getenv("CSK_EXP");
     return e ? std::atoi(e) : 0;
@@ -1039,8 +1079,7 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
                                 : narrow        ? cs_bulk32_kernel<8, 0, true>
                                                 : cs_bulk32_kernel<8, 0>;
                     CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                    int64_t blocks = std::min<int64_t>(ceil_div(units32, 8), (int64_t)di.num_sms);
-                    if (launch_caps().cs_ctas > 0) blocks = std::min<int64_t>(blocks, launch_caps().cs_ctas);
+                    const int64_t blocks = std::min<int64_t>(ceil_div(units32, 8), (int64_t)di.num_sms);
                     prof_mark(st, true);   // right before the launch: host prep is not timed
                     kern<<<(unsigned)blocks, 256, smem, st>>>(code, rows, cols, ncols, ld32, out, LH, (int)plan->k1);
                     CSK_LAUNCH_CHECK();
@@ -1126,6 +1165,13 @@ struct ApplyTarget {
     int64_t ld = 0;
     bool owned = false;
 };
+
+// Footprint the spread copies of a small SA^T should reach (CSK_SPREAD_KB overrides,
+// 0 disables)
+static int64_t spread_target_bytes() {
+    if (const char* e = std::getenv("CSK_SPREAD_KB")) return std::atoll(e) * 1024;
+    return kSpreadBytes;
+}
 
 // Row-major SA^T layout of the B kernels: all columns in one row when ncols <= 66, else the fewest
 // chunks of <= 66 (even) columns; chunk-major (one slice per chunk) when the whole SA^T would take
@@ -1215,7 +1261,9 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
                                              32);
             if (f32acc) {
                 bulk_layout(L, k1, ncols, 4, 8);   // 32-B aligned rows and chunk starts
-                const int64_t ncp = std::max<int64_t>(1, std::min<int64_t>(256, ceil_div(rows, 64 * k1)));
+                // no cap on the copy count: a cap would let the mean depth exceed 64 at small k1 (the 1e-5 bound needs
+                // every bucket sum of a copy to stay far below 1e-5 / u32 = 168 terms)
+                const int64_t ncp = std::max<int64_t>(1, ceil_div(rows, 64 * k1));
                 L.ncopies = (int)ncp;
                 L.rows_per_copy = ceil_div(rows, ncp);
                 L.copy_stride = L.chunk_major ? L.cs * ((ncols + L.cw - 1) / L.cw) : k1 * L.lc;   // floats
@@ -1224,6 +1272,19 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
                 bulk_layout(L, k1, ncols, 8, 4);
                 const int nchunks = (ncols + L.cw - 1) / L.cw;
                 ws_doubles = L.chunk_major ? (size_t)nchunks * L.cs : (size_t)k1 * L.lc;
+                // spread copies for a small SA^T (fp64 B32 kernel only: 16-B aligned columns)
+                const bool b32 = dtype == CSK_F64 && !accumulate &&
+                                 cols_aligned(Cols<double>{static_cast<const double*>(A),
+                                                           static_cast<const double*>(b), lda, (int)n},
+                                              16);
+                if (b32 && !L.chunk_major) {
+                    const int64_t units32 = ceil_div(rows, kB32Rows) * nchunks;
+                    const int64_t ctas = std::min<int64_t>(ceil_div(units32, 8), (int64_t)device_info().num_sms);
+                    const int64_t want = spread_target_bytes() / (int64_t)(ws_doubles * 8);
+                    L.nspread = (int)std::max<int64_t>(1, std::min<int64_t>(want, ctas));
+                    L.spread_stride = (int64_t)ws_doubles;
+                    ws_doubles *= (size_t)L.nspread;
+                }
             }
         } else {
             L.cw = ncols;   // T: its own 32-column chunks, one row of SA^T
@@ -1276,6 +1337,13 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
         }
         return CSK_OK;
     };
+    if (L.nspread > 1) {   // fold the spread copies into copy 0 (the layout every consumer reads)
+        const int64_t ne = L.spread_stride;
+        cs_spread_combine_kernel<<<(unsigned)std::min<int64_t>(ceil_div(ne, 256), 4 * device_info().num_sms), 256, 0,
+                                   st>>>(tgt.buf, ne, L.nspread, L.spread_stride);
+        const csk_status ls = launch_ok("spread combine");
+        if (ls != CSK_OK) return ls;
+    }
     if (rowout != nullptr) {
         if (L.ncopies > 0) {   // fp32 copies -> fp64 row-major workspace (regular layout)
             const int64_t lcd = (ncols + 1) & ~1;

@@ -204,13 +204,6 @@ csk_status rows_from_colmajor(const double* SA, int64_t ld, int64_t k1, int ncol
 csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void* A, int64_t lda,
                          const void* b, void* SA, int64_t ldsa, int variant, cudaStream_t st,
                          int64_t row_begin, int64_t row_end, bool accumulate, RowOut* rowout = nullptr);
-// CTA caps for the NEXT-2 overlap schedule (ms_apply): the CountSketch B kernels and
-// the G-stage launch at most this many CTAs when > 0 (thread-local, set around one launch)
-struct LaunchCaps {
-    int cs_ctas = 0;
-    int gs_ctas = 0;
-};
-LaunchCaps& launch_caps();
 // the plan's cached G (k2 x k1, fp64, column-major with ld *ldg = round_up(k2, 8), rows past k2 zero,
 // followed by kGstageTailPad zero doubles so 128-row tiles may read past the last column)
 constexpr int kGstageTailPad = 256;

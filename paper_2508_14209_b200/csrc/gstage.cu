@@ -33,17 +33,20 @@ namespace csk {
 
 namespace {
 
-constexpr int kGsWarps = 8;
+constexpr int kGsWarps = 4;   // consumer (DMMA) warps; warp kGsWarps is the TMA producer
 constexpr int kSlabK = 4096;
 constexpr int kBK = 16;
 constexpr int kStages = 4;
-constexpr int kMW = 2;   // m8 tiles per warp
 
 __host__ __device__ constexpr int pad16_4(int x) { return ((x + 11) / 16) * 16 + 4; }   // >= x, == 4 mod 16
 
+// NT n8 tiles (BN = 8 NT columns) x MW m8 tiles per consumer warp (BM = 32 MW rows per CTA): MW = 4
+// (128 rows) except for the widest chunk (NT = 9), whose 72 accumulators per thread need MW = 2 to
+// stay inside the 168 registers two 5-warp CTAs per SM allow
 template <int NT>
 struct Cfg {
-    static constexpr int BM = 8 * kGsWarps * kMW;   // 128
+    static constexpr int MW = NT > 8 ? 2 : 4;
+    static constexpr int BM = 8 * kGsWarps * MW;
     static constexpr int BN = 8 * NT;
     static constexpr int LDA = pad16_4(BM);
     static constexpr int LDB = pad16_4(BN);
@@ -139,33 +142,44 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 template <int NT>
-__global__ void __launch_bounds__(kGsWarps * 32, 2) gstage_kernel(GsArgs a) {
+__global__ void __launch_bounds__((kGsWarps + 1) * 32, 2) gstage_kernel(GsArgs a) {
     using C = Cfg<NT>;
     extern __shared__ __align__(16) double gs_smem[];
     __shared__ __align__(8) uint64_t full_bar[kStages];
+    __shared__ __align__(8) uint64_t empty_bar[kStages];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
     const int64_t q0 = range_begin(blockIdx.x, a.total, a.P);
     const int64_t q1 = range_begin(blockIdx.x + 1, a.total, a.P);
     if (q0 >= q1) return;
     const int64_t nq = q1 - q0;
-    if (tid < kStages) mbar_init(&full_bar[tid], 1);
+    if (tid < kStages) {
+        mbar_init(&full_bar[tid], 1);            // the producer's arrive (+ the stage's TMA bytes)
+        mbar_init(&empty_bar[tid], kGsWarps);    // one arrive per consumer warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncthreads();
+    __syncthreads();   // the only CTA-wide barrier: stages are handed over by mbarriers from here on
 
-    // ---- producer: warp 0 moves one k-block into a stage with 1-D bulk copies (TMA engine), one row
-    // per lane: lanes 0..15 the G rows (BM doubles, 1 KB each), lanes 16..31 the Y^T rows (the chunk's
-    // columns rounded up to 16 B); rows past k1 are zeroed in shared memory instead.  Lane 0 posts the
-    // byte count first and arrives after the warp's copies and zero stores are issued.
+    // ---- producer warp (warp kGsWarps): k-block j goes to stage j % S once the consumers released the
+    // stage's previous k-block j - S (empty barrier).  1-D bulk copies (TMA engine), one row per lane:
+    // lanes 0..15 the G rows (BM doubles, 1 KB each), lanes 16..31 the Y^T rows (the chunk's columns
+    // rounded up to 16 B); rows past k1 are zeroed in shared memory instead.  Lane 0 posts the byte
+    // count first and arrives after the warp's copies and zero stores are issued; padding k-blocks of
+    // a short last slab load nothing (the arrive alone completes the phase).  A dedicated warp: with
+    // the producer inside a DMMA warp it ran late behind its own k-blocks (ncu r02: DMMA 77.5%), and
+    // with a CTA barrier per k-block the barrier stall was 26% of the samples (DMMA 82.6%).
     Cursor lc;
     lc.init(q0, a);
-    auto load = [&](int slot) {
-        if (lc.kb < a.KB) {   // padding k-blocks of a short last slab load nothing (nor wait)
+    int64_t produced = 0;
+    auto produce = [&]() {
+        const int slot = (int)(produced % kStages);
+        if (produced >= kStages) mbar_wait(&empty_bar[slot], (uint32_t)((produced / kStages - 1) & 1));
+        uint64_t* bar = &full_bar[slot];
+        if (lc.kb < a.KB) {
             const int64_t k0 = lc.kb * kBK;
             const int nrows = (int)(a.k1 - k0 < kBK ? a.k1 - k0 : kBK);
             const int pieces = (min(a.cw, a.ncols - lc.ch * a.cw) + 1) >> 1;
             const uint32_t bbytes = (uint32_t)pieces * 16;
-            uint64_t* bar = &full_bar[slot];
             if (lane == 0) mbar_expect_only(bar, (uint32_t)nrows * (C::BM * 8 + bbytes));
             __syncwarp();
             double* sA = gs_smem + (size_t)slot * C::STAGE;
@@ -182,47 +196,50 @@ __global__ void __launch_bounds__(kGsWarps * 32, 2) gstage_kernel(GsArgs a) {
                 else
                     for (int e = 0; e < 2 * pieces; ++e) sB[kk * C::LDB + e] = 0.0;
             }
+            if (nrows < kBK) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
-            if (lane == 0) mbar_arrive(bar);
         }
+        if (lane == 0) mbar_arrive(bar);
         lc.next(a);
+        ++produced;
     };
+    if (warp == kGsWarps) {
+        while (produced < nq) produce();
+        return;
+    }
 
-    double acc[kMW][NT][2];
+    // ---- consumer warps: warp w owns rows [32 w, 32 w + 32) of the tile x all BN columns
+    double acc[C::MW][NT][2];
 #pragma unroll
-    for (int i = 0; i < kMW; ++i)
+    for (int i = 0; i < C::MW; ++i)
 #pragma unroll
         for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    if (warp == 0)
-        for (int s = 0; s < kStages - 1 && s < nq; ++s) load(s);
     Cursor cc;
     cc.init(q0, a);
     const int64_t tile0 = cc.tile;
     bool first_flush = true;   // the running sum of this tile's slot is not written yet
-    uint32_t phase = 0;        // bit s: parity of stage s's next completion (padding blocks skip a stage)
     for (int64_t i = 0; i < nq; ++i) {
-        __syncthreads();   // every warp is done with the stage the producer refills next
-        if (warp == 0 && i + kStages - 1 < nq) load((int)((i + kStages - 1) % kStages));
+        const int slot = (int)(i % kStages);
+        mbar_wait(&full_bar[slot], (uint32_t)((i / kStages) & 1));
         if (cc.kb < a.KB) {
-            const int slot = (int)(i % kStages);
-            mbar_wait(&full_bar[slot], (phase >> slot) & 1u);
-            phase ^= 1u << slot;
-            const double* sA = gs_smem + (size_t)(i % kStages) * C::STAGE + 8 * kMW * warp + g;
-            const double* sB = gs_smem + (size_t)(i % kStages) * C::STAGE + C::A_STAGE + g;
+            const double* sA = gs_smem + (size_t)slot * C::STAGE + 8 * C::MW * warp + g;
+            const double* sB = gs_smem + (size_t)slot * C::STAGE + C::A_STAGE + g;
 #pragma unroll
             for (int k4 = 0; k4 < kBK / 4; ++k4) {
-                double fa[kMW], fb[NT];
+                double fa[C::MW], fb[NT];
 #pragma unroll
-                for (int mi = 0; mi < kMW; ++mi) fa[mi] = sA[(4 * k4 + t) * C::LDA + 8 * mi];
+                for (int mi = 0; mi < C::MW; ++mi) fa[mi] = sA[(4 * k4 + t) * C::LDA + 8 * mi];
 #pragma unroll
                 for (int nj = 0; nj < NT; ++nj) fb[nj] = sB[(4 * k4 + t) * C::LDB + 8 * nj];
 #pragma unroll
                 for (int nj = 0; nj < NT; ++nj)
 #pragma unroll
-                    for (int mi = 0; mi < kMW; ++mi) dmma(acc[mi][nj][0], acc[mi][nj][1], fa[mi], fb[nj]);
+                    for (int mi = 0; mi < C::MW; ++mi) dmma(acc[mi][nj][0], acc[mi][nj][1], fa[mi], fb[nj]);
             }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[slot]);   // the warp's shared reads of this stage are done
         const bool cta_end = i + 1 == nq;
         const bool slab_end = cc.kin + 1 == a.VKB;
         const bool tile_end = slab_end && cc.slab + 1 == a.NS;
@@ -231,10 +248,10 @@ __global__ void __launch_bounds__(kGsWarps * 32, 2) gstage_kernel(GsArgs a) {
             // the CTA's own partial slot (L2-resident; each thread touches only its own elements)
             double* P = a.part + ((int64_t)blockIdx.x * a.maxseg + (cc.tile - tile0)) * (C::BM * C::BN);
 #pragma unroll
-            for (int mi = 0; mi < kMW; ++mi)
+            for (int mi = 0; mi < C::MW; ++mi)
 #pragma unroll
                 for (int nj = 0; nj < NT; ++nj) {
-                    const int m = 8 * kMW * warp + 8 * mi + g, n = 8 * nj + 2 * t;
+                    const int m = 8 * C::MW * warp + 8 * mi + g, n = 8 * nj + 2 * t;
                     double* p0 = P + (int64_t)n * C::BM + m;
                     double* p1 = p0 + C::BM;
                     if (first_flush) {
@@ -289,6 +306,8 @@ csk_status launch(GsArgs& a, void* Z, int64_t ldz, bool z_f32, cudaStream_t st) 
     using C = Cfg<NT>;
     auto kern = gstage_kernel<NT>;
     CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    // two CTAs per SM need the largest shared-memory carveout (ncu r02: the driver's default fit one)
+    CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     a.MT = (a.k2 + C::BM - 1) / C::BM;
     a.NCH = (a.ncols + a.cw - 1) / a.cw;
     a.KB = ceil_div(a.k1, kBK);
@@ -299,7 +318,6 @@ csk_status launch(GsArgs& a, void* Z, int64_t ldz, bool z_f32, cudaStream_t st) 
     const int nsm = device_info().num_sms;
     // two CTAs per SM, each with >= 4 k-blocks (the ring needs work to overlap)
     int64_t P = std::min<int64_t>(2 * nsm, std::max<int64_t>(1, a.total / 4));
-    if (launch_caps().gs_ctas > 0) P = std::min<int64_t>(P, launch_caps().gs_ctas);
     if (const char* e = std::getenv("CSK_GS_CTAS")) P = std::max<int64_t>(1, std::min<int64_t>(std::atoll(e), a.total));
     a.P = (int)P;
     a.maxseg = (int)(ceil_div(ceil_div(a.total, P), a.NS * a.VKB) + 1);   // tiles one CTA can touch
@@ -307,7 +325,7 @@ csk_status launch(GsArgs& a, void* Z, int64_t ldz, bool z_f32, cudaStream_t st) 
     double* part = nullptr;
     CSK_CUDA_TRY(csk_malloc_async(&part, part_bytes, st));
     a.part = part;
-    kern<<<(unsigned)P, kGsWarps * 32, C::SMEM, st>>>(a);
+    kern<<<(unsigned)P, (kGsWarps + 1) * 32, C::SMEM, st>>>(a);
     count_launch();
     cudaError_t e1 = cudaGetLastError();
     const unsigned rgrid = (unsigned)((int64_t)a.MT * a.NCH * (C::BM * C::BN / 32));

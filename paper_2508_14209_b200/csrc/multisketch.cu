@@ -568,82 +568,6 @@ csk_status rows_from_colmajor(const double* SA, int64_t ld, int64_t k1, int ncol
     return CSK_OK;
 }
 
-// NEXT-2 prototype: column chunks of <= 66 columns whose SA^T slice fits half of L2; chunk i's
-// CountSketch on st (CTA cap CSK_OVL_CS, default 104), its G-stage on a second stream after an
-// event (CTA cap CSK_OVL_GS, default 88 = 44 SMs at two CTAs each), overlapping chunk i+1's sketch.
-static cudaStream_t side_stream() {
-    static thread_local std::map<int, cudaStream_t> streams;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    auto it = streams.find(dev);
-    if (it == streams.end()) {
-        cudaStream_t s2 = nullptr;
-        if (cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
-        it = streams.emplace(dev, s2).first;
-    }
-    return it->second;
-}
-
-static csk_status ms_apply_overlap(csk_plan_t plan, int64_t k2, int64_t n, const double* A, int64_t lda,
-                                   const double* b, void* Z, int64_t ldz, cudaStream_t st) {
-    const int64_t k1 = plan->k1;
-    const int ncols = (int)(n + (b ? 1 : 0));
-    const int64_t l2h = (int64_t)device_info().l2_bytes / 2;
-    const int64_t fit = std::max<int64_t>(2, (l2h / (8 * k1)) & ~1);
-    const int nch = (int)std::max<int64_t>(ceil_div(ncols, 66), ceil_div(ncols, fit));
-    const int cw = std::min(66, (((ncols + nch - 1) / nch) + 1) & ~1);
-    const double* G = nullptr;
-    int64_t ldg = 0;
-    csk_status s = gauss_get(plan, k2, st, &G, &ldg);
-    if (s != CSK_OK) return s;
-    cudaStream_t s2 = side_stream();
-    CSK_REQUIRE(s2 != nullptr, CSK_ECUDA, "side stream creation failed");
-    const char* ce = std::getenv("CSK_OVL_CS");
-    const char* ge = std::getenv("CSK_OVL_GS");
-    const int cap_cs = ce ? std::atoi(ce) : 104, cap_gs = ge ? std::atoi(ge) : 88;
-    std::vector<cudaEvent_t> evs;
-    auto cleanup = on_exit([&] {
-        for (auto e : evs) cudaEventDestroy(e);
-        launch_caps() = LaunchCaps{};
-    });
-    cudaEvent_t e0;
-    CSK_CUDA_TRY(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
-    evs.push_back(e0);
-    CSK_CUDA_TRY(cudaEventRecord(e0, st));
-    CSK_CUDA_TRY(cudaStreamWaitEvent(s2, e0, 0));   // s2 starts after everything queued on st
-    for (int c0 = 0; c0 < ncols && s == CSK_OK; c0 += cw) {
-        const int nc = std::min(cw, ncols - c0);
-        const bool has_b = b != nullptr && c0 + nc == ncols;
-        const int64_t na = nc - (has_b ? 1 : 0);
-        RowOut ro;
-        launch_caps() = LaunchCaps{cap_cs, 0};
-        s = cs_apply_impl(plan, CSK_F64, na, na > 0 ? A + (int64_t)c0 * lda : nullptr, lda, has_b ? b : nullptr,
-                          nullptr, k1, CSK_VAR_AUTO, st, 0, plan->d, false, &ro);
-        launch_caps() = LaunchCaps{};
-        if (s != CSK_OK) break;
-        cudaEvent_t ev;
-        CSK_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        evs.push_back(ev);
-        CSK_CUDA_TRY(cudaEventRecord(ev, st));
-        CSK_CUDA_TRY(cudaStreamWaitEvent(s2, ev, 0));
-        if (ro.cw > kGstageMaxCw) {
-            ro.cw = 64;
-            ro.cs = 64;
-        }
-        if (ro.ncols <= ro.cw) ro.cs = 0;
-        launch_caps() = LaunchCaps{0, cap_gs};
-        s = gstage_launch(G, ldg, k2, k1, ro, (double*)Z + (int64_t)c0 * ldz, ldz, false, s2);
-        launch_caps() = LaunchCaps{};
-        cudaFreeAsync(ro.ws, s2);
-    }
-    cudaEvent_t done;
-    CSK_CUDA_TRY(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
-    evs.push_back(done);
-    CSK_CUDA_TRY(cudaEventRecord(done, s2));
-    CSK_CUDA_TRY(cudaStreamWaitEvent(st, done, 0));
-    return s;
-}
-
 csk_status ms_apply_impl(csk_plan_t plan, int64_t k2, csk_dtype dtype, int64_t n, const void* A, int64_t lda,
                          const void* b, void* Z, int64_t ldz, cudaStream_t st) {
     CSK_REQUIRE(plan != nullptr, CSK_EINVAL, "plan is NULL");
@@ -658,15 +582,6 @@ csk_status ms_apply_impl(csk_plan_t plan, int64_t k2, csk_dtype dtype, int64_t n
     CSK_REQUIRE(!host_in || dtype == CSK_F64, CSK_EDTYPE, "host-resident inputs are supported for fp64 only");
     const int64_t k1 = plan->k1;
     csk_status s;
-    // NEXT-2: when SA^T is cut into L2-sized column chunks (C3), the
-    // G-stage of chunk i can run beside the CountSketch of chunk i+1 on a second stream, the SMs split
-    // between them (CSK_MS_OVERLAP=1, measured in DESIGN.md 6.6)
-    if (!host_in && dtype == CSK_F64) {
-        const char* ov = std::getenv("CSK_MS_OVERLAP");
-        const int64_t l2h = (int64_t)device_info().l2_bytes / 2;
-        if (ov && std::atoi(ov) == 1 && k1 * ncols * 8 > l2h && ncols > 2)
-            return ms_apply_overlap(plan, k2, n, (const double*)A, lda, (const double*)b, Z, ldz, st);
-    }
     RowOut ro;
     // a3: the CountSketch hands over its fp64 row-major SA^T workspace ("interpreted Y stored in
     // row-major as the transpose ... computed Z^T = Y^T G^T"), so no k1 x ncols transpose is made on the

@@ -11,7 +11,7 @@ import paper_2508_14209_b200 as csk  # noqa: E402
 import synth  # noqa: E402
 
 SHAPES = {"c2": (1 << 24, 64, 8192, 128), "c4": (1 << 23, 128, 32768, 256), "c3": (1 << 22, 256, 131072, 512),
-          "c5": (1 << 27, 64, 8192, 128), "n32": (1 << 23, 32, 2048, 64), "n128": (1 << 22, 128, 32768, 256)}
+          "c5": (1 << 27, 64, 8192, 128), "n32": (1 << 23, 32, 2048, 64), "n8": (1 << 23, 8, 128, 16), "n16": (1 << 23, 16, 512, 32), "n128": (1 << 22, 128, 32768, 256)}
 name = sys.argv[1]
 f32 = "f32" in sys.argv[2:]
 ms = "ms" in sys.argv[2:]

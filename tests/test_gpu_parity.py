@@ -299,11 +299,8 @@ def test_ms_apply_every_countsketch_variant(monkeypatch, variant, d, n, k1, k2):
     assert_within_T(Z, Zo, Zabs, 1e-12)
 
 
-@pytest.mark.parametrize("overlap", ["0", "1"])
-def test_ms_apply_gstage_large_k2_and_k1(monkeypatch, overlap):
-    # k2 = 512, k1 = 131072 (C3's G-stage shape): 4 M-tiles, stream-K over 5 chunk-major chunks; "1" =
-    # the NEXT-2 schedule (chunk i's G-stage on a second stream beside chunk i+1's CountSketch)
-    monkeypatch.setenv("CSK_MS_OVERLAP", overlap)
+def test_ms_apply_gstage_large_k2_and_k1():
+    # k2 = 512, k1 = 131072 (C3's G-stage shape): 4 M-tiles, stream-K over 5 chunk-major chunks
     d, n, k1, k2 = 300007, 256, 131072, 512
     plan = csk.cs_plan(d, k1, 6)
     A = synth.gaussian_matrix(d, n, seed=2)
