@@ -625,6 +625,7 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk64f_kernel(const uint32_t* _
     extern __shared__ __align__(16) float f32_smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int q = lane >> 2, sq = lane & 3;
+    // one tile buffer per warp (two buffers with 6 warps measured 30% slower: fewer loads in flight)
     float* tile = f32_smem + (size_t)warp * (kF32Rows * ldf + 32);
     for (int e = lane; e < kF32Rows * ldf + 32; e += 32) tile[e] = 0.0f;
     __syncwarp();
@@ -957,13 +958,30 @@ static int smem_cpc(int64_t k1, int ncols) {
 }
 
 // Variant selection (BASELINE north_star: "picked per (d, n, k1) from ncu-measured HBM GB/s").
-// See DESIGN.md 6.1d for the measured table this encodes.
+// profiles/r02_variant_table.json (scripts/variant_table.py: all six variants at d = 2^20 and 2^23,
+// n = 8 ... 256, k1 = 2 n^2, fp64 and fp32) is encoded below as rules on the dtype and
+// the SA^T footprint k1 (n+1) w, the quantity that decides between the row-scatter variants: B wins
+// every fp64 row and every fp32 row whose SA^T exceeds 64 KB; for a tiny fp32 SA^T the fp32 row-block
+// copies of B contend in a few L2 lines and X (<= 8 KB) or T (<= 64 KB) is faster.  d did not change
+// any winner (the one exception, fp64 n = 16 at d = 2^20, is T by 3%, within run-to-run noise).
+struct VariantRule {
+    csk_dtype dtype;
+    int64_t max_sat_bytes;   // k1 * ncols * sizeof(element)
+    int variant;
+};
+static const VariantRule kVariantTable[] = {
+    {CSK_F32, 8 << 10, CSK_VAR_TMA_ROW},      // d=2^23 n=8: X 0.960 ms, T 1.035, B 1.210
+    {CSK_F32, 64 << 10, CSK_VAR_ATOMIC_ROW},  // d=2^23 n=16: T 0.633 ms, B 0.702, X 0.970
+    {CSK_F32, INT64_MAX, CSK_VAR_BULK_ROW},   // n >= 32: B (e.g. n=64 0.695 ms vs T 1.380)
+    {CSK_F64, INT64_MAX, CSK_VAR_BULK_ROW},   // every row (e.g. n=8 0.544 ms vs T 1.042, n=256 4.16 vs 8.75)
+};
+
 static int select_variant(int64_t d, int64_t k1, int ncols, csk_dtype dtype, bool has_sort) {
     (void)d;
-    (void)k1;
-    (void)ncols;
-    (void)dtype;
     (void)has_sort;
+    const int64_t bytes = k1 * ncols * (dtype == CSK_F64 ? 8 : 4);
+    for (const VariantRule& r : kVariantTable)
+        if (r.dtype == dtype && bytes <= r.max_sat_bytes) return r.variant;
     return CSK_VAR_BULK_ROW;
 }
 
@@ -1046,13 +1064,14 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
                 if (L.ncopies > 0) {   // fp32 accumulation into bounded-depth copies (default for fp32)
                     int ldf = (cw + 3) & ~3;
                     while (ldf % 32 != 4) ldf += 4;   // == 4 mod 32: conflict-free tile stores
-                    const size_t smem = (size_t)8 * (kF32Rows * ldf + 32) * sizeof(float);
-                    CSK_CUDA_TRY(cudaFuncSetAttribute(cs_bulk64f_kernel<8>,
-                                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                    constexpr int fw = 8;
+                    auto fk = cs_bulk64f_kernel<fw>;
+                    const size_t smem = (size_t)fw * (kF32Rows * ldf + 32) * sizeof(float);
+                    CSK_CUDA_TRY(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
                     const int64_t units = ceil_div(rows, kF32Rows) * ceil_div(ncols, cw);
-                    const int64_t blocks = std::min<int64_t>(ceil_div(units, 8), (int64_t)di.num_sms);
+                    const int64_t blocks = std::min<int64_t>(ceil_div(units, fw), (int64_t)di.num_sms);
                     prof_mark(st, true);
-                    cs_bulk64f_kernel<8><<<(unsigned)blocks, 256, smem, st>>>(
+                    fk<<<(unsigned)blocks, fw * 32, smem, st>>>(
                         code, rows, *reinterpret_cast<const Cols<float>*>(&cols), ncols, ldf,
                         reinterpret_cast<float*>(out), L);
                     CSK_LAUNCH_CHECK();

@@ -316,8 +316,9 @@ csk_status launch(GsArgs& a, void* Z, int64_t ldz, bool z_f32, cudaStream_t st) 
     a.total = (int64_t)a.MT * a.NCH * a.NS * a.VKB;
     CSK_REQUIRE(a.total < (int64_t(1) << 47), CSK_EUNSUPPORTED, "G-stage: k1 too large");
     const int nsm = device_info().num_sms;
-    // two CTAs per SM, each with >= 4 k-blocks (the ring needs work to overlap)
-    int64_t P = std::min<int64_t>(2 * nsm, std::max<int64_t>(1, a.total / 4));
+    // two CTAs per SM, each with >= 16 k-blocks: the ring needs work to overlap, and every extra CTA
+    // adds a partial tile to the fixed-order reduce (C2: 256 CTAs of 4 k-blocks spent 15 us there)
+    int64_t P = std::min<int64_t>(2 * nsm, std::max<int64_t>(1, a.total / 16));
     if (const char* e = std::getenv("CSK_GS_CTAS")) P = std::max<int64_t>(1, std::min<int64_t>(std::atoll(e), a.total));
     a.P = (int)P;
     a.maxseg = (int)(ceil_div(ceil_div(a.total, P), a.NS * a.VKB) + 1);   // tiles one CTA can touch

@@ -539,12 +539,14 @@ def test_cs_apply_fp32_accumulation(monkeypatch, acc, d, n, with_b, k1, off):
     big[off:] = A
     Ad = gpu_colmajor(big)[off:]
     bd = None if b is None else gpu_colmajor(b)
-    SA = host(csk.cs_apply(plan, Ad, b=bd))
     exp, T = oracle.cs_apply(h, s, A, k1, b=b, with_abs=True)
-    assert_within_T(SA, exp, T, 1e-5)
     Ai = synth.integer_matrix(d, n, seed=6, dtype=np.float32)
-    got = host(csk.cs_apply(plan, gpu_colmajor(Ai)))
-    assert np.array_equal(got.astype(np.float64), oracle.cs_apply(h, s, Ai, k1))
+    # "B" forces the bounded-depth copies even where the measured table picks X/T (tiny fp32 SA^T)
+    for variant in ("auto", "B"):
+        SA = host(csk.cs_apply(plan, Ad, b=bd, variant=variant))
+        assert_within_T(SA, exp, T, 1e-5)
+        got = host(csk.cs_apply(plan, gpu_colmajor(Ai), variant=variant))
+        assert np.array_equal(got.astype(np.float64), oracle.cs_apply(h, s, Ai, k1))
 
 
 # ------------------------------------------------ CSK_PLAN_HASH (codes hashed on the fly)
