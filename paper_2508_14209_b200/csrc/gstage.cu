@@ -8,22 +8,22 @@
 // Design:
 //  * the output is tiny (k2 x (n+1)) and K = k1 is long.  Every output tile's K range is cut into
 //    slabs of kSlabK = 4096 (the accumulation-depth bound below); the (tile, slab) k-blocks are
-//    flattened into one range split evenly over the CTAs (stream-K): CTA c takes
-//    [c total / P, (c+1) total / P), keeps one running partial tile per tile it touches (its slabs
-//    added in order), and the reduce kernel adds the CTAs' partials of each tile in CTA order
-//    (= increasing k; deterministic);
-//  * CTA tile BM = 128 rows x BN = 8 NT columns (a column chunk of Y^T, <= 72); 8 warps, warp w owns
-//    rows [16 w, 16 w + 16) x all BN columns: 2 x NT independent DMMA m8n8k4 accumulators; two CTAs
-//    per SM (16 warps: the DMMA issue latency of one warp is hidden by the others -- with one
-//    8-warp CTA the pipe was 62% busy, ncu r02);
-//  * operands staged by the TMA engine (1-D bulk copies, one per G column / Y^T row, issued by one
-//    producer warp; mbarrier completion) into a 4-deep ring; shared rows are padded to ld == 4
-//    (mod 16) doubles so the A fragment (row g, k t) and B fragment (k t, col g) loads of a half-warp
-//    hit 16 distinct double-banks (conflict-free).  Per-thread cp.async cost as many instructions as
-//    the DMMA loop itself (ncu r02);
+//    flattened into one range cut into P contiguous segments (stream-K, >= 32 k-blocks each, up to 4
+//    per CTA slot) that the persistent CTAs grab from a counter -- a CTA whose SM is busy elsewhere
+//    (the pipelined step's solve) just takes fewer.  A segment keeps one running partial per tile it
+//    touches (its slabs added in order) in its own slot, and the reduce kernel adds the segments'
+//    partials of each tile in segment order (= increasing k; deterministic whatever CTA ran them);
+//  * CTA = 4 DMMA warps + 1 TMA producer warp, two CTAs per SM.  CTA tile BM = 32 MW rows x BN = 8 NT
+//    columns (a column chunk of Y^T, <= 72); DMMA warp w owns 8 MW rows x all BN columns: MW x NT
+//    independent m8n8k4 accumulator chains, MW + NT fragment loads per MW NT DMMAs;
+//  * operands staged by the TMA engine (1-D bulk copies, one per G row slice / Y^T row, issued by the
+//    producer warp) into a 4-deep ring handed over by full (TMA bytes) and empty (one arrive per DMMA
+//    warp) mbarriers -- no CTA barrier per k-block; shared rows are padded to ld == 4 (mod 16) doubles
+//    so the A fragment (row g, k t) and B fragment (k t, col g) loads of a half-warp hit 16 distinct
+//    double-banks (conflict-free);
 //  * error bound: one DMMA chain accumulates at most kSlabK = 4096 products; the
-//    ceil(k1 / 4096) slab sums and the CTA partials are then added in fp64, so the error stays
-//    <= (4096 + k1 / 4096 + #CTAs per tile) u |G| T, inside 1e-12 |G| T for k1 <= 2^27.
+//    ceil(k1 / 4096) slab sums and the segment partials are then added in fp64, so the error stays
+//    <= (4096 + k1 / 4096 + #segments per tile) u |G| T, inside 1e-12 |G| T for k1 <= 2^27.
 #include <algorithm>
 #include <cstdlib>
 
@@ -75,9 +75,10 @@ struct GsArgs {
     int64_t VKB;        // k-blocks per slab
     int64_t NS;         // slabs per tile
     int64_t total;      // MT * NCH * NS * VKB (flattened, last slab of a tile padded)
-    int P;              // CTAs
-    int maxseg;         // partial slots per CTA
+    int P;              // segments (stream-K ranges), grabbed dynamically by the CTAs
+    int maxseg;         // partial slots per segment
     double* part;       // P * maxseg partial tiles (BM x BN, column-major)
+    unsigned long long* work;   // segment counter (zeroed before the launch)
 };
 
 // q0(c) = floor(c * total / P): the first flattened k-block of CTA c
@@ -147,125 +148,136 @@ __global__ void __launch_bounds__((kGsWarps + 1) * 32, 2) gstage_kernel(GsArgs a
     extern __shared__ __align__(16) double gs_smem[];
     __shared__ __align__(8) uint64_t full_bar[kStages];
     __shared__ __align__(8) uint64_t empty_bar[kStages];
+    __shared__ int64_t s_seg[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
-    const int64_t q0 = range_begin(blockIdx.x, a.total, a.P);
-    const int64_t q1 = range_begin(blockIdx.x + 1, a.total, a.P);
-    if (q0 >= q1) return;
-    const int64_t nq = q1 - q0;
     if (tid < kStages) {
         mbar_init(&full_bar[tid], 1);            // the producer's arrive (+ the stage's TMA bytes)
         mbar_init(&empty_bar[tid], kGsWarps);    // one arrive per consumer warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncthreads();   // the only CTA-wide barrier: stages are handed over by mbarriers from here on
 
-    // ---- producer warp (warp kGsWarps): k-block j goes to stage j % S once the consumers released the
-    // stage's previous k-block j - S (empty barrier).  1-D bulk copies (TMA engine), one row per lane:
-    // lanes 0..15 the G rows (BM doubles, 1 KB each), lanes 16..31 the Y^T rows (the chunk's columns
-    // rounded up to 16 B); rows past k1 are zeroed in shared memory instead.  Lane 0 posts the byte
-    // count first and arrives after the warp's copies and zero stores are issued; padding k-blocks of
-    // a short last slab load nothing (the arrive alone completes the phase).  A dedicated warp: with
-    // the producer inside a DMMA warp it ran late behind its own k-blocks (ncu r02: DMMA 77.5%), and
-    // with a CTA barrier per k-block the barrier stall was 26% of the samples (DMMA 82.6%).
-    Cursor lc;
-    lc.init(q0, a);
-    int64_t produced = 0;
-    auto produce = [&]() {
-        const int slot = (int)(produced % kStages);
-        if (produced >= kStages) mbar_wait(&empty_bar[slot], (uint32_t)((produced / kStages - 1) & 1));
-        uint64_t* bar = &full_bar[slot];
-        if (lc.kb < a.KB) {
-            const int64_t k0 = lc.kb * kBK;
-            const int nrows = (int)(a.k1 - k0 < kBK ? a.k1 - k0 : kBK);
-            const int pieces = (min(a.cw, a.ncols - lc.ch * a.cw) + 1) >> 1;
-            const uint32_t bbytes = (uint32_t)pieces * 16;
-            if (lane == 0) mbar_expect_only(bar, (uint32_t)nrows * (C::BM * 8 + bbytes));
-            __syncwarp();
-            double* sA = gs_smem + (size_t)slot * C::STAGE;
-            double* sB = sA + C::A_STAGE;
-            const int kk = lane & 15;
-            if (lane < 16) {
-                if (kk < nrows)
-                    bulk_g2s(sA + kk * C::LDA, a.G + (int64_t)lc.mt * C::BM + (k0 + kk) * a.ldg, C::BM * 8, bar);
-                else
-                    for (int e = 0; e < C::BM; ++e) sA[kk * C::LDA + e] = 0.0;
-            } else {
-                if (kk < nrows)
-                    bulk_g2s(sB + kk * C::LDB, a.Yt + (int64_t)lc.ch * a.cs + (k0 + kk) * a.lc, bbytes, bar);
-                else
-                    for (int e = 0; e < 2 * pieces; ++e) sB[kk * C::LDB + e] = 0.0;
-            }
-            if (nrows < kBK) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-        }
-        if (lane == 0) mbar_arrive(bar);
-        lc.next(a);
-        ++produced;
-    };
-    if (warp == kGsWarps) {
-        while (produced < nq) produce();
-        return;
-    }
+    // Segments: the flattened (tile, slab, k-block) range is cut into a.P contiguous stream-K segments
+    // (~4 per CTA) that the persistent CTAs grab from a counter, so a CTA whose SM is still held by
+    // another kernel (the pipelined step's small solve) just takes fewer segments; each segment owns its
+    // partial slots, so the fixed-order reduce (segment order = increasing k) is independent of which
+    // CTA ran it.  Stage slots and mbarrier phases follow the CTA's running k-block count `base`.
+    int64_t base = 0;
+    for (int round = 0;; ++round) {
+        if (tid == 0) s_seg[round & 1] = (int64_t)atomicAdd(a.work, 1ull);
+        __syncthreads();   // (also orders the barrier inits before first use)
+        const int64_t seg = s_seg[round & 1];
+        if (seg >= a.P) break;
+        const int64_t q0 = range_begin(seg, a.total, a.P);
+        const int64_t nq = range_begin(seg + 1, a.total, a.P) - q0;
+        if (nq <= 0) continue;
 
-    // ---- consumer warps: warp w owns rows [32 w, 32 w + 32) of the tile x all BN columns
-    double acc[C::MW][NT][2];
-#pragma unroll
-    for (int i = 0; i < C::MW; ++i)
-#pragma unroll
-        for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-    Cursor cc;
-    cc.init(q0, a);
-    const int64_t tile0 = cc.tile;
-    bool first_flush = true;   // the running sum of this tile's slot is not written yet
-    for (int64_t i = 0; i < nq; ++i) {
-        const int slot = (int)(i % kStages);
-        mbar_wait(&full_bar[slot], (uint32_t)((i / kStages) & 1));
-        if (cc.kb < a.KB) {
-            const double* sA = gs_smem + (size_t)slot * C::STAGE + 8 * C::MW * warp + g;
-            const double* sB = gs_smem + (size_t)slot * C::STAGE + C::A_STAGE + g;
-#pragma unroll
-            for (int k4 = 0; k4 < kBK / 4; ++k4) {
-                double fa[C::MW], fb[NT];
-#pragma unroll
-                for (int mi = 0; mi < C::MW; ++mi) fa[mi] = sA[(4 * k4 + t) * C::LDA + 8 * mi];
-#pragma unroll
-                for (int nj = 0; nj < NT; ++nj) fb[nj] = sB[(4 * k4 + t) * C::LDB + 8 * nj];
-#pragma unroll
-                for (int nj = 0; nj < NT; ++nj)
-#pragma unroll
-                    for (int mi = 0; mi < C::MW; ++mi) dmma(acc[mi][nj][0], acc[mi][nj][1], fa[mi], fb[nj]);
-            }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty_bar[slot]);   // the warp's shared reads of this stage are done
-        const bool cta_end = i + 1 == nq;
-        const bool slab_end = cc.kin + 1 == a.VKB;
-        const bool tile_end = slab_end && cc.slab + 1 == a.NS;
-        if (cta_end || slab_end) {
-            // fold this slab's DMMA chains (<= 4096 products) into the tile's running sum, which lives in
-            // the CTA's own partial slot (L2-resident; each thread touches only its own elements)
-            double* P = a.part + ((int64_t)blockIdx.x * a.maxseg + (cc.tile - tile0)) * (C::BM * C::BN);
-#pragma unroll
-            for (int mi = 0; mi < C::MW; ++mi)
-#pragma unroll
-                for (int nj = 0; nj < NT; ++nj) {
-                    const int m = 8 * C::MW * warp + 8 * mi + g, n = 8 * nj + 2 * t;
-                    double* p0 = P + (int64_t)n * C::BM + m;
-                    double* p1 = p0 + C::BM;
-                    if (first_flush) {
-                        *p0 = acc[mi][nj][0];
-                        *p1 = acc[mi][nj][1];
+        if (warp == kGsWarps) {
+            // ---- producer warp: k-block j (CTA count base + j) goes to stage (base + j) % S once the
+            // consumers released that stage's previous k-block (empty barrier).  1-D bulk copies (TMA
+            // engine), one row per lane: lanes 0..15 the G rows (BM doubles), lanes 16..31 the Y^T rows
+            // (the chunk's columns rounded up to 16 B); rows past k1 are zeroed in shared memory instead.
+            // Lane 0 posts the byte count first and arrives after the warp's copies and zero stores are
+            // issued; padding k-blocks of a short last slab load nothing (the arrive alone completes the
+            // phase).  A dedicated warp: inside a DMMA warp the producer ran late behind its own k-blocks
+            // (ncu r02: DMMA 77.5%); with a CTA barrier per k-block the barrier stall was 26% (82.6%).
+            Cursor lc;
+            lc.init(q0, a);
+            for (int64_t j = 0; j < nq; ++j) {
+                const int64_t pj = base + j;
+                const int slot = (int)(pj % kStages);
+                if (pj >= kStages) mbar_wait(&empty_bar[slot], (uint32_t)((pj / kStages - 1) & 1));
+                uint64_t* bar = &full_bar[slot];
+                if (lc.kb < a.KB) {
+                    const int64_t k0 = lc.kb * kBK;
+                    const int nrows = (int)(a.k1 - k0 < kBK ? a.k1 - k0 : kBK);
+                    const int pieces = (min(a.cw, a.ncols - lc.ch * a.cw) + 1) >> 1;
+                    const uint32_t bbytes = (uint32_t)pieces * 16;
+                    if (lane == 0) mbar_expect_only(bar, (uint32_t)nrows * (C::BM * 8 + bbytes));
+                    __syncwarp();
+                    double* sA = gs_smem + (size_t)slot * C::STAGE;
+                    double* sB = sA + C::A_STAGE;
+                    const int kk = lane & 15;
+                    if (lane < 16) {
+                        if (kk < nrows)
+                            bulk_g2s(sA + kk * C::LDA, a.G + (int64_t)lc.mt * C::BM + (k0 + kk) * a.ldg, C::BM * 8,
+                                     bar);
+                        else
+                            for (int e = 0; e < C::BM; ++e) sA[kk * C::LDA + e] = 0.0;
                     } else {
-                        *p0 += acc[mi][nj][0];
-                        *p1 += acc[mi][nj][1];
+                        if (kk < nrows)
+                            bulk_g2s(sB + kk * C::LDB, a.Yt + (int64_t)lc.ch * a.cs + (k0 + kk) * a.lc, bbytes, bar);
+                        else
+                            for (int e = 0; e < 2 * pieces; ++e) sB[kk * C::LDB + e] = 0.0;
                     }
-                    acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
+                    if (nrows < kBK) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
                 }
-            first_flush = tile_end;
+                if (lane == 0) mbar_arrive(bar);
+                lc.next(a);
+            }
+        } else {
+            // ---- consumer warps: warp w owns rows [8 MW w, 8 MW (w + 1)) of the tile x all BN columns
+            double acc[C::MW][NT][2];
+#pragma unroll
+            for (int i = 0; i < C::MW; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+            Cursor cc;
+            cc.init(q0, a);
+            const int64_t tile0 = cc.tile;
+            bool first_flush = true;   // the running sum of this tile's slot is not written yet
+            for (int64_t i = 0; i < nq; ++i) {
+                const int64_t pi = base + i;
+                const int slot = (int)(pi % kStages);
+                mbar_wait(&full_bar[slot], (uint32_t)((pi / kStages) & 1));
+                if (cc.kb < a.KB) {
+                    const double* sA = gs_smem + (size_t)slot * C::STAGE + 8 * C::MW * warp + g;
+                    const double* sB = gs_smem + (size_t)slot * C::STAGE + C::A_STAGE + g;
+#pragma unroll
+                    for (int k4 = 0; k4 < kBK / 4; ++k4) {
+                        double fa[C::MW], fb[NT];
+#pragma unroll
+                        for (int mi = 0; mi < C::MW; ++mi) fa[mi] = sA[(4 * k4 + t) * C::LDA + 8 * mi];
+#pragma unroll
+                        for (int nj = 0; nj < NT; ++nj) fb[nj] = sB[(4 * k4 + t) * C::LDB + 8 * nj];
+#pragma unroll
+                        for (int nj = 0; nj < NT; ++nj)
+#pragma unroll
+                            for (int mi = 0; mi < C::MW; ++mi) dmma(acc[mi][nj][0], acc[mi][nj][1], fa[mi], fb[nj]);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty_bar[slot]);   // the warp's shared reads of this stage are done
+                const bool seg_end = i + 1 == nq;
+                const bool slab_end = cc.kin + 1 == a.VKB;
+                const bool tile_end = slab_end && cc.slab + 1 == a.NS;
+                if (seg_end || slab_end) {
+                    // fold this slab's DMMA chains (<= 4096 products) into the tile's running sum in the
+                    // segment's own partial slot (L2-resident; each thread touches only its own elements)
+                    double* P = a.part + (seg * a.maxseg + (cc.tile - tile0)) * (C::BM * C::BN);
+#pragma unroll
+                    for (int mi = 0; mi < C::MW; ++mi)
+#pragma unroll
+                        for (int nj = 0; nj < NT; ++nj) {
+                            const int m = 8 * C::MW * warp + 8 * mi + g, n = 8 * nj + 2 * t;
+                            double* p0 = P + (int64_t)n * C::BM + m;
+                            double* p1 = p0 + C::BM;
+                            if (first_flush) {
+                                *p0 = acc[mi][nj][0];
+                                *p1 = acc[mi][nj][1];
+                            } else {
+                                *p0 += acc[mi][nj][0];
+                                *p1 += acc[mi][nj][1];
+                            }
+                            acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
+                        }
+                    first_flush = tile_end;
+                }
+                cc.next(a);
+            }
         }
-        cc.next(a);
+        base += nq;
     }
 }
 
@@ -316,17 +328,28 @@ csk_status launch(GsArgs& a, void* Z, int64_t ldz, bool z_f32, cudaStream_t st) 
     a.total = (int64_t)a.MT * a.NCH * a.NS * a.VKB;
     CSK_REQUIRE(a.total < (int64_t(1) << 47), CSK_EUNSUPPORTED, "G-stage: k1 too large");
     const int nsm = device_info().num_sms;
-    // two CTAs per SM, each with >= 16 k-blocks: the ring needs work to overlap, and every extra CTA
-    // adds a partial tile to the fixed-order reduce (C2: 256 CTAs of 4 k-blocks spent 15 us there)
-    int64_t P = std::min<int64_t>(2 * nsm, std::max<int64_t>(1, a.total / 16));
+    // two CTAs per SM (fewer when there are < 8 k-blocks per CTA); P = 4, 2 or 1 segments per CTA, the
+    // most that leaves >= 24 k-blocks per segment (each segment adds a pipeline fill and a partial tile
+    // per tile it touches to the fixed-order reduce: C2 with 32-k-block segments on 32 CTAs took 48 us,
+    // with 8-k-block segments on 128 CTAs 12 us; C3 takes 4 x 296)
+    int64_t grid = std::min<int64_t>(2 * nsm, std::max<int64_t>(1, a.total / 8));
+    int64_t P = grid;
+    for (int k = 4; k >= 2; k /= 2)
+        if (a.total / (k * grid) >= 24) {
+            P = k * grid;
+            break;
+        }
     if (const char* e = std::getenv("CSK_GS_CTAS")) P = std::max<int64_t>(1, std::min<int64_t>(std::atoll(e), a.total));
     a.P = (int)P;
-    a.maxseg = (int)(ceil_div(ceil_div(a.total, P), a.NS * a.VKB) + 1);   // tiles one CTA can touch
+    grid = std::min<int64_t>(grid, P);
+    a.maxseg = (int)(ceil_div(ceil_div(a.total, P), a.NS * a.VKB) + 1);   // tiles one segment can touch
     const size_t part_bytes = (size_t)P * a.maxseg * C::BM * C::BN * sizeof(double);
     double* part = nullptr;
-    CSK_CUDA_TRY(csk_malloc_async(&part, part_bytes, st));
+    CSK_CUDA_TRY(csk_malloc_async(&part, part_bytes + 16, st));
     a.part = part;
-    kern<<<(unsigned)P, (kGsWarps + 1) * 32, C::SMEM, st>>>(a);
+    a.work = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(part) + part_bytes);
+    CSK_CUDA_TRY(cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), st));
+    kern<<<(unsigned)grid, (kGsWarps + 1) * 32, C::SMEM, st>>>(a);
     count_launch();
     cudaError_t e1 = cudaGetLastError();
     const unsigned rgrid = (unsigned)((int64_t)a.MT * a.NCH * (C::BM * C::BN / 32));

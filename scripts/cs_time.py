@@ -7,6 +7,8 @@ import sys
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if os.environ.get("CSK_PKG_ROOT"):   # A/B: another build of the package (e.g. scratch_ab/old), same inputs
+    sys.path.insert(0, os.environ["CSK_PKG_ROOT"])
 import paper_2508_14209_b200 as csk  # noqa: E402
 import synth  # noqa: E402
 
