@@ -295,11 +295,22 @@ __global__ void __launch_bounds__(256) gstage_reduce_kernel(GsArgs a, int BM, in
     const int r = (int)((blockIdx.x - tile * blocks_per_tile) * 32 + lane);
     const int64_t tq = a.NS * a.VKB;   // flattened k-blocks per tile
     const int c_lo = cta_of(tile * tq, a.total, a.P), c_hi = cta_of((tile + 1) * tq - 1, a.total, a.P);
-    double z = 0.0;
-    for (int cc = c_lo + warp; cc <= c_hi; cc += 8) {
+    auto part_of = [&](int cc) {
         const int64_t slot = (int64_t)cc * a.maxseg + (tile - range_begin(cc, a.total, a.P) / tq);
-        z += a.part[slot * per_tile + r];
+        return a.part[slot * per_tile + r];
+    };
+    // segments c_lo + warp, + 8, + 16, ... added in that order; four loads issued before their adds
+    // (a dependent load per add made the reduce latency-bound: 49 us at C3, ncu r02)
+    double z = 0.0;
+    int cc = c_lo + warp;
+    for (; cc + 24 <= c_hi; cc += 32) {
+        const double v0 = part_of(cc), v1 = part_of(cc + 8), v2 = part_of(cc + 16), v3 = part_of(cc + 24);
+        z += v0;
+        z += v1;
+        z += v2;
+        z += v3;
     }
+    for (; cc <= c_hi; cc += 8) z += part_of(cc);
     red[warp][lane] = z;
     __syncthreads();
     if (warp == 0) {

@@ -52,22 +52,17 @@ __global__ void __launch_bounds__(1024, 1) rc_finish_kernel(const double* __rest
 }
 
 // ---------------------------------------------------------------- fused pass (lines 3-4)
-// One persistent CTA per SM walks 64-row tiles of A.  fp64 tensor cores (DMMA 8x8x4, the native
-// fp64 MMA of sm_100a: every f64 mma.sync shape lowers to it) do both halves:
-//  * TRSM (line 3): warp w owns rows 8w..8w+7 of the tile and solves them alone (rows are
-//    independent): for each 8-column block J, T = A[:, J] - Q[:, <J] R0[<J, J] (2J DMMAs with
-//    the warp's own Q rows as the A operand, R0 from shared memory as B), then the 8x8 diagonal
-//    block by substitution inside each 4-lane row group (shuffles, true division as in Alg 5);
-//    Q rows go to shared memory.  No CTA barrier inside the solve.
-//  * Gram (line 4): after one barrier the 8 warps accumulate Q^T Q over the tile into the upper
-//    8x8 blocks of C (block (I,J), I <= J, dealt round-robin to warps; accumulators stay in
-//    registers for the whole kernel) and z = Q^T b with plain FMAs.
+// One persistent CTA per SM walks 64-row tiles of A; fp64 tensor cores (DMMA 8x8x4, the native fp64
+// MMA of sm_100a: every f64 mma.sync shape lowers to it) do both halves, and Q0 never reaches HBM:
+//  * TRSM (line 3, R24): rows are independent, so a TRSM warp solves its own rows with no CTA
+//    barrier: for each 8-column block J, T = A[:, J] - Q[:, <J] R0[<J, J] (DMMAs with the warp's Q
+//    rows as the A operand and packed R0 from shared memory as B), then Q[:, J] = T W_J with W_J the
+//    8x8 inverse of the diagonal block (two DMMAs);
+//  * Gram (line 4): Gram warps accumulate Q^T Q of the previous tile into the upper 8x8 blocks
+//    (accumulators in registers for the whole kernel) and z = Q^T b with plain FMAs.
 // Each CTA writes its partial [C | z] once; rc_reduce_kernel sums the partials in a fixed order.
 // Shared memory: packed upper R0 (8-column blocks), Q as [row][col] with ld = NP + 4 (== 4 mod 16
-// doubles: the fragment loads of a half-warp touch 16 distinct bank pairs), the A tile staged by
-// cp.async (the next tile's copy overlaps this tile's Gram) and b.
-constexpr int kRcRows = 64;     // rows per tile (8 per warp)
-constexpr int kRcWarps = 8;
+// doubles: the fragment loads of a half-warp touch 16 distinct bank pairs).
 
 __device__ __forceinline__ double ldcs_pred_rc(const double* p, bool pred) {
     double v = 0.0;
@@ -81,168 +76,16 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
                  : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ void rc_cp_async(double* dst, const double* src, int bytes, int src_bytes) {
-    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
-    if (bytes == 16)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
-    else
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
-}
-
 // Packed upper R0: 8-column block J holds rows 0 .. 8J+7 of its columns with ld 8J + 12
 // (== 4 or 12 mod 16: conflict-free fragment loads), at offset 32 J (J-1) + 96 J.
 __host__ __device__ constexpr int rc_r0_off(int J) { return 32 * J * (J - 1) + 96 * J; }
 
-template <int NB>   // NP = 8 * NB padded columns (n <= NP)
-__global__ void __launch_bounds__(kRcWarps * 32, 1) rc_pass_kernel(const double* __restrict__ A, int64_t lda,
-                                                                   const double* __restrict__ b, int64_t d, int n,
-                                                                   const double* __restrict__ R0g, int ldr0g,
-                                                                   double* __restrict__ part, int nc, int al16) {
-    constexpr int NP = 8 * NB, LD = NP + 4, LDA = kRcRows + 4;
-    constexpr int NPAIR = NB / 2, KS = kRcWarps / NPAIR, GK = kRcRows / KS;   // k split of the Gram
-    extern __shared__ __align__(16) double rsm[];
-    double* R0p = rsm;                           // packed upper R0 (rc_r0_off(NB) doubles)
-    double* Qs = R0p + rc_r0_off(NB);            // [kRcRows][LD]   Q rows of the tile
-    double* As = Qs + kRcRows * LD;              // [NP][LDA]       A tile, column-major (cp.async-staged)
-    double* bs = As + NP * LDA;                  // [2][kRcRows]    b tiles (double-buffered)
-    double* invd = bs + 2 * kRcRows;             // [NP]            1 / R0[j][j]
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int g = lane >> 2, t = lane & 3;   // fragment row group / thread in group
-    for (int J = 0; J < NB; ++J)
-        for (int e = threadIdx.x; e < 8 * (8 * J + 8); e += blockDim.x) {
-            const int k = e % (8 * J + 8), j = 8 * J + e / (8 * J + 8);
-            const double v = (k < n && j < n) ? R0g[k + (int64_t)j * ldr0g] : (k == j ? 1.0 : 0.0);
-            R0p[rc_r0_off(J) + (j - 8 * J) * (8 * J + 12) + k] = (k <= j) ? v : 0.0;
-            if (k == j) invd[j] = 1.0 / v;
-        }
-    const int J1 = warp % NPAIR, J2 = NB - 1 - J1, gk0 = (warp / NPAIR) * GK;
-    double acc[NB + 1][2];
-#pragma unroll
-    for (int p = 0; p <= NB; ++p) acc[p][0] = acc[p][1] = 0.0;
-    double zacc = 0.0;   // thread i < NP: z[i]
-    const int64_t ntiles = (d + kRcRows - 1) / kRcRows;
-    // stage a tile's A (n columns x 64 rows) and b into shared memory; rows >= d are zero-filled
-    auto stage = [&](int64_t tile, double* bdst) {
-        const int64_t r0 = tile * kRcRows;
-        if (al16) {
-            for (int e = threadIdx.x; e < (n + 1) * (kRcRows / 2); e += blockDim.x) {
-                const int c = e / (kRcRows / 2), r = 2 * (e % (kRcRows / 2));
-                const int64_t row = r0 + r;
-                const int src = row + 1 < d ? 16 : (row < d ? 8 : 0);
-                const double* gp = c < n ? A + (int64_t)c * lda : b;
-                rc_cp_async(c < n ? As + c * LDA + r : bdst + r, gp + (src ? row : 0), 16, src);
-            }
-        } else {
-            for (int e = threadIdx.x; e < (n + 1) * kRcRows; e += blockDim.x) {
-                const int c = e / kRcRows, r = e % kRcRows;
-                const int64_t row = r0 + r;
-                const double* gp = c < n ? A + (int64_t)c * lda : b;
-                rc_cp_async(c < n ? As + c * LDA + r : bdst + r, gp + (row < d ? row : 0), 8, row < d ? 8 : 0);
-            }
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    int buf = 0;
-    if (blockIdx.x < ntiles) stage(blockIdx.x, bs);
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    __syncthreads();
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        // ---- TRSM: rows 8*warp .. +8, column blocks J = 0 .. NB-1 (warp-local)
-        const double* arow = As + 8 * warp + g;
-        double* qrow = Qs + (8 * warp + g) * LD;
-#pragma unroll 1
-        for (int J = 0; J < NB; ++J) {
-            const int c0 = 8 * J + 2 * t;
-            double t0 = c0 < n ? arow[c0 * LDA] : 0.0;
-            double t1 = c0 + 1 < n ? arow[(c0 + 1) * LDA] : 0.0;
-            // four interleaved accumulation chains over k = 0 .. 8J (DMMA latency, not issue, binds)
-            double u0 = 0.0, u1 = 0.0, v0 = 0.0, v1 = 0.0, w0 = 0.0, w1 = 0.0, y0 = 0.0, y1 = 0.0;
-            const double* qa = Qs + (8 * warp + g) * LD + t;                  // A operand: Q[8w + g][k + t]
-            const double* rb = R0p + rc_r0_off(J) + g * (8 * J + 12) + t;     // B operand: R0[k + t][8J + g]
-            int k = 0;
-            for (; k + 16 <= 8 * J; k += 16) {
-                dmma884(u0, u1, qa[k], rb[k]);
-                dmma884(v0, v1, qa[k + 4], rb[k + 4]);
-                dmma884(w0, w1, qa[k + 8], rb[k + 8]);
-                dmma884(y0, y1, qa[k + 12], rb[k + 12]);
-            }
-            if (k < 8 * J) {
-                dmma884(u0, u1, qa[k], rb[k]);
-                dmma884(v0, v1, qa[k + 4], rb[k + 4]);
-            }
-            t0 -= (u0 + v0) + (w0 + y0);
-            t1 -= (u1 + v1) + (w1 + y1);
-            // 8x8 diagonal block: lanes 0..7 each solve one row in registers (a shuffle chain
-            // across the 4-lane row group cost ~1400 cycles per block; this ~200)
-            *reinterpret_cast<double2*>(qrow + 8 * J + 2 * t) = make_double2(t0, t1);
-            __syncwarp();
-            if (lane < 8) {
-                double* q = Qs + (8 * warp + lane) * LD + 8 * J;
-                const double* rd = R0p + rc_r0_off(J) + 8 * J;      // rd[c' * ldJ + c] = R0[8J+c][8J+c']
-                double v[8];
-#pragma unroll
-                for (int c = 0; c < 8; ++c) v[c] = q[c];
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    v[c] *= invd[8 * J + c];                       // q_c = t_c / R_cc (R19: times 1/R_cc)
-#pragma unroll
-                    for (int c2 = c + 1; c2 < 8; ++c2) v[c2] -= v[c] * rd[c2 * (8 * J + 12) + c];
-                }
-#pragma unroll
-                for (int c = 0; c < 8; c += 2) *reinterpret_cast<double2*>(q + c) = make_double2(v[c], v[c + 1]);
-            }
-            __syncwarp();
-        }
-        __syncthreads();
-        // z = Q^T b for this tile, then the next tile's A and b go out while the Gram runs
-        if (threadIdx.x < NP) {
-            const double* bt = bs + buf * kRcRows;
-            double s = 0.0;
-            for (int r = 0; r < kRcRows; ++r) s += Qs[r * LD + threadIdx.x] * bt[r];
-            zacc += s;
-        }
-        if (tile + gridDim.x < ntiles) stage(tile + gridDim.x, bs + (buf ^ 1) * kRcRows);
-        // ---- Gram: C[8I.., 8J..] += Q[:, I-block]^T Q[:, J-block] over this warp's k rows.
-        // Warp = (column pair, k split): block columns J1 = pair and J2 = NB-1-pair together hold
-        // NB+1 upper blocks (slot s <= J1: (s, J1); else (s-J1-1, J2)), so every warp carries
-        // NB+1 independent accumulation chains and the work is balanced.
-        {
-            const double* qk = Qs + (gk0 + t) * LD + g;
-#pragma unroll 2
-            for (int k = 0; k < GK; k += 4, qk += 4 * LD) {
-                const double b1 = qk[8 * J1], b2 = qk[8 * J2];
-#pragma unroll
-                for (int s2 = 0; s2 <= NB; ++s2) {
-                    const bool first = s2 <= J1;
-                    const int I = first ? s2 : s2 - J1 - 1;
-                    dmma884(acc[s2][0], acc[s2][1], qk[8 * I], first ? b1 : b2);
-                }
-            }
-        }
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-        __syncthreads();   // Qs, As and bs[buf] are rewritten by the next tile
-        buf ^= 1;
-    }
-    // ---- this CTA's partial [C | z] (nc x nc column-major, upper blocks + column n)
-    double* P = part + (size_t)blockIdx.x * nc * nc;   // zeroed by the host; KS warps add into each block
-#pragma unroll
-    for (int s2 = 0; s2 <= NB; ++s2) {
-        const bool first = s2 <= J1;
-        const int I = first ? s2 : s2 - J1 - 1, J = first ? J1 : J2;
-        const int i = 8 * I + g, j0 = 8 * J + 2 * t;
-        if (i < n && j0 < n) atomicAdd(P + i + (int64_t)j0 * nc, acc[s2][0]);
-        if (i < n && j0 + 1 < n) atomicAdd(P + i + (int64_t)(j0 + 1) * nc, acc[s2][1]);
-    }
-    if (threadIdx.x < n) P[threadIdx.x + (int64_t)(nc - 1) * nc] = zacc;
-}
-
 // ------------------------------------------------------------ warp-specialised pipeline
-// The same two halves, overlapped: warps 0-3 are TRSM warps (8 rows each, 32-row tiles), warps
-// 4-7 are Gram warps.  Q tiles are double-buffered in shared memory and handed over with named
-// barriers (FULL[q]: TRSM -> Gram, EMPTY[q]: Gram -> TRSM), so the latency-bound TRSM chain of
-// tile i+1 runs under the DMMA-bound Gram of tile i.  The A tiles (+ b) are double-buffered too
-// and fetched by the TRSM warps with cp.async two tiles ahead.
-constexpr int kWsRows = 32;       // rows per tile (8 per TRSM warp)
+// The two halves overlap: TRSM warps and Gram warps, Q tiles double-buffered in shared memory and
+// handed over with named barriers (FULL[q]: TRSM -> Gram, EMPTY[q]: Gram -> TRSM), so the
+// latency-bound TRSM chain of tile i+1 runs under the DMMA-bound Gram of tile i.  (Round 1 also
+// kept the unpipelined kernel and a 32-row, one-group-per-warp version of this pipeline; both were
+// slower than v3 -- 17.65 / 14.15 ms vs 10.38 ms at C4, DESIGN.md 6.4 -- and were removed in round 2.)
 constexpr int kWsSolve = 4, kWsGram = 4;
 
 __device__ __forceinline__ void nbar_sync(int id, int count) {
@@ -252,209 +95,8 @@ __device__ __forceinline__ void nbar_arrive(int id, int count) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
-template <int NB, bool DIAGINV>
-__global__ void __launch_bounds__((kWsSolve + kWsGram) * 32, 1)
-    rc_pass_ws_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ b, int64_t d, int n,
-                      const double* __restrict__ R0g, int ldr0g, double* __restrict__ part, int nc, int al16) {
-    constexpr int NP = 8 * NB, LD = NP + 4, LDA = kWsRows + 4;
-    constexpr int NPAIR = NB / 2;
-    constexpr int PPW = NPAIR >= kWsGram ? NPAIR / kWsGram : 1;          // column pairs per Gram warp
-    constexpr int KS = NPAIR >= kWsGram ? 1 : kWsGram / NPAIR;           // k split when pairs < warps
-    constexpr int GK = kWsRows / KS;
-    constexpr int NSLOT = PPW * (NB + 1);
-    constexpr int TS = kWsSolve * 32;                                    // TRSM threads
-    extern __shared__ __align__(16) double rsm[];
-    double* R0p = rsm;                                   // packed upper R0
-    double* Qs = R0p + rc_r0_off(NB);                    // [2][kWsRows][LD]
-    double* As = Qs + 2 * kWsRows * LD;                  // [2][NP][LDA]
-    double* bst = As + 2 * NP * LDA;                     // [2][kWsRows]   b staged with A
-    double* bs = bst + 2 * kWsRows;                      // [2][kWsRows]   b of the Q tile
-    double* invd = bs + 2 * kWsRows;                     // [NP]
-    double* Wd = invd + NP;                              // [NB][8 cols][12]: inverses of the 8x8 diagonal blocks
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int g = lane >> 2, t = lane & 3;
-    for (int J = 0; J < NB; ++J)
-        for (int e = threadIdx.x; e < 8 * (8 * J + 8); e += blockDim.x) {
-            const int k = e % (8 * J + 8), j = 8 * J + e / (8 * J + 8);
-            const double v = (k < n && j < n) ? R0g[k + (int64_t)j * ldr0g] : (k == j ? 1.0 : 0.0);
-            R0p[rc_r0_off(J) + (j - 8 * J) * (8 * J + 12) + k] = (k <= j) ? v : 0.0;
-            if (k == j) invd[j] = 1.0 / v;
-        }
-    __syncthreads();
-    // W_J = R_JJ^-1 by back substitution, one thread per (block, column): W[:, c] solves R_JJ w = e_c
-    for (int e = threadIdx.x; e < NB * 8; e += blockDim.x) {
-        const int J = e >> 3, c = e & 7;
-        const double* rd = R0p + rc_r0_off(J) + 8 * J;      // rd[c' * ldJ + r] = R_JJ[r][c']
-        const int ldJ = 8 * J + 12;
-        double w[8];
-#pragma unroll
-        for (int r = 7; r >= 0; --r) {
-            double acc = (r == c) ? 1.0 : 0.0;
-#pragma unroll
-            for (int l = r + 1; l < 8; ++l) acc -= rd[l * ldJ + r] * w[l];
-            w[r] = acc * invd[8 * J + r];
-        }
-#pragma unroll
-        for (int r = 0; r < 8; ++r) Wd[J * 96 + c * 12 + r] = w[r];
-    }
-    __syncthreads();
-    const int64_t ntiles = (d + kWsRows - 1) / kWsRows;
-    const int64_t my = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;   // tiles of this CTA
-    if (warp < kWsSolve) {
-        // ================================================================ TRSM warps
-        const int tid = threadIdx.x;
-        auto stage = [&](int64_t i) {   // tile i of this CTA -> As[i & 1], bst[i & 1]; one commit group always
-            if (i < my) {
-                const int64_t r0 = (blockIdx.x + i * gridDim.x) * kWsRows;
-                double* as = As + (i & 1) * NP * LDA;
-                double* bd = bst + (i & 1) * kWsRows;
-                if (al16) {
-                    for (int e = tid; e < (n + 1) * (kWsRows / 2); e += TS) {
-                        const int c = e / (kWsRows / 2), r = 2 * (e % (kWsRows / 2));
-                        const int64_t row = r0 + r;
-                        const int src = row + 1 < d ? 16 : (row < d ? 8 : 0);
-                        const double* gp = c < n ? A + (int64_t)c * lda : b;
-                        rc_cp_async(c < n ? as + c * LDA + r : bd + r, gp + (src ? row : 0), 16, src);
-                    }
-                } else {
-                    for (int e = tid; e < (n + 1) * kWsRows; e += TS) {
-                        const int c = e / kWsRows, r = e % kWsRows;
-                        const int64_t row = r0 + r;
-                        const double* gp = c < n ? A + (int64_t)c * lda : b;
-                        rc_cp_async(c < n ? as + c * LDA + r : bd + r, gp + (row < d ? row : 0), 8, row < d ? 8 : 0);
-                    }
-                }
-            }
-            asm volatile("cp.async.commit_group;" ::: "memory");
-        };
-        stage(0);
-        stage(1);
-        for (int64_t i = 0; i < my; ++i) {
-            const int q = (int)(i & 1);
-            asm volatile("cp.async.wait_group 1;" ::: "memory");
-            nbar_sync(5, TS);                                  // tile i's A is in As[q]
-            if (i >= 2) nbar_sync(3 + q, 256);                 // EMPTY[q]: the Gram is done with Qs[q]
-            const double* as = As + q * NP * LDA;
-            double* qs = Qs + q * kWsRows * LD;
-            const double* arow = as + 8 * warp + g;
-            double* qrow = qs + (8 * warp + g) * LD;
-#pragma unroll 1
-            for (int J = 0; J < NB; ++J) {
-                const int c0 = 8 * J + 2 * t;
-                double t0 = c0 < n ? arow[c0 * LDA] : 0.0;
-                double t1 = c0 + 1 < n ? arow[(c0 + 1) * LDA] : 0.0;
-                double u0 = 0.0, u1 = 0.0, v0 = 0.0, v1 = 0.0, w0 = 0.0, w1 = 0.0, y0 = 0.0, y1 = 0.0;
-                const double* qa = qs + (8 * warp + g) * LD + t;
-                const double* rb = R0p + rc_r0_off(J) + g * (8 * J + 12) + t;
-                int k = 0;
-                for (; k + 16 <= 8 * J; k += 16) {
-                    dmma884(u0, u1, qa[k], rb[k]);
-                    dmma884(v0, v1, qa[k + 4], rb[k + 4]);
-                    dmma884(w0, w1, qa[k + 8], rb[k + 8]);
-                    dmma884(y0, y1, qa[k + 12], rb[k + 12]);
-                }
-                if (k < 8 * J) {
-                    dmma884(u0, u1, qa[k], rb[k]);
-                    dmma884(v0, v1, qa[k + 4], rb[k + 4]);
-                }
-                t0 -= (u0 + v0) + (w0 + y0);
-                t1 -= (u1 + v1) + (w1 + y1);
-                if (DIAGINV) {
-                    // Q[:, J] = T W_J with W_J = R_JJ^-1 (two DMMAs; A operand T[g][t], T[g][t+4] by shuffles)
-                    const int src0 = (lane & ~3) | (t >> 1), src1 = (lane & ~3) | (2 + (t >> 1));
-                    const double a00 = __shfl_sync(0xffffffffu, t0, src0), a01 = __shfl_sync(0xffffffffu, t1, src0);
-                    const double a10 = __shfl_sync(0xffffffffu, t0, src1), a11 = __shfl_sync(0xffffffffu, t1, src1);
-                    const double* wb = Wd + J * 96 + g * 12 + t;       // B operand: W[k + t][g]
-                    double q0 = 0.0, q1 = 0.0;
-                    dmma884(q0, q1, (t & 1) ? a01 : a00, wb[0]);
-                    dmma884(q0, q1, (t & 1) ? a11 : a10, wb[4]);
-                    *reinterpret_cast<double2*>(qrow + 8 * J + 2 * t) = make_double2(q0, q1);
-                    __syncwarp();
-                } else {
-                *reinterpret_cast<double2*>(qrow + 8 * J + 2 * t) = make_double2(t0, t1);
-                __syncwarp();
-                if (lane < 8) {
-                    double* qq = qs + (8 * warp + lane) * LD + 8 * J;
-                    const double* rd = R0p + rc_r0_off(J) + 8 * J;
-                    double v[8];
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) v[c] = qq[c];
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        v[c] *= invd[8 * J + c];
-#pragma unroll
-                        for (int c2 = c + 1; c2 < 8; ++c2) v[c2] -= v[c] * rd[c2 * (8 * J + 12) + c];
-                    }
-#pragma unroll
-                    for (int c = 0; c < 8; c += 2) *reinterpret_cast<double2*>(qq + c) = make_double2(v[c], v[c + 1]);
-                }
-                __syncwarp();
-                }
-            }
-            if (lane < 8) bs[q * kWsRows + 8 * warp + lane] = bst[q * kWsRows + 8 * warp + lane];
-            __threadfence_block();
-            nbar_arrive(1 + q, 256);                           // FULL[q]
-            nbar_sync(5, TS);                                  // every TRSM warp is done with As[q]
-            stage(i + 2);
-        }
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-        for (int64_t i = (my >= 2 ? my - 2 : 0); i < my; ++i) nbar_sync(3 + (int)(i & 1), 256);   // drain EMPTY
-    } else {
-        // ================================================================ Gram warps
-        const int gw = warp - kWsSolve;
-        const int pair0 = (gw % (kWsGram / KS)) * PPW, gk0 = (gw / (kWsGram / KS)) * GK;
-        double acc[NSLOT][2];
-#pragma unroll
-        for (int p = 0; p < NSLOT; ++p) acc[p][0] = acc[p][1] = 0.0;
-        double zacc0 = 0.0;   // z[gtid] for gtid = threadIdx.x - TS < NP
-        const int gtid = threadIdx.x - TS;
-        for (int64_t i = 0; i < my; ++i) {
-            const int q = (int)(i & 1);
-            nbar_sync(1 + q, 256);                             // FULL[q]
-            const double* qs = Qs + q * kWsRows * LD;
-            const double* qk = qs + (gk0 + t) * LD + g;
-#pragma unroll 2
-            for (int k = 0; k < GK; k += 4, qk += 4 * LD) {
-#pragma unroll
-                for (int pp = 0; pp < PPW; ++pp) {
-                    const int J1 = pair0 + pp, J2 = NB - 1 - J1;
-                    const double b1 = qk[8 * J1], b2 = qk[8 * J2];
-#pragma unroll
-                    for (int s2 = 0; s2 <= NB; ++s2) {
-                        const bool first = s2 <= J1;
-                        const int I = first ? s2 : s2 - J1 - 1;
-                        dmma884(acc[pp * (NB + 1) + s2][0], acc[pp * (NB + 1) + s2][1], qk[8 * I], first ? b1 : b2);
-                    }
-                }
-            }
-            if (gtid < NP) {
-                const double* bt = bs + q * kWsRows;
-                double sz = 0.0;
-#pragma unroll 4
-                for (int r = 0; r < kWsRows; ++r) sz += qs[r * LD + gtid] * bt[r];
-                zacc0 += sz;
-            }
-            nbar_arrive(3 + q, 256);                           // EMPTY[q]
-        }
-        double* P = part + (size_t)blockIdx.x * nc * nc;
-#pragma unroll
-        for (int pp = 0; pp < PPW; ++pp) {
-            const int J1 = pair0 + pp, J2 = NB - 1 - J1;
-#pragma unroll
-            for (int s2 = 0; s2 <= NB; ++s2) {
-                const bool first = s2 <= J1;
-                const int I = first ? s2 : s2 - J1 - 1, J = first ? J1 : J2;
-                const int ii = 8 * I + g, j0 = 8 * J + 2 * t;
-                if (ii < n && j0 < n) atomicAdd(P + ii + (int64_t)j0 * nc, acc[pp * (NB + 1) + s2][0]);
-                if (ii < n && j0 + 1 < n) atomicAdd(P + ii + (int64_t)(j0 + 1) * nc, acc[pp * (NB + 1) + s2][1]);
-            }
-        }
-        if (gtid < n) atomicAdd(P + gtid + (int64_t)(nc - 1) * nc, zacc0);
-    }
-}
-
 // ----------------------------------------------------- v3: two row groups per TRSM warp
-// As rc_pass_ws_kernel, but each TRSM warp solves 16 rows of a 64-row tile as two independent
+// Each TRSM warp solves 16 rows of a 64-row tile as two independent
 // 8-row groups (twice the DMMA chains per warp: the TRSM was the limiter), the R0 B-fragment is
 // shared by both groups, and A is not staged in shared memory: every lane keeps a ring of P
 // prefetched column blocks in registers (the TRSM warps have the Gram warps' register budget).
@@ -785,42 +427,18 @@ static csk_status rc_gram_impl(int64_t d, int64_t n, const double* A, int64_t ld
     if (fused) {
         const int nb = n <= 16 ? 2 : n <= 32 ? 4 : n <= 64 ? 8 : 16;
         const int NP = 8 * nb, LD = NP + 4;
-        const size_t smem =
-            ((size_t)rc_r0_off(nb) + (size_t)kRcRows * LD + (size_t)NP * (kRcRows + 4) + 2 * kRcRows + NP) * 8;
-        const int al16 = ((uintptr_t)A & 15) == 0 && ((uintptr_t)b & 15) == 0 && (lda & 1) == 0;
         const DeviceInfo& di = device_info();
-        const int64_t tiles = ceil_div(d, kRcRows);
+        const int64_t tiles = ceil_div(d, kV3Rows);
         const int grid = (int)std::min<int64_t>(tiles, di.num_sms);
         double* part = nullptr;
         CSK_CUDA_TRY(csk_malloc_async(&part, (size_t)grid * nc * nc * 8, st));
         CSK_CUDA_TRY(cudaMemsetAsync(part, 0, (size_t)grid * nc * nc * 8, st));
-        const char* ke = std::getenv("CSK_RC_KERNEL");   // 1 = unpipelined, 2 = 32-row pipeline (alternatives)
-        const int kv = ke ? std::atoi(ke) : 0;
-        if (kv == 0) {
-            const size_t smem_v3 = ((size_t)rc_r0_off(nb) + 2 * (size_t)kV3Rows * LD + 2 * kV3Rows + NP +
-                                    (size_t)nb * 96) * 8;
-            auto kern = nb == 2 ? rc_pass_v3_kernel<2> : nb == 4 ? rc_pass_v3_kernel<4>
-                      : nb == 8 ? rc_pass_v3_kernel<8> : rc_pass_v3_kernel<16>;
-            CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_v3));
-            kern<<<grid, (kWsSolve + kWsGram) * 32, smem_v3, st>>>(A, lda, b, d, (int)n, R0, (int)ldr0, part, nc);
-        } else if (kv == 1) {
-            auto kern = nb == 2 ? rc_pass_kernel<2> : nb == 4 ? rc_pass_kernel<4> : nb == 8 ? rc_pass_kernel<8>
-                                                                                              : rc_pass_kernel<16>;
-            CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            kern<<<grid, kRcWarps * 32, smem, st>>>(A, lda, b, d, (int)n, R0, (int)ldr0, part, nc, al16);
-        } else {
-            const size_t smem_ws = ((size_t)rc_r0_off(nb) + 2 * (size_t)kWsRows * LD + 2 * (size_t)NP * (kWsRows + 4) +
-                                    4 * kWsRows + NP + (size_t)nb * 96) * 8;
-            const char* de = std::getenv("CSK_RC_DIAG");   // 0 = substitution in registers, else 8x8 inverses
-            const bool inv = !(de && std::atoi(de) == 0);
-            auto kern = inv ? (nb == 2 ? rc_pass_ws_kernel<2, true> : nb == 4 ? rc_pass_ws_kernel<4, true>
-                               : nb == 8 ? rc_pass_ws_kernel<8, true> : rc_pass_ws_kernel<16, true>)
-                            : (nb == 2 ? rc_pass_ws_kernel<2, false> : nb == 4 ? rc_pass_ws_kernel<4, false>
-                               : nb == 8 ? rc_pass_ws_kernel<8, false> : rc_pass_ws_kernel<16, false>);
-            CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ws));
-            kern<<<grid, (kWsSolve + kWsGram) * 32, smem_ws, st>>>(A, lda, b, d, (int)n, R0, (int)ldr0, part, nc,
-                                                                   al16);
-        }
+        const size_t smem_v3 = ((size_t)rc_r0_off(nb) + 2 * (size_t)kV3Rows * LD + 2 * kV3Rows + NP +
+                                (size_t)nb * 96) * 8;
+        auto kern = nb == 2 ? rc_pass_v3_kernel<2> : nb == 4 ? rc_pass_v3_kernel<4>
+                  : nb == 8 ? rc_pass_v3_kernel<8> : rc_pass_v3_kernel<16>;
+        CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_v3));
+        kern<<<grid, (kWsSolve + kWsGram) * 32, smem_v3, st>>>(A, lda, b, d, (int)n, R0, (int)ldr0, part, nc);
         CSK_LAUNCH_CHECK();
         rc_reduce_kernel<<<(unsigned)std::min<int64_t>(ceil_div((int64_t)nc * nc, 256), 1024), 256, 0, st>>>(
             part, grid, (int64_t)nc * nc, Cw);

@@ -5,13 +5,13 @@
 // kept, and H_d = H_{d/L} (x) H_L (Sylvester order: H[p, i] = (-1)^popcount(p & i)), so with
 // i = hi*L + lo and p_j = ph_j*L + pl_j
 //     y_j = k^-1/2 sum_hi (-1)^popcount(ph_j & hi) * (H_L (D a)[hi-block])[pl_j].
-// One pass over A: a CTA takes (column, L-row block) units, applies D while loading the block
-// (coalesced, L = 4096 rows = 32 KB), runs the length-L FWHT on chip (three radix-16 phases in
-// registers with two padded shared-memory exchanges), and adds the k sampled entries, signed by
-// the block's hi index, into per-thread accumulators that are flushed to Y once per column.
+// One pass over A: a warp (or, for k > 512, a 64-thread CTA) takes (column, row block) units, applies
+// D while loading the block (coalesced), runs the block's FWHT on chip in registers with one padded
+// shared-memory exchange, and adds the k sampled entries, signed by the block's hi index, into
+// per-thread accumulators that are flushed to Y once per column.
 // HBM traffic = d * ncols * 8 bytes read (+ d/8 bytes of D bits); the paper's implementation
 // reads and writes A O(log k) times.  Alg 3's radix-4 butterfly order
-// becomes radix-16 in registers; every stage is the same Sylvester factor, so the result is
+// becomes radix-32/64 in registers; every stage is the same Sylvester factor, so the result is
 // H_L regardless of stage order (R22).
 #include <algorithm>
 #include <cmath>
@@ -24,10 +24,7 @@ namespace csk {
 void prof_mark(cudaStream_t st, bool begin);
 
 constexpr int kHL = 4096;            // FWHT block length on chip
-constexpr int kHThreads = 256;       // 16 elements per thread
-constexpr int kHPad = kHL + kHL / 16;
 
-__device__ __forceinline__ int hpad(int i) { return i + (i >> 4); }
 
 // D as packed bits: bit (i & 31) of dbits[i >> 5] = 1 iff D_ii = -1, local row i = global row0 + i
 // (Reading R21: bit 0 of word (g & 3) of Philox(ctr = (lo32(g>>2), hi32(g>>2), 6, 0), key = seed)).
@@ -54,225 +51,10 @@ __global__ void srht_samples_kernel(uint32_t* __restrict__ p, int64_t k, uint64_
     }
 }
 
-__device__ __forceinline__ void fwht16(double (&x)[16]) {
-#pragma unroll
-    for (int h = 1; h < 16; h <<= 1)
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-            if ((i & h) == 0) {
-                const double a = x[i], b = x[i + h];
-                x[i] = a + b;
-                x[i + h] = a - b;
-            }
-}
+// (Round 1's 3-phase radix-16 CTA kernels -- register loads, and a 2-stage TMA ring -- measured 2.44 /
+// 2.40 ms against the warp kernel's 1.87 ms at d = 2^23 x 129, k = 256; removed in round 2.)
 
-// Units u = c * nblk + blk (column-major), CTA b takes the contiguous range [u0, u1).
-template <int R>   // samples per thread: k <= 256 R
-__global__ void __launch_bounds__(kHThreads) srht_kernel(const double* __restrict__ A, int64_t lda,
-                                                         const double* __restrict__ bvec, int n, int ncols,
-                                                         int64_t nblk, int64_t hb0, const uint32_t* __restrict__ dbits,
-                                                         const uint32_t* __restrict__ psamp, int k, double scale,
-                                                         double* __restrict__ Y, int64_t ldy) {
-    __shared__ double xs[kHPad];
-    const int t = threadIdx.x;
-    const int64_t total = nblk * ncols;
-    const int64_t per = (total + gridDim.x - 1) / gridDim.x;
-    const int64_t u0 = blockIdx.x * per, u1 = min(total, u0 + per);
-    if (u0 >= u1) return;
-    // this thread's samples: pl (in-block row), ph (block index)
-    int pl[R];
-    uint32_t ph[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const int j = t + r * kHThreads;
-        const uint32_t pj = j < k ? psamp[j] : 0u;
-        pl[r] = (int)(pj & (kHL - 1));
-        ph[r] = pj / kHL;
-    }
-    double acc[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) acc[r] = 0.0;
-    int cur = (int)(u0 / nblk);
-    for (int64_t u = u0; u < u1; ++u) {
-        const int c = (int)(u / nblk);
-        const int64_t blk = u - (int64_t)c * nblk;
-        if (c != cur) {   // flush the previous column
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int j = t + r * kHThreads;
-                if (j < k) atomicAdd(Y + j + (int64_t)cur * ldy, acc[r] * scale);
-                acc[r] = 0.0;
-            }
-            cur = c;
-        }
-        const double* col = (c < n ? A + (int64_t)c * lda : bvec) + blk * kHL;
-        const uint32_t* db = dbits + blk * (kHL / 32);
-        // phase A: elements e*256 + t, D applied as a sign flip; FWHT over bits 8..11
-        double x[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) x[e] = __ldcs(col + e * kHThreads + t);
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-            const int i = e * kHThreads + t;
-            const uint32_t bit = (__ldg(db + (i >> 5)) >> (i & 31)) & 1u;
-            x[e] = __longlong_as_double(__double_as_longlong(x[e]) ^ ((long long)bit << 63));
-        }
-        fwht16(x);
-#pragma unroll
-        for (int e = 0; e < 16; ++e) xs[hpad(e * kHThreads + t)] = x[e];
-        __syncthreads();
-        // phase B: bits 4..7 (thread = bits 0..3 and 8..11)
-        {
-            const int base = (t >> 4) * 256 + (t & 15);
-#pragma unroll
-            for (int e = 0; e < 16; ++e) x[e] = xs[hpad(base + e * 16)];
-            fwht16(x);
-#pragma unroll
-            for (int e = 0; e < 16; ++e) xs[hpad(base + e * 16)] = x[e];
-        }
-        __syncthreads();
-        // phase C: bits 0..3 (thread = bits 4..11)
-        {
-#pragma unroll
-            for (int e = 0; e < 16; ++e) x[e] = xs[hpad(t * 16 + e)];
-            fwht16(x);
-#pragma unroll
-            for (int e = 0; e < 16; ++e) xs[hpad(t * 16 + e)] = x[e];
-        }
-        __syncthreads();
-        // samples: acc_j += (-1)^popcount(ph_j & hi) X[pl_j], hi = global block index
-        const uint32_t hi = (uint32_t)(hb0 + blk);
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const double v = xs[hpad(pl[r])];
-            acc[r] += (__popc(ph[r] & hi) & 1) ? -v : v;
-        }
-        __syncthreads();   // xs is rewritten by the next unit
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const int j = t + r * kHThreads;
-        if (j < k) atomicAdd(Y + j + (int64_t)cur * ldy, acc[r] * scale);
-    }
-}
-
-// TMA-fed variant: the unit's 32 KB column segment arrives by one cp.async.bulk into a 2-stage
-// ring (unit i+2 is in flight while unit i is transformed), so HBM reads no longer wait on the
-// warps reaching their load instructions.  Needs 16-B aligned columns (A aligned, lda even).
-constexpr int kHStages = 2;
-
-template <int R>
-__global__ void __launch_bounds__(kHThreads, 2) srht_tma_kernel(const double* __restrict__ A, int64_t lda,
-                                                                const double* __restrict__ bvec, int n, int ncols,
-                                                                int64_t nblk, int64_t hb0,
-                                                                const uint32_t* __restrict__ dbits,
-                                                                const uint32_t* __restrict__ psamp, int k, double scale,
-                                                                double* __restrict__ Y, int64_t ldy) {
-    extern __shared__ __align__(128) double hsm[];
-    double* stage = hsm;                          // [kHStages][kHL]
-    double* xs = stage + kHStages * kHL;          // [kHPad]
-    __shared__ __align__(8) uint64_t bar[kHStages];
-    const int t = threadIdx.x;
-    const int64_t total = nblk * ncols;
-    const int64_t per = (total + gridDim.x - 1) / gridDim.x;
-    const int64_t u0 = blockIdx.x * per, u1 = min(total, u0 + per);
-    if (u0 >= u1) return;
-    auto src_of = [&](int64_t u) {
-        const int c = (int)(u / nblk);
-        const int64_t blk = u - (int64_t)c * nblk;
-        return (c < n ? A + (int64_t)c * lda : bvec) + blk * kHL;
-    };
-    if (t == 0) {
-        for (int s = 0; s < kHStages; ++s) mbar_init(&bar[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int s = 0; s < kHStages && u0 + s < u1; ++s) {
-            mbar_expect_tx(&bar[s], kHL * 8);
-            bulk_load_1d(stage + s * kHL, src_of(u0 + s), kHL * 8, &bar[s]);
-        }
-    }
-    __syncthreads();
-    int pl[R];
-    uint32_t ph[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const int j = t + r * kHThreads;
-        const uint32_t pj = j < k ? psamp[j] : 0u;
-        pl[r] = (int)(pj & (kHL - 1));
-        ph[r] = pj / kHL;
-    }
-    double acc[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) acc[r] = 0.0;
-    int cur = (int)(u0 / nblk);
-    for (int64_t u = u0; u < u1; ++u) {
-        const int64_t i = u - u0;
-        const int s = (int)(i % kHStages);
-        const uint32_t parity = (uint32_t)((i / kHStages) & 1);
-        const int c = (int)(u / nblk);
-        const int64_t blk = u - (int64_t)c * nblk;
-        if (c != cur) {
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int j = t + r * kHThreads;
-                if (j < k) atomicAdd(Y + j + (int64_t)cur * ldy, acc[r] * scale);
-                acc[r] = 0.0;
-            }
-            cur = c;
-        }
-        const uint32_t* db = dbits + blk * (kHL / 32);
-        uint32_t dw[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) dw[e] = __ldg(db + ((e * kHThreads + t) >> 5));
-        mbar_wait(&bar[s], parity);
-        const double* st = stage + s * kHL;
-        double x[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-            const int ii = e * kHThreads + t;
-            const uint32_t bit = (dw[e] >> (ii & 31)) & 1u;
-            x[e] = __longlong_as_double(__double_as_longlong(st[ii]) ^ ((long long)bit << 63));
-        }
-        fwht16(x);
-#pragma unroll
-        for (int e = 0; e < 16; ++e) xs[hpad(e * kHThreads + t)] = x[e];
-        __syncthreads();   // every thread is done reading stage s: refill it with unit u + kHStages
-        if (t == 0 && u + kHStages < u1) {
-            mbar_expect_tx(&bar[s], kHL * 8);
-            bulk_load_1d(stage + s * kHL, src_of(u + kHStages), kHL * 8, &bar[s]);
-        }
-        {
-            const int base = (t >> 4) * 256 + (t & 15);
-#pragma unroll
-            for (int e = 0; e < 16; ++e) x[e] = xs[hpad(base + e * 16)];
-            fwht16(x);
-#pragma unroll
-            for (int e = 0; e < 16; ++e) xs[hpad(base + e * 16)] = x[e];
-        }
-        __syncthreads();
-        {
-#pragma unroll
-            for (int e = 0; e < 16; ++e) x[e] = xs[hpad(t * 16 + e)];
-            fwht16(x);
-#pragma unroll
-            for (int e = 0; e < 16; ++e) xs[hpad(t * 16 + e)] = x[e];
-        }
-        __syncthreads();
-        const uint32_t hi = (uint32_t)(hb0 + blk);
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const double v = xs[hpad(pl[r])];
-            acc[r] += (__popc(ph[r] & hi) & 1) ? -v : v;
-        }
-        __syncthreads();
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const int j = t + r * kHThreads;
-        if (j < k) atomicAdd(Y + j + (int64_t)cur * ldy, acc[r] * scale);
-    }
-}
-
-// Shared-memory-lean variant (default): 64 threads per block of L = 4096 rows, 64 elements per
+// Radix-64 CTA variant (default for k > 512): 64 threads per block of L = 4096 rows, 64 elements per
 // thread, so H_L = two radix-64 register phases with ONE padded shared-memory exchange, and only
 // the k sampled positions are written back for the gather (a 4096-bit sample map).  Per 32 KB of
 // A this moves ~68 KB through shared memory (the 3-phase kernels move ~200-260 KB: shared-memory
@@ -663,15 +445,13 @@ csk_status srht_impl(int64_t d, int64_t dglob, int64_t row0, int64_t k, uint64_t
         const DeviceInfo& di = device_info();
         int per_sm = 0;
         const bool al = (n == 0 || (((uintptr_t)A & 15) == 0 && (lda & 1) == 0)) && (!b || ((uintptr_t)b & 15) == 0);
-        const char* e = std::getenv("CSK_SRHT_TMA");
-        const char* v = std::getenv("CSK_SRHT_KERNEL");   // experiment: 1 = 3-phase, 2 = radix-64 blocks
+        const char* v = std::getenv("CSK_SRHT_KERNEL");   // test hook: 2 = radix-64 blocks for any k
         const int kv = v ? std::atoi(v) : 0;
-        const char* wte = std::getenv("CSK_SRHT_WTMA");   // experiment: 0 = register warp kernel for every k
-        const int wt = wte ? std::atoi(wte) : 1;
-        if (kv == 0 && al && ((k > 128 && k <= 256 && wt >= 1) || (k <= 128 && wt == 2))) {
+        if (kv == 0 && al && k > 128 && k <= 256) {
             // the TMA-fed warp kernel: k = 2n = 256 1.87 -> 1.61 ms at d = 2^23 x 129 (the register
-            // kernel is latency-bound there); k <= 128 only on request (CSK_SRHT_WTMA=2)
-            auto kern = k <= 128 ? srht_warp_tma_kernel<4> : srht_warp_tma_kernel<8>;
+            // kernel is latency-bound there); for k <= 128 (1.58 vs 1.46 ms) and k = 512 (3.89 vs
+            // 3.51 ms) the register kernel is faster
+            auto kern = srht_warp_tma_kernel<8>;
             const size_t smem = (size_t)kHWWarps * (kHW + kHWPad) * 8;
             CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             CSK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kHWWarps * 32, smem));
@@ -683,11 +463,8 @@ csk_status srht_impl(int64_t d, int64_t dglob, int64_t row0, int64_t k, uint64_t
             CSK_LAUNCH_CHECK();
         } else if (kv == 0 && k <= 512) {
             auto kern = k <= 128 ? srht_warp_kernel<4> : k <= 256 ? srht_warp_kernel<8> : srht_warp_kernel<16>;
-            // experiment: shared-memory carveout %.  The driver default measured best (1.49 ms at
-            // d=2^24 x 65, k=128): a larger carveout shrinks L1, which stages the in-flight loads.
-            const char* cv = std::getenv("CSK_SRHT_CARVE");
-            if (cv && *cv)
-                CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(cv)));
+            // (the driver's default carveout measured best: 1.49 ms at d = 2^24 x 65, k = 128; a larger
+            // carveout shrinks the L1 that stages the in-flight loads)
             CSK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kHWWarps * 32, 0));
             const int64_t nblk1 = d / kHW, total1 = nblk1 * ncols;
             const int64_t grid = std::min<int64_t>(ceil_div(total1, kHWWarps), (int64_t)di.num_sms * std::max(per_sm, 1));
@@ -695,31 +472,13 @@ csk_status srht_impl(int64_t d, int64_t dglob, int64_t row0, int64_t k, uint64_t
             kern<<<(unsigned)grid, kHWWarps * 32, 0, st>>>(A, lda, b, (int)n, (int)ncols, nblk1, row0 / kHW, dbits,
                                                            psamp, (int)k, scale, Y, ldy);
             CSK_LAUNCH_CHECK();
-        } else if (kv != 1) {
+        } else {   // k > 512, or CSK_SRHT_KERNEL=2 (test hook): radix-64 CTA blocks
             auto kern = k <= 256 ? srht_r64_kernel<4> : k <= 512 ? srht_r64_kernel<8> : srht_r64_kernel<16>;
             CSK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kH64Threads, 0));
             const int64_t grid = std::min<int64_t>(total, (int64_t)di.num_sms * std::max(per_sm, 1));
             prof_mark(st, true);
             kern<<<(unsigned)grid, kH64Threads, 0, st>>>(A, lda, b, (int)n, (int)ncols, nblk, row0 / kHL, dbits,
                                                          psamp, (int)k, scale, Y, ldy);
-            CSK_LAUNCH_CHECK();
-        } else if (al && !(e && std::atoi(e) == 0)) {
-            auto kern = k <= 256 ? srht_tma_kernel<1> : k <= 512 ? srht_tma_kernel<2> : srht_tma_kernel<4>;
-            const size_t smem = ((size_t)kHStages * kHL + kHPad) * 8;
-            CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            CSK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kHThreads, smem));
-            const int64_t grid = std::min<int64_t>(total, (int64_t)di.num_sms * std::max(per_sm, 1));
-            prof_mark(st, true);
-            kern<<<(unsigned)grid, kHThreads, smem, st>>>(A, lda, b, (int)n, (int)ncols, nblk, row0 / kHL, dbits,
-                                                          psamp, (int)k, scale, Y, ldy);
-            CSK_LAUNCH_CHECK();
-        } else {
-            auto kern = k <= 256 ? srht_kernel<1> : k <= 512 ? srht_kernel<2> : srht_kernel<4>;
-            CSK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kHThreads, 0));
-            const int64_t grid = std::min<int64_t>(total, (int64_t)di.num_sms * std::max(per_sm, 1));
-            prof_mark(st, true);
-            kern<<<(unsigned)grid, kHThreads, 0, st>>>(A, lda, b, (int)n, (int)ncols, nblk, row0 / kHL, dbits, psamp,
-                                                       (int)k, scale, Y, ldy);
             CSK_LAUNCH_CHECK();
         }
         prof_mark(st, false);

@@ -58,7 +58,7 @@ for e in ({}, {"CSK_QR_WY": "0"}, {"CSK_QR_WY": "0", "CSK_QR_SINGLE": "1"}, {"CS
     print("ms_solve", e, flush=True)
 csk.ne_lstsq(Ad, bd)
 print("ne_lstsq", flush=True)
-for e in ({}, {"CSK_RC_KERNEL": "1"}, {"CSK_RC_KERNEL": "2"}, {"CSK_RC_PATH": "0"}):
+for e in ({}, {"CSK_RC_PATH": "0"}):
     env(**e)
     csk.rc_lstsq(plan, 16, Ad, bd)
     env(**{k: None for k in e})
@@ -67,7 +67,7 @@ Aw = synth.gaussian_matrix(2048, 136, seed=4)
 csk.rc_lstsq(csk.cs_plan(2048, 4096, 3), 272, cm(Aw), cm(Aw[:, 0].copy()))
 print("rc_lstsq wide", flush=True)
 As = synth.gaussian_matrix(1 << 13, 3, seed=5)
-for e in ({}, {"CSK_SRHT_KERNEL": "2"}, {"CSK_SRHT_KERNEL": "1"}, {"CSK_SRHT_KERNEL": "1", "CSK_SRHT_TMA": "0"}):
+for e in ({}, {"CSK_SRHT_KERNEL": "2"}):
     env(**e)
     csk.srht_apply(cm(As), 40, 1)
     env(**{k: None for k in e})

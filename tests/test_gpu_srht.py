@@ -84,17 +84,13 @@ def test_srht_errors():
     assert e.value.status == csk.csk.EUNSUPPORTED
 
 
-@pytest.mark.parametrize("path", ["warp", "r64", "tma", "ldg"])
+@pytest.mark.parametrize("path", ["warp", "r64"])
 @pytest.mark.parametrize("lda_pad", [0, 1])
 def test_srht_kernel_paths(monkeypatch, path, lda_pad):
-    # default warp-block kernel; the radix-64 CTA kernel; the 3-phase kernels: TMA-fed ring
-    # (16-B aligned columns) and the register-load kernel (forced, or odd lda)
+    # k = 130: the TMA-fed warp kernel (16-B aligned columns) or the register warp kernel (odd lda);
+    # "r64" forces the radix-64 CTA kernel (the default for k > 512)
     if path == "r64":
         monkeypatch.setenv("CSK_SRHT_KERNEL", "2")
-    elif path != "warp":
-        monkeypatch.setenv("CSK_SRHT_KERNEL", "1")
-    if path == "ldg":
-        monkeypatch.setenv("CSK_SRHT_TMA", "0")
     d, n, k = 1 << 15, 7, 130
     A = synth.gaussian_matrix(d, n, seed=8)
     big = np.zeros((d + lda_pad, n), order="F")
