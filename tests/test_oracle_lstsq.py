@@ -135,3 +135,30 @@ def test_kappa_sweep_fig8():
             assert r_ne <= 1e-6
         else:
             assert r_ne > 1e-2 or r_ne > 1e3 * max(r_ms, 1e-16), (kappa, r_ne)
+
+
+def test_residual_norm_closed_forms():
+    # or_residual_norm (P:L338's ||b - Ax||) pinned to values fixed by arithmetic, not by a re-typed
+    # formula: (i) integer cases whose residual is a Pythagorean vector (exact); (ii) x = 0 gives
+    # ||b|| and x solving A x = b exactly gives 0; (iii) a residual orthogonal to range(A) built from a
+    # Householder reflector: b = A x + t u with u a unit vector orthogonal to A's columns -> |t|.
+    A = np.array([[1.0, 0.0], [0.0, 1.0], [0.0, 0.0], [0.0, 0.0]])
+    assert oracle.residual_norm(A, np.array([4.0, -2.0, 3.0, 4.0]), np.array([4.0, -2.0])) == 5.0
+    Ai = np.array([[2.0, 1.0], [1.0, 3.0], [0.0, 1.0]])
+    x = np.array([1.0, 2.0])
+    r = np.array([5.0, 12.0, 0.0])                  # ||r|| = 13 exactly
+    assert oracle.residual_norm(Ai, Ai @ x + r, x) == 13.0
+    rng = np.random.default_rng(11)
+    B = rng.standard_normal((50, 4))
+    b = rng.standard_normal(50)
+    assert oracle.residual_norm(B, b, np.zeros(4)) == pytest.approx(float(np.sqrt(np.sum(b * b))), rel=1e-15, abs=0)
+    assert oracle.residual_norm(Ai, Ai @ x, x) == 0.0
+    # (iii): the last column of a full QR of B is orthogonal to B's range
+    Q, _ = np.linalg.qr(np.column_stack([B, rng.standard_normal(50)]), mode="reduced")
+    u = Q[:, -1] - B @ np.linalg.lstsq(B, Q[:, -1], rcond=None)[0]
+    u /= np.linalg.norm(u)
+    xs = rng.standard_normal(4)
+    for t, tol in ((1e-8, 1e-5), (0.5, 1e-12), (3.0, 1e-12)):   # b's rounding (~1e-15) sets the tolerance
+        assert oracle.residual_norm(B, B @ xs + t * u, xs) == pytest.approx(t, rel=tol, abs=0)
+    # a dropped term or a wrong sign in the accumulation fails one of the above; a transposed operand
+    # fails the non-square integer case (A^T has the wrong shape for x)
