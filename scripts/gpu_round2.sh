@@ -13,7 +13,7 @@ timeout 900 python bench.py > gpurun_out/r2_bench_c2.json 2> gpurun_out/r2_bench
 for c in c4 c3; do timeout 900 python bench.py --config $c > gpurun_out/r2_bench_$c.json 2> gpurun_out/r2_bench_$c.log; echo "bench $c rc=$?"; done
 for c in srht rc; do timeout 900 python bench.py --config $c > gpurun_out/r2_bench_$c.json 2> gpurun_out/r2_bench_$c.log; echo "bench $c rc=$?"; done
 # launch list of the default step (library kernels only: the timed steps, not the input generation)
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:csk -c 120 --csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k "regex:^(cs_|gstage|qr_wy|codes_|gauss|transpose_out)" -c 120 --csv \
     --log-file gpurun_out/r2_launches_c2.csv python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu --no-ls --no-extra --no-c5 > /dev/null 2>&1
 echo "launches rc=$?"
 timeout 600 python scripts/ncu_traffic.py c2 c4 c3; echo "traffic rc=$?"
