@@ -594,3 +594,25 @@ def test_hash_plan_ms_lstsq_matches_stored_codes():
     nb = np.linalg.norm(b)
     check_fitted(A, host(x0) - host(x1), nb, 1e-8)
     assert abs(r0 - r1) <= 1e-8 * nb
+
+
+# ------------------------------------------------ spread SA^T copies (small k1)
+@pytest.mark.parametrize("spread_kb", ["0", "256", "8192"])
+@pytest.mark.parametrize("d,n,k1,with_b", [(200003, 8, 128, True), (100003, 20, 512, False), (70001, 33, 97, True)])
+def test_cs_apply_spread_copies(monkeypatch, spread_kb, d, n, k1, with_b):
+    # CTA c reduces into copy c mod S of a small SA^T and the copies are folded in fixed order: the
+    # result is the same sum (within 1e-12 T; exact on integer A) for no copies, the default target
+    # and one copy per CTA; also through ms_apply (the G-stage reads the folded copy 0)
+    monkeypatch.setenv("CSK_SPREAD_KB", spread_kb)
+    plan = csk.cs_plan(d, k1, 3)
+    h, s = oracle.codes(d, k1, 3)
+    A = synth.gaussian_matrix(d, n, seed=4)
+    b = synth.rhs(A, "easy", seed=4) if with_b else None
+    _check_apply(plan, h, s, A, b, "B")
+    Ai = synth.integer_matrix(d, n, seed=5)
+    got = host(csk.cs_apply(plan, gpu_colmajor(Ai), variant="B"))
+    assert np.array_equal(got, oracle.cs_apply(h, s, Ai, k1))
+    k2 = 2 * (n + 1)
+    Z = host(csk.ms_apply(plan, k2, gpu_colmajor(A), b=None if b is None else gpu_colmajor(b)))
+    Zo, Zabs = oracle.ms_apply(A, k1, k2, seed=3, b=b, with_abs=True)
+    assert_within_T(Z, Zo, Zabs, 1e-12)
