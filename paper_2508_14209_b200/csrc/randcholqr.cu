@@ -317,16 +317,39 @@ __global__ void rc_pack_r0_kernel(const double* __restrict__ R0g, int ldr0g, int
     }
 }
 
+// R0 block column J (packed, 64 J + 96 doubles) followed by W_J (96 doubles): the per-J shared stage
+__host__ __device__ constexpr int rc_blk_doubles(int J) { return 64 * J + 96 + 96; }
+
+__device__ __forceinline__ void rc_cp16(double* dst, const double* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+                 : "memory");
+}
+
 template <int NB>
 __global__ void __launch_bounds__(kWsSolve * 32, 1)
     rc_trsm_kernel(const double* __restrict__ A, int64_t lda, int64_t d, int n, const double* __restrict__ R0p,
                    const double* __restrict__ Wd, double* __restrict__ Q, int64_t ldq) {
     constexpr int NP = 8 * NB, LD = NP + 4;
     constexpr int P = 8;
+    constexpr int SB = rc_blk_doubles(NB - 1);   // stage size (the largest block)
     extern __shared__ __align__(16) double qsm[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t = lane & 3;
     double* qw = qsm + (size_t)warp * 16 * LD;                 // this warp's 16 Q rows
+    double* stg = qsm + (size_t)kWsSolve * 16 * LD;            // [2][SB] R0 block J | W_J, double-buffered
+    // Block J's R0 fragments and diagonal inverse are read by all four warps: one cp.async copy per J
+    // into a shared stage (prefetched one J ahead, one 4-warp barrier per J) instead of every warp
+    // reading them from L2 (ncu r02 at n = 256, d = 2^22 chunk: 6.57 -> 4.53 ms, DMMA 30% -> 42%;
+    // splitting the k loop into eight DMMA chains measured 4.86 ms: the unrolled code then misses in
+    // the instruction cache more often)
+    auto stage = [&](int J, int buf) {
+        double* dst = stg + buf * SB;
+        const double* src = R0p + rc_r0_off(J);
+        const int nb = (64 * J + 96) / 2;   // 16-B chunks of the packed block
+        for (int e = threadIdx.x; e < nb; e += kWsSolve * 32) rc_cp16(dst + 2 * e, src + 2 * e);
+        if (threadIdx.x < 48) rc_cp16(dst + 64 * J + 96 + 2 * threadIdx.x, Wd + J * 96 + 2 * threadIdx.x);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
     const int64_t ntiles = (d + kV3Rows - 1) / kV3Rows;
     const int64_t my = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     double pa0[P], pa1[P], pb0[P], pb1[P];
@@ -343,8 +366,10 @@ __global__ void __launch_bounds__(kWsSolve * 32, 1)
         b0 = ldcs_pred_rc(p0 + rb, vb && c0 < n);
         b1 = ldcs_pred_rc(p1 + rb, vb && c0 + 1 < n);
     };
+    if (my == 0) return;   // uniform per CTA: no barrier below is skipped by part of it
 #pragma unroll
     for (int J = 0; J < P; ++J) load_step(0, J, pa0[J], pa1[J], pb0[J], pb1[J]);
+    stage(0, 0);
     double* qrowA = qw + g * LD;
     double* qrowB = qrowA + 8 * LD;
     for (int64_t i = 0; i < my; ++i) {
@@ -352,6 +377,12 @@ __global__ void __launch_bounds__(kWsSolve * 32, 1)
         // cut the code to 43 KB but measured slower (9.0 vs 6.6 ms per 2^20-row chunk at n = 256)
 #pragma unroll
         for (int J = 0; J < NB; ++J) {
+            // block J has landed in stage J & 1, and every warp is done with stage (J + 1) & 1 (block
+            // J - 1): prefetch the next block (the next tile's block 0 after the last)
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            asm volatile("bar.sync 1, %0;" ::"n"(kWsSolve * 32) : "memory");
+            stage(J + 1 < NB ? J + 1 : 0, (J + 1) & 1);
+            const double* sj = stg + (J & 1) * SB;
             double tA0 = pa0[J % P], tA1 = pa1[J % P], tB0 = pb0[J % P], tB1 = pb1[J % P];
             if (J + P < NB)
                 load_step(i, J + P, pa0[J % P], pa1[J % P], pb0[J % P], pb1[J % P]);
@@ -360,10 +391,10 @@ __global__ void __launch_bounds__(kWsSolve * 32, 1)
             double a00 = 0.0, a01 = 0.0, a10 = 0.0, a11 = 0.0, b00 = 0.0, b01 = 0.0, b10 = 0.0, b11 = 0.0;
             const double* qa = qrowA + t;
             const double* qb = qrowB + t;
-            const double* rb = R0p + rc_r0_off(J) + g * (8 * J + 12) + t;
+            const double* rb = sj + g * (8 * J + 12) + t;
 #pragma unroll
             for (int k = 0; k < 8 * J; k += 8) {
-                const double r0v = __ldg(rb + k), r1v = __ldg(rb + k + 4);
+                const double r0v = rb[k], r1v = rb[k + 4];
                 dmma884(a00, a01, qa[k], r0v);
                 dmma884(b00, b01, qb[k], r0v);
                 dmma884(a10, a11, qa[k + 4], r1v);
@@ -378,8 +409,8 @@ __global__ void __launch_bounds__(kWsSolve * 32, 1)
             const double xa10 = __shfl_sync(0xffffffffu, tA0, src1), xa11 = __shfl_sync(0xffffffffu, tA1, src1);
             const double xb00 = __shfl_sync(0xffffffffu, tB0, src0), xb01 = __shfl_sync(0xffffffffu, tB1, src0);
             const double xb10 = __shfl_sync(0xffffffffu, tB0, src1), xb11 = __shfl_sync(0xffffffffu, tB1, src1);
-            const double* wb = Wd + J * 96 + g * 12 + t;
-            const double w0 = __ldg(wb), w1 = __ldg(wb + 4);
+            const double* wb = sj + 64 * J + 96 + g * 12 + t;
+            const double w0 = wb[0], w1 = wb[4];
             double qa0 = 0.0, qa1 = 0.0, qb0 = 0.0, qb1 = 0.0;
             dmma884(qa0, qa1, (t & 1) ? xa01 : xa00, w0);
             dmma884(qb0, qb1, (t & 1) ? xb01 : xb00, w0);
@@ -396,6 +427,7 @@ __global__ void __launch_bounds__(kWsSolve * 32, 1)
             if (rbase + rr < d) Q[rbase + rr + (int64_t)c * ldq] = qw[rr * LD + c];
         __syncwarp();
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 // C[e] = sum_p part[p][e], fixed order (deterministic for a given grid)
@@ -462,7 +494,7 @@ static csk_status rc_gram_impl(int64_t d, int64_t n, const double* A, int64_t ld
         double* Qw = Wd + wd;
         rc_pack_r0_kernel<<<nb, 256, 0, st>>>(R0, (int)ldr0, (int)n, nb, R0p, Wd);
         CSK_LAUNCH_CHECK();
-        const size_t smem = (size_t)kWsSolve * 16 * LD * 8;
+        const size_t smem = ((size_t)kWsSolve * 16 * LD + 2 * (size_t)rc_blk_doubles(nb - 1)) * 8;
         CSK_CUDA_TRY(cudaFuncSetAttribute(rc_trsm_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         const DeviceInfo& di = device_info();
         const double one = 1.0, zero = 0.0;
