@@ -48,8 +48,11 @@ typedef enum {
 
 typedef enum { CSK_F64 = 0, CSK_F32 = 1 } csk_dtype;
 
-/* cs_apply kernel variants (DESIGN.md section 5).  CSK_VAR_AUTO picks per
- * (d, ncols, k1, dtype) from the measured selection table. */
+/* cs_apply kernel variants (DESIGN.md section 6).  CSK_VAR_AUTO picks per
+ * (dtype, SA^T footprint k1 * ncols * w) from the table measured on B200 over
+ * d = 2^20 and 2^23, n = 8..256 (profiles/r02_variant_table.json):
+ * B for fp64 and for fp32 with SA^T > 64 KB, X (<= 8 KB) or T (<= 64 KB) for a
+ * tiny fp32 SA^T. */
 typedef enum {
     CSK_VAR_AUTO = -1,
     CSK_VAR_ATOMIC_COL = 0,   /* L: one L2 reduction (REDG) per element, column-major target  */
@@ -126,6 +129,9 @@ csk_status cs_apply(csk_plan_t plan, csk_dtype dtype, int64_t n, const void* A, 
  *   A, b    device pointers, or HOST pointers (then streamed through the GPU in
  *           row chunks, copies overlapped with the sketch -- P:L375 linearity).
  *   Workspace for SA (k1 x ncols) comes from the stream-ordered allocator.
+ *   The G-stage is a hand-written fp64 DMMA kernel on the CountSketch's row-major
+ *   SA^T (Z^T = Y^T G^T, no transpose); fp32 input is sketched in fp32
+ *   bounded-depth copies combined in fp64 (R12) and Z is fp32.
  * For a row-partitioned A every rank calls ms_apply on its block
  * with its row0-plan and the same seed, and the caller sums the Z's (NCCL
  * all-reduce) before ms_solve. */
