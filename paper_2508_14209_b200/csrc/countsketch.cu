@@ -702,12 +702,15 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk64f_kernel(const uint32_t* _
         const uint32_t bytes = (uint32_t)(nc4 * 4);
         float* dst[2];
         bool ok[2];
+        // row-block copy of the tile (rows_per_copy is a multiple of the 64-row tile): one 32-bit
+        // division per tile instead of two 64-bit divisions per lane
+        const int64_t copy = (int64_t)((uint32_t)(r0 / kF32Rows) / (uint32_t)(L.rows_per_copy / kF32Rows));
+        float* cbase = SAt + copy * L.copy_stride + (int64_t)ch * L.cs;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int r = lane + 32 * h;
             ok[h] = r0 + r < rows;
-            const int64_t copy = (r0 + r) / L.rows_per_copy;
-            dst[h] = SAt + copy * L.copy_stride + (int64_t)ch * L.cs + (int64_t)code_bucket(h ? cb : ca) * L.lc;
+            dst[h] = cbase + (int64_t)code_bucket(h ? cb : ca) * L.lc;
         }
         if (++u >= uend) {
             unsigned long long ub = 0;
@@ -1284,7 +1287,9 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
                 // every bucket sum of a copy to stay far below 1e-5 / u32 = 168 terms)
                 const int64_t ncp = std::max<int64_t>(1, ceil_div(rows, 64 * k1));
                 L.ncopies = (int)ncp;
-                L.rows_per_copy = ceil_div(rows, ncp);
+                // whole 64-row tiles per copy (the kernel maps a tile to its copy with one division); the
+                // mean bucket depth stays <= 64 + 64 / k1 (<= 128 for k1 = 1, where the depth is exact)
+                L.rows_per_copy = ceil_div(ceil_div(rows, ncp), (int64_t)kF32Rows) * kF32Rows;
                 L.copy_stride = L.chunk_major ? L.cs * ((ncols + L.cw - 1) / L.cw) : k1 * L.lc;   // floats
                 ws_doubles = (size_t)ceil_div(ncp * L.copy_stride, 2);
             } else {
@@ -1327,6 +1332,7 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
         CSK_CUDA_TRY(csk_malloc_async(&tgt.buf, (ws_doubles + 2) * sizeof(double), st));
         CSK_CUDA_TRY(cudaMemsetAsync(tgt.buf, 0, (ws_doubles + 2) * sizeof(double), st));
         L.work = reinterpret_cast<unsigned long long*>(tgt.buf + ws_doubles);
+        if (const char* ge = std::getenv("CSK_GRAB")) L.grab = std::max(1, std::atoi(ge));   // sweep hook
     } else if (variant != CSK_VAR_SORTED && !accumulate) {
         // zero SA (ldsa may exceed k1: clear the k1 x ncols window only)
         if (ldsa == k1) {
