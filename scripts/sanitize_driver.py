@@ -34,7 +34,16 @@ for v in ("L", "T", "S", "G", "B", "X"):
     csk.cs_apply(plan, Ad, b=bd, variant=v)
     print("cs_apply", v, flush=True)
 csk.cs_apply(plan, cm(A.astype(np.float32)), b=cm(b.astype(np.float32)))
+csk.cs_apply(plan, cm(A.astype(np.float32)), b=cm(b.astype(np.float32)), variant="B")   # fp32 copies
 print("cs_apply fp32", flush=True)
+for kb in ("0", "4096"):   # spread SA^T copies off / one per CTA
+    env(CSK_SPREAD_KB=kb)
+    csk.cs_apply(plan, Ad, b=bd, variant="B")
+    env(CSK_SPREAD_KB=None)
+print("cs_apply spread", flush=True)
+Am = synth.gaussian_matrix(8192, 100, seed=6)   # G-stage with 4 DMMA warps x 32 rows (NT = 7) and 2 M tiles
+csk.ms_apply(csk.cs_plan(8192, 4096, 4), 256, cm(Am), b=cm(Am[:, 0].copy()))
+print("ms_apply NT=7 MW=4", flush=True)
 wide = synth.gaussian_matrix(4096, 129, seed=3)
 csk.cs_apply(csk.cs_plan(4096, 256, 2), cm(wide), b=cm(wide[:, 0].copy()))
 print("cs_apply 2 chunks", flush=True)
