@@ -52,6 +52,7 @@ struct RowLayout {
     // funnelled into the few L2 lines of a small SA^T; the copies are summed afterwards in fixed order
     int nspread = 1;
     int64_t spread_stride = 0;
+    int f32_spread = 1;   // fp32 copies: consecutive tiles interleaved over this many copies
     unsigned long long* work = nullptr;   // dynamic work counter of the B kernels (zeroed with the workspace)
     int grab = 8;                         // units per counter grab (4/8/16/32 measured: 8)
     __host__ __device__ int64_t base(int ch, uint32_t bucket) const { return (int64_t)ch * cs + (int64_t)bucket * lc; }
@@ -426,8 +427,22 @@ constexpr int64_t kSpreadBytes = 256ll << 10;   // spread-copy footprint target 
 __device__ __forceinline__ int b32_row(int r, int ld) { return r * ld + 2 * (r >> 3); }
 constexpr int kB32Pad = 6;   // doubles per warp tile beyond 32 rows (the shift of the last group)
 
-template <int W, int EXP = 0, bool PRED = false, bool HASH = false>
-__global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __restrict__ code, int64_t rows,
+// KJ = column pairs a lane holds (2 KJ >= the chunk's columns + pad).  Narrow [A b] (n <= 32) take a
+// narrow instantiation: its smaller register file lets 2 (KJ = 17) or 3 (KJ = 9) CTAs share an SM, so
+// 2-3x the tiles are in flight -- with one 32-row tile per warp, the narrow shapes were bound by the
+// per-tile latency (load, store, bulk issue: ~2.5 us per tile at n = 8 ... 32, the same time for any width).
+template <int KJ>
+constexpr int b32_ctas_per_sm() { return KJ <= 9 ? 3 : KJ <= 17 ? 2 : 1; }
+// register width of the B32 instantiation for a chunk of cw columns (CSK_B32_NARROW=0 disables the
+// narrow ones, for A/B measurements)
+static int b32_kj(int cw) {
+    const char* e = std::getenv("CSK_B32_NARROW");
+    const bool off = e && std::atoi(e) == 0;
+    const int slots = (cw + 1) & ~1;   // columns + the 16-B pad
+    return off ? kBulkMaxCols / 2 : slots <= 18 ? 9 : slots <= 34 ? 17 : kBulkMaxCols / 2;
+}
+template <int W, int EXP = 0, bool PRED = false, bool HASH = false, int KJ = kBulkMaxCols / 2>
+__global__ void __launch_bounds__(W * 32, b32_ctas_per_sm<KJ>()) cs_bulk32_kernel(const uint32_t* __restrict__ code, int64_t rows,
                                                                Cols<double> cols, int ncols, int ldtile,
                                                                double* __restrict__ SAt, RowLayout L, int k1) {
     // EXP: compile-time experiment switches for roofline attribution (0 in production):
@@ -448,7 +463,7 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk32_kernel(const uint32_t* __
     const int nchunks = (ncols + cw - 1) / cw;
     const int64_t ngroups = (rows + kB32Rows - 1) / kB32Rows;
     const int64_t nunits = ngroups * nchunks;
-    constexpr int kJ = kBulkMaxCols / 2;
+    constexpr int kJ = KJ;
     // Work distribution: with L.work (a zeroed counter after the workspace) warps take batches of
     // kGrab consecutive units from one atomic counter, so CTAs that start late (SMs still held by an
     // overlapping kernel, e.g. the previous batch's solve) just take fewer units; else static
@@ -617,8 +632,18 @@ __device__ __forceinline__ void ldcs_v8_pred(const float* p, bool pred, float (&
         : "l"(p), "r"((int)pred));
 }
 
-template <int W>
-__global__ void __launch_bounds__(W * 32, 1) cs_bulk64f_kernel(const uint32_t* __restrict__ code, int64_t rows,
+// KJF = column quads a lane holds (4 KJF >= the chunk's columns + pad): the narrow instantiations
+// (KJF = 5 / 9, n <= 16 / 32) run 3 / 2 CTAs per SM, as the fp64 B32 kernel does.
+template <int KJF>
+constexpr int f32_ctas_per_sm() { return KJF <= 5 ? 3 : KJF <= 9 ? 2 : 1; }
+static int f32_kj(int cw) {
+    const char* e = std::getenv("CSK_B32_NARROW");
+    const bool off = e && std::atoi(e) == 0;
+    const int slots = (cw + 3) & ~3;
+    return off ? kF32MaxCols / 4 : slots <= 20 ? 5 : slots <= 36 ? 9 : kF32MaxCols / 4;
+}
+template <int W, int KJF = kF32MaxCols / 4>
+__global__ void __launch_bounds__(W * 32, f32_ctas_per_sm<KJF>()) cs_bulk64f_kernel(const uint32_t* __restrict__ code, int64_t rows,
                                                                 Cols<float> cols, int ncols, int ldf,
                                                                 float* __restrict__ SAt, RowLayout L) {
     const int cw = L.cw;
@@ -632,7 +657,7 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk64f_kernel(const uint32_t* _
     const int nchunks = (ncols + cw - 1) / cw;
     const int64_t ngroups = (rows + kF32Rows - 1) / kF32Rows;
     const int64_t nunits = ngroups * nchunks;
-    constexpr int kJ = kF32MaxCols / 4;
+    constexpr int kJ = KJF;
     const int kGrab = L.grab;
     int64_t u, uend;
     {
@@ -704,7 +729,12 @@ __global__ void __launch_bounds__(W * 32, 1) cs_bulk64f_kernel(const uint32_t* _
         bool ok[2];
         // row-block copy of the tile (rows_per_copy is a multiple of the 64-row tile): one 32-bit
         // division per tile instead of two 64-bit divisions per lane
-        const int64_t copy = (int64_t)((uint32_t)(r0 / kF32Rows) / (uint32_t)(L.rows_per_copy / kF32Rows));
+        // interleaved in groups of S = L.f32_spread copies: tile g of a block of S * TPC tiles goes to copy
+        // (block) S + g % S, so the tiles in flight at one time (consecutive g) spread over S copies
+        // while each copy still takes TPC tiles (the depth bound is unchanged)
+        const uint32_t gt = (uint32_t)(r0 / kF32Rows), tpc = (uint32_t)(L.rows_per_copy / kF32Rows);
+        const uint32_t S = (uint32_t)L.f32_spread;
+        const int64_t copy = (int64_t)((gt / (S * tpc)) * S + gt % S);
         float* cbase = SAt + copy * L.copy_stride + (int64_t)ch * L.cs;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -748,6 +778,43 @@ __global__ void cs_combine_rows_kernel(const float* __restrict__ SAt, RowLayout 
     }
     Yt[e] = acc;
 }
+
+// many copies (small k1: rows / (64 k1) copies, e.g. 1024 at d = 2^23, k1 = 128): one warp per element,
+// lane l sums copies l, l + 32, ... in fp64, then a fixed butterfly -- deterministic, and 32x shorter
+// than the one-thread chain of the kernels above (which made the combine, not the sketch, the cost
+// of the narrow fp32 shapes).  ROWOUT: fp64 row-major workspace (ms_apply), else column-major float SA.
+template <bool ROWOUT>
+__global__ void __launch_bounds__(256) cs_combine_warp_kernel(const float* __restrict__ SAt, RowLayout L, int64_t k1,
+                                                              int ncols, int64_t lcd, double* __restrict__ Yt,
+                                                              float* __restrict__ SA, int64_t ldsa) {
+    const int lane = threadIdx.x & 31;
+    const int64_t e = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t ne = k1 * (ROWOUT ? lcd : (int64_t)ncols);
+    if (e >= ne) return;
+    int64_t m;
+    int c;
+    if (ROWOUT) {
+        m = e / lcd;
+        c = (int)(e - m * lcd);
+    } else {   // column-major order: consecutive warps write consecutive rows of one column
+        c = (int)(e / k1);
+        m = e - (int64_t)c * k1;
+    }
+    double acc = 0.0;
+    if (c < ncols) {
+        const int64_t off = (int64_t)(c / L.cw) * L.cs + m * L.lc + (c % L.cw);
+        for (int p = lane; p < L.ncopies; p += 32) acc += (double)SAt[p * L.copy_stride + off];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+        if (ROWOUT)
+            Yt[e] = acc;
+        else
+            SA[m + (int64_t)c * ldsa] = (float)acc;
+    }
+}
+constexpr int kCombineWarpCopies = 64;   // ncopies from which the warp-per-element combine is used
 
 // spread copies (fp64 B32): copy 0 <- sum_p copy_p, elementwise, fixed order p = 0, 1, ...
 __global__ void cs_spread_combine_kernel(double* __restrict__ SAt, int64_t n, int nspread, int64_t stride) {
@@ -973,10 +1040,11 @@ struct VariantRule {
     int variant;
 };
 static const VariantRule kVariantTable[] = {
-    {CSK_F32, 8 << 10, CSK_VAR_TMA_ROW},      // d=2^23 n=8: X 0.960 ms, T 1.035, B 1.210
-    {CSK_F32, 64 << 10, CSK_VAR_ATOMIC_ROW},  // d=2^23 n=16: T 0.633 ms, B 0.702, X 0.970
-    {CSK_F32, INT64_MAX, CSK_VAR_BULK_ROW},   // n >= 32: B (e.g. n=64 0.695 ms vs T 1.380)
-    {CSK_F64, INT64_MAX, CSK_VAR_BULK_ROW},   // every row (e.g. n=8 0.544 ms vs T 1.042, n=256 4.16 vs 8.75)
+    // round-2 close: the narrow instantiations (2-3 CTAs per SM), interleaved fp32 copies and the
+    // warp-per-element combine made B the fastest for every measured fp32 row as well
+    // (profiles/r02_variant_table.json; fp32 d=2^23 n=8: B 0.191 ms vs X 0.962, n=16: B 0.206 vs T 0.625)
+    {CSK_F32, INT64_MAX, CSK_VAR_BULK_ROW},
+    {CSK_F64, INT64_MAX, CSK_VAR_BULK_ROW},   // every row (e.g. d=2^23 n=8 0.236 ms vs T 1.036, n=256 4.05 vs 8.57)
 };
 
 static int select_variant(int64_t d, int64_t k1, int ncols, csk_dtype dtype, bool has_sort) {
@@ -1068,11 +1136,13 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
                     int ldf = (cw + 3) & ~3;
                     while (ldf % 32 != 4) ldf += 4;   // == 4 mod 32: conflict-free tile stores
                     constexpr int fw = 8;
-                    auto fk = cs_bulk64f_kernel<fw>;
+                    const int kjf = f32_kj(cw);
+                    auto fk = kjf == 5 ? cs_bulk64f_kernel<fw, 5> : kjf == 9 ? cs_bulk64f_kernel<fw, 9> : cs_bulk64f_kernel<fw>;
+                    const int cps = kjf == 5 ? f32_ctas_per_sm<5>() : kjf == 9 ? f32_ctas_per_sm<9>() : 1;
                     const size_t smem = (size_t)fw * (kF32Rows * ldf + 32) * sizeof(float);
                     CSK_CUDA_TRY(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
                     const int64_t units = ceil_div(rows, kF32Rows) * ceil_div(ncols, cw);
-                    const int64_t blocks = std::min<int64_t>(ceil_div(units, fw), (int64_t)di.num_sms);
+                    const int64_t blocks = std::min<int64_t>(ceil_div(units, fw), (int64_t)di.num_sms * cps);
                     prof_mark(st, true);
                     fk<<<(unsigned)blocks, fw * 32, smem, st>>>(
                         code, rows, *reinterpret_cast<const Cols<float>*>(&cols), ncols, ldf,
@@ -1094,14 +1164,19 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
                         LH.hkey0 = (uint32_t)plan->seed;
                         LH.hkey1 = (uint32_t)(plan->seed >> 32);
                     }
+                    // narrow rows (chunk + pad <= 18 / 34 columns): the 2- / 3-CTA-per-SM instantiations
+                    const int kjn = b32_kj(cw);
                     auto kern = code == nullptr ? (narrow ? cs_bulk32_kernel<8, 0, true, true> : cs_bulk32_kernel<8, 0, false, true>)
                                 : expv == 1     ? cs_bulk32_kernel<8, 1>
                                 : expv == 2     ? cs_bulk32_kernel<8, 2>
                                 : expv == 3     ? cs_bulk32_kernel<8, 3>
+                                : kjn == 9      ? cs_bulk32_kernel<8, 0, true, false, 9>
+                                : kjn == 17     ? cs_bulk32_kernel<8, 0, true, false, 17>
                                 : narrow        ? cs_bulk32_kernel<8, 0, true>
                                                 : cs_bulk32_kernel<8, 0>;
+                    const int cps = code == nullptr || expv != 0 ? 1 : kjn == 9 ? b32_ctas_per_sm<9>() : kjn == 17 ? b32_ctas_per_sm<17>() : 1;
                     CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                    const int64_t blocks = std::min<int64_t>(ceil_div(units32, 8), (int64_t)di.num_sms);
+                    const int64_t blocks = std::min<int64_t>(ceil_div(units32, 8), (int64_t)di.num_sms * cps);
                     prof_mark(st, true);   // right before the launch: host prep is not timed
                     kern<<<(unsigned)blocks, 256, smem, st>>>(code, rows, cols, ncols, ld32, out, LH, (int)plan->k1);
                     CSK_LAUNCH_CHECK();
@@ -1285,7 +1360,15 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
                 bulk_layout(L, k1, ncols, 4, 8);   // 32-B aligned rows and chunk starts
                 // no cap on the copy count: a cap would let the mean depth exceed 64 at small k1 (the 1e-5 bound needs
                 // every bucket sum of a copy to stay far below 1e-5 / u32 = 168 terms)
-                const int64_t ncp = std::max<int64_t>(1, ceil_div(rows, 64 * k1));
+                int64_t ncp = std::max<int64_t>(1, ceil_div(rows, 64 * k1));
+                // a small copy is spread: S consecutive tiles go to S different copies (kernel comment), S
+                // chosen so the S copies in use reach the spread footprint
+                {
+                    const int64_t cbytes = (int64_t)k1 * L.lc * 4 * ((ncols + L.cw - 1) / L.cw);
+                    const int64_t S = std::max<int64_t>(1, std::min<int64_t>(ncp, spread_target_bytes() / std::max<int64_t>(cbytes, 1)));
+                    ncp = ceil_div(ncp, S) * S;
+                    L.f32_spread = (int)S;
+                }
                 L.ncopies = (int)ncp;
                 // whole 64-row tiles per copy (the kernel maps a tile to its copy with one division); the
                 // mean bucket depth stays <= 64 + 64 / k1 (<= 128 for k1 = 1, where the depth is exact)
@@ -1374,8 +1457,12 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
             const int64_t lcd = (ncols + 1) & ~1;
             double* Yt = nullptr;
             CSK_CUDA_TRY(csk_malloc_async(&Yt, (size_t)k1 * lcd * sizeof(double), st));
-            cs_combine_rows_kernel<<<(unsigned)ceil_div(k1 * lcd, 256), 256, 0, st>>>(
-                reinterpret_cast<const float*>(tgt.buf), L, k1, ncols, Yt, lcd);
+            if (L.ncopies >= kCombineWarpCopies)
+                cs_combine_warp_kernel<true><<<(unsigned)ceil_div(k1 * lcd, 8), 256, 0, st>>>(
+                    reinterpret_cast<const float*>(tgt.buf), L, k1, ncols, lcd, Yt, nullptr, 0);
+            else
+                cs_combine_rows_kernel<<<(unsigned)ceil_div(k1 * lcd, 256), 256, 0, st>>>(
+                    reinterpret_cast<const float*>(tgt.buf), L, k1, ncols, Yt, lcd);
             const csk_status ls = launch_ok("fp32 combine");
             if (ls != CSK_OK) {
                 cudaFreeAsync(Yt, st);
@@ -1395,8 +1482,12 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
     if (!tgt.owned) return CSK_OK;
     dim3 grid((unsigned)ceil_div(k1, 32), (unsigned)ceil_div(ncols, 32));
     if (L.ncopies > 0) {
-        cs_combine_f32_kernel<<<grid, dim3(32, 8), 0, st>>>(reinterpret_cast<const float*>(tgt.buf), L, k1, ncols,
-                                                            static_cast<float*>(SA), ldsa);
+        if (L.ncopies >= kCombineWarpCopies)
+            cs_combine_warp_kernel<false><<<(unsigned)ceil_div(k1 * ncols, 8), 256, 0, st>>>(
+                reinterpret_cast<const float*>(tgt.buf), L, k1, ncols, 0, nullptr, static_cast<float*>(SA), ldsa);
+        else
+            cs_combine_f32_kernel<<<grid, dim3(32, 8), 0, st>>>(reinterpret_cast<const float*>(tgt.buf), L, k1, ncols,
+                                                                static_cast<float*>(SA), ldsa);
         return launch_ok("fp32 combine");
     }
     if (variant_rowmajor(variant)) {

@@ -13,7 +13,8 @@ import paper_2508_14209_b200 as csk  # noqa: E402
 import synth  # noqa: E402
 
 SHAPES = {"c2": (1 << 24, 64, 8192, 128), "c4": (1 << 23, 128, 32768, 256), "c3": (1 << 22, 256, 131072, 512),
-          "c5": (1 << 27, 64, 8192, 128), "n32": (1 << 23, 32, 2048, 64), "n8": (1 << 23, 8, 128, 16), "n16": (1 << 23, 16, 512, 32), "n128": (1 << 22, 128, 32768, 256)}
+          "c5": (1 << 27, 64, 8192, 128), "n32": (1 << 23, 32, 2048, 64), "n8": (1 << 23, 8, 128, 16), "n16": (1 << 23, 16, 512, 32), "n128": (1 << 22, 128, 32768, 256),
+          "n32d21": (1 << 21, 32, 2048, 64), "n32d22": (1 << 22, 32, 2048, 64), "n24": (1 << 23, 24, 1152, 48)}
 name = sys.argv[1]
 f32 = "f32" in sys.argv[2:]
 ms = "ms" in sys.argv[2:]

@@ -4,6 +4,8 @@
 //            do, without the A loads); rows/s and sector-RMW/s for fp64 and fp32 rows
 //   dsmem  : red.shared::cluster.add.f64 to random words of a cluster's distributed bucket table
 //            (the cluster-privatised alternative of VERDICT r1 #5), ops/clk/SM
+//   redg   : the same rows reduced by warp-wide red.global (16-B .v4.f32 or scalar .f64) from the LSU,
+//            alone and mixed with the bulk path (a fraction of the rows on each engine)
 //   smem   : private shared-memory buckets, random fp64 read-add-write (no atomics; one warp per
 //            array) -- the per-SM scatter rate of the privatised variant
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o l2red_bench l2red_bench.cu
@@ -47,6 +49,56 @@ __global__ void __launch_bounds__(256, 1) bulk_kernel(char* table, int k1, int r
         asm volatile("cp.async.bulk.wait_group.read 4;" ::: "memory");
     }
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+
+// LSU path: rows reduced by warp-wide red.global (REDG) instead of the TMA engine.  VEC = 4: 16-B
+// red.global.add.v4.f32 chunks (REDG.E.ADD.F32x4), VEC = 1: scalar red.global.add.f64.  Each warp
+// covers 32 rows per iteration, item e = it * 32 + lane -> (row e / cpr, chunk e % cpr).
+// MIX > 0: rows with (r % 8) < MIX go through the bulk path instead (both engines at once).
+template <int VEC, int MIX>
+__global__ void __launch_bounds__(256, 1) redg_kernel(char* table, int k1, int rowb, int64_t rows, int ldrow) {
+    extern __shared__ __align__(16) char sm[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    char* row = sm + (warp * 32 + lane) * ldrow;
+    for (int i = 0; i < rowb / 4; ++i) reinterpret_cast<float*>(row)[i] = 1.0f;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    const uint32_t src = (uint32_t)__cvta_generic_to_shared(row);
+    const int cb = VEC == 4 ? 16 : 8;
+    const int cpr = rowb / cb;   // chunks per row
+    const int64_t nwarps = (int64_t)gridDim.x * 8;
+    for (int64_t u = blockIdx.x * 8 + warp; u * 32 < rows; u += nwarps) {
+        const int64_t rb = u * 32;
+        if (MIX > 0) {
+            const int64_t r = rb + lane;
+            if ((lane & 7) < MIX && r < rows) {
+                const uint32_t m = ((uint64_t)mix((uint32_t)r) * (uint32_t)k1) >> 32;
+                char* dst = table + (int64_t)m * ldrow;
+                if (VEC == 4)
+                    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst),
+                                 "r"(src), "r"(rowb) : "memory");
+                else
+                    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(dst),
+                                 "r"(src), "r"(rowb) : "memory");
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 4;" ::: "memory");
+        }
+        for (int e = lane; e < 32 * cpr; e += 32) {
+            const int rr = e / cpr, ch = e - rr * cpr;
+            const int64_t r = rb + rr;
+            if (r >= rows || (MIX > 0 && (rr & 7) < MIX)) continue;
+            const uint32_t m = ((uint64_t)mix((uint32_t)r) * (uint32_t)k1) >> 32;
+            char* dst = table + (int64_t)m * ldrow + ch * cb;
+            if (VEC == 4)
+                asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(1.0f), "f"(1.0f),
+                             "f"(1.0f), "f"(1.0f) : "memory");
+            else
+                asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(dst), "d"(1.0) : "memory");
+        }
+    }
+    if (MIX > 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // cluster of CL CTAs, each owning k1/CL fp64 buckets of one column in shared memory; every thread adds
@@ -123,6 +175,48 @@ int main(int argc, char** argv) {
         const double sectors = (double)rows * ((c.rowb + 31) / 32);
         printf("bulk %-36s %8.3f ms  %7.2f Grows/s  %7.1f Gsector/s  %7.2f TB/s payload\n", c.name, ms,
                rows / ms / 1e6, sectors / ms / 1e6, rows * (double)c.rowb / ms / 1e9);
+    }
+    {   // same fp64 528-B rows into larger tables (k1 x 544 B: 4.5 / 17.8 / 35.7 / 71 MB): is the rate limited
+        // by contention on the table's lines (then spread copies of SA^T would help at C2) or by the slices?
+        char* big;
+        cudaMalloc(&big, (size_t)131072 * 544);
+        cudaMemset(big, 0, (size_t)131072 * 544);
+        const size_t smem = 256 * (size_t)544;
+        cudaFuncSetAttribute(bulk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        for (int kk : {2048, 8192, 32768, 65536, 131072}) {
+            for (int rep = 0; rep < 2; ++rep) {
+                cudaEventRecord(e0);
+                bulk_kernel<false><<<nsm, 256, smem>>>(big, kk, 528, rows, 544);
+                cudaEventRecord(e1);
+                cudaEventSynchronize(e1);
+            }
+            cudaEventElapsedTime(&ms, e0, e1);
+            printf("bulk f64 528-B rows, table k1 = %6d (%6.1f MB): %8.3f ms  %7.2f TB/s payload\n", kk, kk * 544 / 1e6, ms,
+                   rows * 528.0 / ms / 1e9);
+        }
+        cudaFree(big);
+    }
+    {
+        struct RCase { void (*k)(char*, int, int, int64_t, int); int rowb, ldrow; const char* name; };
+        RCase rc[] = {{redg_kernel<4, 0>, 272, 288, "REDG.F32x4 f32 68 cols (272 B)"},
+                      {redg_kernel<4, 2>, 272, 288, "mix f32: 2/8 rows bulk, 6/8 REDG.F32x4"},
+                      {redg_kernel<4, 4>, 272, 288, "mix f32: 4/8 rows bulk, 4/8 REDG.F32x4"},
+                      {redg_kernel<4, 6>, 272, 288, "mix f32: 6/8 rows bulk, 2/8 REDG.F32x4"},
+                      {redg_kernel<1, 0>, 528, 544, "REDG.F64 f64 66 cols (528 B)"},
+                      {redg_kernel<1, 6>, 528, 544, "mix f64: 6/8 rows bulk, 2/8 REDG.F64"}};
+        for (auto& c : rc) {
+            const size_t smem = 256 * (size_t)c.ldrow;
+            cudaFuncSetAttribute(c.k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            for (int rep = 0; rep < 2; ++rep) {
+                cudaEventRecord(e0);
+                c.k<<<nsm, 256, smem>>>(table, k1, c.rowb, rows, c.ldrow);
+                cudaEventRecord(e1);
+                cudaEventSynchronize(e1);
+            }
+            cudaEventElapsedTime(&ms, e0, e1);
+            printf("redg %-40s %8.3f ms  %7.2f Grows/s  %7.2f TB/s payload  err=%s\n", c.name, ms, rows / ms / 1e6,
+                   rows * (double)c.rowb / ms / 1e9, cudaGetErrorString(cudaGetLastError()));
+        }
     }
     double* out;
     cudaMalloc(&out, 4096 * 8);

@@ -331,9 +331,11 @@ def test_ms_apply_gstage_any_split_deterministic(monkeypatch, ctas):
     del Z2
 
 
-def test_ms_apply_fp32_input():
-    # fp32 [A b]: the sketch accumulates in fp64 (R12), the G-stage runs in fp64, Z is rounded once
-    d, n, k1, k2 = 40000, 33, 2048, 66
+@pytest.mark.parametrize("d,n,k1", [(40000, 33, 2048), (1 << 20, 8, 128)])
+def test_ms_apply_fp32_input(d, n, k1):
+    # fp32 [A b]: the sketch accumulates in bounded-depth fp32 copies summed in fp64 (R12), the G-stage
+    # runs in fp64, Z is rounded once.  (2^20, 8, 128): 128 copies, the warp-per-element combine
+    k2 = 2 * n
     plan = csk.cs_plan(d, k1, 8)
     A = synth.gaussian_matrix(d, n, seed=4, dtype=np.float32)
     b = synth.gaussian_matrix(d, 1, seed=5, dtype=np.float32)[:, 0]
@@ -524,7 +526,9 @@ def test_cs_apply_b32_shapes(d, n, with_b, k1):
 @pytest.mark.parametrize("d,n,with_b,k1,off", [(1 << 21, 64, True, 2048, 0), (300007, 40, False, 512, 0),
                                                (100003, 129, True, 1024, 0), (50001, 7, True, 4096, 1),
                                                (1 << 20, 256, True, 131072, 0), (70008, 65, True, 8192, 0),
-                                               (4104, 3, False, 64, 0), (64008, 66, True, 4096, 8)])
+                                               (4104, 3, False, 64, 0), (64008, 66, True, 4096, 8),
+                                               (1 << 20, 8, True, 128, 0), (1 << 20, 16, False, 512, 8),
+                                               (777777, 30, True, 1800, 0)])
 def test_cs_apply_fp32_accumulation(monkeypatch, acc, d, n, with_b, k1, off):
     # fp32 input: fp32 sums in row-block copies of bounded bucket depth, combined in fp64 ("1", the
     # default: 64-row tiles, 32-B loads), or fp64 accumulation ("0"); both within 1e-5 * sum|terms|
@@ -594,6 +598,27 @@ def test_hash_plan_ms_lstsq_matches_stored_codes():
     nb = np.linalg.norm(b)
     check_fitted(A, host(x0) - host(x1), nb, 1e-8)
     assert abs(r0 - r1) <= 1e-8 * nb
+
+
+# ------------------------------------------------ narrow B32 / fp32 instantiations (2-3 CTAs per SM)
+@pytest.mark.parametrize("narrow", ["1", "0"])
+@pytest.mark.parametrize("d,n,with_b,k1", [(300007, 1, True, 64), (262147, 8, True, 128), (131101, 16, False, 512),
+                                           (200001, 17, True, 578), (150011, 24, True, 1152), (100003, 32, True, 2048),
+                                           (90001, 33, True, 2178), (80021, 33, False, 999)])
+def test_cs_apply_narrow_rows(monkeypatch, narrow, d, n, with_b, k1):
+    # n + b <= 17 / 33 columns run the KJ = 9 / 17 kernels (CSK_B32_NARROW=0: the one-CTA kernel), fp64
+    # within 1e-12 T and exact on integer A; fp32 within 1e-5 T (KJF = 5 / 9); ragged last tiles
+    monkeypatch.setenv("CSK_B32_NARROW", narrow)
+    plan = csk.cs_plan(d, k1, 11)
+    h, s = oracle.codes(d, k1, 11)
+    A = synth.gaussian_matrix(d, n, seed=7)
+    b = synth.rhs(A, "easy", seed=7) if with_b else None
+    _check_apply(plan, h, s, A, b, "B")
+    Ai = synth.integer_matrix(d, n, seed=8)
+    got = host(csk.cs_apply(plan, gpu_colmajor(Ai), variant="B"))
+    assert np.array_equal(got, oracle.cs_apply(h, s, Ai, k1))
+    _check_apply(plan, h, s, A.astype(np.float32), None if b is None else b.astype(np.float32), "B",
+                 dtype=np.float32, rel=1e-5)
 
 
 # ------------------------------------------------ spread SA^T copies (small k1)
