@@ -25,9 +25,40 @@ for _ in range(3):
 torch.cuda.synchronize()
 from torch.profiler import ProfilerActivity, profile  # noqa: E402
 
+# the bench's pipelined step: ms_apply on the main stream, the solve on a second stream (double-buffered)
+s_solve = torch.cuda.Stream()
+Zs = [Z, synth.colmajor_empty(torch, k2, n + 1, torch.float64, "cuda")]
+xs = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(2)]
+st = torch.zeros(64, dtype=torch.int32, device="cuda")
+rs = torch.zeros(64, dtype=torch.float64, device="cuda")
+slot_free = [None, None]
+main = torch.cuda.current_stream()
+
+
+def pipelined(i=[0]):
+    sl = i[0] & 1
+    if slot_free[sl] is not None:
+        slot_free[sl].synchronize()
+        main.wait_event(slot_free[sl])
+    csk.ms_apply(plan, k2, A, b=b, Z=Zs[sl])
+    e = torch.cuda.Event()
+    e.record(main)
+    s_solve.wait_event(e)
+    csk.ms_solve_async(Zs[sl], n, x=xs[sl], status=st[i[0] % 64:i[0] % 64 + 1], sk_resid=rs[i[0] % 64:i[0] % 64 + 1],
+                       stream=s_solve)
+    e2 = torch.cuda.Event()
+    e2.record(s_solve)
+    slot_free[sl] = e2
+    i[0] += 1
+
+
+for _ in range(4):
+    pipelined()
+torch.cuda.synchronize()
 out = {}
 for what, fn in (("cs_apply", lambda: csk.cs_apply(plan, A, b=b, SA=SA)),
-                 ("ms_apply", lambda: csk.ms_apply(plan, k2, A, b=b, Z=Z))):
+                 ("ms_apply", lambda: csk.ms_apply(plan, k2, A, b=b, Z=Z)),
+                 ("pipelined_step", pipelined)):
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         for _ in range(6):
             fn()

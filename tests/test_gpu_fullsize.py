@@ -4,7 +4,7 @@ oracle on the same bytes.
 
 * C2 (d=2^24, n=64 + b, k1=8192, k2=128) and C4 (d=2^23, n=128 + b, k1=32768, k2=256, kappa=1e10):
   SA elementwise within 1e-12 * T, Z within 1e-12 * |G| T, and the C4 least-squares solution within
-  DESIGN.md R16b of the oracle's.
+  DESIGN.md R16b of the oracle's; C2 in fp32 within 1e-5 * T (the fp32 copies path).
 * C3 (d=2^22, n=256 + b, k1=131072, k2=512): a column subset that spans every chunk boundary of the
   chunk-major layout (the CountSketch and the G-stage are column-separable, Eq 2).
 * C5 (d=2^27, n=64 + b: 8.7e9 elements, past 2^31): integer-valued A, row-partitioned plans
@@ -79,6 +79,31 @@ def _full(d, n, k1, k2, kappa=None, check_ls=False):
 
 def test_c2_full_size():
     _full(1 << 24, 64, 8192, 128)
+
+
+def test_c2_full_size_fp32():
+    # C2's fp32 form (BASELINE: "also fp32"): the bounded-depth fp32 copies summed in fp64 (R12) within
+    # 1e-5 * T of the exact fp64 sums of the same fp32 values, and the multisketch Z within 1e-5 |G| T
+    d, n, k1, k2 = 1 << 24, 64, 8192, 128
+    buf = synth.gaussian_matrix_torch(d, n + 1, seed=DATA)
+    b32 = synth.colmajor_empty(torch, d, n + 1, torch.float32, "cuda")
+    b32.copy_(buf)
+    del buf
+    _free()
+    A, b = b32[:, :n], b32[:, n]
+    plan = csk.cs_plan(d, k1, SEED)
+    SA = host(csk.cs_apply(plan, A, b=b))
+    Z = host(csk.ms_apply(plan, k2, A, b=b))
+    assert SA.dtype == np.float32 and Z.dtype == np.float32
+    Ah = _host_colmajor(b32).astype(np.float64)
+    del b32, A, b
+    _free()
+    h, s = harness.codes(d, k1, SEED)
+    SAo, T = harness.cs_apply(h, s, Ah[:, :n], k1, b=Ah[:, n], with_abs=True)
+    assert_within_T(SA.astype(np.float64), SAo, T, 1e-5)
+    G = oracle.gauss(k2, k1, SEED)
+    Zo, Zabs = harness.gemm(G, SAo, T)
+    assert_within_T(Z.astype(np.float64), Zo, Zabs, 1e-5)
 
 
 def test_c4_full_size_with_least_squares():
