@@ -41,6 +41,17 @@ for kb in ("0", "4096"):   # spread SA^T copies off / one per CTA
     csk.cs_apply(plan, Ad, b=bd, variant="B")
     env(CSK_SPREAD_KB=None)
 print("cs_apply spread", flush=True)
+# narrow B instantiations (KJ = 9 / 17, KJF = 5 / 9; 2-3 CTAs per SM) and the warp-per-element fp32
+# combine (2^16 rows at k1 = 16: 64 copies), both outputs (column-major SA, ms_apply's row-major Y)
+A24 = synth.gaussian_matrix(20011, 24, seed=8)
+p24 = csk.cs_plan(20011, 700, 3)
+csk.cs_apply(p24, cm(A24), b=cm(A24[:, 1].copy()), variant="B")
+csk.cs_apply(p24, cm(A24.astype(np.float32)), b=cm(A24[:, 1].astype(np.float32)), variant="B")
+A6 = synth.gaussian_matrix(1 << 16, 6, seed=9, dtype=np.float32)
+p16 = csk.cs_plan(1 << 16, 16, 5)
+csk.cs_apply(p16, cm(A6), b=cm(A6[:, 0].copy()), variant="B")
+csk.ms_apply(p16, 14, cm(A6), b=cm(A6[:, 0].copy()))
+print("cs_apply narrow + warp combine", flush=True)
 Am = synth.gaussian_matrix(8192, 100, seed=6)   # G-stage with 4 DMMA warps x 32 rows (NT = 7) and 2 M tiles
 csk.ms_apply(csk.cs_plan(8192, 4096, 4), 256, cm(Am), b=cm(Am[:, 0].copy()))
 print("ms_apply NT=7 MW=4", flush=True)
