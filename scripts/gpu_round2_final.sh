@@ -1,7 +1,7 @@
 # Round-2 close-out evidence (run with gpurun from the repo root; outputs in gpurun_out/, copied to profiles/ r02_*):
 # the whole -m gpu suite (parity slack), smoke(), bench lines C2 (default) / C4 / C3 / SRHT / rand_cholQR,
 # the Figs 3-5 grid, the csk-kernel launch list of the default step, ncu --set full of the C2 CountSketch and
-# of the narrow (n = 32) instantiation, and the four compute-sanitizer tools.
+# of the narrow (n = 32) instantiation. (compute-sanitizer is closed on the GPU pool since round 2.)
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv
 timeout 2400 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/f_gputests.txt 2>&1
@@ -15,4 +15,3 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k "regex:
 echo "launches rc=$?"
 REPS=1 timeout 900 ncu --set full --import-source on --clock-control none -k regex:cs_bulk32 -s 3 -c 1 -o gpurun_out/f_ncu_c2_cs python scripts/cs_time.py c2 > /dev/null 2>&1; echo "ncu c2 rc=$?"
 REPS=1 timeout 900 ncu --set full --import-source on --clock-control none -k regex:cs_bulk32 -s 3 -c 1 -o gpurun_out/f_ncu_n32_cs python scripts/cs_time.py n32 > /dev/null 2>&1; echo "ncu n32 rc=$?"
-bash scripts/gpu_sanitize.sh
