@@ -774,6 +774,7 @@ __global__ void cs_combine_rows_kernel(const float* __restrict__ SAt, RowLayout 
     double acc = 0.0;
     if (c < ncols) {
         const int64_t off = (int64_t)(c / L.cw) * L.cs + m * L.lc + (c % L.cw);
+        #pragma unroll 8   // the loads of 8 copies in flight; the adds stay in copy order
         for (int p = 0; p < L.ncopies; ++p) acc += (double)SAt[p * L.copy_stride + off];
     }
     Yt[e] = acc;
@@ -803,6 +804,7 @@ __global__ void __launch_bounds__(256) cs_combine_warp_kernel(const float* __res
     double acc = 0.0;
     if (c < ncols) {
         const int64_t off = (int64_t)(c / L.cw) * L.cs + m * L.lc + (c % L.cw);
+        #pragma unroll 8   // the loads of 8 copies in flight; the adds stay in copy order
         for (int p = lane; p < L.ncopies; p += 32) acc += (double)SAt[p * L.copy_stride + off];
     }
 #pragma unroll
@@ -820,6 +822,7 @@ constexpr int kCombineWarpCopies = 64;   // ncopies from which the warp-per-elem
 __global__ void cs_spread_combine_kernel(double* __restrict__ SAt, int64_t n, int nspread, int64_t stride) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
         double acc = SAt[e];
+        #pragma unroll 8   // the loads of 8 copies in flight; the adds stay in copy order
         for (int p = 1; p < nspread; ++p) acc += SAt[p * stride + e];
         SAt[e] = acc;
     }
@@ -837,6 +840,7 @@ __global__ void cs_combine_f32_kernel(const float* __restrict__ SAt, RowLayout L
         double acc = 0.0;
         if (m < k1 && c < ncols) {
             const int64_t off = (int64_t)(c / L.cw) * L.cs + m * L.lc + (c % L.cw);
+            #pragma unroll 8   // the loads of 8 copies in flight; the adds stay in copy order
             for (int q = 0; q < L.ncopies; ++q) acc += (double)SAt[q * L.copy_stride + off];
         }
         t[j][threadIdx.x] = (float)acc;

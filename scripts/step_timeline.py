@@ -1,6 +1,6 @@
 """Kernel timeline of consecutive cs_apply / ms_apply / pipelined steps at C2 (torch.profiler, CUPTI):
 where the time between the CountSketch kernels goes (gaps, G-stage, memsets).
-usage: python scripts/step_timeline.py [c2|c4|c3]"""
+usage: python scripts/step_timeline.py [c2|c4|c3] [f32]"""
 import json
 import os
 import sys
@@ -13,12 +13,18 @@ import synth  # noqa: E402
 
 SHAPES = {"c2": (1 << 24, 64, 8192, 128), "c4": (1 << 23, 128, 32768, 256), "c3": (1 << 22, 256, 131072, 512)}
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
+f32 = "f32" in sys.argv[2:]
 d, n, k1, k2 = SHAPES[name]
 buf = synth.gaussian_matrix_torch(d, n + 1)
+if f32:
+    b32 = synth.colmajor_empty(torch, d, n + 1, torch.float32, "cuda")
+    b32.copy_(buf)
+    del buf
+    buf = b32
 A, b = buf[:, :n], buf[:, n]
 plan = csk.cs_plan(d, k1, 1)
-SA = synth.colmajor_empty(torch, k1, n + 1, torch.float64, "cuda")
-Z = synth.colmajor_empty(torch, k2, n + 1, torch.float64, "cuda")
+SA = synth.colmajor_empty(torch, k1, n + 1, buf.dtype, "cuda")
+Z = synth.colmajor_empty(torch, k2, n + 1, buf.dtype, "cuda")
 for _ in range(3):
     csk.ms_apply(plan, k2, A, b=b, Z=Z)
     csk.cs_apply(plan, A, b=b, SA=SA)
@@ -27,7 +33,7 @@ from torch.profiler import ProfilerActivity, profile  # noqa: E402
 
 # the bench's pipelined step: ms_apply on the main stream, the solve on a second stream (double-buffered)
 s_solve = torch.cuda.Stream()
-Zs = [Z, synth.colmajor_empty(torch, k2, n + 1, torch.float64, "cuda")]
+Zs = [Z, synth.colmajor_empty(torch, k2, n + 1, buf.dtype, "cuda")]
 xs = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(2)]
 st = torch.zeros(64, dtype=torch.int32, device="cuda")
 rs = torch.zeros(64, dtype=torch.float64, device="cuda")
@@ -52,13 +58,14 @@ def pipelined(i=[0]):
     i[0] += 1
 
 
-for _ in range(4):
-    pipelined()
+if not f32:   # the solve takes fp64 Z
+    for _ in range(4):
+        pipelined()
 torch.cuda.synchronize()
 out = {}
 for what, fn in (("cs_apply", lambda: csk.cs_apply(plan, A, b=b, SA=SA)),
                  ("ms_apply", lambda: csk.ms_apply(plan, k2, A, b=b, Z=Z)),
-                 ("pipelined_step", pipelined)):
+                 ("pipelined_step", pipelined))[: 2 if f32 else 3]:
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         for _ in range(6):
             fn()
