@@ -42,6 +42,7 @@ struct WyArgs {
     int ldr;
     double* x;
     SolveStatus* status;
+    int push;   // DSMEM push of V/T to the next panel owner (CSK_QR_PUSH=0 disables, for A/B)
 #ifdef CSK_QR_PROFILE
     long long* prof;   // [P][npan+1][8] clock64 stamps (scripts/qr_wy_prof.cu)
 #endif
@@ -280,6 +281,17 @@ __device__ __forceinline__ void factor_panel(const WyArgs& a, const double* cols
     const int t0 = j0 >> 5;
     const bool pub = a.P > 1;
     double* Vgk = a.Vg + (size_t)kp * kB * ldw;
+    // the owner of panel kp + 1 applies Q_kp to its panel on the critical path of the next step: push
+    // V and T straight into its shared memory (same buffer offset, DSMEM) so it skips the L2 staging
+    // after the cluster barrier (2.7 K cycles per step at 256 x 129, scripts/qr_wy_prof.cu)
+    double* Vrem = nullptr;
+    double* Trem = nullptr;
+    if (pub && a.push && kp + 1 < a.npan) {
+        cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+        const unsigned nxt = (unsigned)((kp + 1) % a.P);
+        Vrem = cl.map_shared_rank(Vout, nxt);
+        Trem = cl.map_shared_rank(Tout, nxt);
+    }
 #pragma unroll
     for (int c = 0; c < kB; ++c)
 #pragma unroll
@@ -288,6 +300,7 @@ __device__ __forceinline__ void factor_panel(const WyArgs& a, const double* cols
             if (tb >= t0 && r < m) {
                 Vout[c * ldw + r] = p[c][u];
                 if (pub) Vgk[c * ldw + r] = p[c][u];
+                if (Vrem) Vrem[c * ldw + r] = p[c][u];
             }
         }
     if (threadIdx.x < kB * kB) {
@@ -297,6 +310,7 @@ __device__ __forceinline__ void factor_panel(const WyArgs& a, const double* cols
             if ((int)threadIdx.x == e) tv = T[e];
         Tout[threadIdx.x] = tv;
         if (pub) a.Tg[(size_t)kp * kB * kB + threadIdx.x] = tv;
+        if (Trem) Trem[threadIdx.x] = tv;
     }
 }
 
@@ -513,7 +527,9 @@ __global__ void __launch_bounds__(kThreads, 1) qr_wy_kernel(WyArgs a) {
         const int owner = k % P, j0 = k * kB, buf = k & 1;
         double* V = Vst + (size_t)buf * kB * ldw;
         double* T = Tst + buf * kB * kB;
-        if (rank != owner) {
+        // the owner of panel k + 1 received V_k and T_k by DSMEM from the owner of panel k (factor_panel)
+        const bool pushed = a.push && P > 1 && k + 1 < npan && rank == (k + 1) % P;
+        if (rank != owner && !pushed) {
             // V rows >= 32*(j0/32) of the 4 columns (16-B vectors; ldw and the row start are even)
             const double* Vgk = a.Vg + (size_t)k * kB * ldw;
             const int r0 = (j0 >> 5) * 32, h = (m - r0 + 1) >> 1;
@@ -611,6 +627,10 @@ csk_status qr_wy_launch(const double* Z, int64_t ldz, int m, int nc, double* Rg,
     a.ldr = ldr;
     a.x = x;
     a.status = status;
+    {
+        const char* pe = std::getenv("CSK_QR_PUSH");
+        a.push = !(pe && std::atoi(pe) == 0);
+    }
 #ifdef CSK_QR_PROFILE
     a.prof = qr_wy_prof_buffer;
 #endif
