@@ -351,6 +351,7 @@ SOLVERS = {
     "wy": {},
     "wy_p4": {"CSK_QR_WY_P": "4"},
     "wy_p16": {"CSK_QR_WY_P": "16"},
+    "wy_p16_l2_staging": {"CSK_QR_WY_P": "16", "CSK_QR_PUSH": "0"},   # V/T staged through L2 only (no DSMEM push)
     "cluster": {"CSK_QR_WY": "0"},
     "single": {"CSK_QR_WY": "0", "CSK_QR_SINGLE": "1"},
 }
