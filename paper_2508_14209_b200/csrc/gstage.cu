@@ -295,8 +295,20 @@ __global__ void __launch_bounds__(256) gstage_reduce_kernel(GsArgs a, int BM, in
     const int r = (int)((blockIdx.x - tile * blocks_per_tile) * 32 + lane);
     const int64_t tq = a.NS * a.VKB;   // flattened k-blocks per tile
     const int c_lo = cta_of(tile * tq, a.total, a.P), c_hi = cta_of((tile + 1) * tq - 1, a.total, a.P);
+    // slot of segment cc for this tile: cc * maxseg + (tile - first tile of cc).  The first tiles come
+    // from one 64-bit division per segment, done once per block into shared memory (a division per
+    // partial load made the reduce ALU-bound: 21 us at C4)
+    constexpr int kMaxSeg = 1024;
+    __shared__ int64_t s_slot[kMaxSeg];
+    const int nseg = c_hi - c_lo + 1;
+    const bool tab = nseg <= kMaxSeg;
+    if (tab)
+        for (int i = threadIdx.x; i < nseg; i += blockDim.x)
+            s_slot[i] = (int64_t)(c_lo + i) * a.maxseg + (tile - range_begin(c_lo + i, a.total, a.P) / tq);
+    __syncthreads();
     auto part_of = [&](int cc) {
-        const int64_t slot = (int64_t)cc * a.maxseg + (tile - range_begin(cc, a.total, a.P) / tq);
+        const int64_t slot = tab ? s_slot[cc - c_lo]
+                                 : (int64_t)cc * a.maxseg + (tile - range_begin(cc, a.total, a.P) / tq);
         return a.part[slot * per_tile + r];
     };
     // segments c_lo + warp, + 8, + 16, ... added in that order; four loads issued before their adds
