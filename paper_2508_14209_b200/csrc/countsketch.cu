@@ -1170,7 +1170,10 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
                     }
                     // narrow rows (chunk + pad <= 18 / 34 columns): the 2- / 3-CTA-per-SM instantiations
                     const int kjn = b32_kj(cw);
-                    auto kern = code == nullptr ? (narrow ? cs_bulk32_kernel<8, 0, true, true> : cs_bulk32_kernel<8, 0, false, true>)
+                    auto kern = code == nullptr ? (kjn == 9    ? cs_bulk32_kernel<8, 0, true, true, 9>
+                                                   : kjn == 17 ? cs_bulk32_kernel<8, 0, true, true, 17>
+                                                   : narrow    ? cs_bulk32_kernel<8, 0, true, true>
+                                                               : cs_bulk32_kernel<8, 0, false, true>)
                                 : expv == 1     ? cs_bulk32_kernel<8, 1>
                                 : expv == 2     ? cs_bulk32_kernel<8, 2>
                                 : expv == 3     ? cs_bulk32_kernel<8, 3>
@@ -1178,7 +1181,7 @@ static csk_status run_variant(int variant, csk_plan_t plan, int ncols, Cols<T> c
                                 : kjn == 17     ? cs_bulk32_kernel<8, 0, true, false, 17>
                                 : narrow        ? cs_bulk32_kernel<8, 0, true>
                                                 : cs_bulk32_kernel<8, 0>;
-                    const int cps = code == nullptr || expv != 0 ? 1 : kjn == 9 ? b32_ctas_per_sm<9>() : kjn == 17 ? b32_ctas_per_sm<17>() : 1;
+                    const int cps = (expv != 0 && code != nullptr) ? 1 : kjn == 9 ? b32_ctas_per_sm<9>() : kjn == 17 ? b32_ctas_per_sm<17>() : 1;
                     CSK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
                     const int64_t blocks = std::min<int64_t>(ceil_div(units32, 8), (int64_t)di.num_sms * cps);
                     prof_mark(st, true);   // right before the launch: host prep is not timed
