@@ -11,7 +11,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2508_14209_b200 as csk  # noqa: E402
 import synth  # noqa: E402
 
-SHAPES = {"c2": (1 << 24, 64, 8192, 128), "c4": (1 << 23, 128, 32768, 256), "c3": (1 << 22, 256, 131072, 512)}
+SHAPES = {"c2": (1 << 24, 64, 8192, 128), "c4": (1 << 23, 128, 32768, 256), "c3": (1 << 22, 256, 131072, 512),
+          "n8": (1 << 23, 8, 128, 16), "n16": (1 << 23, 16, 512, 32), "n32": (1 << 23, 32, 2048, 64)}
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 f32 = "f32" in sys.argv[2:]
 d, n, k1, k2 = SHAPES[name]
