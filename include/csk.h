@@ -48,11 +48,11 @@ typedef enum {
 
 typedef enum { CSK_F64 = 0, CSK_F32 = 1 } csk_dtype;
 
-/* cs_apply kernel variants.  CSK_VAR_AUTO picks per
- * (dtype, SA^T footprint k1 * ncols * w) from the table measured on B200 over
- * d = 2^20 and 2^23, n = 8..256 (profiles/r02_variant_table.json):
- * B for fp64 and for fp32 with SA^T > 64 KB, X (<= 8 KB) or T (<= 64 KB) for a
- * tiny fp32 SA^T. */
+/* cs_apply kernel variants.  CSK_VAR_AUTO picks from the table
+ * measured on B200 over d = 2^20 and 2^23, n = 8..256, fp64 and fp32
+ * (profiles/r02_variant_table.json): B won every row at round-2 close
+ * (its narrow-row instantiations run 2-3 CTAs per SM), so AUTO = B; the other variants
+ * stay selectable (G is the bitwise-reproducible one). */
 typedef enum {
     CSK_VAR_AUTO = -1,
     CSK_VAR_ATOMIC_COL = 0,   /* L: one L2 reduction (REDG) per element, column-major target  */
