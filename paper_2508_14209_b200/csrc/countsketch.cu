@@ -55,6 +55,7 @@ struct RowLayout {
     int f32_spread = 1;   // fp32 copies: consecutive tiles interleaved over this many copies
     unsigned long long* work = nullptr;   // dynamic work counter of the B kernels (zeroed with the workspace)
     int grab = 8;                         // units per counter grab (4/8/16/32 measured: 8)
+    int grab_tail = 1;                    // fp32 kernel: single-unit grabs in the last 2 * grab * warps units
     __host__ __device__ int64_t base(int ch, uint32_t bucket) const { return (int64_t)ch * cs + (int64_t)bucket * lc; }
 };
 
@@ -659,6 +660,7 @@ __global__ void __launch_bounds__(W * 32, f32_ctas_per_sm<KJF>()) cs_bulk64f_ker
     const int64_t nunits = ngroups * nchunks;
     constexpr int kJ = KJF;
     const int kGrab = L.grab;
+    const int64_t tailz = L.grab_tail ? 2 * (int64_t)kGrab * gridDim.x * W : 0;
     int64_t u, uend;
     {
         unsigned long long ub = 0;
@@ -743,11 +745,17 @@ __global__ void __launch_bounds__(W * 32, f32_ctas_per_sm<KJF>()) cs_bulk64f_ker
             dst[h] = cbase + (int64_t)code_bucket(h ? cb : ca) * L.lc;
         }
         if (++u >= uend) {
+            // near the end of the range a grab of kGrab 64-row units is ~kGrab tiles of one warp's time:
+            // the last 2 * kGrab * (warps in the grid) units go out one at a time so the warps finish
+            // together (u is this warp's previous range end, within one round of the counter).  Measured
+            // (profiles/r02_grab_tail_ab.txt): fp32 C2 1.020 -> 1.008 ms; on the fp64 B32 kernel it
+            // gained nothing (C2, C4, C3) or lost (n = 32: +1.8%), so only the fp32 kernel uses it
+            const int g = nunits - u <= tailz ? 1 : kGrab;
             unsigned long long ub = 0;
-            if (lane == 0) ub = atomicAdd(L.work, (unsigned long long)kGrab);
+            if (lane == 0) ub = atomicAdd(L.work, (unsigned long long)g);
             ub = __shfl_sync(0xffffffffu, ub, 0);
             u = (int64_t)ub;
-            uend = min(u + kGrab, nunits);
+            uend = min(u + g, nunits);
         }
         if (u < nunits) fetch();   // next tile's loads in flight while this tile is reduced
 #pragma unroll
@@ -1423,6 +1431,7 @@ csk_status cs_apply_impl(csk_plan_t plan, csk_dtype dtype, int64_t n, const void
         CSK_CUDA_TRY(cudaMemsetAsync(tgt.buf, 0, (ws_doubles + 2) * sizeof(double), st));
         L.work = reinterpret_cast<unsigned long long*>(tgt.buf + ws_doubles);
         if (const char* ge = std::getenv("CSK_GRAB")) L.grab = std::max(1, std::atoi(ge));   // sweep hook
+        if (const char* te = std::getenv("CSK_GRAB_TAIL")) L.grab_tail = std::atoi(te);     // A/B hook
     } else if (variant != CSK_VAR_SORTED && !accumulate) {
         // zero SA (ldsa may exceed k1: clear the k1 x ncols window only)
         if (ldsa == k1) {
